@@ -1,0 +1,218 @@
+/*
+ * libsa -- the Sample-Align-D data-parallel hot path on B200 (sm_100a).
+ *
+ * Saeed & Khokhar, "A Domain Decomposition Strategy for Alignment of Multiple
+ * Biological Sequences on Multiprocessor Platforms", arXiv 0905.1744.
+ * Citations: P:a-b = /root/reference/PAPER.md lines (section / equation /
+ * algorithm given alongside); Z-ids = the readings listed in DESIGN.md §2.
+ *
+ * The five steps (BASELINE.json north_star):
+ *   S1  k-mer count profiles                      sa_kmer_profiles
+ *   S2  k-mer rank vs a pool (Eq. 1 averaged)     sa_kmer_rank (S2a/S2d inside sa_partition)
+ *   S3  rank-based sample-sort partition          sa_partition
+ *   S4  all-to-all redistribution                 sa_redistribute
+ *   S5  all-pairs similarity inside a bucket      sa_bucket_similarity
+ *
+ * Conventions for every call:
+ *   - pointers are DEVICE pointers unless the name ends in _h (host);
+ *   - the caller allocates and frees every input and output; libsa owns only
+ *     its context scratch;
+ *   - work is enqueued on `stream` (a cudaStream_t passed as void*); calls
+ *     are asynchronous except where a host block is documented;
+ *   - errors are returned as sa_status, never thrown or aborted; the message
+ *     is in sa_last_error() (thread-local, valid until the next sa_* call on
+ *     that thread).  On error outputs are unspecified; the context stays
+ *     usable unless SA_E_STATE is returned.
+ *   - there is no CPU fallback: without a usable CUDA device every call that
+ *     computes returns SA_E_CUDA.
+ */
+#ifndef SA_H_
+#define SA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SA_OK = 0,
+  SA_E_INVAL = 1,   /* host-checked argument error (before any launch) */
+  SA_E_RANGE = 2,   /* device-detected: residue >= alphabet, or nk > 65535 */
+  SA_E_CUDA = 3,    /* CUDA runtime error / no device */
+  SA_E_COMM = 4,    /* a communicator callback returned non-zero */
+  SA_E_NOMEM = 5,   /* scratch allocation failed */
+  SA_E_STATE = 6    /* context unusable (sticky CUDA error) */
+} sa_status;
+
+typedef struct sa_ctx sa_ctx;
+
+/* Exact-rank key ("exact ranks"): for a query i ranked against a
+ * pool, key_i = sum_j floor(C_ij * 2^64 / D_ij) as an unsigned 128-bit
+ * integer (lo = low 64 bits).  With V_i = sum_j C_ij / D_ij (Eq. 1 summed,
+ * P:267-269, Eq. 3 in F form P:280-282), 2^64 V_i - npool < key_i <= 2^64 V_i,
+ * so key_b - key_a >= npool certifies V_b > V_a.  Integer sums: the key is
+ * independent of reduction order. */
+typedef struct { uint64_t lo, hi; } sa_key128;
+
+/* A pivot / regular-sample record: global rank key + tie-break. */
+typedef struct {
+  sa_key128 key;        /* global-rank key (pool = global sample S) */
+  int64_t global_idx;   /* index tie-break (reading Z12) */
+  int32_t nk;           /* k-mer count of the sequence */
+  int32_t block;        /* logical block it was sampled from */
+} sa_pivot;
+
+/* Collective operations for sa_partition / sa_redistribute when the
+ * context spans several processes (one per GPU).  Implemented by the caller
+ * (the Python binding uses torch.distributed over NCCL).  Buffers are device
+ * pointers; work must be ordered after prior work on `stream` and later work
+ * on `stream` must observe it.  Return 0 on success. */
+typedef struct {
+  void* user;
+  /* recv[r*bytes .. (r+1)*bytes) <- send of rank r, for r = 0..nranks-1 */
+  int (*allgather)(void* user, const void* send, void* recv, int64_t bytes, void* stream);
+  /* personalised all-to-all of variable byte counts (host arrays of nranks) */
+  int (*alltoallv)(void* user, const void* send, const int64_t* send_bytes_h, const int64_t* send_displs_h,
+                   void* recv, const int64_t* recv_bytes_h, const int64_t* recv_displs_h, void* stream);
+} sa_comm_ops;
+
+/* ------------------------------------------------------------ context ---- */
+sa_status sa_ctx_create(int cuda_device, sa_ctx** out);
+/* Attach a communicator (collective semantics: every rank attaches with the
+ * same nranks).  nranks == 1 (or never attaching) makes every exchange a
+ * local copy.  `ops` is copied; its `user` pointer must stay valid. */
+sa_status sa_ctx_attach_comm(sa_ctx* ctx, const sa_comm_ops* ops, int nranks, int rank);
+sa_status sa_ctx_destroy(sa_ctx* ctx);
+const char* sa_last_error(void);
+/* Number of libsa kernels launched through this process since load. */
+int64_t sa_launch_count(void);
+/* When enabled, libsa records CUDA events around its phases on the call's
+ * stream; sa_ctx_phase_ms returns the durations of the last sa_partition /
+ * sa_bucket_similarity / sa_kmer_rank calls (host-blocking: syncs on the
+ * recorded events).  Phases: see SA_PHASE_*. */
+enum {
+  SA_PHASE_S2A = 0,      /* local rank (min-sum engine, all local blocks)      */
+  SA_PHASE_S2B = 1,      /* local block sort + sample pick                      */
+  SA_PHASE_S2C = 2,      /* sample profile gather / allgather                   */
+  SA_PHASE_S2D = 3,      /* global rank (min-sum engine)                        */
+  SA_PHASE_S3 = 4,       /* block sort, regular samples, pivots, bucket assign  */
+  SA_PHASE_S5 = 5,       /* last sa_bucket_similarity min-sum launch            */
+  SA_PHASE_RANK = 6,     /* last sa_kmer_rank min-sum launch                    */
+  SA_PHASE_COUNT = 7
+};
+sa_status sa_ctx_set_timing(sa_ctx* ctx, int enable);
+sa_status sa_ctx_phase_ms(sa_ctx* ctx, float* ms_h /* [SA_PHASE_COUNT] */);
+
+/* Exact comparison of two ranks over the same pool (host memory, no GPU):
+ * sign of V_a - V_b with V_x = sum_j C_xj / min(nk_x, nk_pool[j]) (terms with
+ * a zero denominator are 0).  Ca_h / Cb_h: numerator rows [npool] (uint16).
+ * Returns -1, 0 or +1; this is the big-integer routine sa_partition uses for
+ * comparisons its keys do not certify. */
+int sa_exact_rank_compare(const uint16_t* Ca_h, int32_t nka, const uint16_t* Cb_h, int32_t nkb,
+                          const int32_t* nk_pool_h, int32_t npool);
+
+/* Row stride (elements) of a profile matrix with `bins` = alphabet^k bins:
+ * bins rounded up to a multiple of 64, the extra bins always zero. */
+int32_t sa_profile_stride(int32_t bins);
+
+/* ------------------------------------------------------ S1: profiles ---- */
+/* c^X for every sequence: profiles[i][t] = number of positions u
+ * with id(x_u .. x_{u+k-1}) = t, id = base-`alphabet` big-endian value of
+ * the word (reading Z21); nkmers[i] = max(0, n_i - k + 1) (Eq. 1 denominator
+ * term).  residues: uint8 codes 0..alphabet-1, CSR by offsets[0..n].
+ * profiles: [n][sa_profile_stride(alphabet^k)] uint16 (padding zeroed).
+ * SA_E_INVAL: NULL pointer with n > 0, k < 1, alphabet < 2, alphabet^k > 65536.
+ * SA_E_RANGE: a residue >= alphabet, or nk > 65535 (counts / numerators are
+ * uint16).  n == 0 is a no-op. */
+sa_status sa_kmer_profiles(sa_ctx* ctx, const uint8_t* residues, const int64_t* offsets, int32_t n,
+                           int32_t k, int32_t alphabet, uint16_t* profiles, int32_t* nkmers, void* stream);
+
+/* ---------------------------------------------------------- S2: rank ---- */
+/* Rank of each query against a pool, Eq. 1 averaged (Eq. 3 in F form, reading
+ * Z1/O1): R_q = (1/npool) sum_j F(q, j), F = C/D with
+ * C = sum_t min(c^q_t, c^j_t) (reading Z3) and D = min(nk_q, nk_j)
+ * (F = 0 if D = 0, reading Z4).  The self term is counted when the query is in
+ * the pool (reading Z11).
+ *   keys[nq]            exact-rank keys (sa_key128, see above)
+ *   rank_f64[nq]        nullable: RN(key) * 2^-64 / npool  (|error| <= 2 ulp + npool*2^-64/npool)
+ *   numerators[nq][npool] nullable: C as uint16, row-major
+ * Profiles use the sa_profile_stride(bins) row stride.
+ * SA_E_INVAL: npool == 0 ("empty pool"), NULL required pointer. */
+sa_status sa_kmer_rank(sa_ctx* ctx, const uint16_t* q_prof, const int32_t* q_nk, int32_t nq,
+                       const uint16_t* pool_prof, const int32_t* pool_nk, int32_t npool, int32_t bins,
+                       sa_key128* keys, double* rank_f64, uint16_t* numerators, void* stream);
+
+/* ----------------------------------------------------- S2-S3: partition -- */
+/* Optional intermediate artifacts for parity checks (every field nullable). */
+typedef struct {
+  sa_key128* local_key;      /* [n_local] S2a keys (pool = own logical block)      */
+  double* local_f64;         /* [n_local] S2a rank fp64                            */
+  int64_t* local_order;      /* [n_local] S2b: global ids, each block sorted        */
+  int64_t* sample_idx;       /* [p*samples_per_block] global sample S, (q, j) order */
+  sa_key128* global_key;     /* [n_local] S2d keys (pool = S)                      */
+  double* global_f64;        /* [n_local] S2d rank fp64                            */
+  int64_t* global_order;     /* [n_local] S3a: global ids, each block sorted        */
+  int64_t* candidates;       /* [p*(p-1)] S3b: sorted regular samples Y (global ids) */
+  int32_t* exact_fallbacks_h;/* host int: ambiguous key comparisons resolved exactly */
+} sa_partition_debug;
+
+/* Algorithm 2 steps 1-11, the rank-based sample sort:
+ *  - p logical blocks; block q = global ids [floor(qN/p), floor((q+1)N/p))
+ *    (reading Z13).  The calling rank (of nranks) holds blocks
+ *    [rank*p/nranks, (rank+1)*p/nranks) as a contiguous shard starting at
+ *    global id first_global with n_local sequences: profiles/nkmers/offsets
+ *    describe that shard (offsets: its residue CSR, used for byte counts).
+ *  - S2a local rank vs own block, S2b sort + k_b samples
+ *    at floor((j+1)w/(k_b+1)), S2c the s = p*k_b sample
+ *    profiles replicated on every rank (profiles instead of residues,
+ *    DESIGN.md §5), S2d rank vs S, S3a sort + p-1 regular samples at
+ *    floor((j+1)w/p), S3b sort Y, pivots Y_{floor(p/2)+jp}
+ *    (reading Z9; every rank derives the same pivots, O2),
+ *    S3c bucket(i) = min{b : (R_i, i) <= pivot_b}, else p-1.
+ *  - every order is by the exact rational rank, ties by global index (O4):
+ *    keys decide when certified; otherwise the pair is resolved exactly on
+ *    the host with big-integer arithmetic (rare).
+ * Outputs: bucket_of[n_local] (device), pivots[p-1] (device),
+ *   counts_h[nranks*p]: counts_h[r*p+b] = sequences of rank r in bucket b,
+ *   bytes_h[nranks*p]: their residue bytes -- the receive sizes for
+ *   sa_redistribute (host; filled on every rank).
+ * Host-blocking: once, at the count exchange (C3); more in the exact path.
+ * SA_E_INVAL: p < 1, n_total < p, nranks does not divide p, the shard does not
+ * match blocks [rank*p/nranks, (rank+1)*p/nranks), samples_per_block < 1 or
+ * larger than a block, NULL required pointers. */
+sa_status sa_partition(sa_ctx* ctx, int32_t p, int32_t samples_per_block,
+                       const uint16_t* profiles, const int32_t* nkmers, const int64_t* offsets, int32_t bins,
+                       int64_t n_total, int64_t first_global, int32_t n_local,
+                       int32_t* bucket_of, sa_pivot* pivots, int64_t* counts_h, int64_t* bytes_h,
+                       sa_partition_debug* dbg, void* stream);
+
+/* ------------------------------------------------- S4: redistribution ---- */
+/* All-to-all personalised redistribution: every
+ * sequence of the local shard goes to the rank owning its bucket (rank r owns
+ * buckets [r*p/nranks, (r+1)*p/nranks)).  Received sequences are ordered by
+ * (bucket, global id) (reading Z17).  Inputs: the shard's residue CSR, the
+ * sa_partition outputs bucket_of / counts_h / bytes_h.  Outputs (device,
+ * caller-sized from counts_h / bytes_h): recv_residues[sum bytes],
+ * recv_offsets[recv_n+1], recv_global_idx[recv_n], recv_bucket[recv_n]. */
+sa_status sa_redistribute(sa_ctx* ctx, int32_t p, const uint8_t* residues, const int64_t* offsets,
+                          int32_t n_local, int64_t first_global, const int32_t* bucket_of,
+                          const int64_t* counts_h, const int64_t* bytes_h,
+                          uint8_t* recv_residues, int64_t* recv_offsets, int64_t* recv_global_idx,
+                          int32_t* recv_bucket, void* stream);
+
+/* -------------------------------------------- S5: bucket similarity ----- */
+/* All-pairs k-mer similarity inside one bucket (the pairwise stage of
+ * distance-based MSA; Eq. 1): for members in the given
+ * order, numerators[i][j] = C_ij (uint16), similarity[i][j] = C_ij / D_ij in
+ * fp64 with one IEEE round-to-nearest division (reading Z19), 0 if D_ij = 0
+ * (so a member with nk = 0 has self-similarity 0, reading Z4).  Both outputs
+ * are full symmetric n x n row-major matrices; each is nullable. */
+sa_status sa_bucket_similarity(sa_ctx* ctx, const uint16_t* profiles, const int32_t* nkmers, int32_t n,
+                               int32_t bins, uint16_t* numerators, double* similarity, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SA_H_ */

@@ -1,0 +1,405 @@
+"""ctypes binding of libsa (include/sa.h) -- argument marshalling only.
+
+Every function here has the name of the C entry point it wraps and does no
+arithmetic of the method: it checks dtypes / devices / contiguity, allocates
+outputs as torch tensors (torch is used for device memory, streams and
+torch.distributed only) and calls the library.  There is no CPU fallback: if
+``libsa.so`` is missing or no CUDA device is usable the call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libsa.so")
+
+SA_OK, SA_E_INVAL, SA_E_RANGE, SA_E_CUDA, SA_E_COMM, SA_E_NOMEM, SA_E_STATE = range(7)
+STATUS_NAMES = {0: "SA_OK", 1: "SA_E_INVAL", 2: "SA_E_RANGE", 3: "SA_E_CUDA", 4: "SA_E_COMM",
+                5: "SA_E_NOMEM", 6: "SA_E_STATE"}
+PHASES = ["S2a", "S2b", "S2c", "S2d", "S3", "S5", "rank"]
+
+EXPORTED = ["sa_ctx_create", "sa_ctx_attach_comm", "sa_ctx_destroy", "sa_last_error", "sa_launch_count",
+            "sa_ctx_set_timing", "sa_ctx_phase_ms", "sa_profile_stride", "sa_kmer_profiles", "sa_kmer_rank",
+            "sa_partition", "sa_redistribute", "sa_bucket_similarity", "sa_exact_rank_compare"]
+
+
+class SaError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class sa_key128(ctypes.Structure):
+    _fields_ = [("lo", ctypes.c_uint64), ("hi", ctypes.c_uint64)]
+
+
+class sa_pivot(ctypes.Structure):
+    _fields_ = [("key", sa_key128), ("global_idx", ctypes.c_int64), ("nk", ctypes.c_int32), ("block", ctypes.c_int32)]
+
+
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                ctypes.c_void_p)
+ALLTOALLV_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64),
+                                ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64),
+                                ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p)
+
+
+class sa_comm_ops(ctypes.Structure):
+    _fields_ = [("user", ctypes.c_void_p), ("allgather", ALLGATHER_FN), ("alltoallv", ALLTOALLV_FN)]
+
+
+class sa_partition_debug(ctypes.Structure):
+    _fields_ = [("local_key", ctypes.c_void_p), ("local_f64", ctypes.c_void_p), ("local_order", ctypes.c_void_p),
+                ("sample_idx", ctypes.c_void_p), ("global_key", ctypes.c_void_p), ("global_f64", ctypes.c_void_p),
+                ("global_order", ctypes.c_void_p), ("candidates", ctypes.c_void_p),
+                ("exact_fallbacks_h", ctypes.POINTER(ctypes.c_int32))]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libsa.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libsa.so not found at {path}; run `python -m paper_0905_1744_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    P, I32, I64, VP = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p
+    sig = {
+        "sa_ctx_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+        "sa_ctx_attach_comm": (ctypes.c_int, [P, ctypes.POINTER(sa_comm_ops), ctypes.c_int, ctypes.c_int]),
+        "sa_ctx_destroy": (ctypes.c_int, [P]),
+        "sa_last_error": (ctypes.c_char_p, []),
+        "sa_launch_count": (I64, []),
+        "sa_ctx_set_timing": (ctypes.c_int, [P, ctypes.c_int]),
+        "sa_ctx_phase_ms": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_float)]),
+        "sa_profile_stride": (I32, [I32]),
+        "sa_kmer_profiles": (ctypes.c_int, [P, P, P, I32, I32, I32, P, P, VP]),
+        "sa_kmer_rank": (ctypes.c_int, [P, P, P, I32, P, P, I32, I32, P, P, P, VP]),
+        "sa_partition": (ctypes.c_int, [P, I32, I32, P, P, P, I32, I64, I64, I32, P, P,
+                                        ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+                                        ctypes.POINTER(sa_partition_debug), VP]),
+        "sa_redistribute": (ctypes.c_int, [P, I32, P, P, I32, I64, P, ctypes.POINTER(ctypes.c_int64),
+                                           ctypes.POINTER(ctypes.c_int64), P, P, P, P, VP]),
+        "sa_bucket_similarity": (ctypes.c_int, [P, P, P, I32, I32, P, P, VP]),
+        "sa_exact_rank_compare": (ctypes.c_int, [P, I32, P, I32, P, I32]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(status: int):
+    if status != SA_OK:
+        raise SaError(status, load_library().sa_last_error().decode(errors="replace"))
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _dev(t, dtype, name):
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
+    if not t.is_cuda:
+        raise ValueError(f"{name}: must be a CUDA tensor (libsa has no CPU path)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous")
+    return t
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def sa_profile_stride(bins: int) -> int:
+    return int(load_library().sa_profile_stride(bins))
+
+
+def sa_exact_rank_compare(Ca, nka: int, Cb, nkb: int, nk_pool) -> int:
+    """Host-side exact sign of V_a - V_b (sa.h); numpy inputs."""
+    Ca = np.ascontiguousarray(Ca, dtype=np.uint16)
+    Cb = np.ascontiguousarray(Cb, dtype=np.uint16)
+    nkp = np.ascontiguousarray(nk_pool, dtype=np.int32)
+    return int(load_library().sa_exact_rank_compare(Ca.ctypes.data, nka, Cb.ctypes.data, nkb, nkp.ctypes.data,
+                                                    nkp.shape[0]))
+
+
+def sa_launch_count() -> int:
+    return int(load_library().sa_launch_count())
+
+
+# ---------------------------------------------------------------- context --
+class Context:
+    """An ``sa_ctx`` bound to one CUDA device (one per process and GPU)."""
+
+    def __init__(self, device: int | None = None):
+        lib = load_library()
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = device
+        h = ctypes.c_void_p()
+        _check(lib.sa_ctx_create(device, ctypes.byref(h)))
+        self.handle = h
+        self.nranks, self.rank = 1, 0
+        self._comm_keepalive = None
+
+    def close(self):
+        if self.handle:
+            load_library().sa_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def attach_comm(self, comm: "TorchComm"):
+        ops = comm.ops()
+        self._comm_keepalive = (comm, ops)
+        _check(load_library().sa_ctx_attach_comm(self.handle, ctypes.byref(ops), comm.nranks, comm.rank))
+        self.nranks, self.rank = comm.nranks, comm.rank
+
+    def set_timing(self, enable: bool = True):
+        _check(load_library().sa_ctx_set_timing(self.handle, int(enable)))
+
+    def phase_ms(self) -> dict:
+        arr = (ctypes.c_float * len(PHASES))()
+        _check(load_library().sa_ctx_phase_ms(self.handle, arr))
+        return {k: float(arr[i]) for i, k in enumerate(PHASES)}
+
+
+# ------------------------------------------------------------- S1 .. S5 ----
+def sa_kmer_profiles(ctx: Context, residues: torch.Tensor, offsets: torch.Tensor, k: int = 3, alphabet: int = 20,
+                     profiles: torch.Tensor | None = None, nkmers: torch.Tensor | None = None, stream=None):
+    """S1: returns (profiles uint16 [n][stride], nkmers int32 [n]) (sa.h)."""
+    _dev(residues, torch.uint8, "residues")
+    _dev(offsets, torch.int64, "offsets")
+    n = offsets.numel() - 1
+    bins = alphabet ** k
+    stride = sa_profile_stride(bins) if bins <= 65536 else bins
+    dev = offsets.device
+    if profiles is None:
+        profiles = torch.empty((max(n, 0), stride), dtype=torch.uint16, device=dev)
+    if nkmers is None:
+        nkmers = torch.empty(max(n, 0), dtype=torch.int32, device=dev)
+    _check(load_library().sa_kmer_profiles(ctx.handle, _ptr(residues), _ptr(offsets), n, k, alphabet,
+                                           _ptr(profiles), _ptr(nkmers), _stream(stream)))
+    return profiles, nkmers
+
+
+def sa_kmer_rank(ctx: Context, q_prof, q_nk, pool_prof, pool_nk, bins: int = 8000, want_f64: bool = True,
+                 want_numerators: bool = False, stream=None):
+    """S2: returns (keys int64 [nq][2] as (lo, hi) bit patterns, rank_f64 | None, numerators | None)."""
+    for t, name in ((q_prof, "q_prof"), (pool_prof, "pool_prof")):
+        _dev(t, torch.uint16, name)
+    _dev(q_nk, torch.int32, "q_nk")
+    _dev(pool_nk, torch.int32, "pool_nk")
+    nq, npool = q_nk.numel(), pool_nk.numel()
+    dev = q_nk.device
+    keys = torch.empty((nq, 2), dtype=torch.int64, device=dev)
+    f64 = torch.empty(nq, dtype=torch.float64, device=dev) if want_f64 else None
+    num = torch.empty((nq, npool), dtype=torch.uint16, device=dev) if want_numerators else None
+    _check(load_library().sa_kmer_rank(ctx.handle, _ptr(q_prof), _ptr(q_nk), nq, _ptr(pool_prof), _ptr(pool_nk),
+                                       npool, bins, _ptr(keys), _ptr(f64), _ptr(num), _stream(stream)))
+    return keys, f64, num
+
+
+@dataclass
+class PartitionOut:
+    bucket_of: torch.Tensor        # int32 [n_local]
+    pivots: torch.Tensor           # int64 [p-1][4] raw sa_pivot records
+    counts: np.ndarray             # int64 [nranks][p]
+    bytes: np.ndarray              # int64 [nranks][p]
+    debug: dict | None = None
+    exact_fallbacks: int = 0
+
+
+def pivot_global_idx(pivots: torch.Tensor) -> torch.Tensor:
+    return pivots[:, 2]
+
+
+def sa_partition(ctx: Context, p: int, samples_per_block: int, profiles, nkmers, offsets, bins: int,
+                 n_total: int, first_global: int, debug: bool = False, stream=None) -> PartitionOut:
+    """S2a-S3c (Algorithm 2 steps 2-11) on this rank's shard; see sa.h."""
+    _dev(profiles, torch.uint16, "profiles")
+    _dev(nkmers, torch.int32, "nkmers")
+    _dev(offsets, torch.int64, "offsets")
+    n_local = nkmers.numel()
+    dev = nkmers.device
+    bucket_of = torch.empty(n_local, dtype=torch.int32, device=dev)
+    pivots = torch.zeros((max(p - 1, 1), 4), dtype=torch.int64, device=dev)   # 32-byte sa_pivot records
+    counts = np.zeros((ctx.nranks, p), dtype=np.int64)
+    nbytes = np.zeros((ctx.nranks, p), dtype=np.int64)
+    dbg_struct = None
+    dbg = None
+    fallbacks = ctypes.c_int32(0)
+    if debug:
+        s = p * samples_per_block
+        dbg = {
+            "local_key": torch.empty((n_local, 2), dtype=torch.int64, device=dev),
+            "local_f64": torch.empty(n_local, dtype=torch.float64, device=dev),
+            "local_order": torch.empty(n_local, dtype=torch.int64, device=dev),
+            "sample_idx": torch.empty(s, dtype=torch.int64, device=dev),
+            "global_key": torch.empty((n_local, 2), dtype=torch.int64, device=dev),
+            "global_f64": torch.empty(n_local, dtype=torch.float64, device=dev),
+            "global_order": torch.empty(n_local, dtype=torch.int64, device=dev),
+            "candidates": torch.empty(max(p * (p - 1), 1), dtype=torch.int64, device=dev),
+        }
+        dbg_struct = sa_partition_debug(*[_ptr(dbg[k]) for k in ["local_key", "local_f64", "local_order",
+                                                                  "sample_idx", "global_key", "global_f64",
+                                                                  "global_order", "candidates"]],
+                                        ctypes.pointer(fallbacks))
+    _check(load_library().sa_partition(
+        ctx.handle, p, samples_per_block, _ptr(profiles), _ptr(nkmers), _ptr(offsets), bins, n_total, first_global,
+        n_local, _ptr(bucket_of), _ptr(pivots),
+        counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), nbytes.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+        ctypes.byref(dbg_struct) if dbg_struct is not None else None, _stream(stream)))
+    return PartitionOut(bucket_of, pivots[:max(p - 1, 0)], counts, nbytes, dbg, int(fallbacks.value))
+
+
+def owned_buckets(p: int, nranks: int, rank: int) -> range:
+    """Buckets [rank*p/nranks, (rank+1)*p/nranks) live on `rank` (sa.h)."""
+    pb = p // nranks
+    return range(rank * pb, (rank + 1) * pb)
+
+
+def recv_sizes(counts: np.ndarray, nbytes: np.ndarray, p: int, nranks: int, rank: int):
+    """Receive-buffer sizes for sa_redistribute: (sequences, residue bytes)."""
+    own = list(owned_buckets(p, nranks, rank))
+    return int(counts[:, own].sum()), int(nbytes[:, own].sum())
+
+
+def sa_redistribute(ctx: Context, p: int, residues, offsets, first_global: int, part: PartitionOut, stream=None):
+    """S4: returns (recv_residues, recv_offsets, recv_global_idx, recv_bucket) ordered by (bucket, global id)."""
+    _dev(residues, torch.uint8, "residues")
+    _dev(offsets, torch.int64, "offsets")
+    n_local = offsets.numel() - 1
+    dev = offsets.device
+    nseq, nres = recv_sizes(part.counts, part.bytes, p, ctx.nranks, ctx.rank)
+    rres = torch.empty(max(nres, 1), dtype=torch.uint8, device=dev)
+    roffs = torch.empty(nseq + 1, dtype=torch.int64, device=dev)
+    rgid = torch.empty(max(nseq, 1), dtype=torch.int64, device=dev)
+    rbkt = torch.empty(max(nseq, 1), dtype=torch.int32, device=dev)
+    counts = np.ascontiguousarray(part.counts, dtype=np.int64)
+    nbytes = np.ascontiguousarray(part.bytes, dtype=np.int64)
+    _check(load_library().sa_redistribute(
+        ctx.handle, p, _ptr(residues), _ptr(offsets), n_local, first_global, _ptr(part.bucket_of),
+        counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), nbytes.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+        _ptr(rres), _ptr(roffs), _ptr(rgid), _ptr(rbkt), _stream(stream)))
+    return rres[:nres], roffs, rgid[:nseq], rbkt[:nseq]
+
+
+def sa_bucket_similarity(ctx: Context, profiles, nkmers, bins: int = 8000, want_numerators: bool = True,
+                         want_similarity: bool = True, numerators=None, similarity=None, stream=None):
+    """S5: returns (numerators uint16 [n][n] | None, similarity f64 [n][n] | None)."""
+    _dev(profiles, torch.uint16, "profiles")
+    _dev(nkmers, torch.int32, "nkmers")
+    n = nkmers.numel()
+    dev = nkmers.device
+    if want_numerators and numerators is None:
+        numerators = torch.empty((n, n), dtype=torch.uint16, device=dev)
+    if want_similarity and similarity is None:
+        similarity = torch.empty((n, n), dtype=torch.float64, device=dev)
+    _check(load_library().sa_bucket_similarity(ctx.handle, _ptr(profiles), _ptr(nkmers), n, bins,
+                                               _ptr(numerators), _ptr(similarity), _stream(stream)))
+    return numerators, similarity
+
+
+# ------------------------------------------------------- communicator -----
+class _ArrayView:
+    """Expose a raw device pointer to torch through __cuda_array_interface__."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None, "stream": None}
+
+
+def raw_tensor(ptr: int, nbytes: int, device) -> torch.Tensor:
+    """uint8 tensor aliasing `nbytes` at `ptr` (device memory, or host memory for CPU tests)."""
+    if nbytes == 0:
+        return torch.empty(0, dtype=torch.uint8, device=device)
+    if torch.device(device).type == "cuda":
+        return torch.as_tensor(_ArrayView(ptr, nbytes), device=device)
+    buf = (ctypes.c_uint8 * nbytes).from_address(ptr)
+    return torch.from_numpy(np.ctypeslib.as_array(buf))
+
+
+class TorchComm:
+    """sa_comm_ops implemented with torch.distributed (NCCL on GPUs; gloo with
+    host buffers in the CPU tests).  Plumbing only: allgather and a variable
+    all-to-all of bytes, ordered on the caller's stream."""
+
+    def __init__(self, group=None, device="cuda"):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.nranks = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.device = torch.device(device)
+        self.errors = []
+
+    def _with_stream(self, stream_ptr):
+        if self.device.type == "cuda" and stream_ptr:
+            return torch.cuda.stream(torch.cuda.ExternalStream(stream_ptr, device=self.device))
+        import contextlib
+        return contextlib.nullcontext()
+
+    def allgather(self, user, send, recv, nbytes, stream):
+        try:
+            with self._with_stream(stream):
+                src = raw_tensor(send, nbytes, self.device)
+                dst = raw_tensor(recv, nbytes * self.nranks, self.device)
+                if send == recv:
+                    src = src.clone()
+                self.dist.all_gather_into_tensor(dst, src, group=self.group)
+            return 0
+        except Exception as e:  # errors cannot cross the C ABI as exceptions
+            self.errors.append(repr(e))
+            return 1
+
+    def alltoallv(self, user, send, sbytes, sdispl, recv, rbytes, rdispl, stream):
+        try:
+            n = self.nranks
+            sb = [int(sbytes[i]) for i in range(n)]
+            rb = [int(rbytes[i]) for i in range(n)]
+            sd = [int(sdispl[i]) for i in range(n)]
+            rd = [int(rdispl[i]) for i in range(n)]
+            assert sd == list(np.cumsum([0] + sb[:-1])) and rd == list(np.cumsum([0] + rb[:-1])), \
+                "displacements must be packed prefix sums"
+            with self._with_stream(stream):
+                src = raw_tensor(send, sum(sb), self.device)
+                dst = raw_tensor(recv, sum(rb), self.device)
+                self.dist.all_to_all_single(dst, src, output_split_sizes=rb, input_split_sizes=sb, group=self.group)
+            return 0
+        except Exception as e:
+            self.errors.append(repr(e))
+            return 1
+
+    def ops(self) -> sa_comm_ops:
+        self._ag = ALLGATHER_FN(self.allgather)
+        self._a2a = ALLTOALLV_FN(self.alltoallv)
+        return sa_comm_ops(None, self._ag, self._a2a)
+
+
+def keys_to_ints(keys: torch.Tensor) -> list:
+    """int64 [n][2] (lo, hi) bit patterns -> Python ints (128-bit keys)."""
+    k = keys.detach().cpu().numpy().view(np.uint64)
+    return [int(lo) | (int(hi) << 64) for lo, hi in k]

@@ -1,0 +1,117 @@
+// libsa internal declarations shared by the .cu translation units.
+// Product code only: nothing here is shared with oracle/ (DESIGN.md §1).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/sa.h"
+
+namespace sa {
+
+// ------------------------------------------------------------- errors ----
+void set_error(const char* fmt, ...);
+sa_status fail(sa_status s, const char* fmt, ...);
+void count_launch(int n = 1);
+
+#define SA_CUDA(call)                                                                \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      return ::sa::fail(SA_E_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,        \
+                        cudaGetErrorString(e_));                                     \
+  } while (0)
+
+#define SA_TRY(expr)                 \
+  do {                               \
+    sa_status s_ = (expr);           \
+    if (s_ != SA_OK) return s_;      \
+  } while (0)
+
+#define SA_LAUNCHED()                                                                \
+  do {                                                                               \
+    ::sa::count_launch();                                                            \
+    cudaError_t e_ = cudaGetLastError();                                             \
+    if (e_ != cudaSuccess)                                                           \
+      return ::sa::fail(SA_E_CUDA, "%s:%d launch: %s", __FILE__, __LINE__,           \
+                        cudaGetErrorString(e_));                                     \
+  } while (0)
+
+// Error flags written by kernels (device-detected range errors).
+enum : uint32_t { ERR_RESIDUE = 1u, ERR_NK = 2u };
+
+// --------------------------------------------------- min-sum engine (K2) --
+// Tile geometry: 128 x 128 pairs per CTA, 256 threads, 8 x 8 pairs per thread,
+// 32 packed words (64 bins) per pipeline stage.
+constexpr int MS_BM = 128;
+constexpr int MS_THREADS = 256;
+constexpr int MS_BKW = 32;
+constexpr int MS_LDW = MS_BKW + 4;   // padded smem row (words): conflict-free LDS.128
+constexpr int MS_STAGES = 4;
+constexpr int MS_SMEM = MS_STAGES * 2 * MS_BM * MS_LDW * 4;
+
+struct MsProblem {
+  const uint32_t* A;       // packed u16x2 rows, stride ldw words
+  const uint32_t* B;
+  const int32_t* nkA;
+  const int32_t* nkB;
+  int32_t na, nb;
+  int32_t sym;             // A == B: upper-triangle tiles only, mirrored outputs
+  int32_t tiles_b;         // ceil(nb / 128)
+  int64_t tile_begin;      // first global tile id of this problem
+  sa_key128* keyA;         // row sums (nullable)
+  sa_key128* keyB;         // column sums for sym off-diagonal tiles (nullable)
+  uint16_t* num;           // [na][ld] numerators (nullable)
+  double* sim;             // [na][ld] C/D (nullable)
+  int64_t ld;
+};
+
+// Launch the engine over `probs` (host array, copied to device scratch).
+// mode: 0 keys only, 1 keys + optional matrices.
+sa_status minsum_launch(const std::vector<MsProblem>& probs, int ldw, cudaStream_t st,
+                        cudaEvent_t ev0, cudaEvent_t ev1);
+sa_status ensure_recip_tables(cudaStream_t st);
+
+// ------------------------------------------------------ profiles (K1) --
+sa_status profiles_launch(const uint8_t* residues, const int64_t* offsets, int32_t n, int32_t k,
+                          int32_t alphabet, int32_t stride, uint16_t* out, int32_t* nk,
+                          uint32_t* err_flag, cudaStream_t st);
+
+// ---------------------------------------------------- ordering (K4-K6) --
+// Sort each segment [seg[s], seg[s+1]) of `keys` by (key, gid) ascending
+// where gid = gid0 + local index.  order_out[seg[s] + pos] = local index.
+// amb[i] = 1 if item i has another item of its segment within `window` of
+// its key (the key order is then not certified); *amb_count += flagged.
+sa_status segment_sort_launch(const sa_key128* keys, int64_t gid0, const int64_t* seg_h, int nseg,
+                              int64_t window, int32_t* order_out, uint8_t* amb, uint32_t* amb_count,
+                              cudaStream_t st);
+// Sort records (pivot candidates) by (key, global_idx): same contract.
+sa_status record_sort_launch(const sa_pivot* rec, int n, int64_t window, int32_t* order_out,
+                             uint8_t* amb, uint32_t* amb_count, cudaStream_t st);
+
+double u128_to_double_host(uint64_t hi, uint64_t lo);
+
+// keys -> fp64 ranks: RN(key) * 2^-64 / npool.
+sa_status keys_to_f64_launch(const sa_key128* keys, int64_t n, int64_t npool, double* out,
+                             cudaStream_t st);
+
+// ---------------------------------------------------- exact fallback ----
+// Exact comparison of V_a = sum_j Ca_j / Da_j and V_b (rows over the same
+// pool, D = min(nk_query, nk_j)).  Returns -1, 0, +1.
+int exact_compare(const uint16_t* Ca, int32_t nka, const uint16_t* Cb, int32_t nkb,
+                  const int32_t* nk_pool, int npool);
+
+}  // namespace sa
+
+struct sa_ctx {
+  int device = 0;
+  int nranks = 1;
+  int rank = 0;
+  sa_comm_ops comm{};
+  bool has_comm = false;
+  bool timing = false;
+  cudaEvent_t ev[2 * SA_PHASE_COUNT] = {};
+  bool ev_used[SA_PHASE_COUNT] = {};
+};

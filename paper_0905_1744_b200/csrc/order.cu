@@ -1,0 +1,478 @@
+// K4-K6 -- ordering, sampling, pivot agreement, bucket assignment and the
+// stable bucket scatter of the redistribution (§3.1.1-3.1.2,
+// P:343-423; Algorithm 2 steps 3-11).
+//
+// Orders are by (exact rank, global index) (O4 / reading Z12).  On the device
+// the rank is its 128-bit key; a comparison is certified when the keys differ
+// by at least the pool size.  Every kernel that orders also
+// flags the items whose order the keys do not certify, so the host can resolve
+// them exactly (sa_partition's exact path).
+#include "common.cuh"
+
+namespace sa {
+
+struct SegSpec {   // segment s = [ (q0+s)*N/P - base, (q0+s+1)*N/P - base )
+  int64_t N, P, q0, base;
+  __host__ __device__ int64_t begin(int64_t s) const { return (q0 + s) * N / P - base; }
+};
+
+__device__ __forceinline__ bool key_lt(const sa_key128& a, int64_t ga, const sa_key128& b, int64_t gb) {
+  if (a.hi != b.hi) return a.hi < b.hi;
+  if (a.lo != b.lo) return a.lo < b.lo;
+  return ga < gb;
+}
+// |a - b| < window (128-bit)
+__device__ __forceinline__ bool key_near(const sa_key128& a, const sa_key128& b, int64_t window) {
+  uint64_t dlo, dhi;
+  const bool a_ge = (a.hi > b.hi) || (a.hi == b.hi && a.lo >= b.lo);
+  if (a_ge) { dlo = a.lo - b.lo; dhi = a.hi - b.hi - (a.lo < b.lo ? 1 : 0); }
+  else      { dlo = b.lo - a.lo; dhi = b.hi - a.hi - (b.lo < a.lo ? 1 : 0); }
+  return dhi == 0 && dlo < (uint64_t)window;
+}
+
+// Counting sort: position of item i inside its segment = #{j : (k_j, g_j) < (k_i, g_i)}.
+// gids == nullptr means g = gid0 + index.
+constexpr int SORT_TILE = 1024;
+__global__ void __launch_bounds__(256)
+segsort_kernel(const sa_key128* __restrict__ keys, const int64_t* __restrict__ gids, int64_t gid0, SegSpec sp,
+               int64_t window, int32_t* __restrict__ order_out, uint8_t* __restrict__ amb,
+               uint32_t* __restrict__ amb_count) {
+  __shared__ sa_key128 sk[SORT_TILE];
+  __shared__ int64_t sg[SORT_TILE];
+  const int64_t s = blockIdx.y;
+  const int64_t b = sp.begin(s), e = sp.begin(s + 1);
+  const int64_t i = b + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b + (int64_t)blockIdx.x * blockDim.x >= e) return;   // CTA-uniform
+  const bool live = i < e;
+  sa_key128 ki = live ? keys[i] : sa_key128{0, 0};
+  const int64_t gi = live ? (gids ? gids[i] : gid0 + i) : 0;
+  int64_t pos = 0;
+  bool near = false;
+  for (int64_t j0 = b; j0 < e; j0 += SORT_TILE) {
+    const int cnt = (int)min((int64_t)SORT_TILE, e - j0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+      sk[t] = keys[j0 + t];
+      sg[t] = gids ? gids[j0 + t] : gid0 + j0 + t;
+    }
+    __syncthreads();
+    if (live) {
+      for (int t = 0; t < cnt; ++t) {
+        const sa_key128 kj = sk[t];
+        const int64_t gj = sg[t];
+        pos += key_lt(kj, gj, ki, gi) ? 1 : 0;
+        near |= (gj != gi) && key_near(kj, ki, window);
+      }
+    }
+  }
+  if (live) {
+    order_out[b + pos] = (int32_t)(i - b);
+    if (amb) amb[i] = near ? 1 : 0;
+    if (near) atomicAdd(amb_count, 1u);
+  }
+}
+
+sa_status segsort_launch_impl(const sa_key128* keys, const int64_t* gids, int64_t gid0, SegSpec sp, int nseg,
+                              int64_t max_seg, int64_t window, int32_t* order_out, uint8_t* amb,
+                              uint32_t* amb_count, cudaStream_t st) {
+  if (nseg <= 0 || max_seg <= 0) return SA_OK;
+  dim3 grid((unsigned)((max_seg + 255) / 256), (unsigned)nseg);
+  segsort_kernel<<<grid, 256, 0, st>>>(keys, gids, gid0, sp, window, order_out, amb, amb_count);
+  SA_LAUNCHED();
+  return SA_OK;
+}
+
+// ------------------------------------------------------- sample picking --
+// out[s*count + j] = gid of the item at sorted position floor((j+1) w_s / den)
+// of segment s (den = count + 1 for the global sample, S:345 / P:348-352;
+// den = p for regular samples).
+__global__ void pick_kernel(const int32_t* __restrict__ order, SegSpec sp, int nseg, int count, int den,
+                            int64_t gid0, int64_t* __restrict__ out_gid, int32_t* __restrict__ out_local) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nseg * count) return;
+  const int s = t / count, j = t % count;
+  const int64_t b = sp.begin(s), w = sp.begin(s + 1) - b;
+  const int64_t pos = ((int64_t)(j + 1) * w) / den;
+  const int64_t local = b + order[b + pos];
+  out_gid[t] = gid0 + local;
+  if (out_local) out_local[t] = (int32_t)local;
+}
+
+// gather profile rows (stride elements) + nk of the selected local items
+__global__ void gather_rows_kernel(const uint16_t* __restrict__ prof, const int32_t* __restrict__ nk,
+                                   const int32_t* __restrict__ sel, int nsel, int stride,
+                                   uint16_t* __restrict__ out, int32_t* __restrict__ out_nk) {
+  for (int r = blockIdx.x; r < nsel; r += gridDim.x) {
+    const int64_t src = sel[r];
+    const uint4* a = reinterpret_cast<const uint4*>(prof + src * stride);
+    uint4* o = reinterpret_cast<uint4*>(out + (int64_t)r * stride);
+    for (int v = threadIdx.x; v < stride / 8; v += blockDim.x) o[v] = a[v];
+    if (threadIdx.x == 0) out_nk[r] = nk[src];
+  }
+}
+
+// regular-sample records (S3a): key, gid, nk, block
+__global__ void make_records_kernel(const int32_t* __restrict__ local, const int64_t* __restrict__ gid,
+                                    int n, const sa_key128* __restrict__ keys, const int32_t* __restrict__ nk,
+                                    int count, int q0, sa_pivot* __restrict__ rec) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  sa_pivot r;
+  r.key = keys[local[t]];
+  r.global_idx = gid[t];
+  r.nk = nk[local[t]];
+  r.block = q0 + t / count;
+  rec[t] = r;
+}
+
+__global__ void split_records_kernel(const sa_pivot* __restrict__ rec, int n, sa_key128* __restrict__ keys,
+                                     int64_t* __restrict__ gids) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  keys[t] = rec[t].key;
+  gids[t] = rec[t].global_idx;
+}
+
+// sorted Y and pivots = Y_{floor(p/2) + j p} (1-based), j = 0..p-2 (Z9)
+__global__ void pivots_kernel(const sa_pivot* __restrict__ rec, const int32_t* __restrict__ order, int n, int p,
+                              int64_t* __restrict__ y_sorted_gid, sa_pivot* __restrict__ pivots) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n && y_sorted_gid) y_sorted_gid[t] = rec[order[t]].global_idx;
+  if (t < p - 1) pivots[t] = rec[order[p / 2 + t * p - 1]];
+}
+
+// ------------------------------------------------------ bucket assignment --
+// bucket(i) = #{pivots strictly below (k_i, g_i)} = smallest b with
+// (k_i, g_i) <= pivot_b.  Flags items whose comparison
+// with some pivot is not certified by the keys.  Per-bucket counts and residue
+// bytes are accumulated for the count exchange (C3).
+__global__ void __launch_bounds__(256)
+assign_kernel(const sa_key128* __restrict__ keys, int64_t gid0, int n, const sa_pivot* __restrict__ pivots, int p,
+              int64_t window, const int64_t* __restrict__ offs, int32_t* __restrict__ bucket_of,
+              uint8_t* __restrict__ amb, uint32_t* __restrict__ amb_count, unsigned long long* __restrict__ counts,
+              unsigned long long* __restrict__ bytes) {
+  extern __shared__ unsigned long long sh[];   // [2p]
+  for (int b = threadIdx.x; b < 2 * p; b += blockDim.x) sh[b] = 0;
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const sa_key128 k = keys[i];
+    const int64_t g = gid0 + i;
+    int bkt = 0;
+    bool near = false;
+    for (int b = 0; b < p - 1; ++b) {
+      const sa_pivot pv = pivots[b];
+      bkt += key_lt(pv.key, pv.global_idx, k, g) ? 1 : 0;
+      near |= (pv.global_idx != g) && key_near(pv.key, k, window);
+    }
+    bucket_of[i] = bkt;
+    if (amb) amb[i] = near ? 1 : 0;
+    if (near) atomicAdd(amb_count, 1u);
+    atomicAdd(&sh[bkt], 1ull);
+    atomicAdd(&sh[p + bkt], (unsigned long long)(offs[i + 1] - offs[i]));
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < p; b += blockDim.x) {
+    if (sh[b]) atomicAdd(&counts[b], sh[b]);
+    if (sh[p + b]) atomicAdd(&bytes[b], sh[p + b]);
+  }
+}
+
+// --------------------------------------------------------- stable scatter --
+// Chunked stable counting sort by bucket: chunk c holds items [256c, 256c+256).
+__global__ void __launch_bounds__(256)
+bucket_hist_kernel(const int32_t* __restrict__ bucket_of, int n, int p, int32_t* __restrict__ hist /*[nchunk][p]*/) {
+  extern __shared__ int32_t hs[];
+  for (int b = threadIdx.x; b < p; b += blockDim.x) hs[b] = 0;
+  __syncthreads();
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i < n) atomicAdd(&hs[bucket_of[i]], 1);
+  __syncthreads();
+  for (int b = threadIdx.x; b < p; b += blockDim.x) hist[(int64_t)blockIdx.x * p + b] = hs[b];
+}
+
+// exclusive offsets, bucket-major then chunk: base[c][b]
+__global__ void bucket_scan_kernel(const int32_t* __restrict__ hist, int nchunk, int p, int64_t* __restrict__ base) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int64_t run = 0;
+  for (int b = 0; b < p; ++b)
+    for (int c = 0; c < nchunk; ++c) {
+      base[(int64_t)c * p + b] = run;
+      run += hist[(int64_t)c * p + b];
+    }
+}
+
+__global__ void __launch_bounds__(256)
+bucket_scatter_kernel(const int32_t* __restrict__ bucket_of, int n, int p, const int64_t* __restrict__ base,
+                      int32_t* __restrict__ perm /* perm[dst] = src */) {
+  extern __shared__ int32_t wc[];   // [8][p]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int t = threadIdx.x; t < 8 * p; t += blockDim.x) wc[t] = 0;
+  __syncthreads();
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  const int b = i < n ? bucket_of[i] : -1 - lane;   // distinct sentinels never match
+  const unsigned mask = __match_any_sync(0xffffffffu, b);
+  const int rank = __popc(mask & ((1u << lane) - 1u));
+  if (i < n && rank == 0) wc[warp * p + b] = __popc(mask);
+  __syncthreads();
+  if (i < n) {
+    int64_t pos = base[(int64_t)blockIdx.x * p + b] + rank;
+    for (int w = 0; w < warp; ++w) pos += wc[w * p + b];
+    perm[pos] = i;
+  }
+}
+
+// lens in permuted order -> lens_out[dst] = len(perm[dst])
+__global__ void perm_meta_kernel(const int32_t* __restrict__ perm, int n, const int64_t* __restrict__ offs,
+                                 const int32_t* __restrict__ bucket_of, int64_t gid0, int64_t* __restrict__ lens,
+                                 int64_t* __restrict__ gid_out, int32_t* __restrict__ bkt_out) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  const int s = perm[d];
+  lens[d] = offs[s + 1] - offs[s];
+  if (gid_out) gid_out[d] = gid0 + s;
+  if (bkt_out) bkt_out[d] = bucket_of[s];
+}
+
+// exclusive scan of int64 (3 phases)
+__global__ void scan_partial_kernel(const int64_t* __restrict__ in, int64_t n, int64_t* __restrict__ part) {
+  __shared__ int64_t sh[256];
+  const int64_t base = (int64_t)blockIdx.x * 1024;
+  int64_t s = 0;
+  for (int t = 0; t < 4; ++t) {
+    const int64_t i = base + threadIdx.x * 4 + t;
+    if (i < n) s += in[i];
+  }
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+__global__ void scan_top_kernel(int64_t* __restrict__ part, int64_t nparts) {
+  if (threadIdx.x != 0) return;
+  int64_t run = 0;
+  for (int64_t i = 0; i < nparts; ++i) { const int64_t v = part[i]; part[i] = run; run += v; }
+  part[nparts] = run;
+}
+__global__ void scan_final_kernel(const int64_t* __restrict__ in, int64_t n, const int64_t* __restrict__ part,
+                                  int64_t* __restrict__ out) {
+  __shared__ int64_t sh[256];
+  const int64_t base = (int64_t)blockIdx.x * 1024;
+  int64_t v[4], s = 0;
+  for (int t = 0; t < 4; ++t) {
+    const int64_t i = base + threadIdx.x * 4 + t;
+    v[t] = i < n ? in[i] : 0;
+    s += v[t];
+  }
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {     // Hillis-Steele inclusive
+    const int64_t x = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
+    __syncthreads();
+    sh[threadIdx.x] += x;
+    __syncthreads();
+  }
+  int64_t run = part[blockIdx.x] + sh[threadIdx.x] - s;
+  for (int t = 0; t < 4; ++t) {
+    const int64_t i = base + threadIdx.x * 4 + t;
+    if (i < n) out[i] = run;
+    run += v[t];
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = part[gridDim.x];
+}
+
+// copy residues of sequence perm[d] to dst + doff[d]  (one warp per sequence)
+__global__ void copy_seqs_kernel(const int32_t* __restrict__ perm, int n, const uint8_t* __restrict__ src,
+                                 const int64_t* __restrict__ soff, uint8_t* __restrict__ dst,
+                                 const int64_t* __restrict__ doff) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int d = warp; d < n; d += nw) {
+    const int s = perm ? perm[d] : d;
+    const int64_t a = soff[s], len = soff[s + 1] - a, o = doff[d];
+    for (int64_t u = lane; u < len; u += 32) dst[o + u] = src[a + u];
+  }
+}
+
+// segment reorder after the all-to-all: seg t copies cnt[t] meta records and
+// nbytes[t] residue bytes from (src_m, src_r) to (dst_m, dst_r)
+struct SegCopy {
+  int64_t src_m, dst_m, cnt, src_r, dst_r, nbytes;
+};
+__global__ void seg_copy_kernel(const SegCopy* __restrict__ segs, int nseg, const int64_t* __restrict__ meta_in,
+                                int64_t* __restrict__ meta_out, const uint8_t* __restrict__ res_in,
+                                uint8_t* __restrict__ res_out) {
+  for (int t = blockIdx.y; t < nseg; t += gridDim.y) {
+    const SegCopy sc = segs[t];
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < sc.cnt * 2; u += (int64_t)gridDim.x * blockDim.x)
+      meta_out[sc.dst_m * 2 + u] = meta_in[sc.src_m * 2 + u];
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < sc.nbytes; u += (int64_t)gridDim.x * blockDim.x)
+      res_out[sc.dst_r + u] = res_in[sc.src_r + u];
+  }
+}
+
+// meta record = {int64 gid, int32 len, int32 bucket}
+__global__ void pack_meta_kernel(const int32_t* __restrict__ perm, int n, const int64_t* __restrict__ offs,
+                                 const int32_t* __restrict__ bucket_of, int64_t gid0, int64_t* __restrict__ meta) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  const int s = perm[d];
+  meta[2 * d] = gid0 + s;
+  const uint64_t lb = (uint64_t)(uint32_t)(offs[s + 1] - offs[s]) | ((uint64_t)(uint32_t)bucket_of[s] << 32);
+  meta[2 * d + 1] = (int64_t)lb;
+}
+__global__ void unpack_meta_kernel(const int64_t* __restrict__ meta, int n, int64_t* __restrict__ gid,
+                                   int64_t* __restrict__ lens, int32_t* __restrict__ bkt) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  gid[d] = meta[2 * d];
+  const uint64_t lb = (uint64_t)meta[2 * d + 1];
+  lens[d] = (int64_t)(uint32_t)(lb & 0xffffffffu);
+  bkt[d] = (int32_t)(uint32_t)(lb >> 32);
+}
+
+// ------------------------------------------------------------- host glue --
+static inline unsigned cdiv(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
+
+sa_status segment_sort_keys(const sa_key128* keys, int64_t gid0, int64_t N, int64_t P, int64_t q0, int64_t base,
+                            int nseg, int64_t window, int32_t* order_out, uint8_t* amb, uint32_t* amb_count,
+                            cudaStream_t st) {
+  SegSpec sp{N, P, q0, base};
+  int64_t maxw = 0;
+  for (int s = 0; s < nseg; ++s) maxw = std::max(maxw, sp.begin(s + 1) - sp.begin(s));
+  return segsort_launch_impl(keys, nullptr, gid0, sp, nseg, maxw, window, order_out, amb, amb_count, st);
+}
+
+sa_status sort_records(const sa_pivot* rec, int n, int64_t window, sa_key128* tmp_keys, int64_t* tmp_gid,
+                       int32_t* order_out, uint8_t* amb, uint32_t* amb_count, cudaStream_t st) {
+  if (n <= 0) return SA_OK;
+  split_records_kernel<<<cdiv(n, 256), 256, 0, st>>>(rec, n, tmp_keys, tmp_gid);
+  SA_LAUNCHED();
+  SegSpec sp{n, 1, 0, 0};
+  return segsort_launch_impl(tmp_keys, tmp_gid, 0, sp, 1, n, window, order_out, amb, amb_count, st);
+}
+
+sa_status pick_launch(const int32_t* order, int64_t N, int64_t P, int64_t q0, int64_t base, int nseg, int count,
+                      int den, int64_t gid0, int64_t* out_gid, int32_t* out_local, cudaStream_t st) {
+  const int tot = nseg * count;
+  if (tot <= 0) return SA_OK;
+  SegSpec sp{N, P, q0, base};
+  pick_kernel<<<cdiv(tot, 128), 128, 0, st>>>(order, sp, nseg, count, den, gid0, out_gid, out_local);
+  SA_LAUNCHED();
+  return SA_OK;
+}
+
+sa_status gather_rows_launch(const uint16_t* prof, const int32_t* nk, const int32_t* sel, int nsel, int stride,
+                             uint16_t* out, int32_t* out_nk, cudaStream_t st) {
+  if (nsel <= 0) return SA_OK;
+  gather_rows_kernel<<<(unsigned)std::min(nsel, 4096), 256, 0, st>>>(prof, nk, sel, nsel, stride, out, out_nk);
+  SA_LAUNCHED();
+  return SA_OK;
+}
+
+sa_status make_records_launch(const int32_t* local, const int64_t* gid, int n, const sa_key128* keys,
+                              const int32_t* nk, int count, int q0, sa_pivot* rec, cudaStream_t st) {
+  if (n <= 0) return SA_OK;
+  make_records_kernel<<<cdiv(n, 128), 128, 0, st>>>(local, gid, n, keys, nk, count, q0, rec);
+  SA_LAUNCHED();
+  return SA_OK;
+}
+
+sa_status pivots_launch(const sa_pivot* rec, const int32_t* order, int n, int p, int64_t* y_sorted_gid,
+                        sa_pivot* pivots, cudaStream_t st) {
+  if (n <= 0) return SA_OK;
+  pivots_kernel<<<cdiv(n, 128), 128, 0, st>>>(rec, order, n, p, y_sorted_gid, pivots);
+  SA_LAUNCHED();
+  return SA_OK;
+}
+
+sa_status assign_launch(const sa_key128* keys, int64_t gid0, int n, const sa_pivot* pivots, int p, int64_t window,
+                        const int64_t* offs, int32_t* bucket_of, uint8_t* amb, uint32_t* amb_count,
+                        unsigned long long* counts, unsigned long long* bytes, cudaStream_t st) {
+  if (n <= 0) return SA_OK;
+  assign_kernel<<<cdiv(n, 256), 256, 2 * p * sizeof(unsigned long long), st>>>(
+      keys, gid0, n, pivots, p, window, offs, bucket_of, amb, amb_count, counts, bytes);
+  SA_LAUNCHED();
+  return SA_OK;
+}
+
+sa_status scan_launch(const int64_t* in, int64_t n, int64_t* out /*[n+1]*/, int64_t* part /*[cdiv(n,1024)+1]*/,
+                      cudaStream_t st) {
+  const int64_t np = (n + 1023) / 1024;
+  if (n <= 0) {
+    SA_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t), st));
+    return SA_OK;
+  }
+  scan_partial_kernel<<<(unsigned)np, 256, 0, st>>>(in, n, part);
+  SA_LAUNCHED();
+  scan_top_kernel<<<1, 32, 0, st>>>(part, np);
+  SA_LAUNCHED();
+  scan_final_kernel<<<(unsigned)np, 256, 0, st>>>(in, n, part, out);
+  SA_LAUNCHED();
+  return SA_OK;
+}
+
+sa_status bucket_perm_launch(const int32_t* bucket_of, int n, int p, int32_t* hist, int64_t* base, int32_t* perm,
+                             cudaStream_t st) {
+  if (n <= 0) return SA_OK;
+  const int nchunk = (int)cdiv(n, 256);
+  bucket_hist_kernel<<<nchunk, 256, p * sizeof(int32_t), st>>>(bucket_of, n, p, hist);
+  SA_LAUNCHED();
+  bucket_scan_kernel<<<1, 32, 0, st>>>(hist, nchunk, p, base);
+  SA_LAUNCHED();
+  bucket_scatter_kernel<<<nchunk, 256, 8 * p * sizeof(int32_t), st>>>(bucket_of, n, p, base, perm);
+  SA_LAUNCHED();
+  return SA_OK;
+}
+
+sa_status perm_meta_launch(const int32_t* perm, int n, const int64_t* offs, const int32_t* bucket_of, int64_t gid0,
+                           int64_t* lens, int64_t* gid_out, int32_t* bkt_out, cudaStream_t st) {
+  if (n <= 0) return SA_OK;
+  perm_meta_kernel<<<cdiv(n, 256), 256, 0, st>>>(perm, n, offs, bucket_of, gid0, lens, gid_out, bkt_out);
+  SA_LAUNCHED();
+  return SA_OK;
+}
+
+sa_status copy_seqs_launch(const int32_t* perm, int n, const uint8_t* src, const int64_t* soff, uint8_t* dst,
+                           const int64_t* doff, cudaStream_t st) {
+  if (n <= 0) return SA_OK;
+  copy_seqs_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 8), 148 * 16), 256, 0, st>>>(perm, n, src, soff, dst, doff);
+  SA_LAUNCHED();
+  return SA_OK;
+}
+
+sa_status pack_meta_launch(const int32_t* perm, int n, const int64_t* offs, const int32_t* bucket_of, int64_t gid0,
+                           int64_t* meta, cudaStream_t st) {
+  if (n <= 0) return SA_OK;
+  pack_meta_kernel<<<cdiv(n, 256), 256, 0, st>>>(perm, n, offs, bucket_of, gid0, meta);
+  SA_LAUNCHED();
+  return SA_OK;
+}
+
+sa_status unpack_meta_launch(const int64_t* meta, int n, int64_t* gid, int64_t* lens, int32_t* bkt, cudaStream_t st) {
+  if (n <= 0) return SA_OK;
+  unpack_meta_kernel<<<cdiv(n, 256), 256, 0, st>>>(meta, n, gid, lens, bkt);
+  SA_LAUNCHED();
+  return SA_OK;
+}
+
+sa_status seg_copy_launch(const void* segs_dev, int nseg, const int64_t* meta_in, int64_t* meta_out,
+                          const uint8_t* res_in, uint8_t* res_out, cudaStream_t st) {
+  if (nseg <= 0) return SA_OK;
+  dim3 grid(64, (unsigned)std::min(nseg, 1024));
+  seg_copy_kernel<<<grid, 256, 0, st>>>(static_cast<const SegCopy*>(segs_dev), nseg, meta_in, meta_out, res_in,
+                                        res_out);
+  SA_LAUNCHED();
+  return SA_OK;
+}
+
+size_t segcopy_size() { return sizeof(SegCopy); }
+void segcopy_fill(void* dst, int t, int64_t src_m, int64_t dst_m, int64_t cnt, int64_t src_r, int64_t dst_r,
+                  int64_t nbytes) {
+  static_cast<SegCopy*>(dst)[t] = SegCopy{src_m, dst_m, cnt, src_r, dst_r, nbytes};
+}
+
+}  // namespace sa

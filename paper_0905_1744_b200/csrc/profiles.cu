@@ -1,0 +1,77 @@
+// K1 -- k-mer count profiles c^X (§3 "k-mer Rank").
+//
+// One CTA builds one profile at a time (persistent grid-stride over
+// sequences): the profile lives in shared memory as packed u16x2 words
+// (2 bins per 32-bit word, 16 KB for 20^3 bins), every k-mer occurrence is one
+// shared-memory atomicAdd of 1 << 16*(id & 1) into word id >> 1 (a lane never
+// carries into its neighbour: a count is <= nk <= 65535, checked), then the
+// whole row -- including the zero padding up to the 64-bin row stride -- is
+// streamed to HBM with 16-byte vector stores.  The kernel is bound by that
+// 16 KB-per-sequence write (K1).
+#include "common.cuh"
+
+namespace sa {
+
+__global__ void __launch_bounds__(256)
+profiles_kernel(const uint8_t* __restrict__ res, const int64_t* __restrict__ offs, int32_t n, int32_t k,
+                int32_t alphabet, int32_t stride, uint16_t* __restrict__ out, int32_t* __restrict__ nk_out,
+                uint32_t* __restrict__ err) {
+  extern __shared__ __align__(16) uint32_t hist[];   // stride / 2 words
+  const int words = stride >> 1;
+  const int vec = words >> 2;                         // uint4 per row (stride % 64 == 0)
+  for (int64_t s = blockIdx.x; s < n; s += gridDim.x) {
+    uint4* h4 = reinterpret_cast<uint4*>(hist);
+    for (int v = threadIdx.x; v < vec; v += blockDim.x) h4[v] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    const int64_t b = offs[s], e = offs[s + 1];
+    const int64_t len = e - b;
+    const int64_t nk = len >= k ? len - k + 1 : 0;
+    const uint8_t* x = res + b;
+    uint32_t bad = 0;
+    for (int64_t u = threadIdx.x; u < len; u += blockDim.x)
+      if (x[u] >= alphabet) bad = 1;
+    for (int64_t u = threadIdx.x; u < nk; u += blockDim.x) {
+      uint32_t id = 0;
+      bool ok = true;
+      for (int t = 0; t < k; ++t) {
+        const uint32_t r = x[u + t];
+        ok &= r < (uint32_t)alphabet;
+        id = id * (uint32_t)alphabet + r;
+      }
+      if (ok) atomicAdd(&hist[id >> 1], 1u << ((id & 1u) << 4));
+    }
+    if (bad) atomicOr(err, ERR_RESIDUE);
+    if (threadIdx.x == 0) {
+      if (nk > 65535) atomicOr(err, ERR_NK);
+      nk_out[s] = (int32_t)nk;
+    }
+    __syncthreads();
+    uint4* o4 = reinterpret_cast<uint4*>(out + s * (int64_t)stride);
+    for (int v = threadIdx.x; v < vec; v += blockDim.x) o4[v] = h4[v];
+    __syncthreads();
+  }
+}
+
+sa_status profiles_launch(const uint8_t* residues, const int64_t* offsets, int32_t n, int32_t k,
+                          int32_t alphabet, int32_t stride, uint16_t* out, int32_t* nk, uint32_t* err_flag,
+                          cudaStream_t st) {
+  if (n <= 0) return SA_OK;
+  const int smem = stride * 2;
+  static int configured_smem = 48 * 1024;
+  if (smem > configured_smem) {
+    SA_CUDA(cudaFuncSetAttribute(profiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured_smem = smem;
+  }
+  int dev = 0, sms = 0, per_sm = 0;
+  SA_CUDA(cudaGetDevice(&dev));
+  SA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  SA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, profiles_kernel, 256, smem));
+  if (per_sm < 1) per_sm = 1;
+  const int64_t grid = (int64_t)sms * per_sm;
+  profiles_kernel<<<(unsigned)(n < grid ? n : grid), 256, smem, st>>>(residues, offsets, n, k, alphabet, stride, out,
+                                                                     nk, err_flag);
+  SA_LAUNCHED();
+  return SA_OK;
+}
+
+}  // namespace sa

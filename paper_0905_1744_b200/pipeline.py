@@ -1,0 +1,99 @@
+"""One pass of the Sample-Align-D hot path on this rank.
+
+    S1  sa_kmer_profiles          residues -> c^X
+    S2a..S3c sa_partition         ranks, samples, pivots, buckets (Alg. 2 steps 2-11)
+    S4  sa_redistribute           sequences -> owner of their bucket
+    S1' sa_kmer_profiles          profiles of the received sequences
+    S5  sa_bucket_similarity      all-pairs C and F inside each owned bucket
+
+Every step runs in libsa kernels; this module only sequences the calls and
+keeps the device buffers (torch tensors) alive.  Sharding follows sa.h:
+rank r of G holds the logical blocks [r p/G, (r+1) p/G) and owns the buckets
+with the same numbers.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import binding as B
+
+
+def block_begin(q: int, n: int, p: int) -> int:
+    return (q * n) // p
+
+
+def shard_range(n_total: int, p: int, nranks: int, rank: int) -> tuple[int, int]:
+    """Global index range [first, last) of this rank's blocks (sa.h, Z13)."""
+    pb = p // nranks
+    return block_begin(rank * pb, n_total, p), block_begin((rank + 1) * pb, n_total, p)
+
+
+@dataclass
+class StepResult:
+    profiles: torch.Tensor
+    nkmers: torch.Tensor
+    part: B.PartitionOut
+    recv_residues: torch.Tensor
+    recv_offsets: torch.Tensor
+    recv_global_idx: torch.Tensor
+    recv_bucket: torch.Tensor
+    bucket_profiles: torch.Tensor
+    bucket_nkmers: torch.Tensor
+    buckets: list = field(default_factory=list)       # [(bucket id, row0, n_b)]
+    numerators: list = field(default_factory=list)    # per owned bucket, uint16 [n_b][n_b] or None
+    similarity: list = field(default_factory=list)    # per owned bucket, f64 [n_b][n_b] or None
+
+    def pairs(self) -> int:
+        return sum(n * (n - 1) // 2 for _, _, n in self.buckets)
+
+
+class HotPath:
+    """Runs steps S1-S5 for one rank; output matrices are reused across steps
+    when the bucket sizes repeat (the bench re-runs the same workload)."""
+
+    def __init__(self, ctx: B.Context, p: int, samples_per_block: int, k: int = 3, alphabet: int = 20,
+                 want_numerators: bool = True, want_similarity: bool = True):
+        self.ctx = ctx
+        self.p = p
+        self.kb = samples_per_block
+        self.k = k
+        self.alphabet = alphabet
+        self.bins = alphabet ** k
+        self.want_num = want_numerators
+        self.want_sim = want_similarity
+        self._out_cache: dict = {}
+
+    def _outputs(self, b: int, n: int, dev):
+        key = (b, n)
+        if key not in self._out_cache:
+            self._out_cache = {kk: v for kk, v in self._out_cache.items() if kk[0] != b}
+            num = torch.empty((n, n), dtype=torch.uint16, device=dev) if self.want_num else None
+            sim = torch.empty((n, n), dtype=torch.float64, device=dev) if self.want_sim else None
+            self._out_cache[key] = (num, sim)
+        return self._out_cache[key]
+
+    def step(self, residues: torch.Tensor, offsets: torch.Tensor, n_total: int, first_global: int,
+             debug: bool = False, stream=None) -> StepResult:
+        ctx = self.ctx
+        prof, nk = B.sa_kmer_profiles(ctx, residues, offsets, self.k, self.alphabet, stream=stream)
+        part = B.sa_partition(ctx, self.p, self.kb, prof, nk, offsets, self.bins, n_total, first_global,
+                              debug=debug, stream=stream)
+        rres, roffs, rgid, rbkt = B.sa_redistribute(ctx, self.p, residues, offsets, first_global, part,
+                                                    stream=stream)
+        bprof, bnk = B.sa_kmer_profiles(ctx, rres, roffs, self.k, self.alphabet, stream=stream)
+        res = StepResult(prof, nk, part, rres, roffs, rgid, rbkt, bprof, bnk)
+        row = 0
+        for b in B.owned_buckets(self.p, ctx.nranks, ctx.rank):
+            n_b = int(part.counts[:, b].sum())
+            num, sim = self._outputs(b, n_b, offsets.device) if n_b > 0 else (None, None)
+            if n_b > 0:
+                B.sa_bucket_similarity(ctx, bprof[row:row + n_b], bnk[row:row + n_b], self.bins,
+                                       want_numerators=self.want_num, want_similarity=self.want_sim,
+                                       numerators=num, similarity=sim, stream=stream)
+            res.buckets.append((b, row, n_b))
+            res.numerators.append(num)
+            res.similarity.append(sim)
+            row += n_b
+        return res

@@ -1,0 +1,283 @@
+"""Parity of the CUDA path (libsa through the C ABI) with the CPU oracle.
+
+Bit-exact for counts, numerators, keys (exact ranks), orders, samples,
+pivots, buckets and redistributed sequences; fp64 similarities and ranks
+within 1e-12 relative (BASELINE.json north_star) -- in practice equal.
+Inputs are the seeded BASELINE.json workloads (sa_synth) and small seeded
+adversarial sets."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import kmer, partition
+from paper_0905_1744_b200 import binding as B
+from paper_0905_1744_b200.pipeline import HotPath, shard_range
+from sa_synth.generator import CONFIGS, from_sequences, generate
+
+from .gpu_util import assert_rel, digest, keys_u64, load_golden, prof_np, require_gpu, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    require_gpu()
+    return B.Context()
+
+
+def _rand_set(seed, n, lo=0, hi=420, alphabet=20, dup=0):
+    rng = np.random.default_rng(seed)
+    seqs = [rng.integers(0, alphabet, size=int(rng.integers(lo, hi + 1))) for _ in range(n)]
+    for t in range(dup):                    # forced duplicates -> exact ties
+        seqs[(7 * t + 3) % n] = seqs[(11 * t) % n].copy()
+    return from_sequences(seqs)
+
+
+# --------------------------------------------------------------- S1 ------
+@pytest.mark.parametrize("c", [1, 2, 5])
+def test_profiles_configs(ctx, c):
+    ds = generate(CONFIGS[c])
+    res, offs = to_dev(ds)
+    P, nk = B.sa_kmer_profiles(ctx, res, offs)
+    Po, nko = kmer.profiles(ds.residues, ds.offsets)
+    assert np.array_equal(prof_np(P, 8000), Po)
+    assert np.array_equal(nk.cpu().numpy(), nko)
+
+
+@pytest.mark.parametrize("alphabet,k", [(20, 3), (4, 3), (2, 5), (20, 1), (3, 2)])
+def test_profiles_small_alphabets_ragged(ctx, alphabet, k):
+    ds = _rand_set(alphabet * 10 + k, 77, 0, 60, alphabet)
+    res, offs = to_dev(ds)
+    P, nk = B.sa_kmer_profiles(ctx, res, offs, k=k, alphabet=alphabet)
+    bins = alphabet ** k
+    Pn = P.cpu().numpy()
+    Po, nko = kmer.profiles(ds.residues, ds.offsets, k, alphabet)
+    assert np.array_equal(Pn[:, :bins], Po)
+    assert not Pn[:, bins:].any()                 # padding to the 64-bin stride is zero
+    assert np.array_equal(nk.cpu().numpy(), nko)  # includes n < k -> 0
+
+
+def test_profiles_errors(ctx):
+    ds = from_sequences([np.array([0, 1, 2, 3], np.uint8), np.array([0, 20, 1, 2], np.uint8)])
+    res, offs = to_dev(ds)
+    with pytest.raises(B.SaError) as e:
+        B.sa_kmer_profiles(ctx, res, offs)
+    assert e.value.status == B.SA_E_RANGE
+    with pytest.raises(B.SaError) as e:
+        B.sa_kmer_profiles(ctx, res, offs, k=0)
+    assert e.value.status == B.SA_E_INVAL
+    with pytest.raises(B.SaError) as e:
+        B.sa_kmer_profiles(ctx, res, offs, k=4, alphabet=20)   # 160000 bins > 65536
+    assert e.value.status == B.SA_E_INVAL
+    # too many k-mers for uint16 counts
+    big = from_sequences([np.zeros(65540, np.uint8)])
+    r2, o2 = to_dev(big)
+    with pytest.raises(B.SaError) as e:
+        B.sa_kmer_profiles(ctx, r2, o2)
+    assert e.value.status == B.SA_E_RANGE
+    # empty set is a no-op
+    P, nk = B.sa_kmer_profiles(ctx, torch.zeros(1, dtype=torch.uint8, device="cuda"),
+                               torch.zeros(1, dtype=torch.int64, device="cuda"))
+    assert P.shape[0] == 0 and nk.shape[0] == 0
+
+
+# --------------------------------------------------------------- S2 ------
+@pytest.mark.parametrize("nq,npool,dup", [(300, 200, 0), (129, 257, 5), (1, 1, 0), (5, 700, 0)])
+def test_kmer_rank_random(ctx, nq, npool, dup):
+    ds = _rand_set(nq * 1000 + npool, nq + npool, 0, 420, dup=dup)
+    res, offs = to_dev(ds)
+    P, nk = B.sa_kmer_profiles(ctx, res, offs)
+    Po, nko = kmer.profiles(ds.residues, ds.offsets)
+    # the pool overlaps the queries (self terms present for the overlap)
+    q0, p0 = 0, max(0, nq - npool // 3)
+    keys, f64, num = B.sa_kmer_rank(ctx, P[q0:q0 + nq], nk[q0:q0 + nq], P[p0:p0 + npool], nk[p0:p0 + npool],
+                                    want_numerators=True)
+    C = kmer.numerator_matrix(Po[q0:q0 + nq], Po[p0:p0 + npool])
+    D = kmer.denominator_matrix(nko[q0:q0 + nq], nko[p0:p0 + npool])
+    assert np.array_equal(num.cpu().numpy(), C)
+    rs = kmer.RankSet(C, D)
+    got = B.keys_to_ints(keys)
+    assert got == rs.keys
+    assert_rel(f64.cpu().numpy(), [rs.f64(i) for i in range(nq)], 1e-12)
+
+
+def test_kmer_rank_empty_pool(ctx):
+    P = torch.zeros((2, 8000), dtype=torch.uint16, device="cuda")
+    nk = torch.ones(2, dtype=torch.int32, device="cuda")
+    with pytest.raises(B.SaError) as e:
+        B.sa_kmer_rank(ctx, P, nk, P[:0], nk[:0])
+    assert e.value.status == B.SA_E_INVAL
+
+
+# --------------------------------------------------------------- S5 ------
+@pytest.mark.parametrize("n,dup,lo", [(300, 0, 0), (257, 20, 0), (128, 0, 2), (1, 0, 5), (2, 0, 0)])
+def test_bucket_similarity_random(ctx, n, dup, lo):
+    ds = _rand_set(n * 7 + dup, n, lo, 420, dup=dup)
+    res, offs = to_dev(ds)
+    P, nk = B.sa_kmer_profiles(ctx, res, offs)
+    Po, nko = kmer.profiles(ds.residues, ds.offsets)
+    num, sim = B.sa_bucket_similarity(ctx, P, nk)
+    Co, Fo = partition.bucket_similarity(Po, nko, np.arange(n))
+    assert np.array_equal(num.cpu().numpy(), Co)
+    s = sim.cpu().numpy()
+    assert_rel(s, Fo, 1e-12)
+    assert np.array_equal(s, Fo)     # one IEEE RN division on both sides
+
+
+# ----------------------------------------------------- S2-S3 partition ---
+def _partition_g1(ctx, c):
+    cfg = CONFIGS[c]
+    ds = generate(cfg)
+    res, offs = to_dev(ds)
+    P, nk = B.sa_kmer_profiles(ctx, res, offs)
+    part = B.sa_partition(ctx, cfg.p, cfg.samples_per_block, P, nk, offs, 8000, ds.n, 0, debug=True)
+    return ds, P, nk, part
+
+
+@pytest.mark.parametrize("c", [1, 2, 5, 3, 4])
+def test_partition_matches_golden(ctx, c):
+    g, meta = load_golden(c)
+    ds, P, nk, part = _partition_g1(ctx, c)
+    assert ds.sha256() == meta["dataset_sha256"]
+    assert digest(prof_np(P, 8000)) == meta["profile_sha256"]          # S1 bit-exact at full size
+    d = part.debug
+    lk, gk = keys_u64(d["local_key"]), keys_u64(d["global_key"])
+    assert digest(lk) == meta["local_key_sha256"]                       # S2a keys (exact ranks)
+    assert digest(gk) == meta["global_key_sha256"]                      # S2d keys
+    assert np.array_equal(d["local_order"].cpu().numpy(), g["local_order"])     # S2b
+    assert np.array_equal(d["sample_idx"].cpu().numpy(), g["sample_idx"])       # S2b/S2c
+    assert np.array_equal(d["global_order"].cpu().numpy(), g["global_order"])   # S3a
+    assert np.array_equal(d["candidates"].cpu().numpy(), g["candidates"])       # S3b Y
+    assert np.array_equal(B.pivot_global_idx(part.pivots).cpu().numpy(), g["pivots"])
+    assert np.array_equal(part.bucket_of.cpu().numpy(), g["bucket_of"])         # S3c
+    assert part.counts[0].tolist() == meta["bucket_sizes"]
+    lf, gf = d["local_f64"].cpu().numpy(), d["global_f64"].cpu().numpy()
+    if "local_f64" in g:
+        assert_rel(lf, g["local_f64"])
+        assert_rel(gf, g["global_f64"])
+    else:
+        idx = g["key_sample_idx"]
+        assert_rel(lf[idx], g["local_f64_sample"])
+        assert_rel(gf[idx], g["global_f64_sample"])
+    assert part.exact_fallbacks == 0      # synthetic data has no uncertified comparisons
+
+
+def test_partition_invariants_any_size(ctx):
+    """Properties that hold at any size: permutation, the
+    regular-sampling bound 2N/p, pivot boundaries respected."""
+    for c in (2, 5):
+        ds, P, nk, part = _partition_g1(ctx, c)
+        cfg = CONFIGS[c]
+        b = part.bucket_of.cpu().numpy()
+        assert b.min() >= 0 and b.max() < cfg.p
+        sizes = np.bincount(b, minlength=cfg.p)
+        assert sizes.sum() == ds.n and sizes.max() <= 2 * ds.n / cfg.p
+        gk = [int(x) for x in B.keys_to_ints(part.debug["global_key"])]
+        piv = B.pivot_global_idx(part.pivots).cpu().numpy()
+        for i in range(ds.n):
+            me = (gk[i], i)
+            if b[i] < cfg.p - 1:
+                assert me <= (gk[piv[b[i]]], int(piv[b[i]]))
+            if b[i] > 0:
+                assert me > (gk[piv[b[i] - 1]], int(piv[b[i] - 1]))
+
+
+def test_partition_errors(ctx):
+    ds = generate(CONFIGS[1])
+    res, offs = to_dev(ds)
+    P, nk = B.sa_kmer_profiles(ctx, res, offs)
+    with pytest.raises(B.SaError) as e:
+        B.sa_partition(ctx, 4, 51, P, nk, offs, 8000, ds.n, 0)          # k_b > block size 50
+    assert e.value.status == B.SA_E_INVAL
+    with pytest.raises(B.SaError) as e:
+        B.sa_partition(ctx, 0, 1, P, nk, offs, 8000, ds.n, 0)
+    assert e.value.status == B.SA_E_INVAL
+
+
+def test_partition_exact_path_duplicates(ctx):
+    """Identical sequences have identical ranks: keys tie, the key order is
+    not certified, and sa_partition resolves every such comparison exactly
+    (big-integer rationals on the host); the result must equal the oracle's
+    exact-rational partition, ties broken by index."""
+    rng = np.random.default_rng(42)
+    base = [rng.integers(0, 20, size=int(rng.integers(40, 300))) for _ in range(24)]
+    seqs = [base[int(rng.integers(0, len(base)))].copy() for _ in range(96)]
+    ds = from_sequences(seqs)
+    res, offs = to_dev(ds)
+    P, nk = B.sa_kmer_profiles(ctx, res, offs)
+    part = B.sa_partition(ctx, 4, 6, P, nk, offs, 8000, ds.n, 0, debug=True)
+    Po, nko = kmer.profiles(ds.residues, ds.offsets)
+    o = partition.partition(Po, nko, 4, 6)
+    d = part.debug
+    assert part.exact_fallbacks > 0
+    assert B.keys_to_ints(d["local_key"]) == o.local_keys()
+    assert B.keys_to_ints(d["global_key"]) == o.global_keys()
+    assert d["local_order"].cpu().numpy().tolist() == [i for q in o.local_order for i in q]
+    assert d["sample_idx"].cpu().numpy().tolist() == o.sample_idx
+    assert d["global_order"].cpu().numpy().tolist() == [i for q in o.global_order for i in q]
+    assert d["candidates"].cpu().numpy().tolist() == o.candidates
+    assert B.pivot_global_idx(part.pivots).cpu().numpy().tolist() == o.pivots
+    assert np.array_equal(part.bucket_of.cpu().numpy(), o.bucket_of)
+
+
+def test_partition_identical_closed_form(ctx):
+    """All sequences identical: the closed-form partition of
+    tests/golden/closed_form_partitions.json (N = 200, p = 4)."""
+    rng = np.random.default_rng(0)
+    s = rng.integers(0, 20, size=40)
+    ds = from_sequences([s] * 200)
+    res, offs = to_dev(ds)
+    P, nk = B.sa_kmer_profiles(ctx, res, offs)
+    part = B.sa_partition(ctx, 4, 16, P, nk, offs, 8000, 200, 0)
+    assert B.pivot_global_idx(part.pivots).cpu().numpy().tolist() == [25, 87, 162]
+    assert part.counts[0].tolist() == [26, 62, 75, 37]
+
+
+# ------------------------------------------------------- S4 + S5 (G=1) ---
+@pytest.mark.parametrize("c", [1, 2])
+def test_hot_path_step_matches_oracle(ctx, c):
+    cfg = CONFIGS[c]
+    ds = generate(cfg)
+    res, offs = to_dev(ds)
+    hp = HotPath(ctx, cfg.p, cfg.samples_per_block)
+    out = hp.step(res, offs, ds.n, 0)
+    Po, nko = kmer.profiles(ds.residues, ds.offsets)
+    o = partition.partition(Po, nko, cfg.p, cfg.samples_per_block)
+    gid = out.recv_global_idx.cpu().numpy()
+    assert np.array_equal(gid, np.concatenate(o.buckets))                 # S4 order (bucket, index)
+    assert np.array_equal(out.recv_bucket.cpu().numpy(), o.bucket_of[gid])
+    rr, ro = out.recv_residues.cpu().numpy(), out.recv_offsets.cpu().numpy()
+    for j, i in enumerate(gid):
+        assert np.array_equal(rr[ro[j]:ro[j + 1]], ds.seq(int(i)))
+    for (b, row, n_b), num, sim in zip(out.buckets, out.numerators, out.similarity):
+        Co, Fo = partition.bucket_similarity(Po, nko, o.buckets[b])
+        assert np.array_equal(num.cpu().numpy(), Co)
+        assert np.array_equal(sim.cpu().numpy(), Fo)
+
+
+def test_hot_path_full_size_sampled(ctx):
+    """Config 4 at full size, in the launch configuration bench.py times:
+    sampled rows of every bucket's matrices against the oracle, computed one
+    row at a time; symmetry and unit diagonal on a sampled block."""
+    cfg = CONFIGS[4]
+    g, meta = load_golden(4)
+    ds = generate(cfg)
+    res, offs = to_dev(ds)
+    hp = HotPath(ctx, cfg.p, cfg.samples_per_block)
+    out = hp.step(res, offs, ds.n, 0)
+    assert np.array_equal(out.part.bucket_of.cpu().numpy(), g["bucket_of"])
+    gid = out.recv_global_idx.cpu().numpy()
+    rng = np.random.default_rng(4)
+    for (b, row, n_b), num, sim in zip(out.buckets, out.numerators, out.similarity):
+        members = gid[row:row + n_b]
+        assert np.array_equal(members, np.flatnonzero(g["bucket_of"] == b))
+        Pm, nkm = kmer.profiles(ds.subset(members).residues, ds.subset(members).offsets)
+        for r in list(rng.choice(n_b, size=3, replace=False)) + [n_b - 1]:
+            Crow = kmer.numerator_matrix(Pm[r:r + 1], Pm)[0]
+            Drow = np.minimum(nkm[r], nkm)
+            assert np.array_equal(num[r].cpu().numpy(), Crow)
+            Frow = np.where(Drow > 0, Crow / np.maximum(Drow, 1), 0.0)
+            assert np.array_equal(sim[r].cpu().numpy(), Frow)
+        blk = num[:200, :200].cpu().numpy()
+        assert np.array_equal(blk, blk.T)
+        assert np.all(np.diag(sim[:200, :200].cpu().numpy()) == 1.0)
