@@ -1,0 +1,387 @@
+"""Benchmark of the Sample-Align-D hot path (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl mine|reference]
+
+A step is one pass of the whole hot path over one batch of synthetic input
+(DESIGN.md §7): S1 profiles, S2a local ranks, S2b samples, S2c sample
+exchange, S2d global ranks, S3 pivots and buckets, S4 redistribution, S1' the
+received profiles, S5 every bucket's all-pairs similarity matrix.  Under
+torchrun each rank (one per GPU) holds p/N logical blocks and owns p/N buckets;
+collectives go through torch.distributed (NCCL).  Rank 0 prints one JSON line.
+
+value   = k-mer similarity sequence-pairs evaluated per second by the whole job
+          (S2a + S2d + S5 pairs, SURVEY §8(d) accounting) / max-over-ranks time
+          of K device-timed steps, inputs resident in HBM;
+e2e     = the same through the public API with the step's inputs copied from
+          pinned host memory and its results (buckets, member ids, uint16
+          numerator matrices) copied back inside the timed region;
+roofline= the dominant kernel (K2 min-sum, S5 launches) in bin-ops/s against
+          the derived integer-pipe peak;
+cpu_baseline = the CPU oracle (oracle/, as it stands) on a bounded sample of
+          the same workload, on the host's cores (rank 0, N = 1 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "k-mer similarity sequence-pairs/s and partition time at 1/2/4/8 B200; % roofline"
+UNIT = "sequence-pairs/s"
+EPS_BINS = 8000                      # 20^3 bin-ops per pair (Eq. 1)
+# ALU-pipe bound of the dense min-sum: 2 warp-instr/clk/SM x 32 lanes x bins per instruction
+BINOPS_PER_SM_CLK = {"u8": 256,       # VABSDIFF4.U8.ACC: 4 bins (sum|a-b| identity)
+                     "u16": 128,      # VIMNMX.U16x2: 2 bins (adds also on the ALU pipe: 85 reachable)
+                     "u16imad": 128}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def workload_desc(cfg):
+    L = cfg.length
+    ln = (f"ancestor length U[{L[1]},{L[2]}]" if L[0] == "uniform"
+          else f"lengths lognormal mean {L[1]} sigma {L[2]} clipped [{L[3]},{L[4]}]")
+    return (f"{cfg.name}: N={cfg.n} protein seqs, {cfg.families} families, {ln}, "
+            f"{int(cfg.p_sub * 100)}% subst + {int(cfg.p_indel * 100)}% indel, k={cfg.k}, p={cfg.p}, "
+            f"{cfg.samples_per_block} samples per block")
+
+
+# ------------------------------------------------------------ clocks -----
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons, pw = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+                pw.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(pw) if pw else None}
+
+
+# -------------------------------------------------------- CPU oracle ------
+def cpu_oracle_sample(ds, cfg, n_sample: int, workers: int):
+    """The oracle (as it stands) on the first n_sample sequences of the
+    workload, partitioned with the workload's p and k_b (capped at the block
+    size) plus every bucket's similarity matrix.  Returns (pairs, seconds)."""
+    from oracle import kmer, partition
+    sub = ds.subset(np.arange(n_sample))
+    t0 = time.perf_counter()
+    P, nk = kmer.profiles(sub.residues, sub.offsets, cfg.k, cfg.alphabet)
+    w = n_sample // cfg.p
+    kb = min(cfg.samples_per_block, w)
+    r = partition.partition(P, nk, cfg.p, kb, workers=workers)
+    s5 = 0
+    for mem in r.buckets:
+        if len(mem):
+            partition.bucket_similarity(P, nk, mem, workers=workers)
+            s5 += len(mem) * (len(mem) - 1) // 2
+    dt = time.perf_counter() - t0
+    bounds = partition.block_bounds(n_sample, cfg.p)
+    s2a = sum((bounds[q + 1] - bounds[q]) * (bounds[q + 1] - bounds[q] - 1) // 2 for q in range(cfg.p))
+    s2d = n_sample * cfg.p * kb
+    return s2a + s2d + s5, dt, kb
+
+
+def run_reference(args, cfg, ds):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import kmer
+    workers = kmer.default_workers()
+    n_s = args.cpu_sample_n
+    for _ in range(args.warmup):
+        cpu_oracle_sample(ds, cfg, n_s, workers)
+    tot_pairs, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        pairs, dt, kb = cpu_oracle_sample(ds, cfg, n_s, workers)
+        tot_pairs += pairs
+        tot_s += dt
+    v = tot_pairs / tot_s
+    sample = (f"oracle profiles + Alg.2 partition (p={cfg.p}, k_b={kb}) + all bucket matrices on the first "
+              f"{n_s} sequences of {cfg.name}, per step")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64/f64 (numpy)",
+            "data": "synthetic", "config": {"workload": workload_desc(cfg), "reference_sample": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- GPU arm ----
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-n", type=int, default=2400)
+    ap.add_argument("--no-similarity", action="store_true", help="S5 numerators only (not the default)")
+    args = ap.parse_args()
+
+    from sa_synth.generator import CONFIGS, generate
+    cfg = CONFIGS[args.config]
+    ds = generate(cfg)
+    if args.impl == "reference":
+        run_reference(args, cfg, ds)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_0905_1744_b200 import binding as B
+    from paper_0905_1744_b200.pipeline import HotPath, shard_range
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if cfg.p % world:
+        raise SystemExit(f"p={cfg.p} is not divisible by {world} GPUs")
+
+    first, last = shard_range(ds.n, cfg.p, world, rank)
+    r0, r1 = int(ds.offsets[first]), int(ds.offsets[last])
+    res_h = torch.from_numpy(ds.residues[r0:r1].copy()).pin_memory()
+    offs_h = torch.from_numpy(ds.offsets[first:last + 1] - ds.offsets[first]).pin_memory()
+    res_d = res_h.to(dev)
+    offs_d = offs_h.to(dev)
+
+    ctx = B.Context(local)
+    if world > 1:
+        ctx.attach_comm(B.TorchComm(device=dev))
+    ctx.set_timing(True)
+    hp = HotPath(ctx, cfg.p, cfg.samples_per_block, want_similarity=not args.no_similarity)
+    st = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    names = ["start", "S1", "S4", "S1b", "S5"]
+    for _ in range(args.warmup):
+        out = hp.step(res_d, offs_d, ds.n, first)
+    torch.cuda.synchronize()
+
+    # ------------------------------------------------ device-timed steps
+    per_step = []
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = B.sa_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(args.steps):
+        ev = {k: torch.cuda.Event(enable_timing=True) for k in names}
+        out = hp.step(res_d, offs_d, ds.n, first, events=ev)
+        ph = ctx.phase_ms()
+        per_step.append((ev, ph))
+    e1.record(st)
+    torch.cuda.synchronize()
+    launches = B.sa_launch_count() - launches0
+    barrier()
+    clk = clocks.stop()
+    total_ms = max_over_ranks(e0.elapsed_time(e1))
+
+    # pair accounting; bucket sizes are known on every rank
+    bounds = [q * ds.n // cfg.p for q in range(cfg.p + 1)]
+    s2a_pairs = sum((bounds[q + 1] - bounds[q]) * (bounds[q + 1] - bounds[q] - 1) // 2 for q in range(cfg.p))
+    s2d_pairs = ds.n * cfg.p * cfg.samples_per_block
+    sizes = out.part.counts.sum(axis=0)
+    s5_pairs = int(sum(int(n) * (int(n) - 1) // 2 for n in sizes))
+    pairs = s2a_pairs + s2d_pairs + s5_pairs
+    value = pairs * args.steps / (total_ms / 1e3)
+
+    def med(f):
+        return statistics.median(f(ev, ph) for ev, ph in per_step)
+
+    part_ms = med(lambda ev, ph: ev["S1"].elapsed_time(ev["S4"]))
+    s5_ms = med(lambda ev, ph: ev["S1b"].elapsed_time(ev["S5"]))
+    phases = {
+        "S1": med(lambda ev, ph: ev["start"].elapsed_time(ev["S1"])),
+        "S2a": med(lambda ev, ph: ph["S2a"]), "S2b": med(lambda ev, ph: ph["S2b"]),
+        "S2c": med(lambda ev, ph: ph["S2c"]), "S2d": med(lambda ev, ph: ph["S2d"]),
+        "S3": med(lambda ev, ph: ph["S3"]),
+        "partition_S2a_to_S4": part_ms,
+        "S1_received": med(lambda ev, ph: ev["S4"].elapsed_time(ev["S1b"])),
+        "S5": s5_ms,
+    }
+    part_ms_max = max_over_ranks(part_ms)
+    s5_ms_max = max_over_ranks(s5_ms)
+
+    # roofline of the dominant kernel: K2 over this rank's S5 launches
+    peaks, peak_src = load_peaks()
+    sm_mhz_peak = float(peaks.get("sm_max_mhz", 1965.0))
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    engine = ctx.engine()
+    per_clk = BINOPS_PER_SM_CLK[engine]
+    peak_binops = per_clk * nsm * sm_mhz_peak * 1e6
+    own = list(B.owned_buckets(cfg.p, world, rank))
+    my_s5_pairs = sum(int(sizes[b]) * (int(sizes[b]) - 1) // 2 for b in own)
+    achieved = my_s5_pairs * EPS_BINS / (s5_ms / 1e3)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "k2_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    roof = {"bound": "alu", "kernel": f"minsum_kernel<sym, {engine}> (K2, S5 bucket matrices)",
+            "engine": engine,
+            "achieved": achieved / 1e12, "peak": peak_binops / 1e12, "unit": "Tbin-op/s",
+            "frac": achieved / peak_binops, "traffic": traffic,
+            "peak_source": (f"derived ({peak_src} sm_max_mhz): {per_clk} bin-ops/clk/SM = ALU pipe 2 warp-instr/"
+                            f"clk/SM (ncu sm__inst_executed_pipe_alu peak) x 32 lanes x {per_clk // 64} bins per "
+                            f"{'VABSDIFF4.U8.ACC' if engine == 'u8' else 'VIMNMX.U16x2'} x {nsm} SMs "
+                            f"x {sm_mhz_peak:.0f} MHz"),
+            "algorithmic": f"{EPS_BINS} bin-ops per pair x {my_s5_pairs} pairs / S5 CUDA-event time"}
+
+    # --------------------------------------------- end-to-end (host buffers)
+    e2e = None
+    if not args.no_e2e:
+        h_out = {}
+
+        def d2h(o):
+            nb = 0
+            pairs_ = [("bucket_of", o.part.bucket_of), ("gid", o.recv_global_idx)]
+            for (b, _, n_b), num in zip(o.buckets, o.numerators):
+                if num is not None:
+                    pairs_.append((f"num{b}", num.view(torch.int16)))
+            for k, t in pairs_:
+                if k not in h_out or h_out[k].shape != t.shape:
+                    h_out[k] = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+                h_out[k].copy_(t, non_blocking=True)
+                nb += t.numel() * t.element_size()
+            return nb
+
+        res_dd = torch.empty_like(res_d)
+        offs_dd = torch.empty_like(offs_d)
+        d2h(out)                      # allocate the pinned result buffers outside the timed region
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(st)
+        d2h_bytes = 0
+        for _ in range(args.steps):
+            res_dd.copy_(res_h, non_blocking=True)
+            offs_dd.copy_(offs_h, non_blocking=True)
+            o = hp.step(res_dd, offs_dd, ds.n, first)
+            d2h_bytes = d2h(o)
+        f1.record(st)
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(f0.elapsed_time(f1))
+        e2e = {"value": pairs * args.steps / (e2e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(res_h.numel() + offs_h.numel() * 8),
+               "d2h_bytes_per_step": int(d2h_bytes), "ms_per_step": e2e_ms / args.steps,
+               "results_copied": "bucket_of, received member ids, uint16 numerator matrices of owned buckets"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import kmer
+        workers = kmer.default_workers()
+        cp, cs, kb = cpu_oracle_sample(ds, cfg, args.cpu_sample_n, workers)
+        cpu = {"value": cp / cs, "unit": UNIT, "cores": workers, "kind": "oracle",
+               "sample": (f"oracle profiles + Alg.2 partition (p={cfg.p}, k_b={kb}) + all bucket matrices on "
+                          f"the first {args.cpu_sample_n} sequences of {cfg.name}: {cp} pairs in {cs:.1f} s")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u16",
+            "data": "synthetic (seeded star-phylogeny protein families, sa_synth)",
+            "config": {"workload": workload_desc(cfg), "N": ds.n, "p": cfg.p,
+                       "samples_per_block": cfg.samples_per_block, "k": cfg.k, "alphabet": cfg.alphabet,
+                       "dataset_sha256": ds.sha256(), "parallelism": f"{world} rank(s), {cfg.p // world} "
+                       "blocks/buckets each",
+                       "l2": "inputs larger than L2 (profiles N x 16 KB = "
+                             f"{ds.n * 16000 / 1e9:.2f} GB per step)"},
+            "partition_ms": part_ms_max, "s5_ms": s5_ms_max,
+            "pairs_per_step": {"S2a": s2a_pairs, "S2d": s2d_pairs, "S5": s5_pairs},
+            "s5_pairs_per_s": s5_pairs / (s5_ms_max / 1e3),
+            "phases_ms_rank0": phases, "bucket_sizes": [int(x) for x in sizes],
+            "exact_fallbacks": out.part.exact_fallbacks,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -103,6 +103,11 @@ enum {
   SA_PHASE_COUNT = 7
 };
 sa_status sa_ctx_set_timing(sa_ctx* ctx, int enable);
+/* Operand encoding of the last min-sum launch on this context:
+ * 0 = uint16 counts (VIMNMX.U16x2 min + add; any count), 1 = uint8 counts
+ * (C = (nk_a + nk_b - sum|a-b|)/2 with VABSDIFF4.U8.ACC; used when every
+ * count is <= 255), 2 = uint16 with FMA-pipe adds (SA_ENGINE=u16imad). */
+int sa_ctx_engine(const sa_ctx* ctx);
 sa_status sa_ctx_phase_ms(sa_ctx* ctx, float* ms_h /* [SA_PHASE_COUNT] */);
 
 /* Exact comparison of two ranks over the same pool (host memory, no GPU):

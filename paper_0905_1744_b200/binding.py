@@ -25,7 +25,7 @@ PHASES = ["S2a", "S2b", "S2c", "S2d", "S3", "S5", "rank"]
 
 EXPORTED = ["sa_ctx_create", "sa_ctx_attach_comm", "sa_ctx_destroy", "sa_last_error", "sa_launch_count",
             "sa_ctx_set_timing", "sa_ctx_phase_ms", "sa_profile_stride", "sa_kmer_profiles", "sa_kmer_rank",
-            "sa_partition", "sa_redistribute", "sa_bucket_similarity", "sa_exact_rank_compare"]
+            "sa_partition", "sa_redistribute", "sa_bucket_similarity", "sa_exact_rank_compare", "sa_ctx_engine"]
 
 
 class SaError(RuntimeError):
@@ -91,6 +91,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                            ctypes.POINTER(ctypes.c_int64), P, P, P, P, VP]),
         "sa_bucket_similarity": (ctypes.c_int, [P, P, P, I32, I32, P, P, VP]),
         "sa_exact_rank_compare": (ctypes.c_int, [P, I32, P, I32, P, I32]),
+        "sa_ctx_engine": (ctypes.c_int, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -176,6 +177,10 @@ class Context:
         self._comm_keepalive = (comm, ops)
         _check(load_library().sa_ctx_attach_comm(self.handle, ctypes.byref(ops), comm.nranks, comm.rank))
         self.nranks, self.rank = comm.nranks, comm.rank
+
+    def engine(self) -> str:
+        """Operand encoding of the last min-sum launch ('u16', 'u8', 'u16imad')."""
+        return {0: "u16", 1: "u8", 2: "u16imad"}.get(int(load_library().sa_ctx_engine(self.handle)), "none")
 
     def set_timing(self, enable: bool = True):
         _check(load_library().sa_ctx_set_timing(self.handle, int(enable)))

@@ -101,7 +101,72 @@ struct Scratch {
 
 static inline int64_t block_begin(int64_t q, int64_t N, int64_t p) { return q * N / p; }
 
-static int32_t profile_stride(int32_t bins) { return ((bins + 63) / 64) * 64; }
+static int32_t profile_stride(int32_t bins) { return stride_u16(bins); }
+
+// Engine choice: SA_ENGINE = auto (default) | u16 | u16imad | u8 (u8 is still
+// only used when every count is <= 255; otherwise the exact u16 engine runs).
+static int engine_mode() {
+  const char* e = getenv("SA_ENGINE");
+  if (!e || !*e || !strcmp(e, "auto") || !strcmp(e, "u8")) return ENC_U8_SAD;
+  if (!strcmp(e, "u16imad")) return ENC_U16_MIN_IMAD;
+  return ENC_U16_MIN;
+}
+
+// Operand rows the min-sum engine reads for a set of u16 profile rows.
+struct Operand {
+  const uint32_t* rows;
+  int ldw;   // row stride in 32-bit words
+};
+
+// Build the u8 (SAD) operand rows of `n` u16 profile rows in scratch memory and
+// fold the largest count into *maxc (device).  Returns nullptr rows on OOM.
+static sa_status make_u8_rows(Scratch& scratch, const uint16_t* p16, int64_t n, int32_t bins, uint32_t* maxc,
+                              Operand* out, cudaStream_t st) {
+  const int32_t s8 = stride_u8(bins);
+  uint8_t* p8 = scratch.alloc<uint8_t>((size_t)std::max<int64_t>(n, 1) * s8);
+  if (!p8) return fail(SA_E_NOMEM, "scratch allocation of u8 operand rows failed");
+  SA_TRY(to_u8_launch(p16, n, stride_u16(bins), bins, p8, s8, maxc, st));
+  out->rows = reinterpret_cast<const uint32_t*>(p8);
+  out->ldw = s8 / 4;
+  return SA_OK;
+}
+
+static sa_status read_max(const uint32_t* d, uint32_t* h, cudaStream_t st) {
+  SA_CUDA(cudaMemcpyAsync(h, d, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  SA_CUDA(cudaStreamSynchronize(st));
+  return SA_OK;
+}
+
+// Operands and encoding for an A x B min-sum problem given u16 rows (B may
+// alias A).  Host-blocking once (the largest count decides the encoding).
+static sa_status select_operands(Scratch& scratch, const uint16_t* A16, int64_t na, const uint16_t* B16, int64_t nb,
+                                 int32_t bins, Operand* oa, Operand* ob, int* enc, cudaStream_t st) {
+  const int ldw16 = stride_u16(bins) / 2;
+  *oa = Operand{reinterpret_cast<const uint32_t*>(A16), ldw16};
+  *ob = Operand{reinterpret_cast<const uint32_t*>(B16), ldw16};
+  const int mode = engine_mode();
+  *enc = mode == ENC_U16_MIN_IMAD ? ENC_U16_MIN_IMAD : ENC_U16_MIN;
+  if (mode != ENC_U8_SAD) return SA_OK;
+  uint32_t* maxc = scratch.alloc<uint32_t>(1);
+  if (!maxc) return fail(SA_E_NOMEM, "scratch allocation failed");
+  SA_CUDA(cudaMemsetAsync(maxc, 0, sizeof(uint32_t), st));
+  Operand a8, b8;
+  if (B16 == A16) {   // same rows (possibly different counts): convert the longer prefix once
+    SA_TRY(make_u8_rows(scratch, A16, std::max(na, nb), bins, maxc, &a8, st));
+    b8 = a8;
+  } else {
+    SA_TRY(make_u8_rows(scratch, A16, na, bins, maxc, &a8, st));
+    SA_TRY(make_u8_rows(scratch, B16, nb, bins, maxc, &b8, st));
+  }
+  uint32_t mh = 0;
+  SA_TRY(read_max(maxc, &mh, st));
+  if (mh <= 255) {
+    *oa = a8;
+    *ob = b8;
+    *enc = ENC_U8_SAD;
+  }
+  return SA_OK;
+}
 
 }  // namespace sa
 
@@ -170,6 +235,8 @@ sa_status sa_ctx_destroy(sa_ctx* ctx) {
   return SA_OK;
 }
 
+int sa_ctx_engine(const sa_ctx* ctx) { return ctx ? ctx->last_enc : -1; }
+
 sa_status sa_ctx_set_timing(sa_ctx* ctx, int enable) {
   if (!ctx) return fail(SA_E_INVAL, "ctx is NULL");
   ctx->timing = enable != 0;
@@ -237,7 +304,7 @@ static sa_status numerator_rows_host(const uint16_t* prof, const int32_t* nk, co
   pr.sym = 0;
   pr.num = num;
   pr.ld = npool;
-  SA_TRY(minsum_launch({pr}, stride / 2, st, nullptr, nullptr));
+  SA_TRY(minsum_launch({pr}, stride / 2, ENC_U16_MIN, st, nullptr, nullptr));
   SA_CUDA(cudaMemcpyAsync(out.data(), num, out.size() * sizeof(uint16_t), cudaMemcpyDeviceToHost, st));
   SA_CUDA(cudaStreamSynchronize(st));
   return SA_OK;
@@ -367,6 +434,20 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
   SA_CUDA(cudaMemsetAsync(lkey, 0, n * sizeof(sa_key128), st));
   SA_CUDA(cudaMemsetAsync(gkey, 0, n * sizeof(sa_key128), st));
 
+  // engine operands: u8 SAD rows when every count fits (the usual case), else u16
+  SA_ALLOC(maxc, uint32_t, 2);
+  SA_CUDA(cudaMemsetAsync(maxc, 0, 2 * sizeof(uint32_t), st));
+  const int mode = engine_mode();
+  Operand loc{reinterpret_cast<const uint32_t*>(a.prof), ldw};
+  int enc_loc = mode == ENC_U16_MIN_IMAD ? ENC_U16_MIN_IMAD : ENC_U16_MIN;
+  if (mode == ENC_U8_SAD) {
+    Operand o8;
+    uint32_t mh = 0;
+    SA_TRY(make_u8_rows(scratch, a.prof, n, a.stride, maxc, &o8, st));
+    SA_TRY(read_max(maxc, &mh, st));
+    if (mh <= 255) { loc = o8; enc_loc = ENC_U8_SAD; }
+  }
+
   // ---- S2a: local rank of every member against its own block
   SA_TRY(rec(ev_begin(c, SA_PHASE_S2A), st));
   {
@@ -375,14 +456,14 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
       const int64_t b = block_begin(q0 + q, a.N, a.p) - a.first;
       const int64_t e = block_begin(q0 + q + 1, a.N, a.p) - a.first;
       MsProblem pr{};
-      pr.A = pr.B = reinterpret_cast<const uint32_t*>(a.prof + b * a.stride);
+      pr.A = pr.B = loc.rows + b * loc.ldw;
       pr.nkA = pr.nkB = a.nk + b;
       pr.na = pr.nb = (int32_t)(e - b);
       pr.sym = 1;
       pr.keyA = pr.keyB = lkey + b;
       probs.push_back(pr);
     }
-    SA_TRY(minsum_launch(probs, ldw, st, nullptr, nullptr));
+    SA_TRY(minsum_launch(probs, loc.ldw, enc_loc, st, nullptr, nullptr));
   }
   SA_TRY(rec(ev_end(c, SA_PHASE_S2A), st));
 
@@ -408,18 +489,29 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
   SA_TRY(rec(ev_end(c, SA_PHASE_S2C), st));
 
   // ---- S2d: global rank against S
-  SA_TRY(rec(ev_begin(c, SA_PHASE_S2D), st));
   {
+    Operand smp{reinterpret_cast<const uint32_t*>(s_prof), ldw};
+    Operand qry{reinterpret_cast<const uint32_t*>(a.prof), ldw};
+    int enc = mode == ENC_U16_MIN_IMAD ? ENC_U16_MIN_IMAD : ENC_U16_MIN;
+    if (enc_loc == ENC_U8_SAD) {
+      Operand o8;
+      uint32_t mh = 0;
+      SA_TRY(make_u8_rows(scratch, s_prof, s_all, a.stride, maxc + 1, &o8, st));
+      SA_TRY(read_max(maxc + 1, &mh, st));
+      if (mh <= 255) { smp = o8; qry = loc; enc = ENC_U8_SAD; }
+    }
+    SA_TRY(rec(ev_begin(c, SA_PHASE_S2D), st));
     MsProblem pr{};
-    pr.A = reinterpret_cast<const uint32_t*>(a.prof);
-    pr.B = reinterpret_cast<const uint32_t*>(s_prof);
+    pr.A = qry.rows;
+    pr.B = smp.rows;
     pr.nkA = a.nk;
     pr.nkB = s_nk;
     pr.na = n;
     pr.nb = s_all;
     pr.sym = 0;
     pr.keyA = gkey;
-    SA_TRY(minsum_launch({pr}, ldw, st, nullptr, nullptr));
+    SA_TRY(minsum_launch({pr}, qry.ldw, enc, st, nullptr, nullptr));
+    c->last_enc = enc;
   }
   SA_TRY(rec(ev_end(c, SA_PHASE_S2D), st));
 
@@ -670,11 +762,14 @@ sa_status sa_kmer_rank(sa_ctx* ctx, const uint16_t* q_prof, const int32_t* q_nk,
   if (!q_prof || !q_nk || !pool_prof || !pool_nk || !keys) return fail(SA_E_INVAL, "NULL required pointer");
   cudaStream_t st = (cudaStream_t)stream;
   SA_CUDA(cudaSetDevice(ctx->device));
-  const int stride = profile_stride(bins);
   SA_CUDA(cudaMemsetAsync(keys, 0, (size_t)nq * sizeof(sa_key128), st));
+  Scratch scratch(st);
+  Operand oa, ob;
+  int enc;
+  SA_TRY(select_operands(scratch, q_prof, nq, pool_prof, npool, bins, &oa, &ob, &enc, st));
   MsProblem pr{};
-  pr.A = reinterpret_cast<const uint32_t*>(q_prof);
-  pr.B = reinterpret_cast<const uint32_t*>(pool_prof);
+  pr.A = oa.rows;
+  pr.B = ob.rows;
   pr.nkA = q_nk;
   pr.nkB = pool_nk;
   pr.na = nq;
@@ -683,7 +778,8 @@ sa_status sa_kmer_rank(sa_ctx* ctx, const uint16_t* q_prof, const int32_t* q_nk,
   pr.keyA = keys;
   pr.num = numerators;
   pr.ld = npool;
-  SA_TRY(minsum_launch({pr}, stride / 2, st, ev_begin(ctx, SA_PHASE_RANK), ev_end(ctx, SA_PHASE_RANK)));
+  SA_TRY(minsum_launch({pr}, oa.ldw, enc, st, ev_begin(ctx, SA_PHASE_RANK), ev_end(ctx, SA_PHASE_RANK)));
+  ctx->last_enc = enc;
   if (rank_f64) SA_TRY(keys_to_f64_launch(keys, nq, npool, rank_f64, st));
   return SA_OK;
 }
@@ -834,15 +930,20 @@ sa_status sa_bucket_similarity(sa_ctx* ctx, const uint16_t* profiles, const int3
   if (!profiles || !nkmers) return fail(SA_E_INVAL, "NULL required pointer");
   cudaStream_t st = (cudaStream_t)stream;
   SA_CUDA(cudaSetDevice(ctx->device));
+  Scratch scratch(st);
+  Operand oa, ob;
+  int enc;
+  SA_TRY(select_operands(scratch, profiles, n, profiles, n, bins, &oa, &ob, &enc, st));
   MsProblem pr{};
-  pr.A = pr.B = reinterpret_cast<const uint32_t*>(profiles);
+  pr.A = pr.B = oa.rows;
   pr.nkA = pr.nkB = nkmers;
   pr.na = pr.nb = n;
   pr.sym = 1;
   pr.num = numerators;
   pr.sim = similarity;
   pr.ld = n;
-  SA_TRY(minsum_launch({pr}, profile_stride(bins) / 2, st, ev_begin(ctx, SA_PHASE_S5), ev_end(ctx, SA_PHASE_S5)));
+  SA_TRY(minsum_launch({pr}, oa.ldw, enc, st, ev_begin(ctx, SA_PHASE_S5), ev_end(ctx, SA_PHASE_S5)));
+  ctx->last_enc = enc;
   return SA_OK;
 }
 

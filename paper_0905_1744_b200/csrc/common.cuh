@@ -68,10 +68,22 @@ struct MsProblem {
   int64_t ld;
 };
 
-// Launch the engine over `probs` (host array, copied to device scratch).
-// mode: 0 keys only, 1 keys + optional matrices.
-sa_status minsum_launch(const std::vector<MsProblem>& probs, int ldw, cudaStream_t st,
+// Profile encodings the engine reads:
+//   ENC_U16_MIN       uint16 counts, 2 bins/word, VIMNMX.U16x2 + IADD3 (any count)
+//   ENC_U16_MIN_IMAD  same, adds issued as IMAD on the FMA pipe (experiment)
+//   ENC_U8_SAD        uint8 counts, 4 bins/word, C = (nk_a + nk_b - sum|a-b|)/2 with
+//                     VABSDIFF4.U8.ACC (every count must be <= 255)
+enum { ENC_U16_MIN = 0, ENC_U8_SAD = 1, ENC_U16_MIN_IMAD = 2 };
+// Row strides: u16 rows are round_up(bins, 64) elements; u8 rows round_up(bins, 128) bytes.
+inline int32_t stride_u16(int32_t bins) { return ((bins + 63) / 64) * 64; }
+inline int32_t stride_u8(int32_t bins) { return ((bins + 127) / 128) * 128; }
+
+// Launch the engine over `probs`; ldw = row stride in 32-bit words.
+sa_status minsum_launch(const std::vector<MsProblem>& probs, int ldw, int enc, cudaStream_t st,
                         cudaEvent_t ev0, cudaEvent_t ev1);
+// uint16 rows -> uint8 rows (zero padded) + atomicMax of every count into *maxc.
+sa_status to_u8_launch(const uint16_t* p16, int64_t n, int32_t stride16, int32_t bins, uint8_t* p8,
+                       int32_t stride8, uint32_t* maxc, cudaStream_t st);
 sa_status ensure_recip_tables(cudaStream_t st);
 
 // ------------------------------------------------------ profiles (K1) --
@@ -114,4 +126,5 @@ struct sa_ctx {
   bool timing = false;
   cudaEvent_t ev[2 * SA_PHASE_COUNT] = {};
   bool ev_used[SA_PHASE_COUNT] = {};
+  int last_enc = -1;
 };

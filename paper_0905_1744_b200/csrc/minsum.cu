@@ -88,9 +88,21 @@ __device__ __forceinline__ void shfl_add(uint64_t& lo, uint32_t& hi, int mask) {
   hi += ohi + ((lo < olo) ? 1u : 0u);
 }
 
-template <bool SYM>
+// acc += sum over the 4 byte lanes of |a - b|  (one VABSDIFF4.U8.ACC)
+__device__ __forceinline__ void vsad4_acc(uint32_t& acc, uint32_t a, uint32_t b) {
+  asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(acc) : "r"(a), "r"(b));
+}
+
+// Numerator of one pair from its accumulator (see the ENC_* encodings).
+template <int ENC>
+__device__ __forceinline__ uint32_t acc_to_C(uint32_t acc, int nka, int nkb) {
+  if (ENC == ENC_U8_SAD) return (uint32_t)(nka + nkb - (int)acc) >> 1;   // sum min = (sum a + sum b - sum|a-b|)/2
+  return (acc & 0xffffu) + (acc >> 16);                                  // the two u16 lanes
+}
+
+template <bool SYM, int ENC>
 __global__ void __launch_bounds__(MS_THREADS, 1)
-minsum_kernel(const __grid_constant__ MsBatch batch, int64_t total_tiles, int ldw) {
+minsum_kernel(const __grid_constant__ MsBatch batch, int64_t total_tiles, int ldw, uint32_t one) {
   extern __shared__ __align__(16) uint32_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ty = (warp >> 1) * 4 + (lane >> 3);  // row group 0..15: rows ty + 16 i
@@ -164,8 +176,25 @@ minsum_kernel(const __grid_constant__ MsBatch batch, int64_t total_tiles, int ld
         for (int i = 0; i < 8; ++i)
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            acc[i][j] += __vminu2(a[i].x, b[j].x) + __vminu2(a[i].y, b[j].y);
-            acc[i][j] += __vminu2(a[i].z, b[j].z) + __vminu2(a[i].w, b[j].w);
+            if (ENC == ENC_U8_SAD) {
+              // 16 bins: four VABSDIFF4.U8.ACC, |a-b| of 4 byte lanes summed into acc
+              vsad4_acc(acc[i][j], a[i].x, b[j].x);
+              vsad4_acc(acc[i][j], a[i].y, b[j].y);
+              vsad4_acc(acc[i][j], a[i].z, b[j].z);
+              vsad4_acc(acc[i][j], a[i].w, b[j].w);
+            } else if (ENC == ENC_U16_MIN_IMAD) {
+              // 8 bins: four VIMNMX.U16x2 (ALU pipe), adds as IMAD on the FMA pipe
+              uint32_t m0 = __vminu2(a[i].x, b[j].x), m1 = __vminu2(a[i].y, b[j].y);
+              uint32_t m2 = __vminu2(a[i].z, b[j].z), m3 = __vminu2(a[i].w, b[j].w);
+              asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(acc[i][j]) : "r"(m0), "r"(one));
+              asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(acc[i][j]) : "r"(m1), "r"(one));
+              asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(acc[i][j]) : "r"(m2), "r"(one));
+              asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(acc[i][j]) : "r"(m3), "r"(one));
+            } else {
+              // 8 bins: four VIMNMX.U16x2 + two IADD3
+              acc[i][j] += __vminu2(a[i].x, b[j].x) + __vminu2(a[i].y, b[j].y);
+              acc[i][j] += __vminu2(a[i].z, b[j].z) + __vminu2(a[i].w, b[j].w);
+            }
           }
       }
     }
@@ -195,7 +224,7 @@ minsum_kernel(const __grid_constant__ MsBatch batch, int64_t total_tiles, int ld
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             if (nkc[j] < 0) continue;
-            const uint32_t C = (acc[i][j] & 0xffffu) + (acc[i][j] >> 16);
+            const uint32_t C = acc_to_C<ENC>(acc[i][j], nkr[i], nkc[j]);
             add_term(lo, hi, C, (uint32_t)min(nkr[i], nkc[j]));
           }
         }
@@ -214,7 +243,7 @@ minsum_kernel(const __grid_constant__ MsBatch batch, int64_t total_tiles, int ld
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               if (nkr[i] < 0) continue;
-              const uint32_t C = (acc[i][j] & 0xffffu) + (acc[i][j] >> 16);
+              const uint32_t C = acc_to_C<ENC>(acc[i][j], nkr[i], nkc[j]);
               add_term(lo, hi, C, (uint32_t)min(nkr[i], nkc[j]));
             }
           }
@@ -233,7 +262,7 @@ minsum_kernel(const __grid_constant__ MsBatch batch, int64_t total_tiles, int ld
         for (int j = 0; j < 8; ++j) {
           if (nkc[j] < 0) continue;
           const int64_t gc = col0 + tx + 16 * j;
-          const uint32_t C = (acc[i][j] & 0xffffu) + (acc[i][j] >> 16);
+          const uint32_t C = acc_to_C<ENC>(acc[i][j], nkr[i], nkc[j]);
           const int D = min(nkr[i], nkc[j]);
           if (P.num) {
             P.num[gr * P.ld + gc] = (uint16_t)C;
@@ -252,7 +281,20 @@ minsum_kernel(const __grid_constant__ MsBatch batch, int64_t total_tiles, int ld
 
 static int g_num_sms = 0;
 
-sa_status minsum_launch(const std::vector<MsProblem>& probs_in, int ldw, cudaStream_t st,
+template <bool SYM, int ENC>
+static sa_status launch_one(const MsBatch& b, int64_t tiles, int ldw, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    SA_CUDA(cudaFuncSetAttribute(minsum_kernel<SYM, ENC>, cudaFuncAttributeMaxDynamicSharedMemorySize, MS_SMEM));
+    configured = true;
+  }
+  const int64_t grid = tiles < g_num_sms ? tiles : g_num_sms;
+  minsum_kernel<SYM, ENC><<<(unsigned)grid, MS_THREADS, MS_SMEM, st>>>(b, tiles, ldw, 1u);
+  SA_LAUNCHED();
+  return SA_OK;
+}
+
+sa_status minsum_launch(const std::vector<MsProblem>& probs_in, int ldw, int enc, cudaStream_t st,
                         cudaEvent_t ev0, cudaEvent_t ev1) {
   if (ldw % MS_BKW != 0) return fail(SA_E_INVAL, "profile row stride must be a multiple of 64 bins");
   SA_TRY(ensure_recip_tables(st));
@@ -260,8 +302,6 @@ sa_status minsum_launch(const std::vector<MsProblem>& probs_in, int ldw, cudaStr
     int dev = 0;
     SA_CUDA(cudaGetDevice(&dev));
     SA_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-    SA_CUDA(cudaFuncSetAttribute(minsum_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, MS_SMEM));
-    SA_CUDA(cudaFuncSetAttribute(minsum_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, MS_SMEM));
   }
   // split into batches of at most MS_MAXPROB problems of the same symmetry
   std::vector<MsProblem> probs;
@@ -282,14 +322,55 @@ sa_status minsum_launch(const std::vector<MsProblem>& probs_in, int ldw, cudaStr
       tiles += sym ? (int64_t)q.tiles_b * (q.tiles_b + 1) / 2 : ta * q.tiles_b;
       b.p[b.n++] = q;
     }
-    const int64_t grid = tiles < g_num_sms ? tiles : g_num_sms;
-    if (sym)
-      minsum_kernel<true><<<(unsigned)grid, MS_THREADS, MS_SMEM, st>>>(b, tiles, ldw);
-    else
-      minsum_kernel<false><<<(unsigned)grid, MS_THREADS, MS_SMEM, st>>>(b, tiles, ldw);
-    SA_LAUNCHED();
+    sa_status rs;
+    if (enc == ENC_U8_SAD) rs = sym ? launch_one<true, ENC_U8_SAD>(b, tiles, ldw, st)
+                                    : launch_one<false, ENC_U8_SAD>(b, tiles, ldw, st);
+    else if (enc == ENC_U16_MIN_IMAD) rs = sym ? launch_one<true, ENC_U16_MIN_IMAD>(b, tiles, ldw, st)
+                                               : launch_one<false, ENC_U16_MIN_IMAD>(b, tiles, ldw, st);
+    else rs = sym ? launch_one<true, ENC_U16_MIN>(b, tiles, ldw, st) : launch_one<false, ENC_U16_MIN>(b, tiles, ldw, st);
+    if (rs != SA_OK) return rs;
   }
   if (ev1) SA_CUDA(cudaEventRecord(ev1, st));
+  return SA_OK;
+}
+
+// ------------------------------------------------- u16 -> u8 operand rows --
+// The SAD encoding needs every count <= 255; the conversion saturates and
+// reports the largest count so the caller can fall back to the u16 engine.
+__global__ void to_u8_kernel(const uint16_t* __restrict__ p16, int64_t n, int stride16, uint8_t* __restrict__ p8,
+                             int stride8, uint32_t* __restrict__ maxc) {
+  const int chunks = stride8 / 8;
+  uint32_t mx = 0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n * chunks;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = idx / chunks;
+    const int t0 = (int)(idx % chunks) * 8;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (t0 < stride16) v = *reinterpret_cast<const uint4*>(p16 + row * stride16 + t0);
+    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t out[2] = {0, 0};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t lo = w[q] & 0xffffu, hi = w[q] >> 16;
+      mx = max(mx, max(lo, hi));
+      const uint32_t b = min(lo, 255u) | (min(hi, 255u) << 8);
+      out[q >> 1] |= b << (16 * (q & 1));
+    }
+    *reinterpret_cast<uint2*>(p8 + row * stride8 + t0) = make_uint2(out[0], out[1]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(maxc, mx);
+}
+
+sa_status to_u8_launch(const uint16_t* p16, int64_t n, int32_t stride16, int32_t bins, uint8_t* p8, int32_t stride8,
+                       uint32_t* maxc, cudaStream_t st) {
+  (void)bins;
+  if (n <= 0) return SA_OK;
+  const int64_t work = n * (stride8 / 8);
+  const int64_t blocks = (work + 255) / 256;
+  to_u8_kernel<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, st>>>(p16, n, stride16, p8, stride8, maxc);
+  SA_LAUNCHED();
   return SA_OK;
 }
 

@@ -75,14 +75,27 @@ class HotPath:
         return self._out_cache[key]
 
     def step(self, residues: torch.Tensor, offsets: torch.Tensor, n_total: int, first_global: int,
-             debug: bool = False, stream=None) -> StepResult:
+             debug: bool = False, stream=None, events: dict | None = None) -> StepResult:
+        """One pass S1..S5.  ``events``: optional dict of torch.cuda.Event
+        recorded on the launch stream at 'start', 'S1', 'S4' (partition and
+        redistribution done), 'S1b' and 'S5' (timing only)."""
         ctx = self.ctx
+        st = stream if stream is not None else torch.cuda.current_stream()
+
+        def mark(name):
+            if events is not None and name in events:
+                events[name].record(st)
+
+        mark("start")
         prof, nk = B.sa_kmer_profiles(ctx, residues, offsets, self.k, self.alphabet, stream=stream)
+        mark("S1")
         part = B.sa_partition(ctx, self.p, self.kb, prof, nk, offsets, self.bins, n_total, first_global,
                               debug=debug, stream=stream)
         rres, roffs, rgid, rbkt = B.sa_redistribute(ctx, self.p, residues, offsets, first_global, part,
                                                     stream=stream)
+        mark("S4")
         bprof, bnk = B.sa_kmer_profiles(ctx, rres, roffs, self.k, self.alphabet, stream=stream)
+        mark("S1b")
         res = StepResult(prof, nk, part, rres, roffs, rgid, rbkt, bprof, bnk)
         row = 0
         for b in B.owned_buckets(self.p, ctx.nranks, ctx.rank):
@@ -96,4 +109,5 @@ class HotPath:
             res.numerators.append(num)
             res.similarity.append(sim)
             row += n_b
+        mark("S5")
         return res

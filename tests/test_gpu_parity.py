@@ -25,6 +25,15 @@ def ctx():
     return B.Context()
 
 
+@pytest.fixture(params=["auto", "u16", "u16imad"])
+def engine(request, monkeypatch):
+    """Run a test under each min-sum operand encoding: auto
+    picks the uint8 SAD engine when every count is <= 255, u16 / u16imad force
+    the uint16 VIMNMX engines."""
+    monkeypatch.setenv("SA_ENGINE", request.param)
+    return request.param
+
+
 def _rand_set(seed, n, lo=0, hi=420, alphabet=20, dup=0):
     rng = np.random.default_rng(seed)
     seqs = [rng.integers(0, alphabet, size=int(rng.integers(lo, hi + 1))) for _ in range(n)]
@@ -83,7 +92,7 @@ def test_profiles_errors(ctx):
 
 # --------------------------------------------------------------- S2 ------
 @pytest.mark.parametrize("nq,npool,dup", [(300, 200, 0), (129, 257, 5), (1, 1, 0), (5, 700, 0)])
-def test_kmer_rank_random(ctx, nq, npool, dup):
+def test_kmer_rank_random(ctx, engine, nq, npool, dup):
     ds = _rand_set(nq * 1000 + npool, nq + npool, 0, 420, dup=dup)
     res, offs = to_dev(ds)
     P, nk = B.sa_kmer_profiles(ctx, res, offs)
@@ -111,17 +120,42 @@ def test_kmer_rank_empty_pool(ctx):
 
 # --------------------------------------------------------------- S5 ------
 @pytest.mark.parametrize("n,dup,lo", [(300, 0, 0), (257, 20, 0), (128, 0, 2), (1, 0, 5), (2, 0, 0)])
-def test_bucket_similarity_random(ctx, n, dup, lo):
+def test_bucket_similarity_random(ctx, engine, n, dup, lo):
     ds = _rand_set(n * 7 + dup, n, lo, 420, dup=dup)
     res, offs = to_dev(ds)
     P, nk = B.sa_kmer_profiles(ctx, res, offs)
     Po, nko = kmer.profiles(ds.residues, ds.offsets)
     num, sim = B.sa_bucket_similarity(ctx, P, nk)
+    assert ctx.engine() == {"auto": "u8", "u16": "u16", "u16imad": "u16imad"}[engine]
     Co, Fo = partition.bucket_similarity(Po, nko, np.arange(n))
     assert np.array_equal(num.cpu().numpy(), Co)
     s = sim.cpu().numpy()
     assert_rel(s, Fo, 1e-12)
     assert np.array_equal(s, Fo)     # one IEEE RN division on both sides
+
+
+def test_large_counts_fall_back_to_u16(ctx, monkeypatch):
+    """A bin count above 255 (here 298 copies of AAA) cannot use the uint8
+    SAD encoding; the auto engine must detect it and stay exact."""
+    monkeypatch.setenv("SA_ENGINE", "auto")
+    rng = np.random.default_rng(8)
+    seqs = [np.zeros(300, np.uint8), np.zeros(260, np.uint8)] + \
+        [rng.integers(0, 20, size=int(rng.integers(3, 400))) for _ in range(140)]
+    seqs[5] = np.concatenate([np.zeros(280, np.uint8), seqs[5]])
+    ds = from_sequences(seqs)
+    res, offs = to_dev(ds)
+    P, nk = B.sa_kmer_profiles(ctx, res, offs)
+    Po, nko = kmer.profiles(ds.residues, ds.offsets)
+    assert Po.max() > 255
+    num, sim = B.sa_bucket_similarity(ctx, P, nk)
+    assert ctx.engine() == "u16"
+    Co, Fo = partition.bucket_similarity(Po, nko, np.arange(len(seqs)))
+    assert np.array_equal(num.cpu().numpy(), Co)
+    assert np.array_equal(sim.cpu().numpy(), Fo)
+    keys, f64, nm = B.sa_kmer_rank(ctx, P[:50], nk[:50], P, nk, want_numerators=True)
+    assert ctx.engine() == "u16"
+    assert np.array_equal(nm.cpu().numpy(), Co[:50])
+    assert B.keys_to_ints(keys) == kmer.RankSet(Co[:50], kmer.denominator_matrix(nko[:50], nko)).keys
 
 
 # ----------------------------------------------------- S2-S3 partition ---
@@ -134,8 +168,10 @@ def _partition_g1(ctx, c):
     return ds, P, nk, part
 
 
-@pytest.mark.parametrize("c", [1, 2, 5, 3, 4])
-def test_partition_matches_golden(ctx, c):
+@pytest.mark.parametrize("c,eng", [(1, "auto"), (2, "auto"), (5, "auto"), (3, "auto"), (4, "auto"),
+                                   (2, "u16"), (5, "u16imad")])
+def test_partition_matches_golden(ctx, monkeypatch, c, eng):
+    monkeypatch.setenv("SA_ENGINE", eng)
     g, meta = load_golden(c)
     ds, P, nk, part = _partition_g1(ctx, c)
     assert ds.sha256() == meta["dataset_sha256"]
