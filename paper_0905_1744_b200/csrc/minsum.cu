@@ -100,7 +100,41 @@ __device__ __forceinline__ uint32_t acc_to_C(uint32_t acc, int nka, int nkb) {
   return (acc & 0xffffu) + (acc >> 16);                                  // the two u16 lanes
 }
 
-template <bool SYM, int ENC>
+template <int FW>
+__device__ __forceinline__ void load_frag(uint32_t (&f)[FW], const uint32_t* p) {
+  if constexpr (FW == 4) {
+    const uint4 v = *reinterpret_cast<const uint4*>(p);
+    f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w;
+  } else {
+    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    f[0] = v.x; f[1] = v.y;
+  }
+}
+
+// One smem stage of the uint8 SAD engine with FW-word fragments (FW = 4: one
+// LDS.128 = 16 bins per row; FW = 2: LDS.64 = 8 bins) and an UNR-way
+// unrolled k loop.  The w-outer order puts 64 independent accumulators
+// between two updates of the same one.
+template <int FW, int UNR>
+__device__ __forceinline__ void sad_stage(const uint32_t* __restrict__ As, const uint32_t* __restrict__ Bs, int ty,
+                                          int tx, uint32_t (&acc)[8][8]) {
+#pragma unroll UNR
+  for (int kq = 0; kq < MS_BKW / FW; ++kq) {
+    uint32_t a[8][FW], b[8][FW];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) load_frag<FW>(a[i], As + (ty + 16 * i) * MS_LDW + kq * FW);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) load_frag<FW>(b[j], Bs + (tx + 16 * j) * MS_LDW + kq * FW);
+#pragma unroll
+    for (int w = 0; w < FW; ++w)
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) vsad4_acc(acc[i][j], a[i][w], b[j][w]);
+  }
+}
+
+template <bool SYM, int ENC, int VAR>
 __global__ void __launch_bounds__(MS_THREADS, 1)
 minsum_kernel(const __grid_constant__ MsBatch batch, int64_t total_tiles, int ldw, uint32_t one) {
   extern __shared__ __align__(16) uint32_t smem[];
@@ -165,6 +199,10 @@ minsum_kernel(const __grid_constant__ MsBatch batch, int64_t total_tiles, int ld
       }
       const uint32_t* As = smem + (kc % MS_STAGES) * STAGE_W;
       const uint32_t* Bs = As + MS_BM * MS_LDW;
+      if (ENC == ENC_U8_SAD && VAR != 0) {
+        sad_stage<(VAR == 1 ? 4 : 2), (VAR == 3 ? 1 : 2)>(As, Bs, ty, tx, acc);
+        continue;
+      }
 #pragma unroll
       for (int kq = 0; kq < MS_BKW / 4; ++kq) {
         uint4 a[8], b[8];
@@ -281,17 +319,40 @@ minsum_kernel(const __grid_constant__ MsBatch batch, int64_t total_tiles, int ld
 
 static int g_num_sms = 0;
 
-template <bool SYM, int ENC>
+template <bool SYM, int ENC, int VAR>
 static sa_status launch_one(const MsBatch& b, int64_t tiles, int ldw, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    SA_CUDA(cudaFuncSetAttribute(minsum_kernel<SYM, ENC>, cudaFuncAttributeMaxDynamicSharedMemorySize, MS_SMEM));
+    SA_CUDA(cudaFuncSetAttribute(minsum_kernel<SYM, ENC, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, MS_SMEM));
     configured = true;
   }
   const int64_t grid = tiles < g_num_sms ? tiles : g_num_sms;
-  minsum_kernel<SYM, ENC><<<(unsigned)grid, MS_THREADS, MS_SMEM, st>>>(b, tiles, ldw, 1u);
+  minsum_kernel<SYM, ENC, VAR><<<(unsigned)grid, MS_THREADS, MS_SMEM, st>>>(b, tiles, ldw, 1u);
   SA_LAUNCHED();
   return SA_OK;
+}
+
+// SAD-engine inner-loop variant (SA_K2_VARIANT, default 0): 0 = uint4
+// fragments, fully unrolled stage; 1 = uint4, 2-way unroll; 2 = uint2, 2-way;
+// 3 = uint2, no unroll.
+static int sad_variant() {
+  const char* e = getenv("SA_K2_VARIANT");
+  const int v = e ? atoi(e) : 0;
+  return (v >= 0 && v <= 3) ? v : 0;
+}
+
+template <bool SYM>
+static sa_status launch_enc(const MsBatch& b, int64_t tiles, int ldw, int enc, cudaStream_t st) {
+  if (enc == ENC_U8_SAD) {
+    switch (sad_variant()) {
+      case 1: return launch_one<SYM, ENC_U8_SAD, 1>(b, tiles, ldw, st);
+      case 2: return launch_one<SYM, ENC_U8_SAD, 2>(b, tiles, ldw, st);
+      case 3: return launch_one<SYM, ENC_U8_SAD, 3>(b, tiles, ldw, st);
+      default: return launch_one<SYM, ENC_U8_SAD, 0>(b, tiles, ldw, st);
+    }
+  }
+  if (enc == ENC_U16_MIN_IMAD) return launch_one<SYM, ENC_U16_MIN_IMAD, 0>(b, tiles, ldw, st);
+  return launch_one<SYM, ENC_U16_MIN, 0>(b, tiles, ldw, st);
 }
 
 sa_status minsum_launch(const std::vector<MsProblem>& probs_in, int ldw, int enc, cudaStream_t st,
@@ -322,12 +383,7 @@ sa_status minsum_launch(const std::vector<MsProblem>& probs_in, int ldw, int enc
       tiles += sym ? (int64_t)q.tiles_b * (q.tiles_b + 1) / 2 : ta * q.tiles_b;
       b.p[b.n++] = q;
     }
-    sa_status rs;
-    if (enc == ENC_U8_SAD) rs = sym ? launch_one<true, ENC_U8_SAD>(b, tiles, ldw, st)
-                                    : launch_one<false, ENC_U8_SAD>(b, tiles, ldw, st);
-    else if (enc == ENC_U16_MIN_IMAD) rs = sym ? launch_one<true, ENC_U16_MIN_IMAD>(b, tiles, ldw, st)
-                                               : launch_one<false, ENC_U16_MIN_IMAD>(b, tiles, ldw, st);
-    else rs = sym ? launch_one<true, ENC_U16_MIN>(b, tiles, ldw, st) : launch_one<false, ENC_U16_MIN>(b, tiles, ldw, st);
+    const sa_status rs = sym ? launch_enc<true>(b, tiles, ldw, enc, st) : launch_enc<false>(b, tiles, ldw, enc, st);
     if (rs != SA_OK) return rs;
   }
   if (ev1) SA_CUDA(cudaEventRecord(ev1, st));

@@ -1,0 +1,73 @@
+"""Multi-rank path of sa_partition / sa_redistribute / S5 on ONE GPU: G ranks
+as threads with their own sa_ctx and a host-barrier communicator
+(tests/threadcomm.py).  Results must not depend on G: the
+partition of G ranks equals the single-rank partition and the oracle's."""
+import numpy as np
+import pytest
+import torch
+
+from paper_0905_1744_b200 import binding as B
+from paper_0905_1744_b200.pipeline import HotPath, shard_range
+from sa_synth.generator import CONFIGS, generate
+
+from .gpu_util import load_golden, require_gpu
+from .threadcomm import run_ranks
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(G, cfg, ds):
+    def fn(rank, ctx):
+        first, last = shard_range(ds.n, cfg.p, G, rank)
+        r0, r1 = int(ds.offsets[first]), int(ds.offsets[last])
+        res = torch.from_numpy(ds.residues[r0:r1].copy()).cuda()
+        offs = torch.from_numpy(ds.offsets[first:last + 1] - ds.offsets[first]).cuda()
+        out = HotPath(ctx, cfg.p, cfg.samples_per_block).step(res, offs, ds.n, first, debug=True)
+        torch.cuda.synchronize()
+        return {
+            "first": first,
+            "bucket_of": out.part.bucket_of.cpu().numpy(),
+            "pivots": B.pivot_global_idx(out.part.pivots).cpu().numpy(),
+            "counts": out.part.counts.copy(),
+            "gid": out.recv_global_idx.cpu().numpy(),
+            "bkt": out.recv_bucket.cpu().numpy(),
+            "res": out.recv_residues.cpu().numpy(), "offs": out.recv_offsets.cpu().numpy(),
+            "sample_idx": out.part.debug["sample_idx"].cpu().numpy(),
+            "candidates": out.part.debug["candidates"].cpu().numpy(),
+            "num": [(b, n, x.view(torch.int16).cpu().numpy().view(np.uint16) if x is not None else None)
+                    for (b, _, n), x in zip(out.buckets, out.numerators)],
+            "sim": [x.cpu().numpy() if x is not None else None for x in out.similarity],
+        }
+    return run_ranks(G, fn)
+
+
+@pytest.mark.parametrize("c,Gs", [(2, (2, 4, 8)), (1, (2, 4))])
+def test_rank_count_invariance(c, Gs):
+    require_gpu()
+    cfg = CONFIGS[c]
+    ds = generate(cfg)
+    g, meta = load_golden(c)
+    ref = _run(1, cfg, ds)[0]
+    assert np.array_equal(ref["bucket_of"], g["bucket_of"])
+    for G in Gs:
+        outs = _run(G, cfg, ds)
+        bucket_of = np.concatenate([o["bucket_of"] for o in outs])
+        assert np.array_equal(bucket_of, g["bucket_of"]), G                 # S3c, every rank's shard
+        for o in outs:
+            assert np.array_equal(o["pivots"], g["pivots"])                 # identical pivots everywhere (O2)
+            assert np.array_equal(o["sample_idx"], g["sample_idx"])         # S2c allgather order
+            assert np.array_equal(o["candidates"], g["candidates"])         # S3b allgather order
+            assert np.array_equal(o["counts"], outs[0]["counts"])           # C3 matrix
+        # S4: rank r holds its buckets in (bucket, global id) order, residues intact
+        gid = np.concatenate([o["gid"] for o in outs])
+        assert np.array_equal(gid, ref["gid"])
+        assert np.array_equal(np.concatenate([o["bkt"] for o in outs]), ref["bkt"])
+        for o in outs:
+            for j, i in enumerate(o["gid"]):
+                assert np.array_equal(o["res"][o["offs"][j]:o["offs"][j + 1]], ds.seq(int(i)))
+        # S5 matrices identical to the single-rank run
+        ref_num = {b: x for b, n, x in ref["num"]}
+        ref_sim = {b: x for (b, n, _), x in zip(ref["num"], ref["sim"])}
+        for o in outs:
+            for (b, n, x), s in zip(o["num"], o["sim"]):
+                assert np.array_equal(x, ref_num[b]) and np.array_equal(s, ref_sim[b])
