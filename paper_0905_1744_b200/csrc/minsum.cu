@@ -18,6 +18,10 @@
 // row stride (36 words) that makes every LDS.128 conflict-free.  The grid is
 // persistent: one CTA per SM strides over a flat list of tiles of up to 16
 // problems (all local blocks of S2a, all buckets of S5).
+#include <cstring>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 
 namespace sa {
@@ -134,35 +138,188 @@ __device__ __forceinline__ void sad_stage(const uint32_t* __restrict__ As, const
   }
 }
 
+template <int ENC>
+__device__ __forceinline__ void compute_stage_u4(const uint32_t* __restrict__ As, const uint32_t* __restrict__ Bs,
+                                                 int ty, int tx, uint32_t (&acc)[8][8], uint32_t one);
+
+// One smem stage (MS_BKW words of 128 A rows and 128 B rows) into the 8 x 8
+// register block of packed accumulators.
+template <int ENC, int VAR>
+__device__ __forceinline__ void compute_stage(const uint32_t* __restrict__ As, const uint32_t* __restrict__ Bs,
+                                              int ty, int tx, uint32_t (&acc)[8][8], uint32_t one) {
+  if constexpr (ENC == ENC_U8_SAD && VAR != 0) {
+    sad_stage<(VAR == 1 ? 4 : 2), (VAR == 3 ? 1 : 2)>(As, Bs, ty, tx, acc);
+  } else {
+    compute_stage_u4<ENC>(As, Bs, ty, tx, acc, one);
+  }
+}
+
+template <int ENC>
+__device__ __forceinline__ void compute_stage_u4(const uint32_t* __restrict__ As, const uint32_t* __restrict__ Bs,
+                                                 int ty, int tx, uint32_t (&acc)[8][8], uint32_t one) {
+#pragma unroll
+  for (int kq = 0; kq < MS_BKW / 4; ++kq) {
+    uint4 a[8], b[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const uint4*>(As + (ty + 16 * i) * MS_LDW + kq * 4);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) b[j] = *reinterpret_cast<const uint4*>(Bs + (tx + 16 * j) * MS_LDW + kq * 4);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if constexpr (ENC == ENC_U8_SAD) {
+          // 16 bins: four VABSDIFF4.U8.ACC, |a-b| of 4 byte lanes summed into acc
+          vsad4_acc(acc[i][j], a[i].x, b[j].x);
+          vsad4_acc(acc[i][j], a[i].y, b[j].y);
+          vsad4_acc(acc[i][j], a[i].z, b[j].z);
+          vsad4_acc(acc[i][j], a[i].w, b[j].w);
+        } else if constexpr (ENC == ENC_U16_MIN_IMAD) {
+          // 8 bins: four VIMNMX.U16x2 (ALU pipe), adds as IMAD on the FMA pipe
+          uint32_t m0 = __vminu2(a[i].x, b[j].x), m1 = __vminu2(a[i].y, b[j].y);
+          uint32_t m2 = __vminu2(a[i].z, b[j].z), m3 = __vminu2(a[i].w, b[j].w);
+          asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(acc[i][j]) : "r"(m0), "r"(one));
+          asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(acc[i][j]) : "r"(m1), "r"(one));
+          asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(acc[i][j]) : "r"(m2), "r"(one));
+          asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(acc[i][j]) : "r"(m3), "r"(one));
+        } else {
+          // 8 bins: four VIMNMX.U16x2 + two IADD3
+          acc[i][j] += __vminu2(a[i].x, b[j].x) + __vminu2(a[i].y, b[j].y);
+          acc[i][j] += __vminu2(a[i].z, b[j].z) + __vminu2(a[i].w, b[j].w);
+        }
+      }
+  }
+}
+
+struct TileInfo {
+  int pi, ti, tj, row0, col0, ra, rb;
+};
+
+template <bool SYM>
+__device__ __forceinline__ TileInfo decode_tile(const MsBatch& batch, int64_t tile) {
+  TileInfo T;
+  int pi = 0;
+  while (pi + 1 < batch.n && batch.p[pi + 1].tile_begin <= tile) ++pi;
+  const MsProblem& P = batch.p[pi];
+  int64_t t = tile - P.tile_begin;
+  if (SYM) {
+    const int nt = P.tiles_b;
+    int ti = 0;
+    while (t >= nt - ti) { t -= nt - ti; ++ti; }
+    T.ti = ti;
+    T.tj = ti + (int)t;
+  } else {
+    T.ti = (int)(t / P.tiles_b);
+    T.tj = (int)(t % P.tiles_b);
+  }
+  T.pi = pi;
+  T.row0 = T.ti * MS_BM;
+  T.col0 = T.tj * MS_BM;
+  T.ra = min(MS_BM, P.na - T.row0);
+  T.rb = min(MS_BM, P.nb - T.col0);
+  return T;
+}
+
+// Fused epilogue of one tile: exact-rank keys and / or the C, F matrices.
+template <bool SYM, int ENC>
+__device__ __forceinline__ void tile_epilogue(const MsProblem& P, const TileInfo& T, int ty, int tx, int lane,
+                                              const uint32_t (&acc)[8][8]) {
+  const bool offdiag = SYM && (T.ti != T.tj);
+  const int row0 = T.row0, col0 = T.col0;
+  int nkr[8], nkc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = ty + 16 * i;
+    nkr[i] = (r < T.ra) ? P.nkA[row0 + r] : -1;
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int c = tx + 16 * j;
+    nkc[j] = (c < T.rb) ? P.nkB[col0 + c] : -1;
+  }
+  if (P.keyA) {
+    // row sums: key_i += sum_j floor(C_ij 2^64 / D_ij)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint64_t lo = 0;
+      uint32_t hi = 0;
+      if (nkr[i] >= 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (nkc[j] < 0) continue;
+          const uint32_t C = acc_to_C<ENC>(acc[i][j], nkr[i], nkc[j]);
+          add_term(lo, hi, C, (uint32_t)min(nkr[i], nkc[j]));
+        }
+      }
+      shfl_add(lo, hi, 1);
+      shfl_add(lo, hi, 2);
+      shfl_add(lo, hi, 4);
+      if ((lane & 7) == 0 && nkr[i] >= 0 && (lo | hi)) atomic_add_key(P.keyA + row0 + ty + 16 * i, lo, hi);
+    }
+    if (offdiag && P.keyB) {
+      // column sums: the mirrored pairs (j, i) of an off-diagonal tile
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        uint64_t lo = 0;
+        uint32_t hi = 0;
+        if (nkc[j] >= 0) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (nkr[i] < 0) continue;
+            const uint32_t C = acc_to_C<ENC>(acc[i][j], nkr[i], nkc[j]);
+            add_term(lo, hi, C, (uint32_t)min(nkr[i], nkc[j]));
+          }
+        }
+        shfl_add(lo, hi, 8);
+        shfl_add(lo, hi, 16);
+        if (lane < 8 && nkc[j] >= 0 && (lo | hi)) atomic_add_key(P.keyB + col0 + tx + 16 * j, lo, hi);
+      }
+    }
+  }
+  if (P.num || P.sim) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (nkr[i] < 0) continue;
+      const int64_t gr = row0 + ty + 16 * i;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (nkc[j] < 0) continue;
+        const int64_t gc = col0 + tx + 16 * j;
+        const uint32_t C = acc_to_C<ENC>(acc[i][j], nkr[i], nkc[j]);
+        const int D = min(nkr[i], nkc[j]);
+        if (P.num) {
+          P.num[gr * P.ld + gc] = (uint16_t)C;
+          if (offdiag) P.num[gc * P.ld + gr] = (uint16_t)C;
+        }
+        if (P.sim) {
+          const double F = D > 0 ? __ddiv_rn((double)C, (double)D) : 0.0;
+          P.sim[gr * P.ld + gc] = F;
+          if (offdiag) P.sim[gc * P.ld + gr] = F;
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------- engine A: cp.async ring ---
+// Every thread copies 8 x 16 B per stage; a CTA-wide barrier per stage.
 template <bool SYM, int ENC, int VAR>
 __global__ void __launch_bounds__(MS_THREADS, 1)
-minsum_kernel(const __grid_constant__ MsBatch batch, int64_t total_tiles, int ldw, uint32_t one) {
+minsum_kernel(const __grid_constant__ MsBatch batch, int64_t total_tiles, int ldw, uint32_t one,
+              const uint32_t* __restrict__ zero_row) {
   extern __shared__ __align__(16) uint32_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ty = (warp >> 1) * 4 + (lane >> 3);  // row group 0..15: rows ty + 16 i
   const int tx = (warp & 1) * 8 + (lane & 7);     // col group 0..15: cols tx + 16 j
   const int nK = ldw / MS_BKW;
   constexpr int STAGE_W = 2 * MS_BM * MS_LDW;
+  (void)zero_row;
 
   for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-    int pi = 0;
-    while (pi + 1 < batch.n && batch.p[pi + 1].tile_begin <= tile) ++pi;
-    const MsProblem& P = batch.p[pi];
-    int64_t t = tile - P.tile_begin;
-    int ti, tj;
-    if (SYM) {
-      const int T = P.tiles_b;
-      ti = 0;
-      while (t >= T - ti) { t -= T - ti; ++ti; }
-      tj = ti + (int)t;
-    } else {
-      ti = (int)(t / P.tiles_b);
-      tj = (int)(t % P.tiles_b);
-    }
-    const int row0 = ti * MS_BM, col0 = tj * MS_BM;
-    const int ra = min(MS_BM, P.na - row0), rb = min(MS_BM, P.nb - col0);
-    const uint32_t* Ag = P.A + (int64_t)row0 * ldw;
-    const uint32_t* Bg = P.B + (int64_t)col0 * ldw;
+    const TileInfo T = decode_tile<SYM>(batch, tile);
+    const MsProblem& P = batch.p[T.pi];
+    const uint32_t* Ag = P.A + (int64_t)T.row0 * ldw;
+    const uint32_t* Bg = P.B + (int64_t)T.col0 * ldw;
 
     auto load = [&](int stage, int kc) {
       uint32_t* sb = smem + stage * STAGE_W;
@@ -172,7 +329,7 @@ minsum_kernel(const __grid_constant__ MsBatch batch, int64_t total_tiles, int ld
         const int r = c >> 3, ch = c & 7;
         const bool isA = r < MS_BM;
         const int rr = isA ? r : r - MS_BM;
-        const bool valid = rr < (isA ? ra : rb);
+        const bool valid = rr < (isA ? T.ra : T.rb);
         const uint32_t* g = (isA ? Ag : Bg) + (int64_t)(valid ? rr : 0) * ldw + kc * MS_BKW + ch * 4;
         cp_async16(smem_u32(sb + r * MS_LDW + ch * 4), g, valid ? 16 : 0);
       }
@@ -198,136 +355,232 @@ minsum_kernel(const __grid_constant__ MsBatch batch, int64_t total_tiles, int ld
         cp_commit();
       }
       const uint32_t* As = smem + (kc % MS_STAGES) * STAGE_W;
-      const uint32_t* Bs = As + MS_BM * MS_LDW;
-      if (ENC == ENC_U8_SAD && VAR != 0) {
-        sad_stage<(VAR == 1 ? 4 : 2), (VAR == 3 ? 1 : 2)>(As, Bs, ty, tx, acc);
-        continue;
-      }
+      compute_stage<ENC, VAR>(As, As + MS_BM * MS_LDW, ty, tx, acc, one);
+    }
+    __syncthreads();   // smem is reloaded by the next tile
+    tile_epilogue<SYM, ENC>(P, T, ty, tx, lane, acc);
+  }
+}
+
+// ------------------------------------------- engine B: TMA + mbarrier ring --
+// One elected thread (warp 0, lane 0) streams the 128-row A and B boxes of
+// every stage of every tile of this CTA with two TMA tensor loads
+// (cp.async.bulk.tensor.2d, SWIZZLE_128B, rows past the end zero-filled by
+// the TMA unit), MS_TMA_STAGES - 2 stages ahead and across tile boundaries
+// (the next tile's first stages land during this tile's epilogue).  Each warp
+// waits on the stage's "full" mbarrier (TMA transaction count) and releases
+// it on the stage's "empty" mbarrier: no CTA-wide barrier in the main loop.
+// The 128-byte swizzle replaces the padded rows of engine A: reading 16-byte
+// chunk c of row r at chunk position c ^ (r & 7) keeps every fragment load
+// bank-conflict-free.
+constexpr int MS_TMA_STAGES = 6;
+constexpr int MS_TMA_ROW_W = MS_BKW;                       // 32 words = 128 B per row per stage
+constexpr int MS_TMA_STAGE_W = 2 * MS_BM * MS_TMA_ROW_W;   // 8192 words = 32 KB
+constexpr int MS_TMA_SMEM = MS_TMA_STAGES * MS_TMA_STAGE_W * 4 + 1024 + 2 * MS_TMA_STAGES * 8;
+
+struct alignas(64) MsMaps {
+  CUtensorMap m[2 * MS_MAXPROB];   // problem p: m[2p] = A rows, m[2p+1] = B rows
+};
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// word pointer of 16-byte chunk c of row r in a SWIZZLE_128B box of 128-byte rows
+__device__ __forceinline__ const uint32_t* swz(const uint32_t* base, int r, int c) {
+  return base + r * MS_TMA_ROW_W + ((c ^ (r & 7)) << 2);
+}
+
+template <int ENC, int FW>
+__device__ __forceinline__ void compute_stage_swz(const uint32_t* __restrict__ As, const uint32_t* __restrict__ Bs,
+                                                  int ty, int tx, uint32_t (&acc)[8][8], uint32_t one) {
 #pragma unroll
-      for (int kq = 0; kq < MS_BKW / 4; ++kq) {
-        uint4 a[8], b[8];
+  for (int kq = 0; kq < MS_BKW / FW; ++kq) {
+    const int o = kq * FW;
+    uint32_t a[8][FW], b[8][FW];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const uint4*>(As + (ty + 16 * i) * MS_LDW + kq * 4);
+    for (int i = 0; i < 8; ++i) load_frag<FW>(a[i], swz(As, ty + 16 * i, o >> 2) + (o & 3));
 #pragma unroll
-        for (int j = 0; j < 8; ++j) b[j] = *reinterpret_cast<const uint4*>(Bs + (tx + 16 * j) * MS_LDW + kq * 4);
+    for (int j = 0; j < 8; ++j) load_frag<FW>(b[j], swz(Bs, tx + 16 * j, o >> 2) + (o & 3));
+    if constexpr (ENC == ENC_U8_SAD) {
+#pragma unroll
+      for (int w = 0; w < FW; ++w)
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) vsad4_acc(acc[i][j], a[i][w], b[j][w]);
+    } else {
+#pragma unroll
+      for (int w = 0; w < FW; w += 2)
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            if (ENC == ENC_U8_SAD) {
-              // 16 bins: four VABSDIFF4.U8.ACC, |a-b| of 4 byte lanes summed into acc
-              vsad4_acc(acc[i][j], a[i].x, b[j].x);
-              vsad4_acc(acc[i][j], a[i].y, b[j].y);
-              vsad4_acc(acc[i][j], a[i].z, b[j].z);
-              vsad4_acc(acc[i][j], a[i].w, b[j].w);
-            } else if (ENC == ENC_U16_MIN_IMAD) {
-              // 8 bins: four VIMNMX.U16x2 (ALU pipe), adds as IMAD on the FMA pipe
-              uint32_t m0 = __vminu2(a[i].x, b[j].x), m1 = __vminu2(a[i].y, b[j].y);
-              uint32_t m2 = __vminu2(a[i].z, b[j].z), m3 = __vminu2(a[i].w, b[j].w);
+            const uint32_t m0 = __vminu2(a[i][w], b[j][w]), m1 = __vminu2(a[i][w + 1], b[j][w + 1]);
+            if constexpr (ENC == ENC_U16_MIN_IMAD) {
               asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(acc[i][j]) : "r"(m0), "r"(one));
               asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(acc[i][j]) : "r"(m1), "r"(one));
-              asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(acc[i][j]) : "r"(m2), "r"(one));
-              asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(acc[i][j]) : "r"(m3), "r"(one));
             } else {
-              // 8 bins: four VIMNMX.U16x2 + two IADD3
-              acc[i][j] += __vminu2(a[i].x, b[j].x) + __vminu2(a[i].y, b[j].y);
-              acc[i][j] += __vminu2(a[i].z, b[j].z) + __vminu2(a[i].w, b[j].w);
+              acc[i][j] += m0 + m1;
             }
           }
-      }
-    }
-    __syncthreads();   // smem is reloaded by the next tile
-
-    // ------------------------------------------------------------ epilogue
-    const bool offdiag = SYM && (ti != tj);
-    int nkr[8], nkc[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int r = ty + 16 * i;
-      nkr[i] = (r < ra) ? P.nkA[row0 + r] : -1;
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int c = tx + 16 * j;
-      nkc[j] = (c < rb) ? P.nkB[col0 + c] : -1;
-    }
-
-    if (P.keyA) {
-      // row sums: key_i += sum_j floor(C_ij 2^64 / D_ij)
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        uint64_t lo = 0;
-        uint32_t hi = 0;
-        if (nkr[i] >= 0) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (nkc[j] < 0) continue;
-            const uint32_t C = acc_to_C<ENC>(acc[i][j], nkr[i], nkc[j]);
-            add_term(lo, hi, C, (uint32_t)min(nkr[i], nkc[j]));
-          }
-        }
-        shfl_add(lo, hi, 1);
-        shfl_add(lo, hi, 2);
-        shfl_add(lo, hi, 4);
-        if ((lane & 7) == 0 && nkr[i] >= 0 && (lo | hi)) atomic_add_key(P.keyA + row0 + ty + 16 * i, lo, hi);
-      }
-      if (offdiag && P.keyB) {
-        // column sums: the mirrored pairs (j, i) of an off-diagonal tile
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          uint64_t lo = 0;
-          uint32_t hi = 0;
-          if (nkc[j] >= 0) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              if (nkr[i] < 0) continue;
-              const uint32_t C = acc_to_C<ENC>(acc[i][j], nkr[i], nkc[j]);
-              add_term(lo, hi, C, (uint32_t)min(nkr[i], nkc[j]));
-            }
-          }
-          shfl_add(lo, hi, 8);
-          shfl_add(lo, hi, 16);
-          if (lane < 8 && nkc[j] >= 0 && (lo | hi)) atomic_add_key(P.keyB + col0 + tx + 16 * j, lo, hi);
-        }
-      }
-    }
-    if (P.num || P.sim) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        if (nkr[i] < 0) continue;
-        const int64_t gr = row0 + ty + 16 * i;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (nkc[j] < 0) continue;
-          const int64_t gc = col0 + tx + 16 * j;
-          const uint32_t C = acc_to_C<ENC>(acc[i][j], nkr[i], nkc[j]);
-          const int D = min(nkr[i], nkc[j]);
-          if (P.num) {
-            P.num[gr * P.ld + gc] = (uint16_t)C;
-            if (offdiag) P.num[gc * P.ld + gr] = (uint16_t)C;
-          }
-          if (P.sim) {
-            const double F = D > 0 ? __ddiv_rn((double)C, (double)D) : 0.0;
-            P.sim[gr * P.ld + gc] = F;
-            if (offdiag) P.sim[gc * P.ld + gr] = F;
-          }
-        }
-      }
     }
   }
 }
 
+template <bool SYM, int ENC, int VAR>
+__global__ void __launch_bounds__(MS_THREADS, 1)
+minsum_tma_kernel(const __grid_constant__ MsBatch batch, const __grid_constant__ MsMaps maps, int64_t total_tiles,
+                  int ldw, uint32_t one) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const uint32_t base_s = (smem_u32(smem_raw) + 1023u) & ~1023u;     // SWIZZLE_128B wants 1 KB alignment
+  uint32_t* smem = reinterpret_cast<uint32_t*>(smem_raw + (base_s - smem_u32(smem_raw)));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + MS_TMA_STAGES * MS_TMA_STAGE_W);
+  uint64_t* empty = full + MS_TMA_STAGES;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ty = (warp >> 1) * 4 + (lane >> 3);
+  const int tx = (warp & 1) * 8 + (lane & 7);
+  const int nK = ldw / MS_BKW;
+  if (tid == 0) {
+    for (int s = 0; s < MS_TMA_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], MS_THREADS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int64_t my_tiles = total_tiles > blockIdx.x ? (total_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t nstages = my_tiles * nK;
+  const bool producer = (tid == 0);
+  int64_t g_load = 0, ld_tile = blockIdx.x;
+  int ld_kc = 0;
+  TileInfo LT{};
+  if (producer && my_tiles) LT = decode_tile<SYM>(batch, ld_tile);
+  auto produce = [&]() {   // one thread: stage g_load into slot g_load % S
+    const int slot = (int)(g_load % MS_TMA_STAGES);
+    if (g_load >= MS_TMA_STAGES) mbar_wait(&empty[slot], (uint32_t)(((g_load / MS_TMA_STAGES) - 1) & 1));
+    mbar_arrive_tx(&full[slot], MS_TMA_STAGE_W * 4);
+    const uint32_t dst = smem_u32(smem + slot * MS_TMA_STAGE_W);
+    tma_load_2d(dst, &maps.m[2 * LT.pi], ld_kc * MS_BKW, LT.row0, &full[slot]);
+    tma_load_2d(dst + MS_BM * MS_TMA_ROW_W * 4, &maps.m[2 * LT.pi + 1], ld_kc * MS_BKW, LT.col0, &full[slot]);
+    ++g_load;
+    if (++ld_kc == nK) {
+      ld_kc = 0;
+      ld_tile += gridDim.x;
+      if (ld_tile < total_tiles) LT = decode_tile<SYM>(batch, ld_tile);
+    }
+  };
+  if (producer)
+    while (g_load < nstages && g_load < MS_TMA_STAGES - 2) produce();
+
+  int64_t g_use = 0;
+  for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    const TileInfo T = decode_tile<SYM>(batch, tile);
+    const MsProblem& P = batch.p[T.pi];
+    uint32_t acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = 0u;
+    for (int kc = 0; kc < nK; ++kc, ++g_use) {
+      if (producer && g_load < nstages) produce();
+      const int slot = (int)(g_use % MS_TMA_STAGES);
+      mbar_wait(&full[slot], (uint32_t)((g_use / MS_TMA_STAGES) & 1));
+      const uint32_t* As = smem + slot * MS_TMA_STAGE_W;
+      compute_stage_swz<ENC, (ENC == ENC_U8_SAD && VAR >= 2) ? 2 : 4>(As, As + MS_BM * MS_TMA_ROW_W, ty, tx, acc,
+                                                                       one);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+    tile_epilogue<SYM, ENC>(P, T, ty, tx, lane, acc);
+  }
+}
+
 static int g_num_sms = 0;
+
+// Pipeline of the engine (SA_K2_PIPE): "tma" (default) = TMA tensor loads +
+// mbarrier ring (engine B), "cpasync" = per-thread cp.async + CTA barrier per
+// stage (engine A).
+static bool use_tma_pipe() {
+  const char* e = getenv("SA_K2_PIPE");
+  return !(e && !strcmp(e, "cpasync"));
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+// 2-D map over `rows` rows of ldw 32-bit words: boxes of 32 words x 128 rows,
+// 128-byte swizzle, rows past the end read as zeros.
+static sa_status encode_rows_map(CUtensorMap* m, const uint32_t* base, int64_t rows, int ldw) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return fail(SA_E_CUDA, "cuTensorMapEncodeTiled is unavailable");
+  const cuuint64_t dims[2] = {(cuuint64_t)ldw, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ldw * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)MS_BKW, (cuuint32_t)MS_BM};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(base), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SA_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return SA_OK;
+}
 
 template <bool SYM, int ENC, int VAR>
 static sa_status launch_one(const MsBatch& b, int64_t tiles, int ldw, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
     SA_CUDA(cudaFuncSetAttribute(minsum_kernel<SYM, ENC, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, MS_SMEM));
+    SA_CUDA(cudaFuncSetAttribute(minsum_tma_kernel<SYM, ENC, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 MS_TMA_SMEM));
     configured = true;
   }
   const int64_t grid = tiles < g_num_sms ? tiles : g_num_sms;
-  minsum_kernel<SYM, ENC, VAR><<<(unsigned)grid, MS_THREADS, MS_SMEM, st>>>(b, tiles, ldw, 1u);
+  if (use_tma_pipe()) {
+    MsMaps maps;
+    std::memset(&maps, 0, sizeof maps);
+    for (int p = 0; p < b.n; ++p) {
+      SA_TRY(encode_rows_map(&maps.m[2 * p], b.p[p].A, b.p[p].na, ldw));
+      SA_TRY(encode_rows_map(&maps.m[2 * p + 1], b.p[p].B, b.p[p].nb, ldw));
+    }
+    minsum_tma_kernel<SYM, ENC, VAR><<<(unsigned)grid, MS_THREADS, MS_TMA_SMEM, st>>>(b, maps, tiles, ldw, 1u);
+  } else {
+    minsum_kernel<SYM, ENC, VAR><<<(unsigned)grid, MS_THREADS, MS_SMEM, st>>>(b, tiles, ldw, 1u, nullptr);
+  }
   SA_LAUNCHED();
   return SA_OK;
 }
