@@ -201,6 +201,17 @@ sa_status sa_ctx_create(int cuda_device, sa_ctx** out) {
   cudaDeviceProp prop;
   SA_CUDA(cudaGetDeviceProperties(&prop, cuda_device));
   if (prop.major != 10) return fail(SA_E_CUDA, "libsa is built for sm_100a; device is sm_%d%d", prop.major, prop.minor);
+  // Scratch comes from the device's stream-ordered pool; keep freed memory in
+  // the pool instead of returning it to the driver at every synchronisation,
+  // so steady-state calls never re-map device memory.
+  {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, cuda_device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+  }
   sa_ctx* c = new sa_ctx();
   c->device = cuda_device;
   for (int i = 0; i < 2 * SA_PHASE_COUNT; ++i) {

@@ -75,10 +75,13 @@ class HotPath:
         return self._out_cache[key]
 
     def step(self, residues: torch.Tensor, offsets: torch.Tensor, n_total: int, first_global: int,
-             debug: bool = False, stream=None, events: dict | None = None) -> StepResult:
+             debug: bool = False, stream=None, events: dict | None = None, on_bucket=None) -> StepResult:
         """One pass S1..S5.  ``events``: optional dict of torch.cuda.Event
         recorded on the launch stream at 'start', 'S1', 'S4' (partition and
-        redistribution done), 'S1b' and 'S5' (timing only)."""
+        redistribution done), 'S1b' and 'S5' (timing only).  ``on_bucket(b,
+        numerators, similarity)`` is called right after bucket b's S5 launch
+        is enqueued (e.g. to start its device-to-host copy on another stream
+        while the next bucket computes)."""
         ctx = self.ctx
         st = stream if stream is not None else torch.cuda.current_stream()
 
@@ -105,6 +108,8 @@ class HotPath:
                 B.sa_bucket_similarity(ctx, bprof[row:row + n_b], bnk[row:row + n_b], self.bins,
                                        want_numerators=self.want_num, want_similarity=self.want_sim,
                                        numerators=num, similarity=sim, stream=stream)
+                if on_bucket is not None:
+                    on_bucket(b, num, sim)
             res.buckets.append((b, row, n_b))
             res.numerators.append(num)
             res.similarity.append(sim)
