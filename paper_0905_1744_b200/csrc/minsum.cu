@@ -221,20 +221,21 @@ __device__ __forceinline__ TileInfo decode_tile(const MsBatch& batch, int64_t ti
 }
 
 // Fused epilogue of one tile: exact-rank keys and / or the C, F matrices.
-template <bool SYM, int ENC>
+template <bool SYM, int ENC, int TN = 8>
 __device__ __forceinline__ void tile_epilogue(const MsProblem& P, const TileInfo& T, int ty, int tx, int lane,
-                                              const uint32_t (&acc)[8][8]) {
+                                              const uint32_t (&acc)[8][TN]) {
+  constexpr int CS = MS_BM / TN;   // column stride of a thread's TN columns
   const bool offdiag = SYM && (T.ti != T.tj);
   const int row0 = T.row0, col0 = T.col0;
-  int nkr[8], nkc[8];
+  int nkr[8], nkc[TN];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int r = ty + 16 * i;
     nkr[i] = (r < T.ra) ? P.nkA[row0 + r] : -1;
   }
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int c = tx + 16 * j;
+  for (int j = 0; j < TN; ++j) {
+    const int c = tx + CS * j;
     nkc[j] = (c < T.rb) ? P.nkB[col0 + c] : -1;
   }
   if (P.keyA) {
@@ -245,7 +246,7 @@ __device__ __forceinline__ void tile_epilogue(const MsProblem& P, const TileInfo
       uint32_t hi = 0;
       if (nkr[i] >= 0) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < TN; ++j) {
           if (nkc[j] < 0) continue;
           const uint32_t C = acc_to_C<ENC>(acc[i][j], nkr[i], nkc[j]);
           add_term(lo, hi, C, (uint32_t)min(nkr[i], nkc[j]));
@@ -259,7 +260,7 @@ __device__ __forceinline__ void tile_epilogue(const MsProblem& P, const TileInfo
     if (offdiag && P.keyB) {
       // column sums: the mirrored pairs (j, i) of an off-diagonal tile
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < TN; ++j) {
         uint64_t lo = 0;
         uint32_t hi = 0;
         if (nkc[j] >= 0) {
@@ -272,7 +273,7 @@ __device__ __forceinline__ void tile_epilogue(const MsProblem& P, const TileInfo
         }
         shfl_add(lo, hi, 8);
         shfl_add(lo, hi, 16);
-        if (lane < 8 && nkc[j] >= 0 && (lo | hi)) atomic_add_key(P.keyB + col0 + tx + 16 * j, lo, hi);
+        if (lane < 8 && nkc[j] >= 0 && (lo | hi)) atomic_add_key(P.keyB + col0 + tx + CS * j, lo, hi);
       }
     }
   }
@@ -282,9 +283,9 @@ __device__ __forceinline__ void tile_epilogue(const MsProblem& P, const TileInfo
       if (nkr[i] < 0) continue;
       const int64_t gr = row0 + ty + 16 * i;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < TN; ++j) {
         if (nkc[j] < 0) continue;
-        const int64_t gc = col0 + tx + 16 * j;
+        const int64_t gc = col0 + tx + CS * j;
         const uint32_t C = acc_to_C<ENC>(acc[i][j], nkr[i], nkc[j]);
         const int D = min(nkr[i], nkc[j]);
         if (P.num) {
@@ -414,31 +415,32 @@ __device__ __forceinline__ const uint32_t* swz(const uint32_t* base, int r, int 
   return base + r * MS_TMA_ROW_W + ((c ^ (r & 7)) << 2);
 }
 
-template <int ENC, int FW>
+template <int ENC, int FW, int TN>
 __device__ __forceinline__ void compute_stage_swz(const uint32_t* __restrict__ As, const uint32_t* __restrict__ Bs,
-                                                  int ty, int tx, uint32_t (&acc)[8][8], uint32_t one) {
+                                                  int ty, int tx, uint32_t (&acc)[8][TN], uint32_t one) {
+  constexpr int CS = MS_BM / TN;
 #pragma unroll
   for (int kq = 0; kq < MS_BKW / FW; ++kq) {
     const int o = kq * FW;
-    uint32_t a[8][FW], b[8][FW];
+    uint32_t a[8][FW], b[TN][FW];
 #pragma unroll
     for (int i = 0; i < 8; ++i) load_frag<FW>(a[i], swz(As, ty + 16 * i, o >> 2) + (o & 3));
 #pragma unroll
-    for (int j = 0; j < 8; ++j) load_frag<FW>(b[j], swz(Bs, tx + 16 * j, o >> 2) + (o & 3));
+    for (int j = 0; j < TN; ++j) load_frag<FW>(b[j], swz(Bs, tx + CS * j, o >> 2) + (o & 3));
     if constexpr (ENC == ENC_U8_SAD) {
 #pragma unroll
       for (int w = 0; w < FW; ++w)
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
-          for (int j = 0; j < 8; ++j) vsad4_acc(acc[i][j], a[i][w], b[j][w]);
+          for (int j = 0; j < TN; ++j) vsad4_acc(acc[i][j], a[i][w], b[j][w]);
     } else {
 #pragma unroll
       for (int w = 0; w < FW; w += 2)
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
+          for (int j = 0; j < TN; ++j) {
             const uint32_t m0 = __vminu2(a[i][w], b[j][w]), m1 = __vminu2(a[i][w + 1], b[j][w + 1]);
             if constexpr (ENC == ENC_U16_MIN_IMAD) {
               asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(acc[i][j]) : "r"(m0), "r"(one));
@@ -451,23 +453,31 @@ __device__ __forceinline__ void compute_stage_swz(const uint32_t* __restrict__ A
   }
 }
 
-template <bool SYM, int ENC, int VAR>
-__global__ void __launch_bounds__(MS_THREADS, 1)
+// TN = columns per thread: 8 -> 256 threads (8 warps, 8 x 8 blocks); 4 -> 512
+// threads (16 warps, 8 x 4 blocks, <= 128 registers: twice the warps per
+// scheduler to hide latency, 12 LDS.128 per 128 VABSDIFF4 instead of 16 per 256).
+template <int TN>
+__host__ __device__ constexpr int tma_threads() { return 16 * (MS_BM / TN); }
+
+template <bool SYM, int ENC, int VAR, int TN>
+__global__ void __launch_bounds__(tma_threads<TN>(), 1)
 minsum_tma_kernel(const __grid_constant__ MsBatch batch, const __grid_constant__ MsMaps maps, int64_t total_tiles,
                   int ldw, uint32_t one) {
+  constexpr int NT = tma_threads<TN>();
+  constexpr int WPR = (MS_BM / TN) / 8;     // warps per row group
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const uint32_t base_s = (smem_u32(smem_raw) + 1023u) & ~1023u;     // SWIZZLE_128B wants 1 KB alignment
   uint32_t* smem = reinterpret_cast<uint32_t*>(smem_raw + (base_s - smem_u32(smem_raw)));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + MS_TMA_STAGES * MS_TMA_STAGE_W);
   uint64_t* empty = full + MS_TMA_STAGES;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ty = (warp >> 1) * 4 + (lane >> 3);
-  const int tx = (warp & 1) * 8 + (lane & 7);
+  const int ty = (warp / WPR) * 4 + (lane >> 3);
+  const int tx = (warp % WPR) * 8 + (lane & 7);
   const int nK = ldw / MS_BKW;
   if (tid == 0) {
     for (int s = 0; s < MS_TMA_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], MS_THREADS / 32);
+      mbar_init(&empty[s], NT / 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -501,22 +511,22 @@ minsum_tma_kernel(const __grid_constant__ MsBatch batch, const __grid_constant__
   for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
     const TileInfo T = decode_tile<SYM>(batch, tile);
     const MsProblem& P = batch.p[T.pi];
-    uint32_t acc[8][8];
+    uint32_t acc[8][TN];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[i][j] = 0u;
+      for (int j = 0; j < TN; ++j) acc[i][j] = 0u;
     for (int kc = 0; kc < nK; ++kc, ++g_use) {
       if (producer && g_load < nstages) produce();
       const int slot = (int)(g_use % MS_TMA_STAGES);
       mbar_wait(&full[slot], (uint32_t)((g_use / MS_TMA_STAGES) & 1));
       const uint32_t* As = smem + slot * MS_TMA_STAGE_W;
-      compute_stage_swz<ENC, (ENC == ENC_U8_SAD && VAR >= 2) ? 2 : 4>(As, As + MS_BM * MS_TMA_ROW_W, ty, tx, acc,
-                                                                       one);
+      compute_stage_swz<ENC, (ENC == ENC_U8_SAD && VAR >= 2) ? 2 : 4, TN>(As, As + MS_BM * MS_TMA_ROW_W, ty, tx,
+                                                                           acc, one);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
     }
-    tile_epilogue<SYM, ENC>(P, T, ty, tx, lane, acc);
+    tile_epilogue<SYM, ENC, TN>(P, T, ty, tx, lane, acc);
   }
 }
 
@@ -528,6 +538,12 @@ static int g_num_sms = 0;
 static bool use_tma_pipe() {
   const char* e = getenv("SA_K2_PIPE");
   return !(e && !strcmp(e, "cpasync"));
+}
+
+// Thread layout of engine B (SA_K2_LAYOUT): 4 = 512 threads x 8x4 (default), 8 = 256 threads x 8x8.
+static int tma_layout() {
+  const char* e = getenv("SA_K2_LAYOUT");
+  return (e && atoi(e) == 8) ? 8 : 4;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -565,7 +581,9 @@ static sa_status launch_one(const MsBatch& b, int64_t tiles, int ldw, cudaStream
   static bool configured = false;
   if (!configured) {
     SA_CUDA(cudaFuncSetAttribute(minsum_kernel<SYM, ENC, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, MS_SMEM));
-    SA_CUDA(cudaFuncSetAttribute(minsum_tma_kernel<SYM, ENC, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SA_CUDA(cudaFuncSetAttribute(minsum_tma_kernel<SYM, ENC, VAR, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 MS_TMA_SMEM));
+    SA_CUDA(cudaFuncSetAttribute(minsum_tma_kernel<SYM, ENC, VAR, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  MS_TMA_SMEM));
     configured = true;
   }
@@ -577,7 +595,12 @@ static sa_status launch_one(const MsBatch& b, int64_t tiles, int ldw, cudaStream
       SA_TRY(encode_rows_map(&maps.m[2 * p], b.p[p].A, b.p[p].na, ldw));
       SA_TRY(encode_rows_map(&maps.m[2 * p + 1], b.p[p].B, b.p[p].nb, ldw));
     }
-    minsum_tma_kernel<SYM, ENC, VAR><<<(unsigned)grid, MS_THREADS, MS_TMA_SMEM, st>>>(b, maps, tiles, ldw, 1u);
+    if (tma_layout() == 4)
+      minsum_tma_kernel<SYM, ENC, VAR, 4><<<(unsigned)grid, tma_threads<4>(), MS_TMA_SMEM, st>>>(b, maps, tiles, ldw,
+                                                                                                1u);
+    else
+      minsum_tma_kernel<SYM, ENC, VAR, 8><<<(unsigned)grid, tma_threads<8>(), MS_TMA_SMEM, st>>>(b, maps, tiles, ldw,
+                                                                                                1u);
   } else {
     minsum_kernel<SYM, ENC, VAR><<<(unsigned)grid, MS_THREADS, MS_SMEM, st>>>(b, tiles, ldw, 1u, nullptr);
   }
