@@ -218,7 +218,10 @@ def main():
         ctx.attach_comm(B.TorchComm(device=dev))
     ctx.set_timing(True)
     hp = HotPath(ctx, cfg.p, cfg.samples_per_block, want_similarity=not args.no_similarity)
-    st = torch.cuda.current_stream()
+    # every step runs on a dedicated (non-default) stream, so the e2e leg's
+    # copy stream is not serialised against it by legacy-stream semantics
+    st = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(st)
 
     def barrier():
         if world > 1:

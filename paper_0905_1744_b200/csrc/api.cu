@@ -131,40 +131,53 @@ static sa_status make_u8_rows(Scratch& scratch, const uint16_t* p16, int64_t n, 
   return SA_OK;
 }
 
-static sa_status read_max(const uint32_t* d, uint32_t* h, cudaStream_t st) {
-  SA_CUDA(cudaMemcpyAsync(h, d, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  SA_CUDA(cudaStreamSynchronize(st));
+// Engine operands of an A x B min-sum problem given its u16 profile rows.  In
+// the default (auto) mode both encodings are prepared: the u8 SAD rows are
+// converted on the device, the largest count is folded into ctx->dcount, and
+// launch_ops enqueues both engines, each guarded by that counter -- the
+// encoding is decided on the device with no host synchronisation.
+struct EngineOps {
+  Operand a16, b16, a8, b8;
+  int mode;                     // ENC_U16_MIN / ENC_U16_MIN_IMAD (forced) or ENC_AUTO
+  const uint32_t* guard = nullptr;
+};
+
+static sa_status prepare_ops(sa_ctx* c, Scratch& scratch, const uint16_t* A16, int64_t na, const uint16_t* B16,
+                             int64_t nb, int32_t bins, bool reset_count, EngineOps* E, cudaStream_t st) {
+  const int ldw16 = stride_u16(bins) / 2;
+  E->a16 = Operand{reinterpret_cast<const uint32_t*>(A16), ldw16};
+  E->b16 = Operand{reinterpret_cast<const uint32_t*>(B16), ldw16};
+  const int mode = engine_mode();
+  if (mode != ENC_U8_SAD) {
+    E->mode = mode == ENC_U16_MIN_IMAD ? ENC_U16_MIN_IMAD : ENC_U16_MIN;
+    return SA_OK;
+  }
+  E->mode = ENC_AUTO;
+  E->guard = c->dcount;
+  if (reset_count) SA_CUDA(cudaMemsetAsync(c->dcount, 0, sizeof(uint32_t), st));
+  if (B16 == A16) {   // same rows (possibly different counts): convert the longer prefix once
+    SA_TRY(make_u8_rows(scratch, A16, std::max(na, nb), bins, c->dcount, &E->a8, st));
+    E->b8 = E->a8;
+  } else {
+    SA_TRY(make_u8_rows(scratch, A16, na, bins, c->dcount, &E->a8, st));
+    SA_TRY(make_u8_rows(scratch, B16, nb, bins, c->dcount, &E->b8, st));
+  }
   return SA_OK;
 }
 
-// Operands and encoding for an A x B min-sum problem given u16 rows (B may
-// alias A).  Host-blocking once (the largest count decides the encoding).
-static sa_status select_operands(Scratch& scratch, const uint16_t* A16, int64_t na, const uint16_t* B16, int64_t nb,
-                                 int32_t bins, Operand* oa, Operand* ob, int* enc, cudaStream_t st) {
-  const int ldw16 = stride_u16(bins) / 2;
-  *oa = Operand{reinterpret_cast<const uint32_t*>(A16), ldw16};
-  *ob = Operand{reinterpret_cast<const uint32_t*>(B16), ldw16};
-  const int mode = engine_mode();
-  *enc = mode == ENC_U16_MIN_IMAD ? ENC_U16_MIN_IMAD : ENC_U16_MIN;
-  if (mode != ENC_U8_SAD) return SA_OK;
-  uint32_t* maxc = scratch.alloc<uint32_t>(1);
-  if (!maxc) return fail(SA_E_NOMEM, "scratch allocation failed");
-  SA_CUDA(cudaMemsetAsync(maxc, 0, sizeof(uint32_t), st));
-  Operand a8, b8;
-  if (B16 == A16) {   // same rows (possibly different counts): convert the longer prefix once
-    SA_TRY(make_u8_rows(scratch, A16, std::max(na, nb), bins, maxc, &a8, st));
-    b8 = a8;
-  } else {
-    SA_TRY(make_u8_rows(scratch, A16, na, bins, maxc, &a8, st));
-    SA_TRY(make_u8_rows(scratch, B16, nb, bins, maxc, &b8, st));
+// Enqueue the problems (A / B pointers given into the u16 operands).
+static sa_status launch_ops(sa_ctx* c, const EngineOps& E, const std::vector<MsProblem>& probs16, cudaStream_t st,
+                            cudaEvent_t ev0, cudaEvent_t ev1) {
+  c->last_enc = E.mode;
+  if (E.mode != ENC_AUTO) return minsum_launch(probs16, E.a16.ldw, E.mode, st, ev0, ev1);
+  std::vector<MsProblem> p8 = probs16;
+  for (auto& p : p8) {
+    const int64_t ra = (p.A - E.a16.rows) / E.a16.ldw, rb = (p.B - E.b16.rows) / E.b16.ldw;
+    p.A = E.a8.rows + ra * E.a8.ldw;
+    p.B = E.b8.rows + rb * E.b8.ldw;
   }
-  uint32_t mh = 0;
-  SA_TRY(read_max(maxc, &mh, st));
-  if (mh <= 255) {
-    *oa = a8;
-    *ob = b8;
-    *enc = ENC_U8_SAD;
-  }
+  SA_TRY(minsum_launch(p8, E.a8.ldw, ENC_U8_SAD, st, ev0, nullptr, E.guard));
+  SA_TRY(minsum_launch(probs16, E.a16.ldw, ENC_U16_MIN, st, nullptr, ev1, E.guard));
   return SA_OK;
 }
 
@@ -214,6 +227,11 @@ sa_status sa_ctx_create(int cuda_device, sa_ctx** out) {
   }
   sa_ctx* c = new sa_ctx();
   c->device = cuda_device;
+  if (cudaMalloc(&c->dcount, 64) != cudaSuccess || cudaHostAlloc(&c->hpinned, 64, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    delete c;
+    return fail(SA_E_NOMEM, "context allocation failed");
+  }
   for (int i = 0; i < 2 * SA_PHASE_COUNT; ++i) {
     if (cudaEventCreate(&c->ev[i]) != cudaSuccess) {
       delete c;
@@ -242,11 +260,23 @@ sa_status sa_ctx_destroy(sa_ctx* ctx) {
   cudaSetDevice(ctx->device);
   for (int i = 0; i < 2 * SA_PHASE_COUNT; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+  if (ctx->dcount) cudaFree(ctx->dcount);
+  if (ctx->hpinned) cudaFreeHost(ctx->hpinned);
   delete ctx;
   return SA_OK;
 }
 
-int sa_ctx_engine(const sa_ctx* ctx) { return ctx ? ctx->last_enc : -1; }
+int sa_ctx_engine(const sa_ctx* ctx) {
+  if (!ctx) return -1;
+  if (ctx->last_enc != ENC_AUTO) return ctx->last_enc;
+  // auto dispatch: the device counter decided (blocking read)
+  if (cudaSetDevice(ctx->device) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess ||
+      cudaMemcpy(ctx->hpinned, ctx->dcount, sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return *ctx->hpinned <= 255 ? ENC_U8_SAD : ENC_U16_MIN;
+}
 
 sa_status sa_ctx_set_timing(sa_ctx* ctx, int enable) {
   if (!ctx) return fail(SA_E_INVAL, "ctx is NULL");
@@ -445,19 +475,10 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
   SA_CUDA(cudaMemsetAsync(lkey, 0, n * sizeof(sa_key128), st));
   SA_CUDA(cudaMemsetAsync(gkey, 0, n * sizeof(sa_key128), st));
 
-  // engine operands: u8 SAD rows when every count fits (the usual case), else u16
-  SA_ALLOC(maxc, uint32_t, 2);
-  SA_CUDA(cudaMemsetAsync(maxc, 0, 2 * sizeof(uint32_t), st));
-  const int mode = engine_mode();
-  Operand loc{reinterpret_cast<const uint32_t*>(a.prof), ldw};
-  int enc_loc = mode == ENC_U16_MIN_IMAD ? ENC_U16_MIN_IMAD : ENC_U16_MIN;
-  if (mode == ENC_U8_SAD) {
-    Operand o8;
-    uint32_t mh = 0;
-    SA_TRY(make_u8_rows(scratch, a.prof, n, a.stride, maxc, &o8, st));
-    SA_TRY(read_max(maxc, &mh, st));
-    if (mh <= 255) { loc = o8; enc_loc = ENC_U8_SAD; }
-  }
+  // engine operands of the local rows (u8 SAD rows when every count fits,
+  // decided on the device; see prepare_ops)
+  EngineOps E;
+  SA_TRY(prepare_ops(c, scratch, a.prof, n, a.prof, n, a.stride, true, &E, st));
 
   // ---- S2a: local rank of every member against its own block
   SA_TRY(rec(ev_begin(c, SA_PHASE_S2A), st));
@@ -467,14 +488,14 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
       const int64_t b = block_begin(q0 + q, a.N, a.p) - a.first;
       const int64_t e = block_begin(q0 + q + 1, a.N, a.p) - a.first;
       MsProblem pr{};
-      pr.A = pr.B = loc.rows + b * loc.ldw;
+      pr.A = pr.B = E.a16.rows + b * E.a16.ldw;
       pr.nkA = pr.nkB = a.nk + b;
       pr.na = pr.nb = (int32_t)(e - b);
       pr.sym = 1;
       pr.keyA = pr.keyB = lkey + b;
       probs.push_back(pr);
     }
-    SA_TRY(minsum_launch(probs, loc.ldw, enc_loc, st, nullptr, nullptr));
+    SA_TRY(launch_ops(c, E, probs, st, nullptr, nullptr));
   }
   SA_TRY(rec(ev_end(c, SA_PHASE_S2A), st));
 
@@ -501,28 +522,22 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
 
   // ---- S2d: global rank against S
   {
-    Operand smp{reinterpret_cast<const uint32_t*>(s_prof), ldw};
-    Operand qry{reinterpret_cast<const uint32_t*>(a.prof), ldw};
-    int enc = mode == ENC_U16_MIN_IMAD ? ENC_U16_MIN_IMAD : ENC_U16_MIN;
-    if (enc_loc == ENC_U8_SAD) {
-      Operand o8;
-      uint32_t mh = 0;
-      SA_TRY(make_u8_rows(scratch, s_prof, s_all, a.stride, maxc + 1, &o8, st));
-      SA_TRY(read_max(maxc + 1, &mh, st));
-      if (mh <= 255) { smp = o8; qry = loc; enc = ENC_U8_SAD; }
-    }
+    // the same local operands; the sample rows' counts fold into the same
+    // device counter, so the engine is valid for both sides
+    EngineOps E2 = E;
+    E2.b16 = Operand{reinterpret_cast<const uint32_t*>(s_prof), ldw};
+    if (E2.mode == ENC_AUTO) SA_TRY(make_u8_rows(scratch, s_prof, s_all, a.stride, c->dcount, &E2.b8, st));
     SA_TRY(rec(ev_begin(c, SA_PHASE_S2D), st));
     MsProblem pr{};
-    pr.A = qry.rows;
-    pr.B = smp.rows;
+    pr.A = E2.a16.rows;
+    pr.B = E2.b16.rows;
     pr.nkA = a.nk;
     pr.nkB = s_nk;
     pr.na = n;
     pr.nb = s_all;
     pr.sym = 0;
     pr.keyA = gkey;
-    SA_TRY(minsum_launch({pr}, qry.ldw, enc, st, nullptr, nullptr));
-    c->last_enc = enc;
+    SA_TRY(launch_ops(c, E2, {pr}, st, nullptr, nullptr));
   }
   SA_TRY(rec(ev_end(c, SA_PHASE_S2D), st));
 
@@ -754,9 +769,9 @@ sa_status sa_kmer_profiles(sa_ctx* ctx, const uint8_t* residues, const int64_t* 
   SA_ALLOC(err, uint32_t, 1);
   SA_CUDA(cudaMemsetAsync(err, 0, 4, st));
   SA_TRY(profiles_launch(residues, offsets, n, k, alphabet, profile_stride((int32_t)bins), profiles, nkmers, err, st));
-  uint32_t h = 0;
-  SA_CUDA(cudaMemcpyAsync(&h, err, 4, cudaMemcpyDeviceToHost, st));
+  SA_CUDA(cudaMemcpyAsync(ctx->hpinned, err, 4, cudaMemcpyDeviceToHost, st));
   SA_CUDA(cudaStreamSynchronize(st));
+  const uint32_t h = *ctx->hpinned;
   if (h & ERR_RESIDUE) return fail(SA_E_RANGE, "residue outside the alphabet (code >= %d)", alphabet);
   if (h & ERR_NK) return fail(SA_E_RANGE, "a sequence has more than 65535 k-mers (uint16 counts)");
   return SA_OK;
@@ -775,12 +790,11 @@ sa_status sa_kmer_rank(sa_ctx* ctx, const uint16_t* q_prof, const int32_t* q_nk,
   SA_CUDA(cudaSetDevice(ctx->device));
   SA_CUDA(cudaMemsetAsync(keys, 0, (size_t)nq * sizeof(sa_key128), st));
   Scratch scratch(st);
-  Operand oa, ob;
-  int enc;
-  SA_TRY(select_operands(scratch, q_prof, nq, pool_prof, npool, bins, &oa, &ob, &enc, st));
+  EngineOps E;
+  SA_TRY(prepare_ops(ctx, scratch, q_prof, nq, pool_prof, npool, bins, true, &E, st));
   MsProblem pr{};
-  pr.A = oa.rows;
-  pr.B = ob.rows;
+  pr.A = E.a16.rows;
+  pr.B = E.b16.rows;
   pr.nkA = q_nk;
   pr.nkB = pool_nk;
   pr.na = nq;
@@ -789,8 +803,7 @@ sa_status sa_kmer_rank(sa_ctx* ctx, const uint16_t* q_prof, const int32_t* q_nk,
   pr.keyA = keys;
   pr.num = numerators;
   pr.ld = npool;
-  SA_TRY(minsum_launch({pr}, oa.ldw, enc, st, ev_begin(ctx, SA_PHASE_RANK), ev_end(ctx, SA_PHASE_RANK)));
-  ctx->last_enc = enc;
+  SA_TRY(launch_ops(ctx, E, {pr}, st, ev_begin(ctx, SA_PHASE_RANK), ev_end(ctx, SA_PHASE_RANK)));
   if (rank_f64) SA_TRY(keys_to_f64_launch(keys, nq, npool, rank_f64, st));
   return SA_OK;
 }
@@ -942,19 +955,17 @@ sa_status sa_bucket_similarity(sa_ctx* ctx, const uint16_t* profiles, const int3
   cudaStream_t st = (cudaStream_t)stream;
   SA_CUDA(cudaSetDevice(ctx->device));
   Scratch scratch(st);
-  Operand oa, ob;
-  int enc;
-  SA_TRY(select_operands(scratch, profiles, n, profiles, n, bins, &oa, &ob, &enc, st));
+  EngineOps E;
+  SA_TRY(prepare_ops(ctx, scratch, profiles, n, profiles, n, bins, true, &E, st));
   MsProblem pr{};
-  pr.A = pr.B = oa.rows;
+  pr.A = pr.B = E.a16.rows;
   pr.nkA = pr.nkB = nkmers;
   pr.na = pr.nb = n;
   pr.sym = 1;
   pr.num = numerators;
   pr.sim = similarity;
   pr.ld = n;
-  SA_TRY(minsum_launch({pr}, oa.ldw, enc, st, ev_begin(ctx, SA_PHASE_S5), ev_end(ctx, SA_PHASE_S5)));
-  ctx->last_enc = enc;
+  SA_TRY(launch_ops(ctx, E, {pr}, st, ev_begin(ctx, SA_PHASE_S5), ev_end(ctx, SA_PHASE_S5)));
   return SA_OK;
 }
 

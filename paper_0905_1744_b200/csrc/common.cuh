@@ -73,14 +73,16 @@ struct MsProblem {
 //   ENC_U16_MIN_IMAD  same, adds issued as IMAD on the FMA pipe (experiment)
 //   ENC_U8_SAD        uint8 counts, 4 bins/word, C = (nk_a + nk_b - sum|a-b|)/2 with
 //                     VABSDIFF4.U8.ACC (every count must be <= 255)
-enum { ENC_U16_MIN = 0, ENC_U8_SAD = 1, ENC_U16_MIN_IMAD = 2 };
+enum { ENC_U16_MIN = 0, ENC_U8_SAD = 1, ENC_U16_MIN_IMAD = 2, ENC_AUTO = 3 };
 // Row strides: u16 rows are round_up(bins, 64) elements; u8 rows round_up(bins, 128) bytes.
 inline int32_t stride_u16(int32_t bins) { return ((bins + 63) / 64) * 64; }
 inline int32_t stride_u8(int32_t bins) { return ((bins + 127) / 128) * 128; }
 
 // Launch the engine over `probs`; ldw = row stride in 32-bit words.
+// guard (nullable): device counter holding the largest count; when set, the
+// launch is a no-op on the device unless the counter selects `enc`.
 sa_status minsum_launch(const std::vector<MsProblem>& probs, int ldw, int enc, cudaStream_t st,
-                        cudaEvent_t ev0, cudaEvent_t ev1);
+                        cudaEvent_t ev0, cudaEvent_t ev1, const uint32_t* guard = nullptr);
 // uint16 rows -> uint8 rows (zero padded) + atomicMax of every count into *maxc.
 sa_status to_u8_launch(const uint16_t* p16, int64_t n, int32_t stride16, int32_t bins, uint8_t* p8,
                        int32_t stride8, uint32_t* maxc, cudaStream_t st);
@@ -126,5 +128,7 @@ struct sa_ctx {
   bool timing = false;
   cudaEvent_t ev[2 * SA_PHASE_COUNT] = {};
   bool ev_used[SA_PHASE_COUNT] = {};
-  int last_enc = -1;
+  int last_enc = -1;            // ENC_* of the last min-sum call, or ENC_AUTO
+  uint32_t* dcount = nullptr;   // device: largest count of the last auto-dispatched call
+  uint32_t* hpinned = nullptr;  // pinned host word for small readbacks
 };

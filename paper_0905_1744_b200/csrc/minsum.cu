@@ -104,6 +104,17 @@ __device__ __forceinline__ uint32_t acc_to_C(uint32_t acc, int nka, int nkb) {
   return (acc & 0xffffu) + (acc >> 16);                                  // the two u16 lanes
 }
 
+// Device-side engine dispatch: both encodings are enqueued and each kernel
+// returns at once unless the largest count (*guard, written by to_u8_kernel)
+// selects it -- u8 SAD when every count is <= 255, u16 otherwise -- so the
+// host never waits for the decision.
+template <int ENC>
+__device__ __forceinline__ bool guard_skip(const uint32_t* guard) {
+  if (!guard) return false;
+  const uint32_t m = *reinterpret_cast<const volatile uint32_t*>(guard);
+  return (m <= 255u) != (ENC == ENC_U8_SAD);
+}
+
 template <int FW>
 __device__ __forceinline__ void load_frag(uint32_t (&f)[FW], const uint32_t* p) {
   if constexpr (FW == 4) {
@@ -307,14 +318,14 @@ __device__ __forceinline__ void tile_epilogue(const MsProblem& P, const TileInfo
 template <bool SYM, int ENC, int VAR>
 __global__ void __launch_bounds__(MS_THREADS, 1)
 minsum_kernel(const __grid_constant__ MsBatch batch, int64_t total_tiles, int ldw, uint32_t one,
-              const uint32_t* __restrict__ zero_row) {
+              const uint32_t* __restrict__ guard) {
+  if (guard_skip<ENC>(guard)) return;
   extern __shared__ __align__(16) uint32_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ty = (warp >> 1) * 4 + (lane >> 3);  // row group 0..15: rows ty + 16 i
   const int tx = (warp & 1) * 8 + (lane & 7);     // col group 0..15: cols tx + 16 j
   const int nK = ldw / MS_BKW;
   constexpr int STAGE_W = 2 * MS_BM * MS_LDW;
-  (void)zero_row;
 
   for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
     const TileInfo T = decode_tile<SYM>(batch, tile);
@@ -462,7 +473,8 @@ __host__ __device__ constexpr int tma_threads() { return 16 * (MS_BM / TN); }
 template <bool SYM, int ENC, int VAR, int TN>
 __global__ void __launch_bounds__(tma_threads<TN>(), 1)
 minsum_tma_kernel(const __grid_constant__ MsBatch batch, const __grid_constant__ MsMaps maps, int64_t total_tiles,
-                  int ldw, uint32_t one) {
+                  int ldw, uint32_t one, const uint32_t* __restrict__ guard) {
+  if (guard_skip<ENC>(guard)) return;
   constexpr int NT = tma_threads<TN>();
   constexpr int WPR = (MS_BM / TN) / 8;     // warps per row group
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -577,7 +589,7 @@ static sa_status encode_rows_map(CUtensorMap* m, const uint32_t* base, int64_t r
 }
 
 template <bool SYM, int ENC, int VAR>
-static sa_status launch_one(const MsBatch& b, int64_t tiles, int ldw, cudaStream_t st) {
+static sa_status launch_one(const MsBatch& b, int64_t tiles, int ldw, const uint32_t* guard, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
     SA_CUDA(cudaFuncSetAttribute(minsum_kernel<SYM, ENC, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, MS_SMEM));
@@ -597,12 +609,12 @@ static sa_status launch_one(const MsBatch& b, int64_t tiles, int ldw, cudaStream
     }
     if (tma_layout() == 4)
       minsum_tma_kernel<SYM, ENC, VAR, 4><<<(unsigned)grid, tma_threads<4>(), MS_TMA_SMEM, st>>>(b, maps, tiles, ldw,
-                                                                                                1u);
+                                                                                                1u, guard);
     else
       minsum_tma_kernel<SYM, ENC, VAR, 8><<<(unsigned)grid, tma_threads<8>(), MS_TMA_SMEM, st>>>(b, maps, tiles, ldw,
-                                                                                                1u);
+                                                                                                1u, guard);
   } else {
-    minsum_kernel<SYM, ENC, VAR><<<(unsigned)grid, MS_THREADS, MS_SMEM, st>>>(b, tiles, ldw, 1u, nullptr);
+    minsum_kernel<SYM, ENC, VAR><<<(unsigned)grid, MS_THREADS, MS_SMEM, st>>>(b, tiles, ldw, 1u, guard);
   }
   SA_LAUNCHED();
   return SA_OK;
@@ -618,21 +630,22 @@ static int sad_variant() {
 }
 
 template <bool SYM>
-static sa_status launch_enc(const MsBatch& b, int64_t tiles, int ldw, int enc, cudaStream_t st) {
+static sa_status launch_enc(const MsBatch& b, int64_t tiles, int ldw, int enc, const uint32_t* guard,
+                            cudaStream_t st) {
   if (enc == ENC_U8_SAD) {
     switch (sad_variant()) {
-      case 1: return launch_one<SYM, ENC_U8_SAD, 1>(b, tiles, ldw, st);
-      case 2: return launch_one<SYM, ENC_U8_SAD, 2>(b, tiles, ldw, st);
-      case 3: return launch_one<SYM, ENC_U8_SAD, 3>(b, tiles, ldw, st);
-      default: return launch_one<SYM, ENC_U8_SAD, 0>(b, tiles, ldw, st);
+      case 1: return launch_one<SYM, ENC_U8_SAD, 1>(b, tiles, ldw, guard, st);
+      case 2: return launch_one<SYM, ENC_U8_SAD, 2>(b, tiles, ldw, guard, st);
+      case 3: return launch_one<SYM, ENC_U8_SAD, 3>(b, tiles, ldw, guard, st);
+      default: return launch_one<SYM, ENC_U8_SAD, 0>(b, tiles, ldw, guard, st);
     }
   }
-  if (enc == ENC_U16_MIN_IMAD) return launch_one<SYM, ENC_U16_MIN_IMAD, 0>(b, tiles, ldw, st);
-  return launch_one<SYM, ENC_U16_MIN, 0>(b, tiles, ldw, st);
+  if (enc == ENC_U16_MIN_IMAD) return launch_one<SYM, ENC_U16_MIN_IMAD, 0>(b, tiles, ldw, guard, st);
+  return launch_one<SYM, ENC_U16_MIN, 0>(b, tiles, ldw, guard, st);
 }
 
 sa_status minsum_launch(const std::vector<MsProblem>& probs_in, int ldw, int enc, cudaStream_t st,
-                        cudaEvent_t ev0, cudaEvent_t ev1) {
+                        cudaEvent_t ev0, cudaEvent_t ev1, const uint32_t* guard) {
   if (ldw % MS_BKW != 0) return fail(SA_E_INVAL, "profile row stride must be a multiple of 64 bins");
   SA_TRY(ensure_recip_tables(st));
   if (g_num_sms == 0) {
@@ -659,7 +672,8 @@ sa_status minsum_launch(const std::vector<MsProblem>& probs_in, int ldw, int enc
       tiles += sym ? (int64_t)q.tiles_b * (q.tiles_b + 1) / 2 : ta * q.tiles_b;
       b.p[b.n++] = q;
     }
-    const sa_status rs = sym ? launch_enc<true>(b, tiles, ldw, enc, st) : launch_enc<false>(b, tiles, ldw, enc, st);
+    const sa_status rs = sym ? launch_enc<true>(b, tiles, ldw, enc, guard, st)
+                             : launch_enc<false>(b, tiles, ldw, enc, guard, st);
     if (rs != SA_OK) return rs;
   }
   if (ev1) SA_CUDA(cudaEventRecord(ev1, st));

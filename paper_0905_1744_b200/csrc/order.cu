@@ -30,55 +30,136 @@ __device__ __forceinline__ bool key_near(const sa_key128& a, const sa_key128& b,
   return dhi == 0 && dlo < (uint64_t)window;
 }
 
-// Counting sort: position of item i inside its segment = #{j : (k_j, g_j) < (k_i, g_i)}.
-// gids == nullptr means g = gid0 + index.
-constexpr int SORT_TILE = 1024;
-__global__ void __launch_bounds__(256)
-segsort_kernel(const sa_key128* __restrict__ keys, const int64_t* __restrict__ gids, int64_t gid0, SegSpec sp,
-               int64_t window, int32_t* __restrict__ order_out, uint8_t* __restrict__ amb,
-               uint32_t* __restrict__ amb_count) {
-  __shared__ sa_key128 sk[SORT_TILE];
-  __shared__ int64_t sg[SORT_TILE];
-  const int64_t s = blockIdx.y;
-  const int64_t b = sp.begin(s), e = sp.begin(s + 1);
-  const int64_t i = b + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b + (int64_t)blockIdx.x * blockDim.x >= e) return;   // CTA-uniform
-  const bool live = i < e;
-  sa_key128 ki = live ? keys[i] : sa_key128{0, 0};
-  const int64_t gi = live ? (gids ? gids[i] : gid0 + i) : 0;
-  int64_t pos = 0;
-  bool near = false;
-  for (int64_t j0 = b; j0 < e; j0 += SORT_TILE) {
-    const int cnt = (int)min((int64_t)SORT_TILE, e - j0);
-    __syncthreads();
-    for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
-      sk[t] = keys[j0 + t];
-      sg[t] = gids ? gids[j0 + t] : gid0 + j0 + t;
-    }
-    __syncthreads();
-    if (live) {
-      for (int t = 0; t < cnt; ++t) {
-        const sa_key128 kj = sk[t];
-        const int64_t gj = sg[t];
-        pos += key_lt(kj, gj, ki, gi) ? 1 : 0;
-        near |= (gj != gi) && key_near(kj, ki, window);
-      }
-    }
+// Exact segment sort by (key, gid) in O(w) expected work per segment.  One CTA
+// per segment:
+//  1. d_i = RN(key_i) as a double and [min, max] over the segment;
+//  2. bucket_i = floor((d_i - min) * nb / (max - min)) -- a monotone
+//     non-decreasing function of the exact key, so every item of a lower
+//     bucket precedes every item of a higher one;
+//  3. counting sort of the buckets, then the position of i inside its bucket
+//     = #{j in the bucket : (k_j, g_j) < (k_i, g_i)} by exact 128-bit compares.
+// Ties and near-ties are exact (the compares use the full keys); skewed or
+// constant keys degrade to quadratic work inside the crowded buckets only.
+// Adjacent sorted keys closer than `window` (the pool size) are counted in
+// *amb_count: the key order is then not certified.
+constexpr int BS_THREADS = 1024;
+constexpr int BS_MAXB = 4096;
+
+__device__ __forceinline__ double key_to_double(const sa_key128& k) {
+  if (k.hi == 0) return __ull2double_rn(k.lo);
+  const int sh = 64 - __clzll((long long)k.hi);
+  uint64_t m, rest;
+  if (sh == 64) { m = k.hi; rest = k.lo; }
+  else { m = (k.hi << (64 - sh)) | (k.lo >> sh); rest = k.lo & ((1ull << sh) - 1); }
+  m |= (rest != 0) ? 1ull : 0ull;
+  return ldexp(__ull2double_rn(m), sh);
+}
+
+__global__ void __launch_bounds__(BS_THREADS)
+bucket_sort_kernel(const sa_key128* __restrict__ keys, const int64_t* __restrict__ gids, int64_t gid0, SegSpec sp,
+                   int64_t window, int32_t* __restrict__ order_out, int32_t* __restrict__ bkt,
+                   int32_t* __restrict__ list, uint32_t* __restrict__ amb_count) {
+  __shared__ int32_t start[BS_MAXB + 1];
+  __shared__ int32_t fill[BS_MAXB];
+  __shared__ int32_t part[BS_THREADS];
+  __shared__ double rmin[BS_THREADS / 32], rmax[BS_THREADS / 32];
+  const int tid = threadIdx.x;
+  const int64_t s = blockIdx.x;
+  const int64_t b = sp.begin(s), e = sp.begin(s + 1), w = e - b;
+  if (w <= 0) return;
+  auto gid = [&](int64_t i) { return gids ? gids[i] : gid0 + i; };
+
+  double mn = 1.0 / 0.0, mx = -1.0 / 0.0;
+  for (int64_t i = b + tid; i < e; i += BS_THREADS) {
+    const double d = key_to_double(keys[i]);
+    mn = fmin(mn, d);
+    mx = fmax(mx, d);
   }
-  if (live) {
-    order_out[b + pos] = (int32_t)(i - b);
-    if (amb) amb[i] = near ? 1 : 0;
-    if (near) atomicAdd(amb_count, 1u);
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   }
+  if ((tid & 31) == 0) { rmin[tid >> 5] = mn; rmax[tid >> 5] = mx; }
+  __syncthreads();
+  mn = rmin[0];
+  mx = rmax[0];
+  for (int t = 1; t < BS_THREADS / 32; ++t) { mn = fmin(mn, rmin[t]); mx = fmax(mx, rmax[t]); }
+  const int64_t nb_want = w / 2 < 1 ? 1 : w / 2;
+  const int nb = (int)(nb_want < BS_MAXB ? nb_want : BS_MAXB);
+  const double scale = mx > mn ? (double)nb / (mx - mn) : 0.0;
+
+  for (int t = tid; t < nb; t += BS_THREADS) start[t] = 0;
+  __syncthreads();
+  for (int64_t i = b + tid; i < e; i += BS_THREADS) {
+    int bk = (int)((key_to_double(keys[i]) - mn) * scale);
+    bk = min(max(bk, 0), nb - 1);
+    bkt[i] = bk;
+    atomicAdd(&start[bk], 1);
+  }
+  __syncthreads();
+  // exclusive scan of the nb counts: 4 per thread, then a block scan
+  int loc[4], sum = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int t = tid * 4 + q;
+    loc[q] = t < nb ? start[t] : 0;
+    sum += loc[q];
+  }
+  part[tid] = sum;
+  __syncthreads();
+  for (int o = 1; o < BS_THREADS; o <<= 1) {
+    const int v = tid >= o ? part[tid - o] : 0;
+    __syncthreads();
+    part[tid] += v;
+    __syncthreads();
+  }
+  int run = part[tid] - sum;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int t = tid * 4 + q;
+    if (t < nb) { start[t] = run; fill[t] = run; }
+    run += loc[q];
+  }
+  if (tid == 0) start[nb] = (int)w;
+  __syncthreads();
+  for (int64_t i = b + tid; i < e; i += BS_THREADS) {
+    const int slot = atomicAdd(&fill[bkt[i]], 1);
+    list[b + slot] = (int32_t)(i - b);
+  }
+  __syncthreads();
+  for (int64_t i = b + tid; i < e; i += BS_THREADS) {
+    const int bk = bkt[i];
+    const sa_key128 ki = keys[i];
+    const int64_t gi = gid(i);
+    int cnt = 0;
+    for (int t = start[bk]; t < start[bk + 1]; ++t) {
+      const int64_t j = b + list[b + t];
+      cnt += (j != i && key_lt(keys[j], gid(j), ki, gi)) ? 1 : 0;
+    }
+    order_out[b + start[bk] + cnt] = (int32_t)(i - b);
+  }
+  __syncthreads();
+  uint32_t near = 0;
+  for (int64_t t = tid; t + 1 < w; t += BS_THREADS)
+    near += key_near(keys[b + order_out[b + t]], keys[b + order_out[b + t + 1]], window) ? 1u : 0u;
+  if (near) atomicAdd(amb_count, near);
 }
 
 sa_status segsort_launch_impl(const sa_key128* keys, const int64_t* gids, int64_t gid0, SegSpec sp, int nseg,
-                              int64_t max_seg, int64_t window, int32_t* order_out, uint8_t* amb,
-                              uint32_t* amb_count, cudaStream_t st) {
-  if (nseg <= 0 || max_seg <= 0) return SA_OK;
-  dim3 grid((unsigned)((max_seg + 255) / 256), (unsigned)nseg);
-  segsort_kernel<<<grid, 256, 0, st>>>(keys, gids, gid0, sp, window, order_out, amb, amb_count);
-  SA_LAUNCHED();
+                              int64_t total, int64_t window, int32_t* order_out, uint32_t* amb_count,
+                              cudaStream_t st) {
+  if (nseg <= 0 || total <= 0) return SA_OK;
+  void* scratch = nullptr;
+  SA_CUDA(cudaMallocAsync(&scratch, (size_t)total * 8, st));
+  int32_t* bkt = static_cast<int32_t*>(scratch);
+  int32_t* list = bkt + total;
+  // segment s covers [sp.begin(s), sp.begin(s + 1)) of these arrays (indices relative to sp.begin(0) = 0)
+  bucket_sort_kernel<<<(unsigned)nseg, BS_THREADS, 0, st>>>(keys, gids, gid0, sp, window, order_out, bkt, list,
+                                                            amb_count);
+  const cudaError_t le = cudaGetLastError();
+  count_launch();
+  cudaFreeAsync(scratch, st);
+  if (le != cudaSuccess) return fail(SA_E_CUDA, "bucket_sort_kernel launch: %s", cudaGetErrorString(le));
   return SA_OK;
 }
 
@@ -340,10 +421,10 @@ static inline unsigned cdiv(int64_t a, int64_t b) { return (unsigned)((a + b - 1
 sa_status segment_sort_keys(const sa_key128* keys, int64_t gid0, int64_t N, int64_t P, int64_t q0, int64_t base,
                             int nseg, int64_t window, int32_t* order_out, uint8_t* amb, uint32_t* amb_count,
                             cudaStream_t st) {
+  (void)amb;
   SegSpec sp{N, P, q0, base};
-  int64_t maxw = 0;
-  for (int s = 0; s < nseg; ++s) maxw = std::max(maxw, sp.begin(s + 1) - sp.begin(s));
-  return segsort_launch_impl(keys, nullptr, gid0, sp, nseg, maxw, window, order_out, amb, amb_count, st);
+  return segsort_launch_impl(keys, nullptr, gid0, sp, nseg, sp.begin(nseg) - sp.begin(0), window, order_out,
+                             amb_count, st);
 }
 
 sa_status sort_records(const sa_pivot* rec, int n, int64_t window, sa_key128* tmp_keys, int64_t* tmp_gid,
@@ -351,8 +432,9 @@ sa_status sort_records(const sa_pivot* rec, int n, int64_t window, sa_key128* tm
   if (n <= 0) return SA_OK;
   split_records_kernel<<<cdiv(n, 256), 256, 0, st>>>(rec, n, tmp_keys, tmp_gid);
   SA_LAUNCHED();
+  (void)amb;
   SegSpec sp{n, 1, 0, 0};
-  return segsort_launch_impl(tmp_keys, tmp_gid, 0, sp, 1, n, window, order_out, amb, amb_count, st);
+  return segsort_launch_impl(tmp_keys, tmp_gid, 0, sp, 1, n, window, order_out, amb_count, st);
 }
 
 sa_status pick_launch(const int32_t* order, int64_t N, int64_t P, int64_t q0, int64_t base, int nseg, int count,
