@@ -277,6 +277,8 @@ def sa_partition(ctx: Context, p: int, samples_per_block: int, profiles, nkmers,
         n_local, _ptr(bucket_of), _ptr(pivots),
         counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), nbytes.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
         ctypes.byref(dbg_struct) if dbg_struct is not None else None, _stream(stream)))
+    if dbg is not None:
+        dbg["candidates"] = dbg["candidates"][:p * (p - 1)]
     return PartitionOut(bucket_of, pivots[:max(p - 1, 0)], counts, nbytes, dbg, int(fallbacks.value))
 
 

@@ -799,8 +799,12 @@ sa_status sa_kmer_rank(sa_ctx* ctx, const uint16_t* q_prof, const int32_t* q_nk,
   pr.nkB = pool_nk;
   pr.na = nq;
   pr.nb = npool;
-  pr.sym = 0;
+  // the pool is the query set itself (a block's local rank, or the centralized
+  // rank of SURVEY N2): C is symmetric, so only the upper-triangle tiles run,
+  // each adding its row sums to key_i and its column sums to key_j
+  pr.sym = (q_prof == pool_prof && q_nk == pool_nk && nq == npool) ? 1 : 0;
   pr.keyA = keys;
+  pr.keyB = pr.sym ? keys : nullptr;
   pr.num = numerators;
   pr.ld = npool;
   SA_TRY(launch_ops(ctx, E, {pr}, st, ev_begin(ctx, SA_PHASE_RANK), ev_end(ctx, SA_PHASE_RANK)));

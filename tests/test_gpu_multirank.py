@@ -41,6 +41,41 @@ def _run(G, cfg, ds):
     return run_ranks(G, fn)
 
 
+@pytest.mark.parametrize("n,p,kb,Gs", [(1003, 6, 7, (1, 2, 3, 6)), (203, 3, 5, (1, 3)), (97, 1, 4, (1,))])
+def test_ragged_blocks_odd_p_match_oracle(n, p, kb, Gs):
+    """N not divisible by p (blocks of unequal size, Z13), odd p (pivot index
+    floor(p/2) + jp, Z9), p = 1 (one bucket): every rank count gives the
+    oracle's partition and buckets."""
+    require_gpu()
+    from oracle import kmer, partition
+    from sa_synth.generator import WorkloadConfig
+    cfg = WorkloadConfig("ragged", n, 1, ("uniform", 30, 400), 0.3, 0.05, p, kb, 11)   # p, k_b for HotPath
+    ds = _mixed(n, seed=11)
+    P, nk = kmer.profiles(ds.residues, ds.offsets)
+    o = partition.partition(P, nk, p, kb)
+    for G in Gs:
+        outs = _run(G, cfg, ds)
+        assert np.array_equal(np.concatenate([x["bucket_of"] for x in outs]), o.bucket_of), G
+        assert np.array_equal(np.concatenate([x["gid"] for x in outs]), np.concatenate(o.buckets)), G
+        for x in outs:
+            assert x["pivots"].tolist() == o.pivots
+            assert x["candidates"].tolist() == o.candidates and x["sample_idx"].tolist() == o.sample_idx
+
+
+def _mixed(n, seed):
+    """n sequences from a few random families (lengths 30..400), seeded."""
+    from sa_synth.generator import from_sequences
+    rng = np.random.default_rng(seed)
+    anc = [rng.integers(0, 20, size=int(rng.integers(30, 400))) for _ in range(7)]
+    seqs = []
+    for i in range(n):
+        a = anc[int(rng.integers(0, 7))].copy()
+        m = rng.random(a.shape[0]) < 0.3
+        a[m] = rng.integers(0, 20, size=int(m.sum()))
+        seqs.append(a)
+    return from_sequences(seqs)
+
+
 @pytest.mark.parametrize("c,Gs", [(2, (2, 4, 8)), (1, (2, 4))])
 def test_rank_count_invariance(c, Gs):
     require_gpu()

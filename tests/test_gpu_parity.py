@@ -110,6 +110,21 @@ def test_kmer_rank_random(ctx, engine, nq, npool, dup):
     assert_rel(f64.cpu().numpy(), [rs.f64(i) for i in range(nq)], 1e-12)
 
 
+@pytest.mark.parametrize("n", [300, 129])
+def test_kmer_rank_self_pool_symmetric_path(ctx, engine, n):
+    """Pool = the queries themselves (upper-triangle tiles + column sums)."""
+    ds = _rand_set(n + 5, n, 0, 420, dup=3)
+    res, offs = to_dev(ds)
+    P, nk = B.sa_kmer_profiles(ctx, res, offs)
+    Po, nko = kmer.profiles(ds.residues, ds.offsets)
+    keys, f64, num = B.sa_kmer_rank(ctx, P, nk, P, nk, want_numerators=True)
+    C = kmer.numerator_matrix(Po, Po)
+    assert np.array_equal(num.cpu().numpy(), C)
+    rs = kmer.RankSet(C, kmer.denominator_matrix(nko, nko))
+    assert B.keys_to_ints(keys) == rs.keys
+    assert_rel(f64.cpu().numpy(), [rs.f64(i) for i in range(n)], 1e-12)
+
+
 def test_kmer_rank_empty_pool(ctx):
     P = torch.zeros((2, 8000), dtype=torch.uint16, device="cuda")
     nk = torch.ones(2, dtype=torch.int32, device="cuda")
