@@ -110,6 +110,22 @@ sa_status sa_ctx_set_timing(sa_ctx* ctx, int enable);
 int sa_ctx_engine(const sa_ctx* ctx);
 sa_status sa_ctx_phase_ms(sa_ctx* ctx, float* ms_h /* [SA_PHASE_COUNT] */);
 
+/* Rank form used by sa_kmer_rank and sa_partition on this context.
+ *   SA_RANK_F  (default, BASELINE.json O1): R_i = mean_j F(i,j); keys are the
+ *              exact-rank keys above; orders are exact.
+ *   SA_RANK_DF (the paper's own Eq. 2-3): R_i =
+ *              mean_j d^F(i,j), d^F = -ln(Delta + F) (Delta > 0; SPEC uses
+ *              0.02, natural log).  key_i = sum_j round(2^52 (ln(1+Delta) -
+ *              ln(Delta + F_ij))) (fixed point, so the sum is deterministic);
+ *              rank_f64 = key 2^-52 / npool - ln(1+Delta).  Orders are by key,
+ *              ties by index, ascending (most similar first); a comparison is
+ *              certified when keys differ by >= 32 npool (log error bound,
+ *              DESIGN.md §2 N1); there is no exact fallback -- uncertified
+ *              comparisons are only counted (sa_partition_debug.uncertified_h).
+ * SA_E_INVAL: unknown form, or Delta <= 0 / not finite for SA_RANK_DF. */
+enum { SA_RANK_F = 0, SA_RANK_DF = 1 };
+sa_status sa_ctx_set_rank_form(sa_ctx* ctx, int form, double delta);
+
 /* Exact comparison of two ranks over the same pool (host memory, no GPU):
  * sign of V_a - V_b with V_x = sum_j C_xj / min(nk_x, nk_pool[j]) (terms with
  * a zero denominator are 0).  Ca_h / Cb_h: numerator rows [npool] (uint16).
@@ -161,6 +177,7 @@ typedef struct {
   int64_t* global_order;     /* [n_local] S3a: global ids, each block sorted        */
   int64_t* candidates;       /* [p*(p-1)] S3b: sorted regular samples Y (global ids) */
   int32_t* exact_fallbacks_h;/* host int: ambiguous key comparisons resolved exactly */
+  int32_t* uncertified_h;    /* host int: (d^F form) comparisons inside the error window */
 } sa_partition_debug;
 
 /* Algorithm 2 steps 1-11, the rank-based sample sort:

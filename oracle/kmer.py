@@ -223,6 +223,9 @@ class RankSet:
             self.K.append(K)
             self.keys.append(rank_key(C[i], D[i]))
 
+    def __len__(self) -> int:
+        return len(self.K)
+
     def fraction(self, i: int) -> Fraction:
         """Exact rank R_i = V_i / |pool|."""
         return Fraction(self.K[i], self.L * self.npool)
@@ -237,3 +240,39 @@ def rank_against(Pq, nkq, Ppool, nkpool, workers: int = 1) -> RankSet:
     C = numerator_matrix(Pq, Ppool, workers)
     D = denominator_matrix(nkq, nkpool)
     return RankSet(C, D)
+
+
+# ------------------------------------------------ d^F rank ----
+def d_F(F: float, delta: float = 0.02) -> float:
+    """Eq. 2: d^F = -ln(Delta + F), natural log; Delta = 0.02 is
+    SPEC's reading of the unstated "small constant" (reading Z2)."""
+    return -math.log(delta + F)
+
+
+class RankSetDF:
+    """Eq. 3 verbatim: R_i = (1/|pool|) sum_j d^{F(i,j)}, in fp64
+    with F = C/D correctly rounded, ``math.log`` and an exactly rounded sum
+    (``math.fsum``).  Not exact (the log is transcendental): ``values[i]``
+    is within a few ulp of the real-valued rank."""
+
+    def __init__(self, C: np.ndarray, D: np.ndarray, delta: float = 0.02):
+        self.npool = C.shape[1]
+        if self.npool == 0:
+            raise ValueError("empty pool")
+        self.delta = delta
+        self.values = []
+        for i in range(C.shape[0]):
+            terms = [d_F(similarity_f64(int(c), int(d)), delta) for c, d in zip(C[i].tolist(), D[i].tolist())]
+            self.values.append(math.fsum(terms) / self.npool)
+
+    def __len__(self) -> int:
+        return len(self.values)
+
+    def f64(self, i: int) -> float:
+        return self.values[i]
+
+
+def rank_against_dF(Pq, nkq, Ppool, nkpool, delta: float = 0.02, workers: int = 1) -> RankSetDF:
+    C = numerator_matrix(Pq, Ppool, workers)
+    D = denominator_matrix(nkq, nkpool)
+    return RankSetDF(C, D, delta)

@@ -86,10 +86,28 @@ class PartitionResult:
     def global_keys(self) -> list:
         return list(self.global_ranks.keys)
 
+    def local_f64(self) -> list:
+        return [rs.f64(i) for rs in self.local for i in range(len(rs))]
+
+    def global_f64(self) -> list:
+        return [self.global_ranks.f64(i) for i in range(len(self.global_ranks))]
+
+
+def _ranks(Pq, nkq, Ppool, nkpool, workers, rank_form, delta):
+    """(RankSet, key function) of a pool: exact F-form ranks ordered by K_i
+    (O1/O4), or the d^F form of Eq. 2-3 ordered by its fp64 value (N1)."""
+    if rank_form == "F":
+        rs = kmer.rank_against(Pq, nkq, Ppool, nkpool, workers)
+        return rs, (lambda i: rs.K[i])
+    rs = kmer.rank_against_dF(Pq, nkq, Ppool, nkpool, delta, workers)
+    return rs, (lambda i: rs.values[i])
+
 
 def partition(P: np.ndarray, nk: np.ndarray, p: int, samples_per_block: int,
-              workers: int = 1) -> PartitionResult:
-    """Algorithm 2 steps 1-11 on profiles ``P`` / ``nk`` of all N sequences."""
+              workers: int = 1, rank_form: str = "F", delta: float = 0.02) -> PartitionResult:
+    """Algorithm 2 steps 1-11 on profiles ``P`` / ``nk`` of all N sequences.
+    rank_form "F": mean similarity, exact (BASELINE.json O1); "dF": mean
+    d^F = -ln(Delta + F), Eq. 2-3 verbatim."""
     n = P.shape[0]
     if p < 1 or n < p:
         raise ValueError("need 1 <= p <= N")
@@ -100,29 +118,29 @@ def partition(P: np.ndarray, nk: np.ndarray, p: int, samples_per_block: int,
         lo, hi = bounds[q], bounds[q + 1]
         if samples_per_block > hi - lo:
             raise ValueError("samples_per_block > block size")
-        rs = kmer.rank_against(P[lo:hi], nk[lo:hi], P[lo:hi], nk[lo:hi], workers)
+        rs, rk = _ranks(P[lo:hi], nk[lo:hi], P[lo:hi], nk[lo:hi], workers, rank_form, delta)
         res.local.append(rs)
-        order = sorted(range(lo, hi), key=lambda i: (rs.K[i - lo], i))
+        order = sorted(range(lo, hi), key=lambda i: (rk(i - lo), i))
         res.local_order.append(order)
         res.sample_idx.extend(choose_local_samples(order, samples_per_block))
     # steps 5-6: global sample S, rank against it
     S = np.asarray(res.sample_idx, dtype=np.int64)
-    g = kmer.rank_against(P, nk, P[S], nk[S], workers)
+    g, gk = _ranks(P, nk, P[S], nk[S], workers, rank_form, delta)
     res.global_ranks = g
     # steps 7-8: block sort by global rank, p-1 regular samples per block
     Y = []
     for q in range(p):
         lo, hi = bounds[q], bounds[q + 1]
-        order = sorted(range(lo, hi), key=lambda i: (g.K[i], i))
+        order = sorted(range(lo, hi), key=lambda i: (gk(i), i))
         res.global_order.append(order)
         if p > 1:
             Y.extend(choose_local_samples(order, p - 1))
     # step 9: sort Y, pick pivots
-    res.candidates = sorted(Y, key=lambda i: (g.K[i], i))
+    res.candidates = sorted(Y, key=lambda i: (gk(i), i))
     res.pivots = select_pivots(res.candidates, p) if p > 1 else []
     # step 11: buckets
-    pk = [(g.K[i], i) for i in res.pivots]
-    res.bucket_of = np.array([assign_bucket((g.K[i], i), pk) for i in range(n)], dtype=np.int32)
+    pk = [(gk(i), i) for i in res.pivots]
+    res.bucket_of = np.array([assign_bucket((gk(i), i), pk) for i in range(n)], dtype=np.int32)
     res.buckets = [np.flatnonzero(res.bucket_of == b).astype(np.int64) for b in range(p)]
     return res
 

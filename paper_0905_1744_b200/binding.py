@@ -25,7 +25,9 @@ PHASES = ["S2a", "S2b", "S2c", "S2d", "S3", "S5", "rank"]
 
 EXPORTED = ["sa_ctx_create", "sa_ctx_attach_comm", "sa_ctx_destroy", "sa_last_error", "sa_launch_count",
             "sa_ctx_set_timing", "sa_ctx_phase_ms", "sa_profile_stride", "sa_kmer_profiles", "sa_kmer_rank",
-            "sa_partition", "sa_redistribute", "sa_bucket_similarity", "sa_exact_rank_compare", "sa_ctx_engine"]
+            "sa_partition", "sa_redistribute", "sa_bucket_similarity", "sa_exact_rank_compare", "sa_ctx_engine",
+            "sa_ctx_set_rank_form"]
+SA_RANK_F, SA_RANK_DF = 0, 1
 
 
 class SaError(RuntimeError):
@@ -57,7 +59,8 @@ class sa_partition_debug(ctypes.Structure):
     _fields_ = [("local_key", ctypes.c_void_p), ("local_f64", ctypes.c_void_p), ("local_order", ctypes.c_void_p),
                 ("sample_idx", ctypes.c_void_p), ("global_key", ctypes.c_void_p), ("global_f64", ctypes.c_void_p),
                 ("global_order", ctypes.c_void_p), ("candidates", ctypes.c_void_p),
-                ("exact_fallbacks_h", ctypes.POINTER(ctypes.c_int32))]
+                ("exact_fallbacks_h", ctypes.POINTER(ctypes.c_int32)),
+                ("uncertified_h", ctypes.POINTER(ctypes.c_int32))]
 
 
 _lib = None
@@ -92,6 +95,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "sa_bucket_similarity": (ctypes.c_int, [P, P, P, I32, I32, P, P, VP]),
         "sa_exact_rank_compare": (ctypes.c_int, [P, I32, P, I32, P, I32]),
         "sa_ctx_engine": (ctypes.c_int, [P]),
+        "sa_ctx_set_rank_form": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_double]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -182,6 +186,10 @@ class Context:
         """Operand encoding of the last min-sum launch ('u16', 'u8', 'u16imad')."""
         return {0: "u16", 1: "u8", 2: "u16imad"}.get(int(load_library().sa_ctx_engine(self.handle)), "none")
 
+    def set_rank_form(self, form: int = SA_RANK_F, delta: float = 0.02):
+        """SA_RANK_F (mean F, exact) or SA_RANK_DF (mean -ln(Delta + F), Eq. 2-3)."""
+        _check(load_library().sa_ctx_set_rank_form(self.handle, int(form), float(delta)))
+
     def set_timing(self, enable: bool = True):
         _check(load_library().sa_ctx_set_timing(self.handle, int(enable)))
 
@@ -235,6 +243,7 @@ class PartitionOut:
     bytes: np.ndarray              # int64 [nranks][p]
     debug: dict | None = None
     exact_fallbacks: int = 0
+    uncertified: int = 0
 
 
 def pivot_global_idx(pivots: torch.Tensor) -> torch.Tensor:
@@ -256,6 +265,7 @@ def sa_partition(ctx: Context, p: int, samples_per_block: int, profiles, nkmers,
     dbg_struct = None
     dbg = None
     fallbacks = ctypes.c_int32(0)
+    uncertified = ctypes.c_int32(0)
     if debug:
         s = p * samples_per_block
         dbg = {
@@ -271,7 +281,7 @@ def sa_partition(ctx: Context, p: int, samples_per_block: int, profiles, nkmers,
         dbg_struct = sa_partition_debug(*[_ptr(dbg[k]) for k in ["local_key", "local_f64", "local_order",
                                                                   "sample_idx", "global_key", "global_f64",
                                                                   "global_order", "candidates"]],
-                                        ctypes.pointer(fallbacks))
+                                        ctypes.pointer(fallbacks), ctypes.pointer(uncertified))
     _check(load_library().sa_partition(
         ctx.handle, p, samples_per_block, _ptr(profiles), _ptr(nkmers), _ptr(offsets), bins, n_total, first_global,
         n_local, _ptr(bucket_of), _ptr(pivots),
@@ -279,7 +289,8 @@ def sa_partition(ctx: Context, p: int, samples_per_block: int, profiles, nkmers,
         ctypes.byref(dbg_struct) if dbg_struct is not None else None, _stream(stream)))
     if dbg is not None:
         dbg["candidates"] = dbg["candidates"][:p * (p - 1)]
-    return PartitionOut(bucket_of, pivots[:max(p - 1, 0)], counts, nbytes, dbg, int(fallbacks.value))
+    return PartitionOut(bucket_of, pivots[:max(p - 1, 0)], counts, nbytes, dbg, int(fallbacks.value),
+                        int(uncertified.value))
 
 
 def owned_buckets(p: int, nranks: int, rank: int) -> range:

@@ -3,6 +3,7 @@
 // in profiles.cu / minsum.cu / order.cu; collectives through the caller's
 // sa_comm_ops (torch.distributed / NCCL in the Python binding).
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstdarg>
 #include <cstring>
@@ -102,6 +103,19 @@ struct Scratch {
 static inline int64_t block_begin(int64_t q, int64_t N, int64_t p) { return q * N / p; }
 
 static int32_t profile_stride(int32_t bins) { return stride_u16(bins); }
+
+// rank form of the context onto a key-producing problem (sa_ctx_set_rank_form)
+static inline void apply_form(const sa_ctx* c, MsProblem& pr) {
+  pr.form = c->rank_form;
+  pr.delta = c->delta;
+  pr.ln1pd = std::log1p(c->delta);
+}
+// key distance below which an order is not certified: npool for exact F keys
+// (2^64 V - npool < key <= 2^64 V); 32 npool for d^F keys (per-term log and
+// rounding error <= 16 units of 2^-52 on either side, DESIGN.md §2 N1)
+static inline int64_t window_of(const sa_ctx* c, int64_t npool) {
+  return c->rank_form == SA_RANK_DF ? 32 * npool : npool;
+}
 
 // Engine choice: SA_ENGINE = auto (default) | u16 | u16imad | u8 (u8 is still
 // only used when every count is <= 255; otherwise the exact u16 engine runs).
@@ -263,6 +277,16 @@ sa_status sa_ctx_destroy(sa_ctx* ctx) {
   if (ctx->dcount) cudaFree(ctx->dcount);
   if (ctx->hpinned) cudaFreeHost(ctx->hpinned);
   delete ctx;
+  return SA_OK;
+}
+
+sa_status sa_ctx_set_rank_form(sa_ctx* ctx, int form, double delta) {
+  g_err.clear();
+  if (!ctx) return fail(SA_E_INVAL, "ctx is NULL");
+  if (form != SA_RANK_F && form != SA_RANK_DF) return fail(SA_E_INVAL, "unknown rank form %d", form);
+  if (form == SA_RANK_DF && !(delta > 0.0 && std::isfinite(delta))) return fail(SA_E_INVAL, "Delta must be > 0");
+  ctx->rank_form = form;
+  if (form == SA_RANK_DF) ctx->delta = delta;
   return SA_OK;
 }
 
@@ -493,6 +517,7 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
       pr.na = pr.nb = (int32_t)(e - b);
       pr.sym = 1;
       pr.keyA = pr.keyB = lkey + b;
+      apply_form(c, pr);
       probs.push_back(pr);
     }
     SA_TRY(launch_ops(c, E, probs, st, nullptr, nullptr));
@@ -501,7 +526,8 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
 
   // ---- S2b: sort each block by (local rank, index); k_b samples
   SA_TRY(rec(ev_begin(c, SA_PHASE_S2B), st));
-  SA_TRY(segment_sort_keys(lkey, a.first, a.N, a.p, q0, a.first, pb, wmax, lorder, nullptr, amb_cnt + 0, st));
+  SA_TRY(segment_sort_keys(lkey, a.first, a.N, a.p, q0, a.first, pb, window_of(c, wmax), lorder, nullptr,
+                           amb_cnt + 0, st));
   if (exact) {
     uint32_t h = 0;
     SA_TRY(read_u32(amb_cnt + 0, &h, st));
@@ -537,13 +563,15 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
     pr.nb = s_all;
     pr.sym = 0;
     pr.keyA = gkey;
+    apply_form(c, pr);
     SA_TRY(launch_ops(c, E2, {pr}, st, nullptr, nullptr));
   }
   SA_TRY(rec(ev_end(c, SA_PHASE_S2D), st));
 
   // ---- S3: block sort, regular samples, pivots, buckets
   SA_TRY(rec(ev_begin(c, SA_PHASE_S3), st));
-  SA_TRY(segment_sort_keys(gkey, a.first, a.N, a.p, q0, a.first, pb, s_all, gorder, nullptr, amb_cnt + 1, st));
+  SA_TRY(segment_sort_keys(gkey, a.first, a.N, a.p, q0, a.first, pb, window_of(c, s_all), gorder, nullptr,
+                           amb_cnt + 1, st));
   if (exact) {
     uint32_t h = 0;
     SA_TRY(read_u32(amb_cnt + 1, &h, st));
@@ -566,7 +594,7 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
     SA_TRY(pick_launch(gorder, a.N, a.p, q0, a.first, pb, a.p - 1, a.p, a.first, cand_gid, cand_local, st));
     SA_TRY(make_records_launch(cand_local, cand_gid, ncand_loc, gkey, a.nk, a.p - 1, (int)q0, rec_loc, st));
     SA_TRY(comm_allgather(c, rec_loc, rec_all, (int64_t)ncand_loc * sizeof(sa_pivot), st));
-    SA_TRY(sort_records(rec_all, ncand, s_all, tmp_k, tmp_g, yorder, nullptr, amb_cnt + 2, st));
+    SA_TRY(sort_records(rec_all, ncand, window_of(c, s_all), tmp_k, tmp_g, yorder, nullptr, amb_cnt + 2, st));
 
     std::vector<uint16_t> candC;        // exact path: C rows of every candidate vs S
     std::vector<sa_pivot> rec_h;
@@ -605,8 +633,8 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
       SA_CUDA(cudaMemcpyAsync(yorder, yo.data(), ncand * sizeof(int32_t), cudaMemcpyHostToDevice, st));
     }
     SA_TRY(pivots_launch(rec_all, yorder, ncand, a.p, y_gid, a.pivots, st));
-    SA_TRY(assign_launch(gkey, a.first, n, a.pivots, a.p, s_all, a.offs, a.bucket_of, nullptr, amb_cnt + 3, counts_d,
-                         counts_d + a.p, st));
+    SA_TRY(assign_launch(gkey, a.first, n, a.pivots, a.p, window_of(c, s_all), a.offs, a.bucket_of, nullptr,
+                         amb_cnt + 3, counts_d, counts_d + a.p, st));
     if (exact) {
       uint32_t h = 0;
       SA_TRY(read_u32(amb_cnt + 3, &h, st));
@@ -707,9 +735,11 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
       for (int q = 0; q < pb; ++q) {
         const int64_t b = block_begin(q0 + q, a.N, a.p) - a.first;
         const int64_t e = block_begin(q0 + q + 1, a.N, a.p) - a.first;
-        if (d->local_f64) SA_TRY(keys_to_f64_launch(lkey + b, e - b, e - b, d->local_f64 + b, st));
+        if (d->local_f64)
+          SA_TRY(keys_to_f64_launch(lkey + b, e - b, e - b, d->local_f64 + b, st, c->rank_form, std::log1p(c->delta)));
       }
-      if (d->global_f64) SA_TRY(keys_to_f64_launch(gkey, n, s_all, d->global_f64, st));
+      if (d->global_f64)
+        SA_TRY(keys_to_f64_launch(gkey, n, s_all, d->global_f64, st, c->rank_form, std::log1p(c->delta)));
     }
     if (d->local_order) {
       // order (segment offsets) -> global ids
@@ -807,8 +837,9 @@ sa_status sa_kmer_rank(sa_ctx* ctx, const uint16_t* q_prof, const int32_t* q_nk,
   pr.keyB = pr.sym ? keys : nullptr;
   pr.num = numerators;
   pr.ld = npool;
+  apply_form(ctx, pr);
   SA_TRY(launch_ops(ctx, E, {pr}, st, ev_begin(ctx, SA_PHASE_RANK), ev_end(ctx, SA_PHASE_RANK)));
-  if (rank_f64) SA_TRY(keys_to_f64_launch(keys, nq, npool, rank_f64, st));
+  if (rank_f64) SA_TRY(keys_to_f64_launch(keys, nq, npool, rank_f64, st, ctx->rank_form, std::log1p(ctx->delta)));
   return SA_OK;
 }
 
@@ -845,7 +876,8 @@ sa_status sa_partition(sa_ctx* ctx, int32_t p, int32_t samples_per_block, const 
   int64_t amb = 0;
   int resolved = 0;
   SA_TRY(partition_pass(ctx, a, false, &amb, &resolved, st));
-  if (amb > 0) {
+  if (dbg && dbg->uncertified_h) *dbg->uncertified_h = ctx->rank_form == SA_RANK_DF ? (int32_t)amb : 0;
+  if (amb > 0 && ctx->rank_form == SA_RANK_F) {
     // some order was not certified by the keys on some rank: redo the pass
     // with exact resolution everywhere (collectively -- every rank saw amb).
     SA_TRY(partition_pass(ctx, a, true, &amb, &resolved, st));

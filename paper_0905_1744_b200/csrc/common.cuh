@@ -66,7 +66,14 @@ struct MsProblem {
   uint16_t* num;           // [na][ld] numerators (nullable)
   double* sim;             // [na][ld] C/D (nullable)
   int64_t ld;
+  int32_t form;            // SA_RANK_F: key += floor(C 2^64 / D); SA_RANK_DF: key += dF term (below)
+  double delta;            // SA_RANK_DF: the Delta of Eq. 2
+  double ln1pd;            // SA_RANK_DF: ln(1 + Delta) (host-computed)
 };
+
+// d^F key term (Eq. 2): round(2^52 (ln(1+Delta) - ln(Delta + F)))
+// >= 0, so sum_j d^F(i, j) = key_i 2^-52 - npool ln(1+Delta).
+constexpr double DF_SCALE = 4503599627370496.0;   // 2^52
 
 // Profile encodings the engine reads:
 //   ENC_U16_MIN       uint16 counts, 2 bins/word, VIMNMX.U16x2 + IADD3 (any count)
@@ -107,9 +114,10 @@ sa_status record_sort_launch(const sa_pivot* rec, int n, int64_t window, int32_t
 
 double u128_to_double_host(uint64_t hi, uint64_t lo);
 
-// keys -> fp64 ranks: RN(key) * 2^-64 / npool.
+// keys -> fp64 ranks: RN(key) * 2^-64 / npool (F form) or
+// RN(key) * 2^-52 / npool - ln(1+Delta) (d^F form).
 sa_status keys_to_f64_launch(const sa_key128* keys, int64_t n, int64_t npool, double* out,
-                             cudaStream_t st);
+                             cudaStream_t st, int form = SA_RANK_F, double ln1pd = 0.0);
 
 // ---------------------------------------------------- exact fallback ----
 // Exact comparison of V_a = sum_j Ca_j / Da_j and V_b (rows over the same
@@ -129,6 +137,8 @@ struct sa_ctx {
   cudaEvent_t ev[2 * SA_PHASE_COUNT] = {};
   bool ev_used[SA_PHASE_COUNT] = {};
   int last_enc = -1;            // ENC_* of the last min-sum call, or ENC_AUTO
+  int rank_form = SA_RANK_F;    // sa_ctx_set_rank_form
+  double delta = 0.02;
   uint32_t* dcount = nullptr;   // device: largest count of the last auto-dispatched call
   uint32_t* hpinned = nullptr;  // pinned host word for small readbacks
 };

@@ -78,6 +78,22 @@ __device__ __forceinline__ void add_term(uint64_t& lo, uint32_t& hi, uint32_t C,
   hi += (lo < t) ? 1u : 0u;
 }
 
+// d^F key term: round(2^52 (ln(1+Delta) - ln(Delta + C/D))), F = 0 when D = 0.
+__device__ __forceinline__ void add_dF_term(uint64_t& lo, uint32_t& hi, uint32_t C, uint32_t D, double delta,
+                                            double ln1pd) {
+  const double F = D > 0 ? __ddiv_rn((double)C, (double)D) : 0.0;
+  double t = ln1pd - log(delta + F);
+  t = t > 0.0 ? t : 0.0;
+  const uint64_t q = __double2ull_rn(t * DF_SCALE);
+  lo += q;
+  hi += (lo < q) ? 1u : 0u;
+}
+
+__device__ __forceinline__ void key_term(const MsProblem& P, uint64_t& lo, uint32_t& hi, uint32_t C, uint32_t D) {
+  if (P.form == SA_RANK_DF) add_dF_term(lo, hi, C, D, P.delta, P.ln1pd);
+  else add_term(lo, hi, C, D);
+}
+
 __device__ __forceinline__ void atomic_add_key(sa_key128* k, uint64_t lo, uint64_t hi) {
   unsigned long long old = atomicAdd(reinterpret_cast<unsigned long long*>(&k->lo), (unsigned long long)lo);
   uint64_t carry = ((uint64_t)old + lo < (uint64_t)old) ? 1ull : 0ull;
@@ -260,7 +276,7 @@ __device__ __forceinline__ void tile_epilogue(const MsProblem& P, const TileInfo
         for (int j = 0; j < TN; ++j) {
           if (nkc[j] < 0) continue;
           const uint32_t C = acc_to_C<ENC>(acc[i][j], nkr[i], nkc[j]);
-          add_term(lo, hi, C, (uint32_t)min(nkr[i], nkc[j]));
+          key_term(P, lo, hi, C, (uint32_t)min(nkr[i], nkc[j]));
         }
       }
       shfl_add(lo, hi, 1);
@@ -279,7 +295,7 @@ __device__ __forceinline__ void tile_epilogue(const MsProblem& P, const TileInfo
           for (int i = 0; i < 8; ++i) {
             if (nkr[i] < 0) continue;
             const uint32_t C = acc_to_C<ENC>(acc[i][j], nkr[i], nkc[j]);
-            add_term(lo, hi, C, (uint32_t)min(nkr[i], nkc[j]));
+            key_term(P, lo, hi, C, (uint32_t)min(nkr[i], nkc[j]));
           }
         }
         shfl_add(lo, hi, 8);
@@ -747,18 +763,24 @@ __host__ __device__ inline double u128_to_double(uint64_t hi, uint64_t lo) {
 
 double u128_to_double_host(uint64_t hi, uint64_t lo) { return u128_to_double(hi, lo); }
 
-__global__ void keys_to_f64_kernel(const sa_key128* __restrict__ keys, int64_t n, double inv_scale_den,
+__global__ void keys_to_f64_kernel(const sa_key128* __restrict__ keys, int64_t n, int form, double ln1pd,
                                    int64_t npool, double* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double v = ldexp(u128_to_double(keys[i].hi, keys[i].lo), -64);
-    out[i] = __ddiv_rn(v, (double)npool);
+    if (form == SA_RANK_DF) {
+      const double v = ldexp(u128_to_double(keys[i].hi, keys[i].lo), -52);
+      out[i] = __ddiv_rn(v, (double)npool) - ln1pd;
+    } else {
+      const double v = ldexp(u128_to_double(keys[i].hi, keys[i].lo), -64);
+      out[i] = __ddiv_rn(v, (double)npool);
+    }
   }
 }
 
-sa_status keys_to_f64_launch(const sa_key128* keys, int64_t n, int64_t npool, double* out, cudaStream_t st) {
+sa_status keys_to_f64_launch(const sa_key128* keys, int64_t n, int64_t npool, double* out, cudaStream_t st,
+                             int form, double ln1pd) {
   if (n <= 0) return SA_OK;
   const int64_t blocks = (n + 255) / 256;
-  keys_to_f64_kernel<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(keys, n, 0.0, npool, out);
+  keys_to_f64_kernel<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(keys, n, form, ln1pd, npool, out);
   SA_LAUNCHED();
   return SA_OK;
 }

@@ -332,3 +332,61 @@ def test_hot_path_full_size_sampled(ctx):
         blk = num[:200, :200].cpu().numpy()
         assert np.array_equal(blk, blk.T)
         assert np.all(np.diag(sim[:200, :200].cpu().numpy()) == 1.0)
+
+
+# ------------------------------------------------- d^F rank ----
+def _close(a, b, tol=1e-12):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    assert np.all(np.abs(a - b) <= tol * np.maximum(1.0, np.abs(b))), np.max(np.abs(a - b))
+
+
+@pytest.mark.parametrize("nq,npool", [(300, 200), (5, 700)])
+def test_kmer_rank_dF_form(ctx, engine, nq, npool):
+    ds = _rand_set(nq * 31 + npool, nq + npool, 0, 420, dup=2)
+    res, offs = to_dev(ds)
+    P, nk = B.sa_kmer_profiles(ctx, res, offs)
+    Po, nko = kmer.profiles(ds.residues, ds.offsets)
+    p0 = max(0, nq - npool // 3)
+    ctx.set_rank_form(B.SA_RANK_DF, 0.02)
+    try:
+        keys, f64, _ = B.sa_kmer_rank(ctx, P[:nq], nk[:nq], P[p0:p0 + npool], nk[p0:p0 + npool])
+    finally:
+        ctx.set_rank_form(B.SA_RANK_F)
+    C = kmer.numerator_matrix(Po[:nq], Po[p0:p0 + npool])
+    rs = kmer.RankSetDF(C, kmer.denominator_matrix(nko[:nq], nko[p0:p0 + npool]), 0.02)
+    _close(f64.cpu().numpy(), rs.values)
+
+
+def test_rank_form_errors(ctx):
+    with pytest.raises(B.SaError):
+        ctx.set_rank_form(7)
+    with pytest.raises(B.SaError):
+        ctx.set_rank_form(B.SA_RANK_DF, 0.0)
+
+
+@pytest.mark.parametrize("c", [1, 2, 5])
+def test_partition_dF_matches_oracle(ctx, c):
+    """The paper's own distance rank (Eq. 2-3): orders, samples, pivots and
+    buckets equal the oracle's wherever the fp64 window certifies them (here:
+    everywhere, `uncertified == 0`); ranks within 1e-12."""
+    cfg = CONFIGS[c]
+    ds = generate(cfg)
+    res, offs = to_dev(ds)
+    P, nk = B.sa_kmer_profiles(ctx, res, offs)
+    ctx.set_rank_form(B.SA_RANK_DF, 0.02)
+    try:
+        part = B.sa_partition(ctx, cfg.p, cfg.samples_per_block, P, nk, offs, 8000, ds.n, 0, debug=True)
+    finally:
+        ctx.set_rank_form(B.SA_RANK_F)
+    Po, nko = kmer.profiles(ds.residues, ds.offsets)
+    o = partition.partition(Po, nko, cfg.p, cfg.samples_per_block, workers=kmer.default_workers(), rank_form="dF")
+    d = part.debug
+    assert part.uncertified == 0
+    _close(d["local_f64"].cpu().numpy(), o.local_f64())
+    _close(d["global_f64"].cpu().numpy(), o.global_f64())
+    assert d["local_order"].cpu().numpy().tolist() == [i for q in o.local_order for i in q]
+    assert d["sample_idx"].cpu().numpy().tolist() == o.sample_idx
+    assert d["global_order"].cpu().numpy().tolist() == [i for q in o.global_order for i in q]
+    assert d["candidates"].cpu().numpy().tolist() == o.candidates
+    assert B.pivot_global_idx(part.pivots).cpu().numpy().tolist() == o.pivots
+    assert np.array_equal(part.bucket_of.cpu().numpy(), o.bucket_of)

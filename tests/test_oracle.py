@@ -3,6 +3,7 @@ something other than itself: SPEC/paper worked examples (tests/golden), brute
 force enumeration, closed forms, exact ``Fraction`` arithmetic or invariants
 the paper proves."""
 import itertools
+import math
 import json
 import os
 from collections import Counter
@@ -325,3 +326,53 @@ def test_bucket_similarity_diagonal_symmetry():
         assert F[i, i] == (1.0 if nk[i] >= 1 else 0.0)
         for j in range(15):
             assert F[i, j] == float(kmer.similarity(P[i], P[j], nk[i], nk[j]))
+
+
+# ------------------------------------------------- d^F rank ----
+def test_dF_spec_examples():
+    """SPEC S:124-126, S:133-134, S:141-143 with Delta = 0.02.  SPEC's
+    hand-computed 0.37594 / 0.17807 carry a rounding slip of ~4e-5 (the exact
+    values are 0.375906 / 0.178050), hence abs = 1e-4 on those two."""
+    assert kmer.d_F(1.0) == pytest.approx(-0.01980, abs=5e-6)
+    assert kmer.d_F(2 / 3) == pytest.approx(0.37594, abs=1e-4)
+    assert kmer.d_F(0.0) == pytest.approx(3.91202, abs=5e-6)
+    # pool [X, Y] with F(X,Y) = 2/3: R_X = (d(X,X) + d(X,Y)) / 2
+    x, y = codes("ACAC"), codes("ACCA")
+    px, py = kmer.profile(x, 2, 20), kmer.profile(y, 2, 20)
+    C = np.array([[kmer.numerator(px, px), kmer.numerator(px, py)]])
+    D = np.array([[3, 3]])
+    assert kmer.RankSetDF(C, D).values[0] == pytest.approx(0.17807, abs=1e-4)
+    # pool = [X]: -ln(1 + Delta); two disjoint samples: -ln(Delta)
+    assert kmer.RankSetDF(np.array([[3]]), np.array([[3]])).values[0] == pytest.approx(-math.log(1.02), rel=1e-15)
+    assert kmer.RankSetDF(np.array([[0, 0]]), np.array([[3, 5]])).values[0] == pytest.approx(-math.log(0.02),
+                                                                                            rel=1e-15)
+
+
+def test_dF_rank_is_mean_distance_and_order_reverses_monotone_case():
+    """R^dF is the plain mean of -ln(Delta + F); when every F of one query
+    dominates the other's term by term, its distance rank is smaller."""
+    rng = np.random.default_rng(4)
+    for _ in range(50):
+        npool = int(rng.integers(1, 20))
+        D = rng.integers(1, 40, size=(2, npool))
+        C = np.minimum((rng.random((2, npool)) * (D + 1)).astype(np.int64), D)
+        D[1] = D[0]
+        C[1] = np.minimum(C[0] + rng.integers(0, 3, size=npool), D[0])   # F1 >= F0 termwise
+        rs = kmer.RankSetDF(C, D)
+        want = [sum(-math.log(0.02 + (c / d)) for c, d in zip(C[i], D[i])) / npool for i in range(2)]
+        assert rs.values == pytest.approx(want, rel=1e-14)
+        assert rs.values[1] <= rs.values[0]
+
+
+def test_dF_partition_closed_form_and_invariants():
+    with open(os.path.join(os.path.dirname(__file__), "golden", "closed_form_partitions.json")) as f:
+        c = json.load(f)["cases"][1]
+    P, nk = _identical(c["N"])
+    r = partition.partition(P, nk, c["p"], c["samples_per_block"], rank_form="dF")
+    assert r.pivots == c["pivots"] and [len(b) for b in r.buckets] == c["sizes"]
+    ds = generate(CONFIGS[1])
+    P, nk = kmer.profiles(ds.residues, ds.offsets)
+    r = partition.partition(P, nk, 4, 16, rank_form="dF")
+    allm = np.concatenate(r.buckets)
+    assert np.array_equal(np.sort(allm), np.arange(ds.n))
+    assert max(len(b) for b in r.buckets) <= 2 * ds.n / 4
