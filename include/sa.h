@@ -81,7 +81,8 @@ typedef struct {
 /* ------------------------------------------------------------ context ---- */
 sa_status sa_ctx_create(int cuda_device, sa_ctx** out);
 /* Attach a communicator (collective semantics: every rank attaches with the
- * same nranks).  nranks == 1 (or never attaching) makes every exchange a
+ * same nranks).  Once callbacks are attached every exchange goes through them,
+ * also for nranks == 1; a context that never attaches makes every exchange a
  * local copy.  `ops` is copied; its `user` pointer must stay valid. */
 sa_status sa_ctx_attach_comm(sa_ctx* ctx, const sa_comm_ops* ops, int nranks, int rank);
 sa_status sa_ctx_destroy(sa_ctx* ctx);

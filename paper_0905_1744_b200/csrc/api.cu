@@ -264,7 +264,10 @@ sa_status sa_ctx_attach_comm(sa_ctx* ctx, const sa_comm_ops* ops, int nranks, in
     return fail(SA_E_INVAL, "nranks > 1 needs allgather and alltoallv callbacks");
   ctx->nranks = nranks;
   ctx->rank = rank;
-  ctx->has_comm = nranks > 1;
+  // attached callbacks are used even for one rank (exercises the collective
+  // path end to end, e.g. a 1-rank NCCL group); without them, exchanges are
+  // local copies
+  ctx->has_comm = ops && ops->allgather && ops->alltoallv;
   if (ops) ctx->comm = *ops;
   return SA_OK;
 }
@@ -336,7 +339,7 @@ static inline sa_status rec(cudaEvent_t e, cudaStream_t st) {
 }
 
 static sa_status comm_allgather(sa_ctx* c, const void* send, void* recv, int64_t bytes, cudaStream_t st) {
-  if (c->nranks == 1) {
+  if (!c->has_comm) {
     if (send != recv && bytes > 0) SA_CUDA(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, st));
     return SA_OK;
   }
@@ -908,7 +911,7 @@ sa_status sa_redistribute(sa_ctx* ctx, int32_t p, const uint8_t* residues, const
   SA_ALLOC(lens, int64_t, std::max(n, 1));
   SA_ALLOC(part, int64_t, (n + 1023) / 1024 + 2);
   SA_TRY(bucket_perm_launch(bucket_of, n, p, hist, base, perm, st));
-  if (G == 1) {
+  if (!ctx->has_comm) {   // single rank, no communicator: the send layout is the receive layout
     SA_TRY(perm_meta_launch(perm, n, offsets, bucket_of, first_global, lens, recv_global_idx, recv_bucket, st));
     SA_TRY(scan_launch(lens, n, recv_offsets, part, st));
     SA_TRY(copy_seqs_launch(perm, n, residues, offsets, recv_residues, recv_offsets, st));

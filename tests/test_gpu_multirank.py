@@ -106,3 +106,44 @@ def test_rank_count_invariance(c, Gs):
         for o in outs:
             for (b, n, x), s in zip(o["num"], o["sim"]):
                 assert np.array_equal(x, ref_num[b]) and np.array_equal(s, ref_sim[b])
+
+
+def test_nccl_communicator_one_rank_matches():
+    """The torch.distributed / NCCL communicator (TorchComm) driven by libsa's
+    callbacks on a 1-rank NCCL group: every collective of sa_partition and
+    sa_redistribute goes through all_gather_into_tensor / all_to_all_single on
+    raw device buffers and the caller's stream; results equal the golden."""
+    require_gpu()
+    import socket
+
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cfg = CONFIGS[2]
+    ds = generate(cfg)
+    g, meta = load_golden(2)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        ctx = B.Context(0)
+        comm = B.TorchComm(device="cuda")
+        ctx.attach_comm(comm)
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            res = torch.from_numpy(ds.residues.copy()).cuda()
+            offs = torch.from_numpy(ds.offsets.copy()).cuda()
+            out = HotPath(ctx, cfg.p, cfg.samples_per_block).step(res, offs, ds.n, 0, debug=True)
+        torch.cuda.synchronize()
+        assert not comm.errors, comm.errors
+        assert np.array_equal(out.part.bucket_of.cpu().numpy(), g["bucket_of"])
+        assert np.array_equal(out.part.debug["sample_idx"].cpu().numpy(), g["sample_idx"])
+        assert np.array_equal(out.part.debug["candidates"].cpu().numpy(), g["candidates"])
+        gid = out.recv_global_idx.cpu().numpy()
+        assert np.array_equal(gid, np.concatenate([np.flatnonzero(g["bucket_of"] == b) for b in range(cfg.p)]))
+        rr, ro = out.recv_residues.cpu().numpy(), out.recv_offsets.cpu().numpy()
+        for j in range(0, len(gid), 97):
+            assert np.array_equal(rr[ro[j]:ro[j + 1]], ds.seq(int(gid[j])))
+    finally:
+        dist.destroy_process_group()
