@@ -392,6 +392,13 @@ def main():
             "partition_ms": part_ms_max, "s5_ms": s5_ms_max,
             "pairs_per_step": {"S2a": s2a_pairs, "S2d": s2d_pairs, "S5": s5_pairs},
             "s5_pairs_per_s": s5_pairs / (s5_ms_max / 1e3),
+            # rank-0 views of the other rows of the BASELINE.md reporting template
+            "s2_pairs_per_s_rank0": (s2a_pairs + s2d_pairs) / world / ((phases["S2a"] + phases["S2d"]) / 1e3),
+            "s1_hbm_rank0": {
+                "bytes": int(res_h.numel() + offs_h.numel() * 8 + (last - first) * (16000 + 4)),
+                "ms": phases["S1"],
+                "frac_of_hbm": (res_h.numel() + offs_h.numel() * 8 + (last - first) * 16004) /
+                               (phases["S1"] / 1e3) / (float(peaks.get("hbm_gbs", 6551.0)) * 1e9)},
             "phases_ms_rank0": phases, "bucket_sizes": [int(x) for x in sizes],
             "exact_fallbacks": out.part.exact_fallbacks,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
