@@ -15,8 +15,10 @@ value   = k-mer similarity sequence-pairs evaluated per second by the whole job
 e2e     = the same through the public API with the step's inputs copied from
           pinned host memory and its results (buckets, member ids, uint16
           numerator matrices) copied back inside the timed region;
-roofline= the dominant kernel (K2 min-sum, S5 launches) in bin-ops/s against
-          the derived integer-pipe peak (DESIGN.md §4);
+roofline= the dominant kernel over the S5 launches: K2T (tensor-core threshold
+          layers, default) in TOP/s against the u8 tensor peak (DESIGN.md
+          §4b), or K2 (SAD / u16 fallback) in bin-ops/s against the derived
+          integer-pipe peak (DESIGN.md §4);
 cpu_baseline = the CPU oracle (oracle/, as it stands) on a bounded sample of
           the same workload, on the host's cores (rank 0, N = 1 only).
 """
@@ -292,25 +294,56 @@ def main():
     sm_mhz_peak = float(peaks.get("sm_max_mhz", 1965.0))
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     engine = ctx.engine()
-    per_clk = BINOPS_PER_SM_CLK[engine]
-    peak_binops = per_clk * nsm * sm_mhz_peak * 1e6
     own = list(B.owned_buckets(cfg.p, world, rank))
     my_s5_pairs = sum(int(sizes[b]) * (int(sizes[b]) - 1) // 2 for b in own)
-    achieved = my_s5_pairs * EPS_BINS / (s5_ms / 1e3)
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "k2_traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
-    roof = {"bound": "alu", "kernel": f"minsum_kernel<sym, {engine}> (K2, S5 bucket matrices)",
-            "engine": engine,
-            "achieved": achieved / 1e12, "peak": peak_binops / 1e12, "unit": "Tbin-op/s",
-            "frac": achieved / peak_binops, "traffic": traffic,
-            "peak_source": (f"derived ({peak_src} sm_max_mhz): {per_clk} bin-ops/clk/SM = ALU pipe 2 warp-instr/"
-                            f"clk/SM (ncu sm__inst_executed_pipe_alu peak) x 32 lanes x {per_clk // 64} bins per "
-                            f"{'VABSDIFF4.U8.ACC' if engine == 'u8' else 'VIMNMX.U16x2'} x {nsm} SMs "
-                            f"x {sm_mhz_peak:.0f} MHz"),
-            "algorithmic": f"{EPS_BINS} bin-ops per pair x {my_s5_pairs} pairs / S5 CUDA-event time"}
+    if engine == "tc":
+        # K2T: the S5 buckets as exact 0/1 threshold-layer
+        # contractions on the tensor cores; algorithmic work = 2 K'_b ops per
+        # pair (K'_b = kept layer columns of bucket b, read back after the timed
+        # region by re-running each bucket once) against the u8 tensor peak.
+        kcols = {}
+        for b, row, n_b in out.buckets:
+            if n_b > 1:
+                B.sa_bucket_similarity(ctx, out.bucket_profiles[row:row + n_b], out.bucket_nkmers[row:row + n_b],
+                                       hp.bins, numerators=out.numerators[own.index(b)],
+                                       similarity=out.similarity[own.index(b)],
+                                       want_similarity=not args.no_similarity)
+                kcols[b] = ctx.tc_columns()[0]
+        ops = sum(2.0 * kcols[b] * int(sizes[b]) * (int(sizes[b]) - 1) / 2 for b in kcols)
+        bf16 = float(peaks.get("bf16_tflops", 1590.0))
+        peak = 2.0 * bf16 * 1e12          # u8 dense = 2 x bf16 dense (4.5 / 2.25 PF nominal)
+        achieved = ops / (s5_ms / 1e3)
+        tpath = os.path.join(ROOT, "profiles", "k2t_traffic.json")
+        if os.path.exists(tpath):
+            with open(tpath) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        roof = {"bound": "tensor", "kernel": "tc::gemm_kernel<KeyMatEpi> (K2T, S5 bucket matrices)",
+                "engine": engine, "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TOP/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "peak_source": (f"{peak_src} bf16_tflops {bf16:.1f} (burst, MEASURED_PEAKS.json) x 2 = u8 dense "
+                                f"(nominal 4.5 / 2.25 PF ratio)"),
+                "algorithmic": (f"2 K'_b ops per pair, K'_b = kept threshold-layer columns "
+                                f"{[kcols[b] for b in sorted(kcols)]} x {my_s5_pairs} pairs / S5 phase CUDA-event "
+                                f"time (includes the operand build kernels)"),
+                "binops_per_s_equiv": my_s5_pairs * EPS_BINS / (s5_ms / 1e3) / 1e12}
+    else:
+        per_clk = BINOPS_PER_SM_CLK[engine]
+        peak_binops = per_clk * nsm * sm_mhz_peak * 1e6
+        achieved = my_s5_pairs * EPS_BINS / (s5_ms / 1e3)
+        tpath = os.path.join(ROOT, "profiles", "k2_traffic.json")
+        if os.path.exists(tpath):
+            with open(tpath) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        roof = {"bound": "alu", "kernel": f"minsum_kernel<sym, {engine}> (K2, S5 bucket matrices)",
+                "engine": engine,
+                "achieved": achieved / 1e12, "peak": peak_binops / 1e12, "unit": "Tbin-op/s",
+                "frac": achieved / peak_binops, "traffic": traffic,
+                "peak_source": (f"derived ({peak_src} sm_max_mhz): {per_clk} bin-ops/clk/SM = ALU pipe 2 warp-"
+                                f"instr/clk/SM (ncu sm__inst_executed_pipe_alu peak) x 32 lanes x {per_clk // 64} "
+                                f"bins per {'VABSDIFF4.U8.ACC' if engine == 'u8' else 'VIMNMX.U16x2'} x {nsm} SMs "
+                                f"x {sm_mhz_peak:.0f} MHz"),
+                "algorithmic": f"{EPS_BINS} bin-ops per pair x {my_s5_pairs} pairs / S5 CUDA-event time"}
 
     # --------------------------------------------- end-to-end (host buffers)
     e2e = None
@@ -381,7 +414,8 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u16",
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": {"tc": "u8 (0/1 threshold layers, s32 accumulate)", "u8": "u8"}.get(engine, "u16"),
             "data": "synthetic (seeded star-phylogeny protein families, sa_synth)",
             "config": {"workload": workload_desc(cfg), "N": ds.n, "p": cfg.p,
                        "samples_per_block": cfg.samples_per_block, "k": cfg.k, "alphabet": cfg.alphabet,

@@ -107,8 +107,20 @@ sa_status sa_ctx_set_timing(sa_ctx* ctx, int enable);
 /* Operand encoding of the last min-sum launch on this context:
  * 0 = uint16 counts (VIMNMX.U16x2 min + add; any count), 1 = uint8 counts
  * (C = (nk_a + nk_b - sum|a-b|)/2 with VABSDIFF4.U8.ACC; used when every
- * count is <= 255), 2 = uint16 with FMA-pipe adds (SA_ENGINE=u16imad). */
+ * count is <= 255), 2 = uint16 with FMA-pipe adds (SA_ENGINE=u16imad),
+ * 4 = tensor cores: 0/1 threshold layers min(a,b) = sum_r [a>=r][b>=r] as a
+ * u8 tcgen05 GEMM (K2T; the default when every count is <= 32
+ * and the kept layer columns fit, else the call falls back to 1 / 0 on the
+ * device).  SA_ENGINE = auto|tc (default), sad|u8 (no K2T), u16, u16imad.
+ * In the auto modes this call synchronises the device to read the choice. */
 int sa_ctx_engine(const sa_ctx* ctx);
+/* K2T only: the kept threshold-layer columns K' of each problem of the last
+ * min-sum call on this context (the contraction length per pair; DESIGN.md
+ * §4b), in call order, at most `max` of them.  Returns how many were written
+ * (0 when the last call did not run K2T, -1 on a CUDA error).  Synchronises
+ * the device.  Problems are: one per block (sa_partition S2a), one (S2d,
+ * sa_kmer_rank), one per sa_bucket_similarity call. */
+int32_t sa_ctx_tc_columns(const sa_ctx* ctx, int32_t* cols_h, int32_t max);
 sa_status sa_ctx_phase_ms(sa_ctx* ctx, float* ms_h /* [SA_PHASE_COUNT] */);
 
 /* Rank form used by sa_kmer_rank and sa_partition on this context.

@@ -26,7 +26,7 @@ PHASES = ["S2a", "S2b", "S2c", "S2d", "S3", "S5", "rank"]
 EXPORTED = ["sa_ctx_create", "sa_ctx_attach_comm", "sa_ctx_destroy", "sa_last_error", "sa_launch_count",
             "sa_ctx_set_timing", "sa_ctx_phase_ms", "sa_profile_stride", "sa_kmer_profiles", "sa_kmer_rank",
             "sa_partition", "sa_redistribute", "sa_bucket_similarity", "sa_exact_rank_compare", "sa_ctx_engine",
-            "sa_ctx_set_rank_form"]
+            "sa_ctx_set_rank_form", "sa_ctx_tc_columns"]
 SA_RANK_F, SA_RANK_DF = 0, 1
 
 
@@ -95,6 +95,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "sa_bucket_similarity": (ctypes.c_int, [P, P, P, I32, I32, P, P, VP]),
         "sa_exact_rank_compare": (ctypes.c_int, [P, I32, P, I32, P, I32]),
         "sa_ctx_engine": (ctypes.c_int, [P]),
+        "sa_ctx_tc_columns": (ctypes.c_int32, [P, P, ctypes.c_int32]),
         "sa_ctx_set_rank_form": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_double]),
     }
     for name, (res, args) in sig.items():
@@ -184,7 +185,16 @@ class Context:
 
     def engine(self) -> str:
         """Operand encoding of the last min-sum launch ('u16', 'u8', 'u16imad')."""
-        return {0: "u16", 1: "u8", 2: "u16imad"}.get(int(load_library().sa_ctx_engine(self.handle)), "none")
+        return {0: "u16", 1: "u8", 2: "u16imad", 4: "tc"}.get(int(load_library().sa_ctx_engine(self.handle)), "none")
+
+    def tc_columns(self) -> list[int]:
+        """K2T only: kept threshold-layer columns K' of each problem of the last
+        min-sum call ([] when a fallback engine ran)."""
+        buf = (ctypes.c_int32 * 64)()
+        n = int(load_library().sa_ctx_tc_columns(self.handle, ctypes.cast(buf, ctypes.c_void_p), 64))
+        if n < 0:
+            raise SaError(SA_E_CUDA, "sa_ctx_tc_columns failed")
+        return list(buf[:n])
 
     def set_rank_form(self, form: int = SA_RANK_F, delta: float = 0.02):
         """SA_RANK_F (mean F, exact) or SA_RANK_DF (mean -ln(Delta + F), Eq. 2-3)."""

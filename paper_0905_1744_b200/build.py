@@ -1,12 +1,13 @@
 """Build libsa.so (sm_100a) in-tree: ``python -m paper_0905_1744_b200.build``.
 
-One nvcc invocation compiles the CUDA kernels (csrc/*.cu) and the host exact
-fallback (csrc/exact.cpp) into ``paper_0905_1744_b200/lib/libsa.so`` with the
-CUDA runtime linked statically, so the library does not depend on whichever
+One nvcc per translation unit (in parallel) compiles the CUDA kernels
+(csrc/*.cu) and the host exact fallback (csrc/exact.cpp); they are linked into
+``paper_0905_1744_b200/lib/libsa.so`` with the CUDA runtime linked statically, so the library does not depend on whichever
 libcudart PyTorch ships.  nvcc cross-compiles without a GPU.
 """
 from __future__ import annotations
 
+import concurrent.futures
 import glob
 import os
 import subprocess
@@ -35,19 +36,47 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(f) <= t for f in sources() + headers() + [__file__])
 
 
+def _obj(src: str) -> str:
+    return os.path.join(os.path.dirname(LIB), "obj", os.path.basename(src) + ".o")
+
+
+def _flags(verbose: bool):
+    return [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", os.path.join(ROOT, "include"),
+            "-Xptxas", "-v" if verbose else "-O3"]
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every translation unit in parallel (one nvcc per file; an object
+    is rebuilt when its source, a header or this script is newer), then link."""
     if not force and up_to_date():
         return LIB
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
-           "-cudart", "static", "-I", os.path.join(ROOT, "include"), "-Xptxas", "-v" if verbose else "-O3",
-           *sources(), "-o", LIB + ".tmp"]
+    os.makedirs(os.path.join(os.path.dirname(LIB), "obj"), exist_ok=True)
+    newest_dep = max(os.path.getmtime(f) for f in headers() + [__file__])
+
+    def compile_one(src):
+        obj = _obj(src)
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(newest_dep, os.path.getmtime(src)):
+            return src, None
+        r = subprocess.run([NVCC, *_flags(verbose), "-c", src, "-o", obj + ".tmp"], capture_output=True, text=True)
+        if r.returncode == 0:
+            os.replace(obj + ".tmp", obj)
+        return src, r
+
+    with concurrent.futures.ThreadPoolExecutor(max_workers=len(sources())) as ex:
+        results = list(ex.map(compile_one, sources()))
+    for src, r in results:
+        if r is None:
+            continue
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"libsa build failed: {os.path.basename(src)}")
+        if verbose:
+            sys.stderr.write(r.stderr)
+    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", *[_obj(s) for s in sources()], "-o", LIB + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("libsa build failed")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("libsa link failed")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -72,34 +72,6 @@ void segcopy_fill(void* dst, int t, int64_t src_m, int64_t dst_m, int64_t cnt, i
                   int64_t nbytes);
 
 // ---------------------------------------------------------- scratch ------
-// Stream-ordered scratch: allocations are freed on the same stream when the
-// Scratch goes out of scope, so kernels enqueued before still see them.
-struct Scratch {
-  cudaStream_t st;
-  std::vector<void*> ptrs;
-  bool oom = false;
-  explicit Scratch(cudaStream_t s) : st(s) {}
-  ~Scratch() {
-    for (void* p : ptrs) cudaFreeAsync(p, st);
-  }
-  template <class T>
-  T* alloc(size_t n) {
-    void* p = nullptr;
-    const size_t bytes = std::max<size_t>(n * sizeof(T), 16);
-    if (cudaMallocAsync(&p, bytes, st) != cudaSuccess) {
-      cudaGetLastError();
-      oom = true;
-      return nullptr;
-    }
-    ptrs.push_back(p);
-    return static_cast<T*>(p);
-  }
-};
-
-#define SA_ALLOC(var, T, n)                                                        \
-  T* var = scratch.alloc<T>(n);                                                    \
-  if (!var) return fail(SA_E_NOMEM, "scratch allocation of %zu x %s failed", (size_t)(n), #T)
-
 static inline int64_t block_begin(int64_t q, int64_t N, int64_t p) { return q * N / p; }
 
 static int32_t profile_stride(int32_t bins) { return stride_u16(bins); }
@@ -117,13 +89,19 @@ static inline int64_t window_of(const sa_ctx* c, int64_t npool) {
   return c->rank_form == SA_RANK_DF ? 32 * npool : npool;
 }
 
-// Engine choice: SA_ENGINE = auto (default) | u16 | u16imad | u8 (u8 is still
-// only used when every count is <= 255; otherwise the exact u16 engine runs).
-static int engine_mode() {
+// Engine choice: SA_ENGINE = auto | tc (default: the tensor-core engine K2T
+// when the launch is feasible, else the u8 SAD engine when every count is
+// <= 255, else u16) | sad / u8 (the same without K2T) | u16 | u16imad (forced).
+struct EngineMode {
+  int enc;    // ENC_AUTO or a forced ENC_*
+  bool tc;    // auto mode: try K2T first
+};
+static EngineMode engine_mode() {
   const char* e = getenv("SA_ENGINE");
-  if (!e || !*e || !strcmp(e, "auto") || !strcmp(e, "u8")) return ENC_U8_SAD;
-  if (!strcmp(e, "u16imad")) return ENC_U16_MIN_IMAD;
-  return ENC_U16_MIN;
+  if (!e || !*e || !strcmp(e, "auto") || !strcmp(e, "tc")) return {ENC_AUTO, true};
+  if (!strcmp(e, "sad") || !strcmp(e, "u8")) return {ENC_AUTO, false};
+  if (!strcmp(e, "u16imad")) return {ENC_U16_MIN_IMAD, false};
+  return {ENC_U16_MIN, false};
 }
 
 // Operand rows the min-sum engine reads for a set of u16 profile rows.
@@ -132,49 +110,63 @@ struct Operand {
   int ldw;   // row stride in 32-bit words
 };
 
+// Engine operands of an A x B min-sum problem given its u16 profile rows.  In
+// the auto modes every encoding is prepared and the choice is made on the
+// device, with no host synchronisation: K2T's own kernels decide whether the
+// launch fits it (minsum_tc.cuh), the u8 SAD rows are converted on the device
+// and the largest count is folded into ctx->dcount, and launch_ops enqueues
+// every engine, each guarded by those words.  With K2T the u8 conversions are
+// deferred to launch_ops and guarded too (they are only read by the fallback).
+struct EngineOps {
+  Operand a16, b16, a8, b8;
+  int mode;                     // ENC_U16_MIN / ENC_U16_MIN_IMAD (forced) or ENC_AUTO
+  bool tc = false;              // auto mode: K2T first
+  int32_t bins = 0;
+  uint32_t* guard = nullptr;
+  struct Conv {
+    const uint16_t* p16;
+    int64_t n;
+    uint8_t* p8;
+  };
+  std::vector<Conv> conv;       // deferred (guarded) u8 conversions
+};
+
 // Build the u8 (SAD) operand rows of `n` u16 profile rows in scratch memory and
-// fold the largest count into *maxc (device).  Returns nullptr rows on OOM.
+// fold the largest count into *maxc (device); with K2T the conversion is only
+// recorded in E->conv.
 static sa_status make_u8_rows(Scratch& scratch, const uint16_t* p16, int64_t n, int32_t bins, uint32_t* maxc,
-                              Operand* out, cudaStream_t st) {
+                              Operand* out, cudaStream_t st, EngineOps* E) {
   const int32_t s8 = stride_u8(bins);
   uint8_t* p8 = scratch.alloc<uint8_t>((size_t)std::max<int64_t>(n, 1) * s8);
   if (!p8) return fail(SA_E_NOMEM, "scratch allocation of u8 operand rows failed");
-  SA_TRY(to_u8_launch(p16, n, stride_u16(bins), bins, p8, s8, maxc, st));
+  if (E && E->tc) E->conv.push_back({p16, n, p8});
+  else SA_TRY(to_u8_launch(p16, n, stride_u16(bins), bins, p8, s8, maxc, st));
   out->rows = reinterpret_cast<const uint32_t*>(p8);
   out->ldw = s8 / 4;
   return SA_OK;
 }
-
-// Engine operands of an A x B min-sum problem given its u16 profile rows.  In
-// the default (auto) mode both encodings are prepared: the u8 SAD rows are
-// converted on the device, the largest count is folded into ctx->dcount, and
-// launch_ops enqueues both engines, each guarded by that counter -- the
-// encoding is decided on the device with no host synchronisation.
-struct EngineOps {
-  Operand a16, b16, a8, b8;
-  int mode;                     // ENC_U16_MIN / ENC_U16_MIN_IMAD (forced) or ENC_AUTO
-  const uint32_t* guard = nullptr;
-};
 
 static sa_status prepare_ops(sa_ctx* c, Scratch& scratch, const uint16_t* A16, int64_t na, const uint16_t* B16,
                              int64_t nb, int32_t bins, bool reset_count, EngineOps* E, cudaStream_t st) {
   const int ldw16 = stride_u16(bins) / 2;
   E->a16 = Operand{reinterpret_cast<const uint32_t*>(A16), ldw16};
   E->b16 = Operand{reinterpret_cast<const uint32_t*>(B16), ldw16};
-  const int mode = engine_mode();
-  if (mode != ENC_U8_SAD) {
-    E->mode = mode == ENC_U16_MIN_IMAD ? ENC_U16_MIN_IMAD : ENC_U16_MIN;
+  E->bins = bins;
+  const EngineMode m = engine_mode();
+  if (m.enc != ENC_AUTO) {
+    E->mode = m.enc;
     return SA_OK;
   }
   E->mode = ENC_AUTO;
+  E->tc = m.tc && bins <= TC_MAX_BINS;
   E->guard = c->dcount;
-  if (reset_count) SA_CUDA(cudaMemsetAsync(c->dcount, 0, sizeof(uint32_t), st));
+  if (reset_count) SA_CUDA(cudaMemsetAsync(c->dcount, 0, 4 * sizeof(uint32_t), st));
   if (B16 == A16) {   // same rows (possibly different counts): convert the longer prefix once
-    SA_TRY(make_u8_rows(scratch, A16, std::max(na, nb), bins, c->dcount, &E->a8, st));
+    SA_TRY(make_u8_rows(scratch, A16, std::max(na, nb), bins, c->dcount, &E->a8, st, E));
     E->b8 = E->a8;
   } else {
-    SA_TRY(make_u8_rows(scratch, A16, na, bins, c->dcount, &E->a8, st));
-    SA_TRY(make_u8_rows(scratch, B16, nb, bins, c->dcount, &E->b8, st));
+    SA_TRY(make_u8_rows(scratch, A16, na, bins, c->dcount, &E->a8, st, E));
+    SA_TRY(make_u8_rows(scratch, B16, nb, bins, c->dcount, &E->b8, st, E));
   }
   return SA_OK;
 }
@@ -183,15 +175,26 @@ static sa_status prepare_ops(sa_ctx* c, Scratch& scratch, const uint16_t* A16, i
 static sa_status launch_ops(sa_ctx* c, const EngineOps& E, const std::vector<MsProblem>& probs16, cudaStream_t st,
                             cudaEvent_t ev0, cudaEvent_t ev1) {
   c->last_enc = E.mode;
+  c->last_tc = E.tc;
+  c->last_tc_probs = 0;
   if (E.mode != ENC_AUTO) return minsum_launch(probs16, E.a16.ldw, E.mode, st, ev0, ev1);
+  if (ev0) SA_CUDA(cudaEventRecord(ev0, st));
+  SA_CUDA(cudaMemsetAsync(E.guard + 2, E.tc ? 1 : 0, sizeof(uint32_t), st));
+  if (E.tc) {
+    c->last_tc_probs = (int)probs16.size();
+    SA_TRY(tc_launch(probs16, E.a16.ldw, E.bins, E.guard, E.guard + SA_TC_COLS_AT, st, nullptr, nullptr));
+    for (const auto& cv : E.conv)
+      SA_TRY(to_u8_launch(cv.p16, cv.n, stride_u16(E.bins), E.bins, cv.p8, stride_u8(E.bins), E.guard, st, true));
+  }
   std::vector<MsProblem> p8 = probs16;
   for (auto& p : p8) {
     const int64_t ra = (p.A - E.a16.rows) / E.a16.ldw, rb = (p.B - E.b16.rows) / E.b16.ldw;
     p.A = E.a8.rows + ra * E.a8.ldw;
     p.B = E.b8.rows + rb * E.b8.ldw;
   }
-  SA_TRY(minsum_launch(p8, E.a8.ldw, ENC_U8_SAD, st, ev0, nullptr, E.guard));
-  SA_TRY(minsum_launch(probs16, E.a16.ldw, ENC_U16_MIN, st, nullptr, ev1, E.guard));
+  SA_TRY(minsum_launch(p8, E.a8.ldw, ENC_U8_SAD, st, nullptr, nullptr, E.guard));
+  SA_TRY(minsum_launch(probs16, E.a16.ldw, ENC_U16_MIN, st, nullptr, nullptr, E.guard));
+  if (ev1) SA_CUDA(cudaEventRecord(ev1, st));
   return SA_OK;
 }
 
@@ -241,7 +244,8 @@ sa_status sa_ctx_create(int cuda_device, sa_ctx** out) {
   }
   sa_ctx* c = new sa_ctx();
   c->device = cuda_device;
-  if (cudaMalloc(&c->dcount, 64) != cudaSuccess || cudaHostAlloc(&c->hpinned, 64, cudaHostAllocDefault) != cudaSuccess) {
+  if (cudaMalloc(&c->dcount, SA_DCOUNT_WORDS * 4) != cudaSuccess ||
+      cudaHostAlloc(&c->hpinned, SA_DCOUNT_WORDS * 4, cudaHostAllocDefault) != cudaSuccess) {
     cudaGetLastError();
     delete c;
     return fail(SA_E_NOMEM, "context allocation failed");
@@ -296,13 +300,27 @@ sa_status sa_ctx_set_rank_form(sa_ctx* ctx, int form, double delta) {
 int sa_ctx_engine(const sa_ctx* ctx) {
   if (!ctx) return -1;
   if (ctx->last_enc != ENC_AUTO) return ctx->last_enc;
-  // auto dispatch: the device counter decided (blocking read)
+  // auto dispatch: the device words decided (blocking read)
   if (cudaSetDevice(ctx->device) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess ||
-      cudaMemcpy(ctx->hpinned, ctx->dcount, sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess) {
+      cudaMemcpy(ctx->hpinned, ctx->dcount, 3 * sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess) {
     cudaGetLastError();
     return -1;
   }
-  return *ctx->hpinned <= 255 ? ENC_U8_SAD : ENC_U16_MIN;
+  if (ctx->hpinned[2] && !ctx->hpinned[1]) return ENC_TC;
+  return ctx->hpinned[0] <= 255 ? ENC_U8_SAD : ENC_U16_MIN;
+}
+
+int32_t sa_ctx_tc_columns(const sa_ctx* ctx, int32_t* cols_h, int32_t max) {
+  if (!ctx || !ctx->last_tc || ctx->last_tc_probs <= 0) return 0;
+  if (cudaSetDevice(ctx->device) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess ||
+      cudaMemcpy(ctx->hpinned, ctx->dcount, SA_DCOUNT_WORDS * 4, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  if (!(ctx->hpinned[2] && !ctx->hpinned[1])) return 0;   // K2T declined: a fallback engine ran
+  const int n = std::min(ctx->last_tc_probs, SA_TC_COLS_MAX);
+  for (int i = 0; i < n && i < max; ++i) cols_h[i] = (int32_t)ctx->hpinned[SA_TC_COLS_AT + i];
+  return n;
 }
 
 sa_status sa_ctx_set_timing(sa_ctx* ctx, int enable) {
@@ -555,7 +573,7 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
     // device counter, so the engine is valid for both sides
     EngineOps E2 = E;
     E2.b16 = Operand{reinterpret_cast<const uint32_t*>(s_prof), ldw};
-    if (E2.mode == ENC_AUTO) SA_TRY(make_u8_rows(scratch, s_prof, s_all, a.stride, c->dcount, &E2.b8, st));
+    if (E2.mode == ENC_AUTO) SA_TRY(make_u8_rows(scratch, s_prof, s_all, a.stride, c->dcount, &E2.b8, st, &E2));
     SA_TRY(rec(ev_begin(c, SA_PHASE_S2D), st));
     MsProblem pr{};
     pr.A = E2.a16.rows;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -38,6 +39,34 @@ void count_launch(int n = 1);
       return ::sa::fail(SA_E_CUDA, "%s:%d launch: %s", __FILE__, __LINE__,           \
                         cudaGetErrorString(e_));                                     \
   } while (0)
+
+// Stream-ordered scratch: allocations are freed on the same stream when the
+// Scratch goes out of scope, so kernels enqueued before still see them.
+struct Scratch {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  bool oom = false;
+  explicit Scratch(cudaStream_t s) : st(s) {}
+  ~Scratch() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+  template <class T>
+  T* alloc(size_t n) {
+    void* p = nullptr;
+    const size_t bytes = std::max<size_t>(n * sizeof(T), 16);
+    if (cudaMallocAsync(&p, bytes, st) != cudaSuccess) {
+      cudaGetLastError();
+      oom = true;
+      return nullptr;
+    }
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+};
+
+#define SA_ALLOC(var, T, n)                                                        \
+  T* var = scratch.alloc<T>(n);                                                    \
+  if (!var) return fail(SA_E_NOMEM, "scratch allocation of %zu x %s failed", (size_t)(n), #T)
 
 // Error flags written by kernels (device-detected range errors).
 enum : uint32_t { ERR_RESIDUE = 1u, ERR_NK = 2u };
@@ -80,7 +109,8 @@ constexpr double DF_SCALE = 4503599627370496.0;   // 2^52
 //   ENC_U16_MIN_IMAD  same, adds issued as IMAD on the FMA pipe (experiment)
 //   ENC_U8_SAD        uint8 counts, 4 bins/word, C = (nk_a + nk_b - sum|a-b|)/2 with
 //                     VABSDIFF4.U8.ACC (every count must be <= 255)
-enum { ENC_U16_MIN = 0, ENC_U8_SAD = 1, ENC_U16_MIN_IMAD = 2, ENC_AUTO = 3 };
+//   ENC_TC            0/1 threshold layers on the tensor cores (K2T, minsum_tc.cuh)
+enum { ENC_U16_MIN = 0, ENC_U8_SAD = 1, ENC_U16_MIN_IMAD = 2, ENC_AUTO = 3, ENC_TC = 4 };
 // Row strides: u16 rows are round_up(bins, 64) elements; u8 rows round_up(bins, 128) bytes.
 inline int32_t stride_u16(int32_t bins) { return ((bins + 63) / 64) * 64; }
 inline int32_t stride_u8(int32_t bins) { return ((bins + 127) / 128) * 128; }
@@ -91,8 +121,20 @@ inline int32_t stride_u8(int32_t bins) { return ((bins + 127) / 128) * 128; }
 sa_status minsum_launch(const std::vector<MsProblem>& probs, int ldw, int enc, cudaStream_t st,
                         cudaEvent_t ev0, cudaEvent_t ev1, const uint32_t* guard = nullptr);
 // uint16 rows -> uint8 rows (zero padded) + atomicMax of every count into *maxc.
+// guarded: skip when the tensor-core engine handled the call (maxc = guard words).
 sa_status to_u8_launch(const uint16_t* p16, int64_t n, int32_t stride16, int32_t bins, uint8_t* p8,
-                       int32_t stride8, uint32_t* maxc, cudaStream_t st);
+                       int32_t stride8, uint32_t* maxc, cudaStream_t st, bool guarded = false);
+// K2T: the tensor-core engine over `probs` (u16 operand rows, ldw16 words per
+// row).  state = guard words [largest count, infeasible, enabled]; when the
+// launch is infeasible (a count > 32 or too many layer columns) its kernels
+// return at once and the guarded engines above must be enqueued after it.
+// cols_out[i] (device, nullable) = kept layer columns K' of problem i (i < SA_TC_COLS_MAX).
+constexpr int TC_MAX_BINS = 8192;
+constexpr int SA_DCOUNT_WORDS = 256;   // ctx->dcount: [0..3] guard words, [16..80) K2T column counts
+constexpr int SA_TC_COLS_AT = 16;
+constexpr int SA_TC_COLS_MAX = 64;
+sa_status tc_launch(const std::vector<MsProblem>& probs, int ldw16, int32_t bins, uint32_t* state,
+                    uint32_t* cols_out, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1);
 sa_status ensure_recip_tables(cudaStream_t st);
 
 // ------------------------------------------------------ profiles (K1) --
@@ -137,6 +179,8 @@ struct sa_ctx {
   cudaEvent_t ev[2 * SA_PHASE_COUNT] = {};
   bool ev_used[SA_PHASE_COUNT] = {};
   int last_enc = -1;            // ENC_* of the last min-sum call, or ENC_AUTO
+  bool last_tc = false;         // the last auto call tried the tensor-core engine first
+  int last_tc_probs = 0;        // problems of that K2T call
   int rank_form = SA_RANK_F;    // sa_ctx_set_rank_form
   double delta = 0.02;
   uint32_t* dcount = nullptr;   // device: largest count of the last auto-dispatched call

@@ -23,39 +23,17 @@
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
+#include "keyterm.cuh"
 
 namespace sa {
 
-__device__ uint64_t g_rtab[65536];   // floor(2^64 / d), d >= 2
-__device__ uint32_t g_etab[65536];   // 2^64 mod d
+sa_status ensure_recip_tables(cudaStream_t st) { return ensure_recip_tables_tu(st); }
 
 constexpr int MS_MAXPROB = 16;
 struct MsBatch {
   MsProblem p[MS_MAXPROB];
   int n;
 };
-
-__global__ void recip_kernel() {
-  int d = blockIdx.x * blockDim.x + threadIdx.x;
-  if (d >= 65536) return;
-  if (d < 2) { g_rtab[d] = 0; g_etab[d] = 0; return; }
-  uint64_t r = ~0ull / (uint64_t)d;
-  uint64_t e = ~0ull % (uint64_t)d + 1;   // (2^64 - 1) mod d + 1
-  if (e == (uint64_t)d) { r += 1; e = 0; }
-  g_rtab[d] = r;
-  g_etab[d] = (uint32_t)e;
-}
-
-sa_status ensure_recip_tables(cudaStream_t st) {
-  static bool ready[64] = {};
-  int dev = 0;
-  SA_CUDA(cudaGetDevice(&dev));
-  if (dev < 64 && ready[dev]) return SA_OK;
-  recip_kernel<<<256, 256, 0, st>>>();
-  SA_LAUNCHED();
-  if (dev < 64) ready[dev] = true;
-  return SA_OK;
-}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -69,43 +47,9 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// floor(C * 2^64 / D) accumulated into a 96-bit (lo, hi) register pair.
-__device__ __forceinline__ void add_term(uint64_t& lo, uint32_t& hi, uint32_t C, uint32_t D) {
-  if (D == 0 || C == 0) return;
-  if (C == D) { hi += 1; return; }      // the term is exactly 2^64
-  uint64_t t = (uint64_t)C * g_rtab[D] + (uint64_t)((C * g_etab[D]) / D);
-  lo += t;
-  hi += (lo < t) ? 1u : 0u;
-}
-
-// d^F key term: round(2^52 (ln(1+Delta) - ln(Delta + C/D))), F = 0 when D = 0.
-__device__ __forceinline__ void add_dF_term(uint64_t& lo, uint32_t& hi, uint32_t C, uint32_t D, double delta,
-                                            double ln1pd) {
-  const double F = D > 0 ? __ddiv_rn((double)C, (double)D) : 0.0;
-  double t = ln1pd - log(delta + F);
-  t = t > 0.0 ? t : 0.0;
-  const uint64_t q = __double2ull_rn(t * DF_SCALE);
-  lo += q;
-  hi += (lo < q) ? 1u : 0u;
-}
-
 __device__ __forceinline__ void key_term(const MsProblem& P, uint64_t& lo, uint32_t& hi, uint32_t C, uint32_t D) {
   if (P.form == SA_RANK_DF) add_dF_term(lo, hi, C, D, P.delta, P.ln1pd);
   else add_term(lo, hi, C, D);
-}
-
-__device__ __forceinline__ void atomic_add_key(sa_key128* k, uint64_t lo, uint64_t hi) {
-  unsigned long long old = atomicAdd(reinterpret_cast<unsigned long long*>(&k->lo), (unsigned long long)lo);
-  uint64_t carry = ((uint64_t)old + lo < (uint64_t)old) ? 1ull : 0ull;
-  uint64_t h = hi + carry;
-  if (h) atomicAdd(reinterpret_cast<unsigned long long*>(&k->hi), (unsigned long long)h);
-}
-
-__device__ __forceinline__ void shfl_add(uint64_t& lo, uint32_t& hi, int mask) {
-  uint64_t olo = __shfl_xor_sync(0xffffffffu, lo, mask);
-  uint32_t ohi = __shfl_xor_sync(0xffffffffu, hi, mask);
-  lo += olo;
-  hi += ohi + ((lo < olo) ? 1u : 0u);
 }
 
 // acc += sum over the 4 byte lanes of |a - b|  (one VABSDIFF4.U8.ACC)
@@ -124,9 +68,17 @@ __device__ __forceinline__ uint32_t acc_to_C(uint32_t acc, int nka, int nkb) {
 // returns at once unless the largest count (*guard, written by to_u8_kernel)
 // selects it -- u8 SAD when every count is <= 255, u16 otherwise -- so the
 // host never waits for the decision.
+// guard[0] = largest count, guard[1] = the tensor-core engine (K2T) found the
+// launch infeasible, guard[2] = K2T enabled for this call: when K2T ran, these
+// engines return at once.
+__device__ __forceinline__ bool tc_handled(const uint32_t* guard) {
+  const volatile uint32_t* g = guard;
+  return g[2] != 0u && g[1] == 0u;
+}
 template <int ENC>
 __device__ __forceinline__ bool guard_skip(const uint32_t* guard) {
   if (!guard) return false;
+  if (tc_handled(guard)) return true;
   const uint32_t m = *reinterpret_cast<const volatile uint32_t*>(guard);
   return (m <= 255u) != (ENC == ENC_U8_SAD);
 }
@@ -574,20 +526,6 @@ static int tma_layout() {
   return (e && atoi(e) == 8) ? 8 : 4;
 }
 
-static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    else
-      cudaGetLastError();
-  }
-  return fn;
-}
-
 // 2-D map over `rows` rows of ldw 32-bit words: boxes of 32 words x 128 rows,
 // 128-byte swizzle, rows past the end read as zeros.
 static sa_status encode_rows_map(CUtensorMap* m, const uint32_t* base, int64_t rows, int ldw) {
@@ -700,7 +638,8 @@ sa_status minsum_launch(const std::vector<MsProblem>& probs_in, int ldw, int enc
 // The SAD encoding needs every count <= 255; the conversion saturates and
 // reports the largest count so the caller can fall back to the u16 engine.
 __global__ void to_u8_kernel(const uint16_t* __restrict__ p16, int64_t n, int stride16, uint8_t* __restrict__ p8,
-                             int stride8, uint32_t* __restrict__ maxc) {
+                             int stride8, uint32_t* __restrict__ maxc, bool guarded) {
+  if (guarded && tc_handled(maxc)) return;   // maxc = the guard words (K2T ran: rows unused)
   const int chunks = stride8 / 8;
   uint32_t mx = 0;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n * chunks;
@@ -726,12 +665,12 @@ __global__ void to_u8_kernel(const uint16_t* __restrict__ p16, int64_t n, int st
 }
 
 sa_status to_u8_launch(const uint16_t* p16, int64_t n, int32_t stride16, int32_t bins, uint8_t* p8, int32_t stride8,
-                       uint32_t* maxc, cudaStream_t st) {
+                       uint32_t* maxc, cudaStream_t st, bool guarded) {
   (void)bins;
   if (n <= 0) return SA_OK;
   const int64_t work = n * (stride8 / 8);
   const int64_t blocks = (work + 255) / 256;
-  to_u8_kernel<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, st>>>(p16, n, stride16, p8, stride8, maxc);
+  to_u8_kernel<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, st>>>(p16, n, stride16, p8, stride8, maxc, guarded);
   SA_LAUNCHED();
   return SA_OK;
 }
@@ -786,3 +725,4 @@ sa_status keys_to_f64_launch(const sa_key128* keys, int64_t n, int64_t npool, do
 }
 
 }  // namespace sa
+

@@ -1,0 +1,309 @@
+// K2T -- the tensor-core form of the min-sum engine (SURVEY.md §8(f) N3(iii),
+// DESIGN.md §4b): Eq. 1's numerator C_ij = sum_t min(c^i_t, c^j_t)
+// written as an exact 0/1 contraction over threshold
+// layers,
+//     min(a, b) = sum_{r >= 1} [a >= r] [b >= r],
+// so C = A' B'^T with A'[i][(r, t)] = [c^i_t >= r] -- a dense u8 GEMM with s32
+// accumulators (tcgen05.mma kind::i8).  Sums are integers < 2^31: exact.
+//
+// This header holds the device side shared by libsa (minsum_tc.cu) and the
+// standalone descriptor probe (tools/tc_probe.cu): PTX wrappers, the tile
+// schedule and the warp-specialised persistent kernel.  The epilogue is a
+// template parameter.
+//
+// Kernel anatomy (one CTA per SM, 320 threads):
+//   warp 8  lane 0: TMA producer -- per stage one 128-row x 128-byte box of A
+//                   and one 256-row x 128-byte box of B (SWIZZLE_128B), into a
+//                   4-stage ring guarded by full/empty mbarriers;
+//   warp 9  lane 0: MMA issuer -- 4 x tcgen05.mma.cta_group::1.kind::i8
+//                   (M=128, N=256, K=32) per stage into one of two TMEM
+//                   accumulators (2 x 256 columns), tcgen05.commit frees the
+//                   stage / publishes the accumulator;
+//   warps 0-7:      epilogue -- warp w reads TMEM lanes 32(w%4).. (tile rows)
+//                   and columns 128(w/4).. with tcgen05.ld.32x32b.x32, calls
+//                   Epi::chunk for every 32 columns, then releases the buffer.
+#pragma once
+#include <cuda.h>
+#include <cstdint>
+
+namespace sa {
+namespace tc {
+
+constexpr int BM = 128;          // tile rows (UMMA M)
+constexpr int BN = 256;          // tile columns (UMMA N)
+constexpr int BK = 128;          // bytes (= u8 elements of K) per stage
+constexpr int UK = 32;           // K per tcgen05.mma kind::i8
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK;
+constexpr int B_BYTES = BN * BK;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = (EPI_WARPS + 2) * 32;
+constexpr int TMEM_COLS = 2 * BN;
+constexpr int XPOSE_WORDS = 32 * 33;   // per epilogue warp: a padded 32 x 32 transpose buffer
+constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + EPI_WARPS * XPOSE_WORDS * 4;
+constexpr int MAXPROB = 16;
+
+// ----------------------------------------------------------------- PTX ----
+__device__ __forceinline__ uint32_t s_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void bar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "TC_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra TC_WAIT_%=;\n"
+      "}\n" ::"r"(s_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(s_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_addr(slot)), "r"(cols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols));
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// D[tmem] (+)= A[smem] . B[smem]^T, u8 x u8 -> s32
+__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor of a K-major operand tile in the canonical
+// SWIZZLE_128B layout TMA writes: rows of 128 bytes, 8-row (1024 B) atoms.
+// LBO is unused for swizzled K-major layouts (1), SBO = 1024 B between 8-row
+// groups, version 1 (sm_100), layout type 2 = SWIZZLE_128B.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// Instruction descriptor: s32 accumulator, u8 x u8, both K-major, M = BM, N = BN.
+__host__ __device__ constexpr uint32_t idesc_i8() {
+  return (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+// ------------------------------------------------------------ schedule ----
+// One problem = rows [0, na) of A' against rows [0, nb) of B' over kblocks
+// 128-byte K blocks (read from device memory: the column count is decided on
+// the device).  sym: A' == B', only tiles touching the upper triangle
+// (col block J >= I / 2 for 128-row / 256-column tiles).
+struct Problem {
+  int32_t na, nb;
+  int32_t sym;
+  int32_t tiles_n;            // ceil(nb / BN)
+  int64_t tile_begin;         // first global tile of this problem
+  const int32_t* kblocks;     // device: K' / 128 (>= 1)
+  int32_t map;                // tensor maps m[2 map] (A rows, box 128) and m[2 map + 1] (B rows, box 256)
+  int32_t pad_;
+};
+struct Batch {
+  Problem p[MAXPROB];
+  int n;
+};
+struct alignas(64) Maps {
+  CUtensorMap m[2 * MAXPROB];
+};
+
+struct Tile {
+  int pi, row0, col0, ra, rb;
+};
+
+// tiles of a problem
+__host__ __device__ inline int64_t problem_tiles(int64_t na, int64_t nb, bool sym) {
+  const int64_t tm = (na + BM - 1) / BM, tn = (nb + BN - 1) / BN;
+  if (!sym) return tm * tn;
+  int64_t t = 0;
+  for (int64_t i = 0; i < tm; ++i) t += tn - i / 2;
+  return t;
+}
+
+__device__ __forceinline__ Tile decode(const Batch& b, int64_t tile) {
+  int pi = 0;
+  while (pi + 1 < b.n && b.p[pi + 1].tile_begin <= tile) ++pi;
+  const Problem& P = b.p[pi];
+  int64_t t = tile - P.tile_begin;
+  int ti, tj;
+  if (P.sym) {
+    ti = 0;
+    while (t >= P.tiles_n - ti / 2) { t -= P.tiles_n - ti / 2; ++ti; }
+    tj = ti / 2 + (int)t;
+  } else {
+    ti = (int)(t / P.tiles_n);
+    tj = (int)(t % P.tiles_n);
+  }
+  Tile T;
+  T.pi = pi;
+  T.row0 = ti * BM;
+  T.col0 = tj * BN;
+  T.ra = min(BM, P.na - T.row0);
+  T.rb = min(BN, P.nb - T.col0);
+  return T;
+}
+
+// -------------------------------------------------------------- kernel ----
+// Epi (const, a kernel parameter) must provide a per-thread `State` and
+//   __device__ bool skip() const;                                  // device-side dispatch guard
+//   __device__ void begin(State&, const Tile&, int row) const;     // per thread, per tile
+//   __device__ void chunk(State&, const Tile&, int row, int col, const uint32_t (&v)[32], int lane,
+//                         uint32_t* xpose) const;                  // all 32 lanes, converged
+//   __device__ void end(State&, const Tile&, int row) const;
+// row = tile row of this thread (0..127), col = first tile column of the chunk,
+// xpose = this warp's 32 x 33 word shared-memory scratch.
+template <class Epi>
+__global__ void __launch_bounds__(THREADS, 1)
+gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps maps, int64_t total_tiles, Epi epi) {
+  if (epi.skip()) return;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const uint32_t raw_s = s_addr(smem_raw);
+  const uint32_t base_s = (raw_s + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (base_s - raw_s);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint32_t* xpose_all = reinterpret_cast<uint32_t*>(smem + STAGES * STAGE_BYTES + 256);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == EPI_WARPS && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      bar_init(&full[s], 1);
+      bar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      bar_init(&tfull[b], 1);
+      bar_init(&tempty[b], EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == EPI_WARPS + 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+
+  if (warp == EPI_WARPS) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int64_t g = 0;
+      for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        const Tile T = decode(batch, tile);
+        const Problem& P = batch.p[T.pi];
+        const int nkb = *reinterpret_cast<const volatile int32_t*>(P.kblocks);
+        const CUtensorMap* ma = &maps.m[2 * P.map];
+        const CUtensorMap* mb = &maps.m[2 * P.map + 1];
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const int slot = (int)(g % STAGES);
+          if (g >= STAGES) bar_wait(&empty[slot], (uint32_t)(((g / STAGES) - 1) & 1));
+          bar_arrive_tx(&full[slot], STAGE_BYTES);
+          const uint32_t dst = base_s + slot * STAGE_BYTES;
+          tma_2d(dst, ma, kb * BK, T.row0, &full[slot]);
+          tma_2d(dst + A_BYTES, mb, kb * BK, T.col0, &full[slot]);
+        }
+      }
+    }
+  } else if (warp == EPI_WARPS + 1) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_i8();
+      int64_t g = 0, lt = 0;
+      for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
+        const Tile T = decode(batch, tile);
+        const Problem& P = batch.p[T.pi];
+        const int nkb = *reinterpret_cast<const volatile int32_t*>(P.kblocks);
+        const int buf = (int)(lt & 1);
+        if (lt >= 2) bar_wait(&tempty[buf], (uint32_t)(((lt >> 1) - 1) & 1));
+        fence_after();
+        const uint32_t d = tmem_base + (uint32_t)(buf * BN);
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const int slot = (int)(g % STAGES);
+          bar_wait(&full[slot], (uint32_t)((g / STAGES) & 1));
+          fence_after();
+          const uint32_t sa_ = base_s + slot * STAGE_BYTES;
+          const uint64_t da = sw128_desc(sa_), db = sw128_desc(sa_ + A_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)
+            mma_i8(d, da + (uint64_t)((k * UK) >> 4), db + (uint64_t)((k * UK) >> 4), idesc, (kb | k) != 0);
+          mma_commit(&empty[slot]);
+        }
+        mma_commit(&tfull[buf]);
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue warps
+    const int quad = warp & 3, half = warp >> 2;
+    const int row = quad * 32 + lane;
+    uint32_t* xpose = xpose_all + warp * XPOSE_WORDS;
+    typename Epi::State es;
+    int64_t lt = 0;
+    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
+      const Tile T = decode(batch, tile);
+      const int buf = (int)(lt & 1);
+      bar_wait(&tfull[buf], (uint32_t)((lt >> 1) & 1));
+      fence_after();
+      epi.begin(es, T, row);
+#pragma unroll 1
+      for (int ch = 0; ch < BN / 2 / 32; ++ch) {
+        const int col = half * (BN / 2) + ch * 32;
+        uint32_t v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + col), v);
+        epi.chunk(es, T, row, col, v, lane, xpose);
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) bar_arrive(&tempty[buf]);
+      epi.end(es, T, row);
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == EPI_WARPS + 1) tmem_dealloc(tmem_base, TMEM_COLS);
+}
+
+}  // namespace tc
+}  // namespace sa

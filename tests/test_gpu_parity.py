@@ -25,13 +25,17 @@ def ctx():
     return B.Context()
 
 
-@pytest.fixture(params=["auto", "u16", "u16imad"])
+@pytest.fixture(params=["auto", "sad", "u16", "u16imad"])
 def engine(request, monkeypatch):
-    """Run a test under each min-sum operand encoding: auto
-    picks the uint8 SAD engine when every count is <= 255, u16 / u16imad force
-    the uint16 VIMNMX engines."""
+    """Run a test under each min-sum engine: auto runs the
+    tensor-core threshold-layer engine (K2T) when the launch fits it, sad the
+    uint8 SAD engine when every count is <= 255, u16 / u16imad force the
+    uint16 VIMNMX engines."""
     monkeypatch.setenv("SA_ENGINE", request.param)
     return request.param
+
+
+ENGINE_NAME = {"auto": "tc", "sad": "u8", "u16": "u16", "u16imad": "u16imad"}
 
 
 def _rand_set(seed, n, lo=0, hi=420, alphabet=20, dup=0):
@@ -141,12 +145,78 @@ def test_bucket_similarity_random(ctx, engine, n, dup, lo):
     P, nk = B.sa_kmer_profiles(ctx, res, offs)
     Po, nko = kmer.profiles(ds.residues, ds.offsets)
     num, sim = B.sa_bucket_similarity(ctx, P, nk)
-    assert ctx.engine() == {"auto": "u8", "u16": "u16", "u16imad": "u16imad"}[engine]
+    assert ctx.engine() == ENGINE_NAME[engine]
     Co, Fo = partition.bucket_similarity(Po, nko, np.arange(n))
     assert np.array_equal(num.cpu().numpy(), Co)
     s = sim.cpu().numpy()
     assert_rel(s, Fo, 1e-12)
     assert np.array_equal(s, Fo)     # one IEEE RN division on both sides
+
+
+def test_tc_falls_back_on_deep_counts(ctx, monkeypatch):
+    """K2T tracks 32 threshold layers: a bin count of 33..255 must hand the call
+    to the uint8 SAD engine on the device, exactly."""
+    monkeypatch.setenv("SA_ENGINE", "auto")
+    rng = np.random.default_rng(81)
+    seqs = [rng.integers(0, 20, size=int(rng.integers(3, 400))) for _ in range(150)]
+    seqs[3] = np.concatenate([np.full(40, 4, np.uint8), seqs[3]])     # 38 x EEE
+    seqs[77] = np.concatenate([np.full(36, 4, np.uint8), seqs[77]])
+    ds = from_sequences(seqs)
+    res, offs = to_dev(ds)
+    P, nk = B.sa_kmer_profiles(ctx, res, offs)
+    Po, nko = kmer.profiles(ds.residues, ds.offsets)
+    assert 32 < Po.max() <= 255
+    num, sim = B.sa_bucket_similarity(ctx, P, nk)
+    assert ctx.engine() == "u8"
+    Co, Fo = partition.bucket_similarity(Po, nko, np.arange(len(seqs)))
+    assert np.array_equal(num.cpu().numpy(), Co)
+    assert np.array_equal(sim.cpu().numpy(), Fo)
+
+
+def test_tc_falls_back_on_column_overflow(ctx, monkeypatch):
+    """Long sequences whose 3-mers repeat ~6 times keep more than 32768 layer
+    columns: K2T must decline and the SAD engine must run, exactly."""
+    monkeypatch.setenv("SA_ENGINE", "auto")
+    rng = np.random.default_rng(82)
+    seqs = [rng.integers(0, 20, size=48000) for _ in range(3)] + \
+        [rng.integers(0, 20, size=int(rng.integers(3, 400))) for _ in range(20)]
+    ds = from_sequences(seqs)
+    res, offs = to_dev(ds)
+    P, nk = B.sa_kmer_profiles(ctx, res, offs)
+    Po, nko = kmer.profiles(ds.residues, ds.offsets)
+    assert Po.max() <= 32
+    num, sim = B.sa_bucket_similarity(ctx, P, nk)
+    assert ctx.engine() == "u8"
+    Co, Fo = partition.bucket_similarity(Po, nko, np.arange(len(seqs)))
+    assert np.array_equal(num.cpu().numpy(), Co)
+    assert np.array_equal(sim.cpu().numpy(), Fo)
+
+
+@pytest.mark.parametrize("n,hi,dup", [(600, 420, 0), (531, 3000, 40), (129, 60, 0), (256, 700, 9)])
+def test_tc_layers_random(ctx, monkeypatch, n, hi, dup):
+    """K2T against the oracle on ragged sets that span several 128 x 256 tiles,
+    with repeated 3-mers (several threshold layers) and duplicate rows; keys of
+    the self-pool (symmetric: row + mirrored column sums) and of a rectangular
+    pool, numerators and F."""
+    monkeypatch.setenv("SA_ENGINE", "auto")
+    ds = _rand_set(9000 + n, n, 0, hi, dup=dup)
+    res, offs = to_dev(ds)
+    P, nk = B.sa_kmer_profiles(ctx, res, offs)
+    Po, nko = kmer.profiles(ds.residues, ds.offsets)
+    num, sim = B.sa_bucket_similarity(ctx, P, nk)
+    assert ctx.engine() == "tc"
+    Co, Fo = partition.bucket_similarity(Po, nko, np.arange(n))
+    assert np.array_equal(num.cpu().numpy(), Co)
+    assert np.array_equal(sim.cpu().numpy(), Fo)
+    D = kmer.denominator_matrix(nko, nko)
+    keys, _, _ = B.sa_kmer_rank(ctx, P, nk, P, nk)
+    assert ctx.engine() == "tc"
+    assert B.keys_to_ints(keys) == kmer.RankSet(Co, D).keys
+    q = n // 3
+    keys, _, nm = B.sa_kmer_rank(ctx, P[:q], nk[:q], P[q:], nk[q:], want_numerators=True)
+    assert ctx.engine() == "tc"
+    assert np.array_equal(nm.cpu().numpy(), Co[:q, q:])
+    assert B.keys_to_ints(keys) == kmer.RankSet(Co[:q, q:], D[:q, q:]).keys
 
 
 def test_large_counts_fall_back_to_u16(ctx, monkeypatch):
