@@ -121,6 +121,11 @@ int sa_ctx_engine(const sa_ctx* ctx);
  * the device.  Problems are: one per block (sa_partition S2a), one (S2d,
  * sa_kmer_rank), one per sa_bucket_similarity call. */
 int32_t sa_ctx_tc_columns(const sa_ctx* ctx, int32_t* cols_h, int32_t max);
+/* Self-test of the division-free F = C / D the K2T matrix epilogue uses
+ * (Markstein correction on RN(1/D)): compares it bit for bit
+ * with IEEE round-to-nearest division for every 0 <= C <= D <= 65535 on
+ * `cuda_device` and returns the number of mismatches (expected 0). */
+sa_status sa_selftest_f_division(int32_t cuda_device, int64_t* mismatches_h);
 sa_status sa_ctx_phase_ms(sa_ctx* ctx, float* ms_h /* [SA_PHASE_COUNT] */);
 
 /* Rank form used by sa_kmer_rank and sa_partition on this context.

@@ -26,7 +26,7 @@ PHASES = ["S2a", "S2b", "S2c", "S2d", "S3", "S5", "rank"]
 EXPORTED = ["sa_ctx_create", "sa_ctx_attach_comm", "sa_ctx_destroy", "sa_last_error", "sa_launch_count",
             "sa_ctx_set_timing", "sa_ctx_phase_ms", "sa_profile_stride", "sa_kmer_profiles", "sa_kmer_rank",
             "sa_partition", "sa_redistribute", "sa_bucket_similarity", "sa_exact_rank_compare", "sa_ctx_engine",
-            "sa_ctx_set_rank_form", "sa_ctx_tc_columns"]
+            "sa_ctx_set_rank_form", "sa_ctx_tc_columns", "sa_selftest_f_division"]
 SA_RANK_F, SA_RANK_DF = 0, 1
 
 
@@ -96,6 +96,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "sa_exact_rank_compare": (ctypes.c_int, [P, I32, P, I32, P, I32]),
         "sa_ctx_engine": (ctypes.c_int, [P]),
         "sa_ctx_tc_columns": (ctypes.c_int32, [P, P, ctypes.c_int32]),
+        "sa_selftest_f_division": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(ctypes.c_int64)]),
         "sa_ctx_set_rank_form": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_double]),
     }
     for name, (res, args) in sig.items():
@@ -226,6 +227,14 @@ def sa_kmer_profiles(ctx: Context, residues: torch.Tensor, offsets: torch.Tensor
     _check(load_library().sa_kmer_profiles(ctx.handle, _ptr(residues), _ptr(offsets), n, k, alphabet,
                                            _ptr(profiles), _ptr(nkmers), _stream(stream)))
     return profiles, nkmers
+
+
+def selftest_f_division(device: int = 0) -> int:
+    """Mismatches of the K2T epilogue's division-free F = C/D against IEEE RN
+    division over every 0 <= C <= D <= 65535 (expected 0)."""
+    n = ctypes.c_int64(-1)
+    _check(load_library().sa_selftest_f_division(device, ctypes.byref(n)))
+    return int(n.value)
 
 
 def sa_kmer_rank(ctx: Context, q_prof, q_nk, pool_prof, pool_nk, bins: int = 8000, want_f64: bool = True,

@@ -323,6 +323,13 @@ int32_t sa_ctx_tc_columns(const sa_ctx* ctx, int32_t* cols_h, int32_t max) {
   return n;
 }
 
+sa_status sa_selftest_f_division(int32_t cuda_device, int64_t* mismatches_h) {
+  g_err.clear();
+  if (!mismatches_h) return fail(SA_E_INVAL, "NULL argument");
+  SA_CUDA(cudaSetDevice(cuda_device));
+  return f_division_selftest(mismatches_h);
+}
+
 sa_status sa_ctx_set_timing(sa_ctx* ctx, int enable) {
   if (!ctx) return fail(SA_E_INVAL, "ctx is NULL");
   ctx->timing = enable != 0;

@@ -130,6 +130,7 @@ sa_status to_u8_launch(const uint16_t* p16, int64_t n, int32_t stride16, int32_t
 // return at once and the guarded engines above must be enqueued after it.
 // cols_out[i] (device, nullable) = kept layer columns K' of problem i (i < SA_TC_COLS_MAX).
 constexpr int TC_MAX_BINS = 8192;
+sa_status f_division_selftest(int64_t* mismatches_h);
 constexpr int SA_DCOUNT_WORDS = 256;   // ctx->dcount: [0..3] guard words, [16..80) K2T column counts
 constexpr int SA_TC_COLS_AT = 16;
 constexpr int SA_TC_COLS_MAX = 64;

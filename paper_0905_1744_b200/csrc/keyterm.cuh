@@ -14,10 +14,12 @@ namespace sa {
 
 static __device__ uint64_t g_rtab[65536];   // floor(2^64 / d), d >= 2
 static __device__ uint32_t g_etab[65536];   // 2^64 mod d
+static __device__ double g_rcp[65536];      // RN(1 / d), d >= 1
 
 static __global__ void recip_kernel() {
   int d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= 65536) return;
+  g_rcp[d] = d ? __drcp_rn((double)d) : 0.0;
   if (d < 2) { g_rtab[d] = 0; g_etab[d] = 0; return; }
   uint64_t r = ~0ull / (uint64_t)d;
   uint64_t e = ~0ull % (uint64_t)d + 1;   // (2^64 - 1) mod d + 1
@@ -44,6 +46,19 @@ __device__ __forceinline__ void add_term(uint64_t& lo, uint32_t& hi, uint32_t C,
   uint64_t t = (uint64_t)C * g_rtab[D] + (uint64_t)((C * g_etab[D]) / D);
   lo += t;
   hi += (lo < t) ? 1u : 0u;
+}
+
+// F = C / D rounded to nearest (Z19) without a division: with y = RN(1/D),
+// q0 = RN(C y) is within an ulp of C/D, the remainder r = C - q0 D is exact
+// (FMA) and RN(q0 + r y) is the correctly rounded quotient (Markstein's
+// correction).  Verified against __ddiv_rn for every 0 <= C <= D <= 65535 by
+// sa_selftest_f_division (tests/test_gpu_parity.py).
+__device__ __forceinline__ double f_ratio(uint32_t C, uint32_t D) {
+  if (D == 0) return 0.0;
+  const double y = g_rcp[D], c = (double)C, d = (double)D;
+  const double q0 = c * y;
+  const double r = fma(-q0, d, c);
+  return fma(r, y, q0);
 }
 
 // d^F key term: round(2^52 (ln(1+Delta) - ln(Delta + C/D))), F = 0 when D = 0.

@@ -47,59 +47,122 @@ __device__ __forceinline__ bool tc_infeasible(const uint32_t* state) {
   return reinterpret_cast<const volatile uint32_t*>(state)[1] != 0u;
 }
 
-struct TcSide {
-  const uint16_t* rows;
-  int64_t n;
-};
+// Rows of all sides of a launch, flattened: side s = rows [row_begin[s], row_begin[s+1]).
 struct TcSides {
-  TcSide s[2 * tc::MAXPROB];
+  const uint16_t* rows[2 * tc::MAXPROB];
+  int64_t row_begin[2 * tc::MAXPROB + 1];
   int n;
 };
 
 // ---------------------------------------------------------- histogram ----
-__global__ void __launch_bounds__(512)
-tc_hist_kernel(const __grid_constant__ TcSides sides, int stride16, uint32_t* __restrict__ planes,
-               uint32_t* __restrict__ state) {
-  extern __shared__ uint32_t sp[];   // [2][TC_PLANE]
-  const TcSide S = sides.s[blockIdx.y];
-  for (int w = threadIdx.x; w < 2 * TC_PLANE; w += blockDim.x) sp[w] = 0u;
-  __syncthreads();
-  uint32_t mx = 0;
-  const int chunks = stride16 / 8;
-  for (int64_t r = blockIdx.x; r < S.n; r += gridDim.x) {
-    const uint4* row = reinterpret_cast<const uint4*>(S.rows + r * (int64_t)stride16);
-    for (int c = threadIdx.x; c < chunks; c += blockDim.x) {
-      const uint4 w4 = row[c];
-      if ((w4.x | w4.y | w4.z | w4.w) == 0u) continue;
-      const uint32_t ws[4] = {w4.x, w4.y, w4.z, w4.w};
+// Thread w of a CTA owns plane word w (bins 32 w .. 32 w + 31) of every layer:
+// for each of its rows it loads those 32 counts (64 bytes) and updates, per
+// layer l reached, seen1 |= m, seen2 |= seen1_old & m with m = [count >= l]
+// -- registers for the first TC_HREG layers, its own shared-memory words for
+// deeper ones; no atomics until the flush into the global planes.
+constexpr int TC_HREG = 8;
+constexpr int TC_HIST_THREADS = TC_WPL;   // 256
+constexpr int TC_HIST_ROWS = 4;
+
+__device__ __forceinline__ uint32_t layer_mask(const uint32_t (&v)[16], uint32_t L2) {
+  uint32_t m = 0;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const uint32_t v = (ws[q >> 1] >> (16 * (q & 1))) & 0xffffu;
-        if (!v) continue;
-        mx = max(mx, v);
-        const int t = c * 8 + q;
-        const uint32_t bit = 1u << (t & 31);
-        const int L = min((int)v, TC_LCAP);
-        for (int l = 0; l < L; ++l) {
-          const int word = l * TC_WPL + (t >> 5);
-          const uint32_t old = atomicOr(&sp[word], bit);
-          if (old & bit) atomicOr(&sp[TC_PLANE + word], bit);
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t c = __vsetgeu2(v[i], L2);   // 1 per half with count >= layer
+    m |= ((c | (c >> 15)) & 3u) << (2 * i);
+  }
+  return m;
+}
+
+__global__ void __launch_bounds__(TC_HIST_THREADS)
+tc_hist_kernel(const __grid_constant__ TcSides S, int stride16, uint32_t* __restrict__ planes,
+               uint32_t* __restrict__ state) {
+  extern __shared__ uint32_t deep[];   // [2][TC_LCAP - TC_HREG][TC_WPL], word w owned by thread w
+  constexpr int ND = TC_LCAP - TC_HREG;
+  const int w = threadIdx.x;
+  const bool active = w * 32 < stride16;
+  for (int l = 0; l < 2 * ND; ++l) deep[l * TC_WPL + w] = 0u;
+  const int64_t R = S.row_begin[S.n];
+  const int64_t r0 = blockIdx.x * R / gridDim.x, r1 = (blockIdx.x + 1) * R / gridDim.x;
+  uint32_t s1[TC_HREG], s2[TC_HREG];
+#pragma unroll
+  for (int l = 0; l < TC_HREG; ++l) s1[l] = s2[l] = 0u;
+  uint32_t mx = 0;
+  int side = -1, deepest = 0;
+  auto flush = [&](int sd) {
+    uint32_t* g1 = planes + (int64_t)sd * 2 * TC_PLANE;
+    uint32_t* g2 = g1 + TC_PLANE;
+#pragma unroll
+    for (int l = 0; l < TC_HREG; ++l) {
+      uint32_t t2 = s2[l];
+      if (s1[l]) t2 |= atomicOr(&g1[l * TC_WPL + w], s1[l]) & s1[l];   // seen by another CTA too
+      if (t2) atomicOr(&g2[l * TC_WPL + w], t2);
+      s1[l] = s2[l] = 0u;
+    }
+    for (int l = 0; l < deepest; ++l) {
+      const uint32_t d1 = deep[l * TC_WPL + w];
+      uint32_t d2 = deep[(ND + l) * TC_WPL + w];
+      if (d1) d2 |= atomicOr(&g1[(TC_HREG + l) * TC_WPL + w], d1) & d1;
+      if (d2) atomicOr(&g2[(TC_HREG + l) * TC_WPL + w], d2);
+      deep[l * TC_WPL + w] = deep[(ND + l) * TC_WPL + w] = 0u;
+    }
+    deepest = 0;
+  };
+  int64_t g = r0;
+  while (g < r1) {
+    int t = side < 0 ? 0 : side;
+    while (g >= S.row_begin[t + 1]) ++t;
+    if (t != side) {
+      if (side >= 0 && active) flush(side);
+      side = t;
+    }
+    const int cnt = (int)min((int64_t)TC_HIST_ROWS, min(r1, S.row_begin[t + 1]) - g);
+    if (active) {
+      uint4 raw[TC_HIST_ROWS][4];
+      const uint16_t* base = S.rows[t] + (g - S.row_begin[t]) * (int64_t)stride16 + w * 32;
+#pragma unroll
+      for (int h = 0; h < TC_HIST_ROWS; ++h)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          raw[h][k] = h < cnt ? reinterpret_cast<const uint4*>(base + h * (int64_t)stride16)[k] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int h = 0; h < TC_HIST_ROWS; ++h) {
+        uint32_t v[16];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          v[4 * k] = raw[h][k].x;
+          v[4 * k + 1] = raw[h][k].y;
+          v[4 * k + 2] = raw[h][k].z;
+          v[4 * k + 3] = raw[h][k].w;
+        }
+        uint32_t vm = v[0];
+#pragma unroll
+        for (int i = 1; i < 16; ++i) vm = __vmaxu2(vm, v[i]);
+        const uint32_t vmax = max(vm & 0xffffu, vm >> 16);
+        mx = max(mx, vmax);
+#pragma unroll
+        for (int l = 0; l < TC_HREG; ++l) {
+          if ((uint32_t)l >= vmax) break;
+          const uint32_t m = layer_mask(v, (uint32_t)(l + 1) * 0x00010001u);
+          s2[l] |= s1[l] & m;
+          s1[l] |= m;
+        }
+        const int top = (int)min(vmax, (uint32_t)TC_LCAP);
+        for (int l = TC_HREG; l < top; ++l) {
+          const uint32_t m = layer_mask(v, (uint32_t)(l + 1) * 0x00010001u);
+          uint32_t* d1 = &deep[(l - TC_HREG) * TC_WPL + w];
+          deep[(ND + l - TC_HREG) * TC_WPL + w] |= *d1 & m;
+          *d1 |= m;
+          deepest = max(deepest, l - TC_HREG + 1);
         }
       }
     }
+    g += cnt;
   }
+  if (side >= 0 && active) flush(side);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0 && mx) atomicMax(&state[0], mx);
-  __syncthreads();
-  uint32_t* g1 = planes + (int64_t)blockIdx.y * 2 * TC_PLANE;
-  uint32_t* g2 = g1 + TC_PLANE;
-  for (int w = threadIdx.x; w < TC_PLANE; w += blockDim.x) {
-    const uint32_t s1 = sp[w];
-    uint32_t s2 = sp[TC_PLANE + w];
-    if (s1) s2 |= atomicOr(&g1[w], s1) & s1;   // a bit another CTA already saw is now seen twice
-    if (s2) atomicOr(&g2[w], s2);
-  }
+  if ((w & 31) == 0 && mx) atomicMax(&state[0], mx);
 }
 
 // ------------------------------------------------------ column select ----
@@ -109,16 +172,28 @@ struct TcSel {
   int first;                                        // index of problem 0 in the whole call
 };
 
+// One CTA (1024 threads = 32 warps) per problem; warp w owns layer w + 1
+// (256 plane words, 8 per thread).  Kept columns per layer never increase
+// with the layer (a pair reaching layer l + 1 in a bin also reaches l), so the
+// layers holding at least half of the bins form a prefix: those are stored
+// "dense" -- every bin, in bin order, dw = round_up(bins, 16) columns per
+// layer (a column no pair shares only adds zeros off the diagonal, which the
+// epilogue overrides) -- and the build kernel encodes them with vector loads.
+// The remaining layers list their kept (layer, bin) columns.
 __global__ void __launch_bounds__(1024)
-tc_select_kernel(const __grid_constant__ TcSel sel, const uint32_t* __restrict__ planes,
-                 uint32_t* __restrict__ collist, int32_t* __restrict__ kblocks, uint32_t* __restrict__ state,
-                 uint32_t* __restrict__ cols_out) {
-  __shared__ uint32_t warp_tot[32];
+tc_select_kernel(const __grid_constant__ TcSel sel, const uint32_t* __restrict__ planes, int bins,
+                 uint32_t* __restrict__ collist, int32_t* __restrict__ kblocks, int32_t* __restrict__ ndense,
+                 uint32_t* __restrict__ state, uint32_t* __restrict__ cols_out) {
+  __shared__ uint32_t warp_cnt[32];
+  __shared__ uint32_t warp_pos[32];
+  __shared__ uint32_t s_total, s_nd;
   const int q = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr int PER = TC_PLANE / 1024;   // 8 words per thread
+  static_assert(TC_WPL == 32 * PER, "one warp per layer");
   const uint32_t* a = planes + (int64_t)sel.side_a[q] * 2 * TC_PLANE;
   const uint32_t* b = sel.side_b[q] >= 0 ? planes + (int64_t)sel.side_b[q] * 2 * TC_PLANE : nullptr;
+  const int dw = (bins + 15) & ~15;
   uint32_t m[PER];
   uint32_t cnt = 0;
 #pragma unroll
@@ -127,28 +202,28 @@ tc_select_kernel(const __grid_constant__ TcSel sel, const uint32_t* __restrict__
     m[i] = b ? (a[w] & b[w]) : a[TC_PLANE + w];
     cnt += __popc(m[i]);
   }
-  // block exclusive scan of cnt
-  uint32_t x = cnt;
+  uint32_t x = cnt;   // inclusive scan inside the warp (= layer)
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
-  if (lane == 31) warp_tot[wid] = x;
+  if (lane == 31) warp_cnt[wid] = x;
   __syncthreads();
-  if (wid == 0) {
-    uint32_t t = warp_tot[lane];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
-      if (lane >= o) t += y;
+  if (tid == 0) {
+    uint32_t nd = 0;
+    while (nd < 32 && 2 * warp_cnt[nd] >= (uint32_t)bins && warp_cnt[nd] > 0) ++nd;
+    uint32_t pos = nd * (uint32_t)dw;
+    for (int w = 0; w < 32; ++w) {
+      warp_pos[w] = w < (int)nd ? (uint32_t)w * dw : pos;
+      if (w >= (int)nd) pos += warp_cnt[w];
     }
-    warp_tot[lane] = t;   // inclusive
+    s_total = pos;
+    s_nd = nd;
   }
   __syncthreads();
-  const uint32_t total = warp_tot[31];
+  const uint32_t total = s_total, nd = s_nd;
   if (tid == 0 && cols_out && sel.first + q < SA_TC_COLS_MAX) cols_out[sel.first + q] = total;
-  uint32_t pos = x - cnt + (wid ? warp_tot[wid - 1] : 0u);
   const uint32_t kpad = max(128u, (total + 127u) & ~127u);
   const bool too_many = kpad > (uint32_t)TC_KCAP;
   const bool deep = reinterpret_cast<const volatile uint32_t*>(state)[0] > (uint32_t)TC_LCAP;
@@ -156,80 +231,128 @@ tc_select_kernel(const __grid_constant__ TcSel sel, const uint32_t* __restrict__
     if (tid == 0) {
       atomicOr(&state[1], 1u);
       kblocks[q] = 1;
+      ndense[q] = 0;
     }
     return;
   }
   uint32_t* out = collist + (int64_t)q * TC_KCAP;
+  const uint32_t layer = (uint32_t)wid + 1u;
+  if ((uint32_t)wid < nd) {
+    for (int t = lane; t < dw; t += 32) out[wid * dw + t] = t < bins ? ((uint32_t)t | (layer << 16)) : 0u;
+  } else {
+    uint32_t pos = warp_pos[wid] + x - cnt;
 #pragma unroll
-  for (int i = 0; i < PER; ++i) {
-    const int w = tid * PER + i;
-    const uint32_t layer = (uint32_t)(w / TC_WPL) + 1u;
-    const uint32_t bin0 = (uint32_t)(w % TC_WPL) * 32u;
-    uint32_t mm = m[i];
-    while (mm) {
-      const int bpos = __ffs(mm) - 1;
-      mm &= mm - 1;
-      out[pos++] = (bin0 + (uint32_t)bpos) | (layer << 16);
+    for (int i = 0; i < PER; ++i) {
+      const uint32_t bin0 = (uint32_t)(lane * PER + i) * 32u;
+      uint32_t mm = m[i];
+      while (mm) {
+        const int bpos = __ffs(mm) - 1;
+        mm &= mm - 1;
+        out[pos++] = (bin0 + (uint32_t)bpos) | (layer << 16);
+      }
     }
   }
   for (uint32_t p = total + tid; p < kpad; p += blockDim.x) out[p] = 0u;   // layer 0: padding column
-  if (tid == 0) kblocks[q] = (int32_t)(kpad / 128u);
+  if (tid == 0) {
+    kblocks[q] = (int32_t)(kpad / 128u);
+    ndense[q] = (int32_t)nd;
+  }
 }
 
 // ------------------------------------------------------- operand rows ----
-struct TcBuild {
-  const uint16_t* rows[2 * tc::MAXPROB];
+// Row r of side s -> out[s] + r * TC_KCAP: the side's problem's columns.
+// Dense layers (prefix): thread c of a row reads bins 16 c .. 16 c + 15 once
+// (two 16-byte loads) and writes one 16-byte chunk per dense layer; listed
+// (sparse) columns: 16 entries per chunk, the counts gathered from the row
+// (just read: L1 / L2).  TC_BUILD_ROWS rows per iteration keep loads in flight.
+struct TcOut {
   uint8_t* out[2 * tc::MAXPROB];
-  int64_t row_begin[2 * tc::MAXPROB + 1];   // prefix of row counts over targets
   int prob[2 * tc::MAXPROB];
-  int n;
 };
 
 constexpr int TC_BUILD_THREADS = 512;
+constexpr int TC_BUILD_ROWS = 4;
 
 __global__ void __launch_bounds__(TC_BUILD_THREADS)
-tc_build_kernel(const __grid_constant__ TcBuild B, int stride16, const uint32_t* __restrict__ collist,
-                const int32_t* __restrict__ kblocks, const uint32_t* __restrict__ state) {
+tc_build_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut O, int stride16, int bins,
+                const uint32_t* __restrict__ collist, const int32_t* __restrict__ kblocks,
+                const int32_t* __restrict__ ndense, const uint32_t* __restrict__ state) {
   if (tc_infeasible(state)) return;
-  extern __shared__ __align__(16) uint32_t sm[];
-  uint32_t* cols = sm;                                          // TC_KCAP entries
-  uint16_t* row = reinterpret_cast<uint16_t*>(sm + TC_KCAP);    // stride16 counts
-  const int64_t R = B.row_begin[B.n];
+  const int64_t R = S.row_begin[S.n];
   const int64_t r0 = blockIdx.x * R / gridDim.x, r1 = (blockIdx.x + 1) * R / gridDim.x;
-  int tgt = -1, kpad = 0;
-  for (int64_t g = r0; g < r1; ++g) {
-    int t = tgt < 0 ? 0 : tgt;
-    while (g >= B.row_begin[t + 1]) ++t;
-    __syncthreads();   // previous row (and column list) fully consumed
-    if (t != tgt) {
-      tgt = t;
-      const int q = B.prob[t];
-      kpad = kblocks[q] * 128;
-      const uint4* src = reinterpret_cast<const uint4*>(collist + (int64_t)q * TC_KCAP);
-      for (int i = threadIdx.x; i < kpad / 4; i += blockDim.x) reinterpret_cast<uint4*>(cols)[i] = src[i];
+  const int tid = threadIdx.x;
+  const int dwc = ((bins + 15) & ~15) / 16;   // chunks per dense layer
+  int side = -1, kch = 0, nd = 0, q = 0;
+  int64_t g = r0;
+  while (g < r1) {
+    int t = side < 0 ? 0 : side;
+    while (g >= S.row_begin[t + 1]) ++t;
+    if (t != side) {
+      side = t;
+      q = O.prob[t];
+      kch = kblocks[q] * 8;
+      nd = ndense[q];
     }
-    const int64_t r = g - B.row_begin[t];
-    const uint4* src = reinterpret_cast<const uint4*>(B.rows[t] + r * (int64_t)stride16);
-    for (int i = threadIdx.x; i < stride16 / 8; i += blockDim.x) reinterpret_cast<uint4*>(row)[i] = src[i];
-    __syncthreads();
-    uint4* dst = reinterpret_cast<uint4*>(B.out[t] + r * (int64_t)TC_KCAP);
-    for (int c = threadIdx.x; c < kpad / 16; c += blockDim.x) {
-      uint32_t o[4];
+    const int cnt = (int)min((int64_t)TC_BUILD_ROWS, min(r1, S.row_begin[t + 1]) - g);
+    const int64_t r = g - S.row_begin[t];
+    const uint16_t* rows = S.rows[t] + r * (int64_t)stride16;
+    uint8_t* outp = O.out[t] + r * (int64_t)TC_KCAP;
+    // dense layers
+    for (int c = tid; c < dwc && nd > 0; c += TC_BUILD_THREADS) {
+      uint4 v[TC_BUILD_ROWS][2];
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const uint4 e = reinterpret_cast<const uint4*>(cols)[c * 4 + w];
-        const uint32_t es[4] = {e.x, e.y, e.z, e.w};
-        uint32_t word = 0;
+      for (int h = 0; h < TC_BUILD_ROWS; ++h)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t layer = es[k] >> 16;
-          const uint32_t bitv = (layer != 0u && (uint32_t)row[es[k] & 0xffffu] >= layer) ? 1u : 0u;
-          word |= bitv << (8 * k);
+        for (int k = 0; k < 2; ++k)
+          v[h][k] = h < cnt ? reinterpret_cast<const uint4*>(rows + h * (int64_t)stride16 + c * 16)[k]
+                            : make_uint4(0, 0, 0, 0);
+      for (int l = 0; l < nd; ++l) {
+        const uint32_t L2 = (uint32_t)(l + 1) * 0x00010001u;
+#pragma unroll
+        for (int h = 0; h < TC_BUILD_ROWS; ++h) {
+          if (h >= cnt) break;
+          const uint32_t vs[8] = {v[h][0].x, v[h][0].y, v[h][0].z, v[h][0].w,
+                                  v[h][1].x, v[h][1].y, v[h][1].z, v[h][1].w};
+          uint32_t o[4];
+#pragma unroll
+          for (int wd = 0; wd < 4; ++wd) {
+            const uint32_t c0 = __vsetgeu2(vs[2 * wd], L2), c1 = __vsetgeu2(vs[2 * wd + 1], L2);
+            o[wd] = (c0 & 1u) | ((c0 >> 16) << 8) | ((c1 & 1u) << 16) | ((c1 >> 16) << 24);
+          }
+          reinterpret_cast<uint4*>(outp + h * (int64_t)TC_KCAP)[l * dwc + c] = make_uint4(o[0], o[1], o[2], o[3]);
         }
-        o[w] = word;
       }
-      dst[c] = make_uint4(o[0], o[1], o[2], o[3]);
     }
+    // listed columns (and the zero padding up to the 128-column K block)
+    const uint32_t* cl = collist + (int64_t)q * TC_KCAP;
+    for (int c = nd * dwc + tid; c < kch; c += TC_BUILD_THREADS) {
+      uint32_t e[16];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint4 x = reinterpret_cast<const uint4*>(cl + c * 16)[k];
+        e[4 * k] = x.x;
+        e[4 * k + 1] = x.y;
+        e[4 * k + 2] = x.z;
+        e[4 * k + 3] = x.w;
+      }
+      for (int h = 0; h < cnt; ++h) {
+        const uint16_t* row = rows + h * (int64_t)stride16;
+        uint32_t o[4];
+#pragma unroll
+        for (int wd = 0; wd < 4; ++wd) {
+          uint32_t word = 0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const uint32_t en = e[4 * wd + b];
+            const uint32_t layer = en >> 16;
+            word |= ((layer != 0u && (uint32_t)__ldg(row + (en & 0xffffu)) >= layer) ? 1u : 0u) << (8 * b);
+          }
+          o[wd] = word;
+        }
+        reinterpret_cast<uint4*>(outp + h * (int64_t)TC_KCAP)[c] = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+    }
+    g += cnt;
   }
 }
 
@@ -350,10 +473,7 @@ struct KeyMatEpi {
           if (s.nk_r < 0 || nk_c < 0 || gc <= s.row_g) continue;
           const int64_t o = (int64_t)gc * E.ld + s.row_g;
           if (E.num) E.num[o] = (uint16_t)C[j];
-          if (E.sim) {
-            const int D = min(s.nk_r, nk_c);
-            E.sim[o] = D > 0 ? __ddiv_rn((double)C[j], (double)D) : 0.0;
-          }
+          if (E.sim) E.sim[o] = f_ratio(C[j], (uint32_t)min(s.nk_r, nk_c));
         }
       }
       // direct half through a 32 x 32 transpose: lanes = consecutive columns
@@ -370,10 +490,7 @@ struct KeyMatEpi {
         const uint32_t Cv = xpose[i * 33 + lane];
         const int64_t o = (int64_t)rg * E.ld + gc;
         if (E.num) E.num[o] = (uint16_t)Cv;
-        if (E.sim) {
-          const int D = min(nk_ri, nk_cl);
-          E.sim[o] = D > 0 ? __ddiv_rn((double)Cv, (double)D) : 0.0;
-        }
+        if (E.sim) E.sim[o] = f_ratio(Cv, (uint32_t)min(nk_ri, nk_cl));
       }
       __syncwarp();
     }
@@ -391,12 +508,22 @@ struct KeyMatEpi {
   }
 };
 
+// ---------------------------------------------------- division self-test ----
+__global__ void f_division_check_kernel(unsigned long long* bad) {
+  const uint32_t D = blockIdx.x + 1;
+  unsigned long long nb = 0;
+  for (uint32_t C = threadIdx.x; C <= D; C += blockDim.x) {
+    const double a = f_ratio(C, D), b = __ddiv_rn((double)C, (double)D);
+    nb += (__double_as_longlong(a) != __double_as_longlong(b)) ? 1ull : 0ull;
+  }
+  if (nb) atomicAdd(bad, nb);
+}
+
 // ------------------------------------------------------------- host ----
 static sa_status tc_encode_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int box_rows);
 
 sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t bins, uint32_t* state,
                     uint32_t* cols_out, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1) {
-  (void)bins;
   SA_TRY(ensure_recip_tables_tu(st));
   static int g_num_sms = 0;
   if (g_num_sms == 0) {
@@ -406,9 +533,8 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
   }
   static bool configured = false;
   if (!configured) {
-    SA_CUDA(cudaFuncSetAttribute(tc_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TC_PLANE * 4));
-    SA_CUDA(cudaFuncSetAttribute(tc_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 TC_KCAP * 4 + 8192 * 2));
+    SA_CUDA(cudaFuncSetAttribute(tc_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 2 * (TC_LCAP - TC_HREG) * TC_WPL * 4));
     SA_CUDA(cudaFuncSetAttribute(tc::gemm_kernel<KeyMatEpi>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM));
     configured = true;
   }
@@ -422,54 +548,45 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     const size_t i1 = std::min(probs.size(), i0 + (size_t)tc::MAXPROB);
     const int np = (int)(i1 - i0);
     Scratch scratch(st);
-    // sides and selection
+    // sides (A rows of every problem, plus B rows of rectangular ones) and selection
     TcSides sides{};
+    TcOut outs{};
     TcSel sel{};
     sel.n = np;
     sel.first = (int)i0;
+    std::vector<int64_t> side_n;
+    auto add_side = [&](const uint32_t* rows, int64_t n, int q) {
+      sides.rows[sides.n] = reinterpret_cast<const uint16_t*>(rows);
+      sides.row_begin[sides.n + 1] = sides.row_begin[sides.n] + n;
+      outs.prob[sides.n] = q;
+      side_n.push_back(n);
+      return sides.n++;
+    };
     for (int q = 0; q < np; ++q) {
       const MsProblem& P = probs[i0 + q];
-      sel.side_a[q] = sides.n;
-      sides.s[sides.n++] = TcSide{reinterpret_cast<const uint16_t*>(P.A), P.na};
-      if (P.sym) {
-        sel.side_b[q] = -1;
-      } else {
-        sel.side_b[q] = sides.n;
-        sides.s[sides.n++] = TcSide{reinterpret_cast<const uint16_t*>(P.B), P.nb};
-      }
+      sel.side_a[q] = add_side(P.A, P.na, q);
+      sel.side_b[q] = P.sym ? -1 : add_side(P.B, P.nb, q);
     }
     SA_ALLOC(planes, uint32_t, (size_t)sides.n * 2 * TC_PLANE);
     SA_ALLOC(collist, uint32_t, (size_t)np * TC_KCAP);
     SA_ALLOC(kblocks, int32_t, np);
+    SA_ALLOC(ndense, int32_t, np);
     SA_CUDA(cudaMemsetAsync(planes, 0, (size_t)sides.n * 2 * TC_PLANE * 4, st));
-    int64_t maxn = 1;
-    for (int s = 0; s < sides.n; ++s) maxn = std::max(maxn, sides.s[s].n);
-    const int hx = (int)std::max<int64_t>(1, std::min<int64_t>(maxn, (3 * g_num_sms + sides.n - 1) / sides.n));
-    tc_hist_kernel<<<dim3(hx, sides.n), 512, 2 * TC_PLANE * 4, st>>>(sides, stride16, planes, state);
+    const int64_t R = sides.row_begin[sides.n];
+    const int hx = (int)std::max<int64_t>(1, std::min<int64_t>((R + TC_HIST_ROWS - 1) / TC_HIST_ROWS, 4 * g_num_sms));
+    tc_hist_kernel<<<hx, TC_HIST_THREADS, 2 * (TC_LCAP - TC_HREG) * TC_WPL * 4, st>>>(sides, stride16, planes, state);
     SA_LAUNCHED();
-    tc_select_kernel<<<np, 1024, 0, st>>>(sel, planes, collist, kblocks, state, cols_out);
+    tc_select_kernel<<<np, 1024, 0, st>>>(sel, planes, bins, collist, kblocks, ndense, state, cols_out);
     SA_LAUNCHED();
-    // operand rows: one target per side (the side's problem's column list)
-    TcBuild bl{};
+    // operand rows: one output per side (its problem's column list)
     uint8_t* side_out[2 * tc::MAXPROB];
-    bl.row_begin[0] = 0;
-    for (int q = 0; q < np; ++q) {
-      const int sa_ = sel.side_a[q], sb = sel.side_b[q];
-      for (int s : {sa_, sb}) {
-        if (s < 0) continue;
-        uint8_t* o = scratch.alloc<uint8_t>((size_t)sides.s[s].n * TC_KCAP);
-        if (!o) return fail(SA_E_NOMEM, "scratch allocation of K2T operand rows failed");
-        side_out[s] = o;
-        bl.rows[bl.n] = sides.s[s].rows;
-        bl.out[bl.n] = o;
-        bl.prob[bl.n] = q;
-        bl.row_begin[bl.n + 1] = bl.row_begin[bl.n] + sides.s[s].n;
-        ++bl.n;
-      }
+    for (int sd = 0; sd < sides.n; ++sd) {
+      uint8_t* o = scratch.alloc<uint8_t>((size_t)side_n[sd] * TC_KCAP);
+      if (!o) return fail(SA_E_NOMEM, "scratch allocation of K2T operand rows failed");
+      side_out[sd] = outs.out[sd] = o;
     }
-    const int64_t R = bl.row_begin[bl.n];
-    const int bx = (int)std::min<int64_t>(R, 2 * g_num_sms);
-    tc_build_kernel<<<bx, TC_BUILD_THREADS, TC_KCAP * 4 + 8192 * 2, st>>>(bl, stride16, collist, kblocks, state);
+    const int bx = (int)std::max<int64_t>(1, std::min<int64_t>((R + TC_BUILD_ROWS - 1) / TC_BUILD_ROWS, 4 * g_num_sms));
+    tc_build_kernel<<<bx, TC_BUILD_THREADS, 0, st>>>(sides, outs, stride16, bins, collist, kblocks, ndense, state);
     SA_LAUNCHED();
     // GEMM
     tc::Batch batch{};
@@ -513,6 +630,22 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     i0 = i1;
   }
   if (ev1) SA_CUDA(cudaEventRecord(ev1, st));
+  return SA_OK;
+}
+
+sa_status f_division_selftest(int64_t* mismatches_h) {
+  SA_TRY(ensure_recip_tables_tu(0));
+  unsigned long long* d = nullptr;
+  SA_CUDA(cudaMalloc(&d, sizeof(unsigned long long)));
+  SA_CUDA(cudaMemset(d, 0, sizeof(unsigned long long)));
+  f_division_check_kernel<<<65535, 256>>>(d);
+  const cudaError_t e = cudaGetLastError();
+  unsigned long long h = 0;
+  if (e == cudaSuccess) cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(SA_E_CUDA, "division self-test launch: %s", cudaGetErrorString(e));
+  SA_CUDA(cudaGetLastError());
+  *mismatches_h = (int64_t)h;
   return SA_OK;
 }
 

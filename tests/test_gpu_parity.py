@@ -153,6 +153,13 @@ def test_bucket_similarity_random(ctx, engine, n, dup, lo):
     assert np.array_equal(s, Fo)     # one IEEE RN division on both sides
 
 
+def test_f_division_free_is_ieee_rn(ctx):
+    """The K2T matrix epilogue computes F = C/D as fma(r, RN(1/D), q0) with
+    q0 = RN(C RN(1/D)) and r = C - q0 D (Markstein): bit-identical to IEEE RN
+    division for every 0 <= C <= D <= 65535 (the whole domain of Eq. 1's F)."""
+    assert B.selftest_f_division(0) == 0
+
+
 def test_tc_falls_back_on_deep_counts(ctx, monkeypatch):
     """K2T tracks 32 threshold layers: a bin count of 33..255 must hand the call
     to the uint8 SAD engine on the device, exactly."""
