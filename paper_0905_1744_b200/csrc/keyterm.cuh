@@ -53,13 +53,19 @@ __device__ __forceinline__ void add_term(uint64_t& lo, uint32_t& hi, uint32_t C,
 // (FMA) and RN(q0 + r y) is the correctly rounded quotient (Markstein's
 // correction).  Verified against __ddiv_rn for every 0 <= C <= D <= 65535 by
 // sa_selftest_f_division (tests/test_gpu_parity.py).
-__device__ __forceinline__ double f_ratio(uint32_t C, uint32_t D) {
-  if (D == 0) return 0.0;
-  const double y = g_rcp[D], c = (double)C, d = (double)D;
+// The same with d = (double)D and y = RN(1/D) supplied (y = 0 for D = 0 gives 0).
+__device__ __forceinline__ double f_ratio_y(uint32_t C, double d, double y) {
+  // (double)C for C < 2^32 without the quarter-rate I2F.F64: 2^52 + C, minus 2^52 (exact)
+  const double c = __hiloint2double(0x43300000, (int)C) - 4503599627370496.0;
   const double q0 = c * y;
   const double r = fma(-q0, d, c);
   return fma(r, y, q0);
 }
+__device__ __forceinline__ double f_ratio(uint32_t C, uint32_t D) {
+  if (D == 0) return 0.0;
+  return f_ratio_y(C, (double)D, g_rcp[D]);
+}
+__device__ __forceinline__ double rcp_of(int n) { return n > 0 ? g_rcp[n] : 0.0; }
 
 // d^F key term: round(2^52 (ln(1+Delta) - ln(Delta + C/D))), F = 0 when D = 0.
 __device__ __forceinline__ void add_dF_term(uint64_t& lo, uint32_t& hi, uint32_t C, uint32_t D, double delta,

@@ -376,6 +376,12 @@ __device__ __forceinline__ void add96(uint64_t& lo, uint32_t& hi, uint64_t blo, 
   hi += bhi + ((lo < blo) ? 1u : 0u);
 }
 
+// MODE: which outputs this instantiation can write (EPI_KEYS | EPI_NUM |
+// EPI_SIM); a launch picks the smallest one covering its problems, so the
+// key path and the matrix path each get their own register allocation.
+enum { EPI_KEYS = 1, EPI_NUM = 2, EPI_SIM = 4, EPI_ALL = 7 };
+
+template <int MODE>
 struct KeyMatEpi {
   TcEpiProb e[tc::MAXPROB];
   const uint32_t* state;
@@ -385,6 +391,7 @@ struct KeyMatEpi {
     uint32_t hi;
     int nk_r;
     int row_g;
+    double d_r, y_r;   // (double)nk_r and RN(1 / nk_r): F = C / min(nk_r, nk_c) without a division
   };
 
   __device__ bool skip() const { return tc_infeasible(state); }
@@ -395,6 +402,10 @@ struct KeyMatEpi {
     s.hi = 0;
     s.row_g = T.row0 + row;
     s.nk_r = row < T.ra ? E.nkA[s.row_g] : -1;
+    if ((MODE & EPI_SIM) && E.sim) {
+      s.d_r = (double)max(s.nk_r, 0);
+      s.y_r = rcp_of(s.nk_r);
+    }
   }
 
   __device__ void chunk(State& s, const tc::Tile& T, int row, int col, const uint32_t (&v)[32], int lane,
@@ -407,7 +418,7 @@ struct KeyMatEpi {
 #pragma unroll
     for (int j = 0; j < 32; ++j) C[j] = (sym && c0 + j == s.row_g) ? (uint32_t)s.nk_r : v[j];
 
-    if (E.keyA) {
+    if ((MODE & EPI_KEYS) && E.keyA) {
       const bool colsum = sym && E.keyB;
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
@@ -463,17 +474,24 @@ struct KeyMatEpi {
       }
     }
 
-    if (E.num || E.sim) {
+    if ((MODE & (EPI_NUM | EPI_SIM)) && (E.num || E.sim)) {
+      const bool want_sim = (MODE & EPI_SIM) && E.sim;
+      // per-lane column side of D = min(nk_r, nk_c) for the division-free F
+      const double d_cl = (double)max(nk_cl, 0), y_cl = want_sim ? rcp_of(nk_cl) : 0.0;
       // mirrored half (symmetric): lanes = consecutive rows -> coalesced columns
       if (sym) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int nk_c = __shfl_sync(0xffffffffu, nk_cl, j);
+          const double d_c = __shfl_sync(0xffffffffu, d_cl, j), y_c = __shfl_sync(0xffffffffu, y_cl, j);
           const int gc = c0 + j;
           if (s.nk_r < 0 || nk_c < 0 || gc <= s.row_g) continue;
           const int64_t o = (int64_t)gc * E.ld + s.row_g;
           if (E.num) E.num[o] = (uint16_t)C[j];
-          if (E.sim) E.sim[o] = f_ratio(C[j], (uint32_t)min(s.nk_r, nk_c));
+          if (want_sim) {
+            const bool rmin = s.nk_r <= nk_c;
+            E.sim[o] = f_ratio_y(C[j], rmin ? s.d_r : d_c, rmin ? s.y_r : y_c);
+          }
         }
       }
       // direct half through a 32 x 32 transpose: lanes = consecutive columns
@@ -485,12 +503,16 @@ struct KeyMatEpi {
 #pragma unroll 4
       for (int i = 0; i < 32; ++i) {
         const int nk_ri = __shfl_sync(0xffffffffu, s.nk_r, i);
+        const double d_ri = __shfl_sync(0xffffffffu, s.d_r, i), y_ri = __shfl_sync(0xffffffffu, s.y_r, i);
         const int rg = rbase + i;
         if (nk_ri < 0 || nk_cl < 0 || (sym && gc < rg)) continue;
         const uint32_t Cv = xpose[i * 33 + lane];
         const int64_t o = (int64_t)rg * E.ld + gc;
         if (E.num) E.num[o] = (uint16_t)Cv;
-        if (E.sim) E.sim[o] = f_ratio(Cv, (uint32_t)min(nk_ri, nk_cl));
+        if (want_sim) {
+          const bool rmin = nk_ri <= nk_cl;
+          E.sim[o] = f_ratio_y(Cv, rmin ? d_ri : d_cl, rmin ? y_ri : y_cl);
+        }
       }
       __syncwarp();
     }
@@ -498,7 +520,7 @@ struct KeyMatEpi {
 
   __device__ void end(State& s, const tc::Tile& T, int row) const {
     const TcEpiProb& E = e[T.pi];
-    if (E.keyA && s.nk_r >= 0 && (s.lo | s.hi)) atomic_add_key(E.keyA + s.row_g, s.lo, s.hi);
+    if ((MODE & EPI_KEYS) && E.keyA && s.nk_r >= 0 && (s.lo | s.hi)) atomic_add_key(E.keyA + s.row_g, s.lo, s.hi);
     (void)row;
   }
 
@@ -507,6 +529,38 @@ struct KeyMatEpi {
     else add_term(lo, hi, C, D);
   }
 };
+
+// ------------------------------------------------------------- F pass ----
+// F = C / min(nk_row, nk_col) elementwise over an na x nb numerator matrix
+// (row stride ld), written as fp64 (Z19: IEEE RN, via f_ratio).  Used for
+// S5's similarity matrix after a numerator-only GEMM epilogue: a coalesced
+// HBM-bound pass (2 bytes read, 8 written per entry) at full occupancy instead
+// of fp64 work inside the tensor-core kernel's epilogue.
+__global__ void __launch_bounds__(256)
+ratio_kernel(const uint16_t* __restrict__ num, const int32_t* __restrict__ nkA, const int32_t* __restrict__ nkB,
+             int64_t na, int64_t nb, int64_t ld, double* __restrict__ sim, const uint32_t* __restrict__ state) {
+  if (state && tc_infeasible(state)) return;   // K2T declined: the fallback engine wrote sim itself
+  for (int64_t i = blockIdx.x; i < na; i += gridDim.x) {
+    const int nki = nkA[i];
+    const uint16_t* nr = num + i * ld;
+    double* sr = sim + i * ld;
+#pragma unroll 4
+    for (int64_t j = threadIdx.x; j < nb; j += blockDim.x) {
+      const int D = min(nki, nkB[j]);
+      sr[j] = D > 0 ? f_ratio(nr[j], (uint32_t)D) : 0.0;
+    }
+  }
+}
+
+sa_status ratio_launch(const uint16_t* num, const int32_t* nkA, const int32_t* nkB, int64_t na, int64_t nb,
+                       int64_t ld, double* sim, cudaStream_t st, const uint32_t* state) {
+  if (na <= 0 || nb <= 0) return SA_OK;
+  SA_TRY(ensure_recip_tables_tu(st));
+  const int64_t blocks = std::min<int64_t>(na, 148 * 8);
+  ratio_kernel<<<(unsigned)blocks, 256, 0, st>>>(num, nkA, nkB, na, nb, ld, sim, state);
+  SA_LAUNCHED();
+  return SA_OK;
+}
 
 // ---------------------------------------------------- division self-test ----
 __global__ void f_division_check_kernel(unsigned long long* bad) {
@@ -535,10 +589,19 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
   if (!configured) {
     SA_CUDA(cudaFuncSetAttribute(tc_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  2 * (TC_LCAP - TC_HREG) * TC_WPL * 4));
-    SA_CUDA(cudaFuncSetAttribute(tc::gemm_kernel<KeyMatEpi>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM));
+    SA_CUDA(cudaFuncSetAttribute(tc::gemm_kernel<KeyMatEpi<EPI_KEYS>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tc::SMEM));
+    SA_CUDA(cudaFuncSetAttribute(tc::gemm_kernel<KeyMatEpi<EPI_NUM>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tc::SMEM));
+    SA_CUDA(cudaFuncSetAttribute(tc::gemm_kernel<KeyMatEpi<EPI_ALL>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tc::SMEM));
     configured = true;
   }
   const int stride16 = 2 * ldw16;
+  static const bool fpass = [] {
+    const char* e = getenv("SA_K2T_FPASS");
+    return e && atoi(e) != 0;
+  }();
   std::vector<MsProblem> probs;
   for (const auto& p : probs_in)
     if (p.na > 0 && p.nb > 0) probs.push_back(p);
@@ -592,7 +655,8 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     tc::Batch batch{};
     tc::Maps maps;
     std::memset(&maps, 0, sizeof maps);
-    KeyMatEpi epi{};
+    KeyMatEpi<EPI_ALL> epi{};
+    int mode = 0;
     epi.state = state;
     int64_t tiles = 0;
     for (int q = 0; q < np; ++q) {
@@ -615,18 +679,39 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       E.nkB = P.nkB;
       E.keyA = P.keyA;
       E.keyB = P.sym ? P.keyB : nullptr;
+      // S5's F: in the tensor-core epilogue (default), or (SA_K2T_FPASS=1) numerators
+      // there and F by ratio_kernel after
       E.num = P.num;
-      E.sim = P.sim;
+      E.sim = fpass ? nullptr : P.sim;
+      if (fpass && P.sim && !P.num) {
+        E.num = scratch.alloc<uint16_t>((size_t)P.na * P.ld);
+        if (!E.num) return fail(SA_E_NOMEM, "scratch allocation of K2T numerators failed");
+      }
       E.ld = P.ld;
       E.form = P.form;
       E.delta = P.delta;
       E.ln1pd = P.ln1pd;
       E.sym = P.sym;
+      mode |= (P.keyA ? EPI_KEYS : 0) | (E.num ? EPI_NUM : 0) | (E.sim ? EPI_SIM : 0);
     }
     batch.n = np;
     const int64_t grid = tiles < g_num_sms ? tiles : g_num_sms;
-    tc::gemm_kernel<KeyMatEpi><<<(unsigned)grid, tc::THREADS, tc::SMEM, st>>>(batch, maps, tiles, epi);
+    if (mode == EPI_KEYS) {
+      KeyMatEpi<EPI_KEYS> k;
+      std::memcpy(&k, &epi, sizeof k);
+      tc::gemm_kernel<KeyMatEpi<EPI_KEYS>><<<(unsigned)grid, tc::THREADS, tc::SMEM, st>>>(batch, maps, tiles, k);
+    } else if ((mode & ~EPI_NUM) == 0) {
+      KeyMatEpi<EPI_NUM> k;
+      std::memcpy(&k, &epi, sizeof k);
+      tc::gemm_kernel<KeyMatEpi<EPI_NUM>><<<(unsigned)grid, tc::THREADS, tc::SMEM, st>>>(batch, maps, tiles, k);
+    } else {
+      tc::gemm_kernel<KeyMatEpi<EPI_ALL>><<<(unsigned)grid, tc::THREADS, tc::SMEM, st>>>(batch, maps, tiles, epi);
+    }
     SA_LAUNCHED();
+    for (int q = 0; q < np; ++q) {
+      const MsProblem& P = probs[i0 + q];
+      if (fpass && P.sim) SA_TRY(ratio_launch(epi.e[q].num, P.nkA, P.nkB, P.na, P.nb, P.ld, P.sim, st, state));
+    }
     i0 = i1;
   }
   if (ev1) SA_CUDA(cudaEventRecord(ev1, st));

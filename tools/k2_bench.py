@@ -52,6 +52,16 @@ def main():
     peak = 128 * 148 * 1965e6
     print(json.dumps({"n": n, "ms": ms, "pairs_per_s": pairs / ms * 1e3,
                       "binops_per_s": pairs * 8000 / ms * 1e3, "frac_of_peak": pairs * 8000 / ms * 1e3 / peak}))
+    print(json.dumps({"engine": ctx.engine(), "tc_columns": ctx.tc_columns() if ctx.engine() == "tc" else None}))
+    # symmetric keys (S2a shape: the block's own local rank)
+    B.sa_kmer_rank(ctx, P, nk, P, nk, want_f64=False)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    B.sa_kmer_rank(ctx, P, nk, P, nk, want_f64=False)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    print(json.dumps({"sym_keys": n, "ms": ms, "pairs_per_s": pairs / ms * 1e3}))
     # rectangular (S2d shape)
     q = P[: min(n, 12500)]
     qn = nk[: q.shape[0]]
