@@ -302,14 +302,11 @@ def main():
         # contractions on the tensor cores; algorithmic work = 2 K'_b ops per
         # pair (K'_b = kept layer columns of bucket b, read back after the timed
         # region by re-running each bucket once) against the u8 tensor peak.
-        kcols = {}
-        for b, row, n_b in out.buckets:
-            if n_b > 1:
-                B.sa_bucket_similarity(ctx, out.bucket_profiles[row:row + n_b], out.bucket_nkmers[row:row + n_b],
-                                       hp.bins, numerators=out.numerators[own.index(b)],
-                                       similarity=out.similarity[own.index(b)],
-                                       want_similarity=not args.no_similarity)
-                kcols[b] = ctx.tc_columns()[0]
+        nz = [(b, row, n_b) for b, row, n_b in out.buckets if n_b > 0]
+        B.sa_bucket_similarity_batch(ctx, out.bucket_profiles, out.bucket_nkmers,
+                                     [r for _, r, _ in out.buckets] + [sum(n for _, _, n in out.buckets)],
+                                     hp.bins, numerators=out.numerators, similarity=out.similarity)
+        kcols = dict(zip([b for b, _, _ in nz], ctx.tc_columns()))
         ops = sum(2.0 * kcols[b] * int(sizes[b]) * (int(sizes[b]) - 1) / 2 for b in kcols)
         bf16 = float(peaks.get("bf16_tflops", 1590.0))
         peak = 2.0 * bf16 * 1e12          # u8 dense = 2 x bf16 dense (4.5 / 2.25 PF nominal)

@@ -252,6 +252,19 @@ sa_status sa_redistribute(sa_ctx* ctx, int32_t p, const uint8_t* residues, const
 sa_status sa_bucket_similarity(sa_ctx* ctx, const uint16_t* profiles, const int32_t* nkmers, int32_t n,
                                int32_t bins, uint16_t* numerators, double* similarity, void* stream);
 
+/* The same for several buckets in one call (one engine launch over all of
+ * them: the operand preparation and the tile schedule are shared, so many
+ * small buckets cost no more launches than one large one).  Bucket b is rows
+ * [row_begin_h[b], row_begin_h[b+1]) of `profiles` / `nkmers` (the layout
+ * sa_redistribute produces: buckets contiguous, members ascending by global
+ * id); its outputs are numerators_h[b] / similarity_h[b] (host arrays of
+ * device pointers, each [n_b][n_b]; the arrays and any entry are nullable).
+ * Empty buckets are skipped.  SA_E_INVAL: nbuckets < 0, row_begin_h not
+ * non-decreasing from 0, bad bins, NULL profiles / nkmers with rows. */
+sa_status sa_bucket_similarity_batch(sa_ctx* ctx, int32_t nbuckets, const uint16_t* profiles, const int32_t* nkmers,
+                                     const int64_t* row_begin_h, int32_t bins, uint16_t* const* numerators_h,
+                                     double* const* similarity_h, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

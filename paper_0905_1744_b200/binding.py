@@ -26,7 +26,8 @@ PHASES = ["S2a", "S2b", "S2c", "S2d", "S3", "S5", "rank"]
 EXPORTED = ["sa_ctx_create", "sa_ctx_attach_comm", "sa_ctx_destroy", "sa_last_error", "sa_launch_count",
             "sa_ctx_set_timing", "sa_ctx_phase_ms", "sa_profile_stride", "sa_kmer_profiles", "sa_kmer_rank",
             "sa_partition", "sa_redistribute", "sa_bucket_similarity", "sa_exact_rank_compare", "sa_ctx_engine",
-            "sa_ctx_set_rank_form", "sa_ctx_tc_columns", "sa_selftest_f_division"]
+            "sa_ctx_set_rank_form", "sa_ctx_tc_columns", "sa_selftest_f_division",
+            "sa_bucket_similarity_batch"]
 SA_RANK_F, SA_RANK_DF = 0, 1
 
 
@@ -93,6 +94,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "sa_redistribute": (ctypes.c_int, [P, I32, P, P, I32, I64, P, ctypes.POINTER(ctypes.c_int64),
                                            ctypes.POINTER(ctypes.c_int64), P, P, P, P, VP]),
         "sa_bucket_similarity": (ctypes.c_int, [P, P, P, I32, I32, P, P, VP]),
+        "sa_bucket_similarity_batch": (ctypes.c_int, [P, I32, P, P, ctypes.POINTER(ctypes.c_int64), I32,
+                                                      ctypes.POINTER(ctypes.c_void_p),
+                                                      ctypes.POINTER(ctypes.c_void_p), VP]),
         "sa_exact_rank_compare": (ctypes.c_int, [P, I32, P, I32, P, I32]),
         "sa_ctx_engine": (ctypes.c_int, [P]),
         "sa_ctx_tc_columns": (ctypes.c_int32, [P, P, ctypes.c_int32]),
@@ -357,6 +361,31 @@ def sa_bucket_similarity(ctx: Context, profiles, nkmers, bins: int = 8000, want_
         similarity = torch.empty((n, n), dtype=torch.float64, device=dev)
     _check(load_library().sa_bucket_similarity(ctx.handle, _ptr(profiles), _ptr(nkmers), n, bins,
                                                _ptr(numerators), _ptr(similarity), _stream(stream)))
+    return numerators, similarity
+
+
+def sa_bucket_similarity_batch(ctx: Context, profiles, nkmers, row_begin, bins: int = 8000,
+                               want_numerators: bool = True, want_similarity: bool = True,
+                               numerators=None, similarity=None, stream=None):
+    """S5 over several buckets in one call: bucket b = rows [row_begin[b],
+    row_begin[b+1]).  Returns (list of numerators | None, list of similarity | None),
+    one entry per bucket (None for empty buckets or when not wanted)."""
+    _dev(profiles, torch.uint16, "profiles")
+    _dev(nkmers, torch.int32, "nkmers")
+    nb = len(row_begin) - 1
+    dev = nkmers.device
+    sizes = [int(row_begin[b + 1]) - int(row_begin[b]) for b in range(nb)]
+    if numerators is None:
+        numerators = [torch.empty((n, n), dtype=torch.uint16, device=dev) if want_numerators and n else None
+                      for n in sizes]
+    if similarity is None:
+        similarity = [torch.empty((n, n), dtype=torch.float64, device=dev) if want_similarity and n else None
+                      for n in sizes]
+    rb = (ctypes.c_int64 * (nb + 1))(*[int(x) for x in row_begin])
+    nums = (ctypes.c_void_p * max(nb, 1))(*[(t.data_ptr() if t is not None else None) for t in numerators])
+    sims = (ctypes.c_void_p * max(nb, 1))(*[(t.data_ptr() if t is not None else None) for t in similarity])
+    _check(load_library().sa_bucket_similarity_batch(ctx.handle, nb, _ptr(profiles), _ptr(nkmers), rb, bins,
+                                                     nums, sims, _stream(stream)))
     return numerators, similarity
 
 

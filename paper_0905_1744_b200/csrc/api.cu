@@ -1033,4 +1033,43 @@ sa_status sa_bucket_similarity(sa_ctx* ctx, const uint16_t* profiles, const int3
   return SA_OK;
 }
 
+sa_status sa_bucket_similarity_batch(sa_ctx* ctx, int32_t nbuckets, const uint16_t* profiles, const int32_t* nkmers,
+                                     const int64_t* row_begin_h, int32_t bins, uint16_t* const* numerators_h,
+                                     double* const* similarity_h, void* stream) {
+  g_err.clear();
+  if (!ctx) return fail(SA_E_INVAL, "ctx is NULL");
+  if (nbuckets < 0 || bins < 1 || bins > 65536) return fail(SA_E_INVAL, "bad nbuckets / bins");
+  if (nbuckets == 0) return SA_OK;
+  if (!row_begin_h) return fail(SA_E_INVAL, "NULL row_begin_h");
+  if (row_begin_h[0] != 0) return fail(SA_E_INVAL, "row_begin_h[0] must be 0");
+  for (int b = 0; b < nbuckets; ++b) {
+    if (row_begin_h[b + 1] < row_begin_h[b]) return fail(SA_E_INVAL, "row_begin_h must be non-decreasing");
+    if (row_begin_h[b + 1] - row_begin_h[b] > INT32_MAX) return fail(SA_E_INVAL, "bucket too large");
+  }
+  const int64_t n = row_begin_h[nbuckets];
+  if (n == 0) return SA_OK;
+  if (!profiles || !nkmers) return fail(SA_E_INVAL, "NULL required pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  SA_CUDA(cudaSetDevice(ctx->device));
+  Scratch scratch(st);
+  EngineOps E;
+  SA_TRY(prepare_ops(ctx, scratch, profiles, n, profiles, n, bins, true, &E, st));
+  std::vector<MsProblem> probs;
+  for (int b = 0; b < nbuckets; ++b) {
+    const int64_t r0 = row_begin_h[b], nb = row_begin_h[b + 1] - r0;
+    if (nb == 0) continue;
+    MsProblem pr{};
+    pr.A = pr.B = E.a16.rows + r0 * E.a16.ldw;
+    pr.nkA = pr.nkB = nkmers + r0;
+    pr.na = pr.nb = (int32_t)nb;
+    pr.sym = 1;
+    pr.num = numerators_h ? numerators_h[b] : nullptr;
+    pr.sim = similarity_h ? similarity_h[b] : nullptr;
+    pr.ld = nb;
+    probs.push_back(pr);
+  }
+  SA_TRY(launch_ops(ctx, E, probs, st, ev_begin(ctx, SA_PHASE_S5), ev_end(ctx, SA_PHASE_S5)));
+  return SA_OK;
+}
+
 }  // extern "C"

@@ -100,19 +100,28 @@ class HotPath:
         bprof, bnk = B.sa_kmer_profiles(ctx, rres, roffs, self.k, self.alphabet, stream=stream)
         mark("S1b")
         res = StepResult(prof, nk, part, rres, roffs, rgid, rbkt, bprof, bnk)
+        owned = list(B.owned_buckets(self.p, ctx.nranks, ctx.rank))
         row = 0
-        for b in B.owned_buckets(self.p, ctx.nranks, ctx.rank):
+        for b in owned:
             n_b = int(part.counts[:, b].sum())
             num, sim = self._outputs(b, n_b, offsets.device) if n_b > 0 else (None, None)
-            if n_b > 0:
-                B.sa_bucket_similarity(ctx, bprof[row:row + n_b], bnk[row:row + n_b], self.bins,
-                                       want_numerators=self.want_num, want_similarity=self.want_sim,
-                                       numerators=num, similarity=sim, stream=stream)
-                if on_bucket is not None:
-                    on_bucket(b, num, sim)
             res.buckets.append((b, row, n_b))
             res.numerators.append(num)
             res.similarity.append(sim)
             row += n_b
+        if on_bucket is None:
+            # every owned bucket in one engine launch (sa_bucket_similarity_batch)
+            rb = [r for _, r, _ in res.buckets] + [row]
+            B.sa_bucket_similarity_batch(ctx, bprof, bnk, rb, self.bins, numerators=res.numerators,
+                                         similarity=res.similarity, stream=stream)
+        else:
+            # one call per bucket, so the caller can start bucket b's copy while
+            # the next bucket computes
+            for (b, r0, n_b), num, sim in zip(res.buckets, res.numerators, res.similarity):
+                if n_b > 0:
+                    B.sa_bucket_similarity(ctx, bprof[r0:r0 + n_b], bnk[r0:r0 + n_b], self.bins,
+                                           want_numerators=self.want_num, want_similarity=self.want_sim,
+                                           numerators=num, similarity=sim, stream=stream)
+                    on_bucket(b, num, sim)
         mark("S5")
         return res

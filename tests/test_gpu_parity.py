@@ -160,6 +160,28 @@ def test_f_division_free_is_ieee_rn(ctx):
     assert B.selftest_f_division(0) == 0
 
 
+@pytest.mark.parametrize("sizes", [[0, 300, 1, 129, 0, 257], [2, 0, 0, 3]])
+def test_bucket_similarity_batch(ctx, engine, sizes):
+    """sa_bucket_similarity_batch: every bucket of a ragged batch (empty ones
+    included) equals the oracle's bucket matrices, in one engine launch."""
+    n = sum(sizes)
+    ds = _rand_set(4242 + n, n, 0, 420, dup=3)
+    res, offs = to_dev(ds)
+    P, nk = B.sa_kmer_profiles(ctx, res, offs)
+    Po, nko = kmer.profiles(ds.residues, ds.offsets)
+    rb = np.concatenate([[0], np.cumsum(sizes)])
+    nums, sims = B.sa_bucket_similarity_batch(ctx, P, nk, rb)
+    if n > 1:
+        assert ctx.engine() == ENGINE_NAME[engine]
+    for b, sz in enumerate(sizes):
+        if sz == 0:
+            assert nums[b] is None and sims[b] is None
+            continue
+        Co, Fo = partition.bucket_similarity(Po, nko, np.arange(rb[b], rb[b + 1]))
+        assert np.array_equal(nums[b].cpu().numpy(), Co)
+        assert np.array_equal(sims[b].cpu().numpy(), Fo)
+
+
 def test_tc_falls_back_on_deep_counts(ctx, monkeypatch):
     """K2T tracks 32 threshold layers: a bin count of 33..255 must hand the call
     to the uint8 SAD engine on the device, exactly."""
