@@ -264,15 +264,59 @@ tc_select_kernel(const __grid_constant__ TcSel sel, const uint32_t* __restrict__
 // Dense layers (prefix): thread c of a row reads bins 16 c .. 16 c + 15 once
 // (two 16-byte loads) and writes one 16-byte chunk per dense layer; listed
 // (sparse) columns: 16 entries per chunk, the counts gathered from the row
-// (just read: L1 / L2).  TC_BUILD_ROWS rows per iteration keep loads in flight.
+// (L1 / L2).
 struct TcOut {
   uint8_t* out[2 * tc::MAXPROB];
   int prob[2 * tc::MAXPROB];
 };
 
-constexpr int TC_BUILD_THREADS = 512;
-constexpr int TC_BUILD_ROWS = 4;
+// Dense layers: one thread per (row, 16-bin chunk) of every side, all dense
+// layers of that chunk from one 32-byte load.  Counts are <= TC_LCAP here (the
+// launch is feasible), so for each u16 half h: h >= L <=> bit 15 of
+// h + 0x8000 - L (no carry between the halves).
+__global__ void __launch_bounds__(256)
+tc_dense_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut O, int stride16, int bins,
+                const int32_t* __restrict__ ndense, const uint32_t* __restrict__ state) {
+  if (tc_infeasible(state)) return;
+  const int dwc = ((bins + 15) & ~15) / 16;
+  const int64_t items = S.row_begin[S.n] * dwc;
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = it / dwc;
+    const int c = (int)(it - g * dwc);
+    int lo = 0, hi = S.n - 1;   // side of row g: last s with row_begin[s] <= g
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (S.row_begin[mid] <= g) lo = mid;
+      else hi = mid - 1;
+    }
+    const int nd = ndense[O.prob[lo]];
+    if (nd == 0) continue;
+    const int64_t r = g - S.row_begin[lo];
+    const uint4* src = reinterpret_cast<const uint4*>(S.rows[lo] + r * (int64_t)stride16 + c * 16);
+    const uint4 v0 = src[0], v1 = src[1];
+    const uint32_t vs[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+    uint4* dst = reinterpret_cast<uint4*>(O.out[lo] + r * (int64_t)TC_KCAP) + c;
+    for (int l = 0; l < nd; ++l) {
+      const uint32_t bias = (0x8000u - (uint32_t)(l + 1)) * 0x00010001u;
+      uint32_t o[4];
+#pragma unroll
+      for (int wd = 0; wd < 4; ++wd) {
+        const uint32_t m0 = ((vs[2 * wd] + bias) >> 15) & 0x00010001u;   // bytes 0, 2
+        const uint32_t m1 = ((vs[2 * wd + 1] + bias) >> 15) & 0x00010001u;
+        o[wd] = __byte_perm(m0, m1, 0x6420);
+      }
+      dst[l * dwc] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
 
+constexpr int TC_BUILD_THREADS = 512;
+
+// Listed (sparse) columns and the zero padding up to the 128-column K block:
+// the CTA's rows are taken in batches that give every thread one (row, chunk)
+// item: 16 entries from the column list (L1 / L2), 16 counts gathered from
+// the row, one 16-byte store.
 __global__ void __launch_bounds__(TC_BUILD_THREADS)
 tc_build_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut O, int stride16, int bins,
                 const uint32_t* __restrict__ collist, const int32_t* __restrict__ kblocks,
@@ -282,7 +326,7 @@ tc_build_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut
   const int64_t r0 = blockIdx.x * R / gridDim.x, r1 = (blockIdx.x + 1) * R / gridDim.x;
   const int tid = threadIdx.x;
   const int dwc = ((bins + 15) & ~15) / 16;   // chunks per dense layer
-  int side = -1, kch = 0, nd = 0, q = 0;
+  int side = -1, c0 = 0, ns = 0, q = 0;
   int64_t g = r0;
   while (g < r1) {
     int t = side < 0 ? 0 : side;
@@ -290,67 +334,34 @@ tc_build_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut
     if (t != side) {
       side = t;
       q = O.prob[t];
-      kch = kblocks[q] * 8;
-      nd = ndense[q];
+      c0 = ndense[q] * dwc;                 // first listed chunk
+      ns = kblocks[q] * 8 - c0;             // listed + padding chunks per row (may be 0)
     }
-    const int cnt = (int)min((int64_t)TC_BUILD_ROWS, min(r1, S.row_begin[t + 1]) - g);
-    const int64_t r = g - S.row_begin[t];
-    const uint16_t* rows = S.rows[t] + r * (int64_t)stride16;
-    uint8_t* outp = O.out[t] + r * (int64_t)TC_KCAP;
-    // dense layers
-    for (int c = tid; c < dwc && nd > 0; c += TC_BUILD_THREADS) {
-      uint4 v[TC_BUILD_ROWS][2];
-#pragma unroll
-      for (int h = 0; h < TC_BUILD_ROWS; ++h)
-#pragma unroll
-        for (int k = 0; k < 2; ++k)
-          v[h][k] = h < cnt ? reinterpret_cast<const uint4*>(rows + h * (int64_t)stride16 + c * 16)[k]
-                            : make_uint4(0, 0, 0, 0);
-      for (int l = 0; l < nd; ++l) {
-        const uint32_t L2 = (uint32_t)(l + 1) * 0x00010001u;
-#pragma unroll
-        for (int h = 0; h < TC_BUILD_ROWS; ++h) {
-          if (h >= cnt) break;
-          const uint32_t vs[8] = {v[h][0].x, v[h][0].y, v[h][0].z, v[h][0].w,
-                                  v[h][1].x, v[h][1].y, v[h][1].z, v[h][1].w};
-          uint32_t o[4];
-#pragma unroll
-          for (int wd = 0; wd < 4; ++wd) {
-            const uint32_t c0 = __vsetgeu2(vs[2 * wd], L2), c1 = __vsetgeu2(vs[2 * wd + 1], L2);
-            o[wd] = (c0 & 1u) | ((c0 >> 16) << 8) | ((c1 & 1u) << 16) | ((c1 >> 16) << 24);
-          }
-          reinterpret_cast<uint4*>(outp + h * (int64_t)TC_KCAP)[l * dwc + c] = make_uint4(o[0], o[1], o[2], o[3]);
-        }
-      }
+    if (ns <= 0) {   // every column of this side is in a dense layer
+      g = min(r1, S.row_begin[t + 1]);
+      continue;
     }
-    // listed columns (and the zero padding up to the 128-column K block)
+    const int rows_per = max(1, TC_BUILD_THREADS / ns);
+    const int cnt = (int)min((int64_t)rows_per, min(r1, S.row_begin[t + 1]) - g);
+    const int64_t rbase = g - S.row_begin[t];
     const uint32_t* cl = collist + (int64_t)q * TC_KCAP;
-    for (int c = nd * dwc + tid; c < kch; c += TC_BUILD_THREADS) {
-      uint32_t e[16];
+    for (int item = tid; item < cnt * ns; item += TC_BUILD_THREADS) {
+      const int h = item / ns, c = c0 + item % ns;
+      const uint16_t* row = S.rows[t] + (rbase + h) * (int64_t)stride16;
+      uint32_t o[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const uint4 x = reinterpret_cast<const uint4*>(cl + c * 16)[k];
-        e[4 * k] = x.x;
-        e[4 * k + 1] = x.y;
-        e[4 * k + 2] = x.z;
-        e[4 * k + 3] = x.w;
-      }
-      for (int h = 0; h < cnt; ++h) {
-        const uint16_t* row = rows + h * (int64_t)stride16;
-        uint32_t o[4];
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(cl + c * 16) + k);
+        const uint32_t es[4] = {x.x, x.y, x.z, x.w};
+        uint32_t word = 0;
 #pragma unroll
-        for (int wd = 0; wd < 4; ++wd) {
-          uint32_t word = 0;
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const uint32_t en = e[4 * wd + b];
-            const uint32_t layer = en >> 16;
-            word |= ((layer != 0u && (uint32_t)__ldg(row + (en & 0xffffu)) >= layer) ? 1u : 0u) << (8 * b);
-          }
-          o[wd] = word;
+        for (int b = 0; b < 4; ++b) {
+          const uint32_t layer = es[b] >> 16;
+          word |= ((layer != 0u && (uint32_t)__ldg(row + (es[b] & 0xffffu)) >= layer) ? 1u : 0u) << (8 * b);
         }
-        reinterpret_cast<uint4*>(outp + h * (int64_t)TC_KCAP)[c] = make_uint4(o[0], o[1], o[2], o[3]);
+        o[k] = word;
       }
+      reinterpret_cast<uint4*>(O.out[t] + (rbase + h) * (int64_t)TC_KCAP)[c] = make_uint4(o[0], o[1], o[2], o[3]);
     }
     g += cnt;
   }
@@ -648,7 +659,9 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       if (!o) return fail(SA_E_NOMEM, "scratch allocation of K2T operand rows failed");
       side_out[sd] = outs.out[sd] = o;
     }
-    const int bx = (int)std::max<int64_t>(1, std::min<int64_t>((R + TC_BUILD_ROWS - 1) / TC_BUILD_ROWS, 4 * g_num_sms));
+    const int bx = (int)std::max<int64_t>(1, std::min<int64_t>(R, 4 * g_num_sms));
+    tc_dense_kernel<<<8 * g_num_sms, 256, 0, st>>>(sides, outs, stride16, bins, ndense, state);
+    SA_LAUNCHED();
     tc_build_kernel<<<bx, TC_BUILD_THREADS, 0, st>>>(sides, outs, stride16, bins, collist, kblocks, ndense, state);
     SA_LAUNCHED();
     // GEMM
