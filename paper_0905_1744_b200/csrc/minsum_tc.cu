@@ -419,20 +419,24 @@ struct KeyMatEpi {
     }
   }
 
-  __device__ void chunk(State& s, const tc::Tile& T, int row, int col, const uint32_t (&v)[32], int lane,
+  // CW columns [col, col + CW) of this thread's row; lanes = 32 consecutive rows.
+  template <int CW>
+  __device__ void chunk(State& s, const tc::Tile& T, int row, int col, const uint32_t (&v)[CW], int lane,
                         uint32_t* xpose) const {
+    static_assert(CW == 16 || CW == 32, "chunk width");
     const TcEpiProb& E = e[T.pi];
     const bool sym = E.sym != 0;
-    const int c0 = T.col0 + col;                        // global column of j = 0
-    const int nk_cl = (col + lane < T.rb) ? E.nkB[c0 + lane] : -1;   // column c0 + lane
-    uint32_t C[32];
+    const int c0 = T.col0 + col;                          // global column of j = 0
+    const int cl = lane % CW;                             // the column a lane describes
+    const int nk_cl = (col + cl < T.rb) ? E.nkB[c0 + cl] : -1;
+    uint32_t C[CW];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) C[j] = (sym && c0 + j == s.row_g) ? (uint32_t)s.nk_r : v[j];
+    for (int j = 0; j < CW; ++j) C[j] = (sym && c0 + j == s.row_g) ? (uint32_t)s.nk_r : v[j];
 
     if ((MODE & EPI_KEYS) && E.keyA) {
       const bool colsum = sym && E.keyB;
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
+      for (int g = 0; g < CW / 8; ++g) {
         uint64_t tlo[8];
         uint32_t thi[8];
 #pragma unroll
@@ -492,7 +496,7 @@ struct KeyMatEpi {
       // mirrored half (symmetric): lanes = consecutive rows -> coalesced columns
       if (sym) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < CW; ++j) {
           const int nk_c = __shfl_sync(0xffffffffu, nk_cl, j);
           const double d_c = __shfl_sync(0xffffffffu, d_cl, j), y_c = __shfl_sync(0xffffffffu, y_cl, j);
           const int gc = c0 + j;
@@ -505,19 +509,22 @@ struct KeyMatEpi {
           }
         }
       }
-      // direct half through a 32 x 32 transpose: lanes = consecutive columns
+      // direct half through a 32 x CW transpose: lanes = consecutive columns
+      // (32 / CW rows per pass)
 #pragma unroll
-      for (int j = 0; j < 32; ++j) xpose[lane * 33 + j] = C[j];
+      for (int j = 0; j < CW; ++j) xpose[tc::xpose_at<CW>(lane, j)] = C[j];
       __syncwarp();
       const int rbase = s.row_g - lane;
-      const int gc = c0 + lane;
+      const int gc = c0 + cl;
+      constexpr int RPP = 32 / CW;                        // rows per pass
 #pragma unroll 4
-      for (int i = 0; i < 32; ++i) {
+      for (int p = 0; p < 32 / RPP; ++p) {
+        const int i = p * RPP + lane / CW;
         const int nk_ri = __shfl_sync(0xffffffffu, s.nk_r, i);
         const double d_ri = __shfl_sync(0xffffffffu, s.d_r, i), y_ri = __shfl_sync(0xffffffffu, s.y_r, i);
         const int rg = rbase + i;
         if (nk_ri < 0 || nk_cl < 0 || (sym && gc < rg)) continue;
-        const uint32_t Cv = xpose[i * 33 + lane];
+        const uint32_t Cv = xpose[tc::xpose_at<CW>(i, cl)];
         const int64_t o = (int64_t)rg * E.ld + gc;
         if (E.num) E.num[o] = (uint16_t)Cv;
         if (want_sim) {
@@ -585,6 +592,21 @@ __global__ void f_division_check_kernel(unsigned long long* bad) {
 }
 
 // ------------------------------------------------------------- host ----
+template <class Epi, int EW, int CW>
+static sa_status tc_configure() {
+  SA_CUDA(cudaFuncSetAttribute(tc::gemm_kernel<Epi, EW, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               tc::smem_of(EW, CW)));
+  return SA_OK;
+}
+template <class Epi, int EW, int CW>
+static void tc_gemm(int64_t grid, const tc::Batch& batch, const tc::Maps& maps, int64_t tiles,
+                    const KeyMatEpi<EPI_ALL>& epi, cudaStream_t st) {
+  Epi k;
+  static_assert(sizeof k == sizeof epi, "epilogue layouts");
+  std::memcpy(&k, &epi, sizeof k);
+  tc::gemm_kernel<Epi, EW, CW><<<(unsigned)grid, tc::threads_of(EW), tc::smem_of(EW, CW), st>>>(batch, maps, tiles, k);
+}
+
 static sa_status tc_encode_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int box_rows);
 
 sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t bins, uint32_t* state,
@@ -600,12 +622,12 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
   if (!configured) {
     SA_CUDA(cudaFuncSetAttribute(tc_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  2 * (TC_LCAP - TC_HREG) * TC_WPL * 4));
-    SA_CUDA(cudaFuncSetAttribute(tc::gemm_kernel<KeyMatEpi<EPI_KEYS>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 tc::SMEM));
-    SA_CUDA(cudaFuncSetAttribute(tc::gemm_kernel<KeyMatEpi<EPI_NUM>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 tc::SMEM));
-    SA_CUDA(cudaFuncSetAttribute(tc::gemm_kernel<KeyMatEpi<EPI_ALL>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 tc::SMEM));
+    sa_status cs = tc_configure<KeyMatEpi<EPI_KEYS>, 8, 32>();
+    if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM>, 16, 16>();
+    if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16>();
+    if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_ALL>, 8, 32>();
+    if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_KEYS>, 16, 16>();
+    if (cs != SA_OK) return cs;
     configured = true;
   }
   const int stride16 = 2 * ldw16;
@@ -709,17 +731,18 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     }
     batch.n = np;
     const int64_t grid = tiles < g_num_sms ? tiles : g_num_sms;
-    if (mode == EPI_KEYS) {
-      KeyMatEpi<EPI_KEYS> k;
-      std::memcpy(&k, &epi, sizeof k);
-      tc::gemm_kernel<KeyMatEpi<EPI_KEYS>><<<(unsigned)grid, tc::THREADS, tc::SMEM, st>>>(batch, maps, tiles, k);
-    } else if ((mode & ~EPI_NUM) == 0) {
-      KeyMatEpi<EPI_NUM> k;
-      std::memcpy(&k, &epi, sizeof k);
-      tc::gemm_kernel<KeyMatEpi<EPI_NUM>><<<(unsigned)grid, tc::THREADS, tc::SMEM, st>>>(batch, maps, tiles, k);
-    } else {
-      tc::gemm_kernel<KeyMatEpi<EPI_ALL>><<<(unsigned)grid, tc::THREADS, tc::SMEM, st>>>(batch, maps, tiles, epi);
-    }
+    // 16 epilogue warps x 16-column chunks (more warps to hide the store / F /
+    // key-term latency, fewer registers each); keys and matrices together
+    // (a rank call that also wants numerators) use 8 warps x 32 columns
+    static const bool keys16 = [] {   // SA_K2T_KEYS16=0: the 8-warp x 32-column key epilogue
+      const char* e = getenv("SA_K2T_KEYS16");
+      return !(e && atoi(e) == 0);
+    }();
+    if (mode == EPI_KEYS && keys16) tc_gemm<KeyMatEpi<EPI_KEYS>, 16, 16>(grid, batch, maps, tiles, epi, st);
+    else if (mode == EPI_KEYS) tc_gemm<KeyMatEpi<EPI_KEYS>, 8, 32>(grid, batch, maps, tiles, epi, st);
+    else if (mode == EPI_NUM) tc_gemm<KeyMatEpi<EPI_NUM>, 16, 16>(grid, batch, maps, tiles, epi, st);
+    else if ((mode & EPI_KEYS) == 0) tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16>(grid, batch, maps, tiles, epi, st);
+    else tc_gemm<KeyMatEpi<EPI_ALL>, 8, 32>(grid, batch, maps, tiles, epi, st);
     SA_LAUNCHED();
     for (int q = 0; q < np; ++q) {
       const MsProblem& P = probs[i0 + q];

@@ -37,11 +37,24 @@ constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK;
 constexpr int B_BYTES = BN * BK;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int EPI_WARPS = 8;
-constexpr int THREADS = (EPI_WARPS + 2) * 32;
 constexpr int TMEM_COLS = 2 * BN;
-constexpr int XPOSE_WORDS = 32 * 33;   // per epilogue warp: a padded 32 x 32 transpose buffer
-constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + EPI_WARPS * XPOSE_WORDS * 4;
+// Epilogue geometry (template parameters of gemm_kernel): EW epilogue warps
+// (a multiple of 4: warp w reads TMEM lanes 32 (w % 4) .. and the w / 4-th
+// column slice), CW columns per tcgen05.ld chunk (16 or 32), a padded
+// 32 x CW transpose buffer per epilogue warp.
+__host__ __device__ constexpr int threads_of(int EW) { return (EW + 2) * 32; }
+// 32 x 32 chunks: rows padded to 33 words; 32 x 16 chunks: unpadded rows,
+// columns XOR-swizzled by the row (xpose_at) -- keeps the 16-warp layout
+// inside the 227 KB shared-memory limit.
+__host__ __device__ constexpr int xpose_words(int CW) { return CW == 32 ? 32 * 33 : 32 * CW; }
+template <int CW>
+__device__ __forceinline__ int xpose_at(int row, int col) {
+  if constexpr (CW == 32) return row * 33 + col;
+  else return row * CW + (col ^ (row & (CW - 1)));
+}
+__host__ __device__ constexpr int smem_of(int EW, int CW) {
+  return STAGES * STAGE_BYTES + 1024 + 256 + EW * xpose_words(CW) * 4;
+}
 constexpr int MAXPROB = 16;
 
 // ----------------------------------------------------------------- PTX ----
@@ -97,6 +110,14 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s_addr(bar))
                : "memory");
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -107,6 +128,12 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int CW>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t (&v)[CW]) {
+  if constexpr (CW == 16) tmem_ld16(taddr, v);
+  else tmem_ld32(taddr, v);
 }
 
 // Shared-memory matrix descriptor of a K-major operand tile in the canonical
@@ -218,14 +245,16 @@ __device__ __forceinline__ Tile decode(const Batch& b, int64_t tile) {
 // Epi (const, a kernel parameter) must provide a per-thread `State` and
 //   __device__ bool skip() const;                                  // device-side dispatch guard
 //   __device__ void begin(State&, const Tile&, int row) const;     // per thread, per tile
-//   __device__ void chunk(State&, const Tile&, int row, int col, const uint32_t (&v)[32], int lane,
-//                         uint32_t* xpose) const;                  // all 32 lanes, converged
+//   template <int CW> __device__ void chunk(State&, const Tile&, int row, int col, const uint32_t (&v)[CW],
+//                         int lane, uint32_t* xpose) const;        // all 32 lanes, converged
 //   __device__ void end(State&, const Tile&, int row) const;
 // row = tile row of this thread (0..127), col = first tile column of the chunk,
-// xpose = this warp's 32 x 33 word shared-memory scratch.
-template <class Epi>
-__global__ void __launch_bounds__(THREADS, 1)
+// xpose = this warp's 32 x (CW + 1) word shared-memory scratch.
+template <class Epi, int EW, int CW>
+__global__ void __launch_bounds__(threads_of(EW), 1)
 gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps maps, int64_t total_tiles, Epi epi) {
+  static_assert(EW % 4 == 0 && (BN / (EW / 4)) % CW == 0, "epilogue geometry");
+  constexpr int EPI_WARPS = EW;
   if (epi.skip()) return;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const uint32_t raw_s = s_addr(smem_raw);
@@ -305,9 +334,10 @@ gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps ma
     }
   } else {
     // ------------------------------------------------ epilogue warps
-    const int quad = warp & 3, half = warp >> 2;
+    const int quad = warp & 3, part = warp >> 2;
     const int row = quad * 32 + lane;
-    uint32_t* xpose = xpose_all + warp * XPOSE_WORDS;
+    uint32_t* xpose = xpose_all + warp * xpose_words(CW);
+    constexpr int SLICE = BN / (EW / 4);   // columns per epilogue warp
     typename Epi::State es;
     int64_t lt = 0;
     for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
@@ -317,11 +347,11 @@ gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps ma
       fence_after();
       epi.begin(es, T, row);
 #pragma unroll 1
-      for (int ch = 0; ch < BN / 2 / 32; ++ch) {
-        const int col = half * (BN / 2) + ch * 32;
-        uint32_t v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + col), v);
-        epi.chunk(es, T, row, col, v, lane, xpose);
+      for (int ch = 0; ch < SLICE / CW; ++ch) {
+        const int col = part * SLICE + ch * CW;
+        uint32_t v[CW];
+        tmem_ld<CW>(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + col), v);
+        epi.template chunk<CW>(es, T, row, col, v, lane, xpose);
       }
       fence_before();
       __syncwarp();

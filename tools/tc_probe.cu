@@ -24,12 +24,13 @@ struct WriteEpi {
   struct State {};
   __device__ bool skip() const { return false; }
   __device__ void begin(State&, const Tile&, int) const {}
-  __device__ void chunk(State&, const Tile& T, int row, int col, const uint32_t (&v)[32], int, uint32_t*) const {
+  template <int CW>
+  __device__ void chunk(State&, const Tile& T, int row, int col, const uint32_t (&v)[CW], int, uint32_t*) const {
     if (row >= T.ra) return;
     const int pi = T.pi;
     int32_t* out = C + (int64_t)pi * 0 + (int64_t)(T.row0 + row) * ldc + T.col0 + col;
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
+    for (int j = 0; j < CW; ++j)
       if (col + j < T.rb) out[j] = (int32_t)v[j];
   }
   __device__ void end(State&, const Tile&, int) const {}
@@ -91,10 +92,10 @@ int main(int argc, char** argv) {
   const int64_t tiles = problem_tiles(M, Nb, sym);
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-  CK(cudaFuncSetAttribute(gemm_kernel<WriteEpi>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  CK(cudaFuncSetAttribute(gemm_kernel<WriteEpi, 8, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_of(8, 32)));
   WriteEpi epi{dC, Nb};
   const int grid = (int)(tiles < sms ? tiles : sms);
-  gemm_kernel<WriteEpi><<<grid, THREADS, SMEM>>>(batch, maps, tiles, epi);
+  gemm_kernel<WriteEpi, 8, 32><<<grid, threads_of(8), smem_of(8, 32)>>>(batch, maps, tiles, epi);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   std::vector<int32_t> C((size_t)M * Nb);
@@ -120,7 +121,7 @@ int main(int argc, char** argv) {
   CK(cudaEventCreate(&e1));
   const int reps = 5;
   CK(cudaEventRecord(e0));
-  for (int r = 0; r < reps; ++r) gemm_kernel<WriteEpi><<<grid, THREADS, SMEM>>>(batch, maps, tiles, epi);
+  for (int r = 0; r < reps; ++r) gemm_kernel<WriteEpi, 8, 32><<<grid, threads_of(8), smem_of(8, 32)>>>(batch, maps, tiles, epi);
   CK(cudaEventRecord(e1));
   CK(cudaEventSynchronize(e1));
   float ms = 0;
