@@ -381,6 +381,12 @@ struct TcEpiProb {
   int32_t sym;
 };
 
+// Output matrices are written once and never re-read by the kernel: streaming
+// stores (st.global.cs) keep them from evicting the operand rows the tiles
+// re-read from L2.
+__device__ __forceinline__ void st_out(uint16_t* p, uint16_t v) { __stcs(reinterpret_cast<unsigned short*>(p), v); }
+__device__ __forceinline__ void st_out(double* p, double v) { __stcs(p, v); }
+
 // 96-bit (lo, hi) add
 __device__ __forceinline__ void add96(uint64_t& lo, uint32_t& hi, uint64_t blo, uint32_t bhi) {
   lo += blo;
@@ -502,10 +508,10 @@ struct KeyMatEpi {
           const int gc = c0 + j;
           if (s.nk_r < 0 || nk_c < 0 || gc <= s.row_g) continue;
           const int64_t o = (int64_t)gc * E.ld + s.row_g;
-          if (E.num) E.num[o] = (uint16_t)C[j];
+          if (E.num) st_out(E.num + o, (uint16_t)C[j]);
           if (want_sim) {
             const bool rmin = s.nk_r <= nk_c;
-            E.sim[o] = f_ratio_y(C[j], rmin ? s.d_r : d_c, rmin ? s.y_r : y_c);
+            st_out(E.sim + o, f_ratio_y(C[j], rmin ? s.d_r : d_c, rmin ? s.y_r : y_c));
           }
         }
       }
@@ -526,10 +532,10 @@ struct KeyMatEpi {
         if (nk_ri < 0 || nk_cl < 0 || (sym && gc < rg)) continue;
         const uint32_t Cv = xpose[tc::xpose_at<CW>(i, cl)];
         const int64_t o = (int64_t)rg * E.ld + gc;
-        if (E.num) E.num[o] = (uint16_t)Cv;
+        if (E.num) st_out(E.num + o, (uint16_t)Cv);
         if (want_sim) {
           const bool rmin = nk_ri <= nk_cl;
-          E.sim[o] = f_ratio_y(Cv, rmin ? d_ri : d_cl, rmin ? y_ri : y_cl);
+          st_out(E.sim + o, f_ratio_y(Cv, rmin ? d_ri : d_cl, rmin ? y_ri : y_cl));
         }
       }
       __syncwarp();
@@ -730,6 +736,12 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       mode |= (P.keyA ? EPI_KEYS : 0) | (E.num ? EPI_NUM : 0) | (E.sim ? EPI_SIM : 0);
     }
     batch.n = np;
+    static const int group = [] {   // SA_K2T_GROUP: row blocks per group of the tile order
+      const char* e = getenv("SA_K2T_GROUP");
+      const int g = e ? atoi(e) : 16;
+      return g >= 1 && g <= 64 ? g : 16;
+    }();
+    batch.group = group;
     const int64_t grid = tiles < g_num_sms ? tiles : g_num_sms;
     // 16 epilogue warps x 16-column chunks (more warps to hide the store / F /
     // key-term latency, fewer registers each); keys and matrices together

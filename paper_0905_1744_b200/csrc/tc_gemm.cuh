@@ -170,6 +170,7 @@ struct Problem {
 struct Batch {
   Problem p[MAXPROB];
   int n;
+  int group;   // GROUP: row blocks per group of the tile order (below)
 };
 struct alignas(64) Maps {
   CUtensorMap m[2 * MAXPROB];
@@ -188,13 +189,12 @@ __host__ __device__ inline int64_t problem_tiles(int64_t na, int64_t nb, bool sy
   return t;
 }
 
-// Tile order inside a problem: groups of GROUP row blocks; in a group, column
+// Tile order inside a problem: groups of GROUP (Batch::group) row blocks; in a group, column
 // block by column block, the group's rows inside (column-major).  The ~148
 // tiles in flight then share ~148 / GROUP column blocks of B and GROUP row
-// blocks of A (config 4 bucket: ~76 MB + 16 MB, inside the 126 MB L2) instead
-// of sweeping all of B every wave.  Symmetric problems keep the tiles with
+// blocks of A (config 4 bucket, GROUP = 16: ~38 MB + 34 MB, inside the 126 MB
+// L2) instead of sweeping all of B every wave.  Symmetric problems keep the tiles with
 // column block J >= I / 2.
-constexpr int GROUP = 8;
 
 // tiles of rows [0, i1) of a symmetric problem: sum_{i < i1} (tn - floor(i / 2))
 __device__ __forceinline__ int64_t sym_tiles_before(int i1, int tn) {
@@ -208,6 +208,7 @@ __device__ __forceinline__ Tile decode(const Batch& b, int64_t tile) {
   const Problem& P = b.p[pi];
   int64_t t = tile - P.tile_begin;
   const int tm = (P.na + BM - 1) / BM, tn = P.tiles_n;
+  const int GROUP = b.group;
   int ti, tj;
   if (!P.sym) {
     const int64_t full = (int64_t)GROUP * tn;     // tiles of a full group

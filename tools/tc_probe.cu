@@ -77,6 +77,7 @@ int main(int argc, char** argv) {
   CK(cudaMemcpy(dkb, &kb, 4, cudaMemcpyHostToDevice));
   Batch batch{};
   batch.n = 1;
+  batch.group = 8;
   Problem& P = batch.p[0];
   P.na = M;
   P.nb = Nb;
