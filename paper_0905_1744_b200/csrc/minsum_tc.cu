@@ -181,7 +181,7 @@ struct TcSel {
 // epilogue overrides) -- and the build kernel encodes them with vector loads.
 // The remaining layers list their kept (layer, bin) columns.
 __global__ void __launch_bounds__(1024)
-tc_select_kernel(const __grid_constant__ TcSel sel, const uint32_t* __restrict__ planes, int bins,
+tc_select_kernel(const __grid_constant__ TcSel sel, const uint32_t* __restrict__ planes, int bins, int kbc,
                  uint32_t* __restrict__ collist, int32_t* __restrict__ kblocks, int32_t* __restrict__ ndense,
                  uint32_t* __restrict__ state, uint32_t* __restrict__ cols_out) {
   __shared__ uint32_t warp_cnt[32];
@@ -224,7 +224,7 @@ tc_select_kernel(const __grid_constant__ TcSel sel, const uint32_t* __restrict__
   __syncthreads();
   const uint32_t total = s_total, nd = s_nd;
   if (tid == 0 && cols_out && sel.first + q < SA_TC_COLS_MAX) cols_out[sel.first + q] = total;
-  const uint32_t kpad = max(128u, (total + 127u) & ~127u);
+  const uint32_t kpad = max((uint32_t)kbc, (total + kbc - 1u) / kbc * kbc);   // kbc columns per K block
   const bool too_many = kpad > (uint32_t)TC_KCAP;
   const bool deep = reinterpret_cast<const volatile uint32_t*>(state)[0] > (uint32_t)TC_LCAP;
   if (too_many || deep) {
@@ -254,7 +254,7 @@ tc_select_kernel(const __grid_constant__ TcSel sel, const uint32_t* __restrict__
   }
   for (uint32_t p = total + tid; p < kpad; p += blockDim.x) out[p] = 0u;   // layer 0: padding column
   if (tid == 0) {
-    kblocks[q] = (int32_t)(kpad / 128u);
+    kblocks[q] = (int32_t)(kpad / (uint32_t)kbc);
     ndense[q] = (int32_t)nd;
   }
 }
@@ -274,9 +274,13 @@ struct TcOut {
 // layers of that chunk from one 32-byte load.  Counts are <= TC_LCAP here (the
 // launch is feasible), so for each u16 half h: h >= L <=> bit 15 of
 // h + 0x8000 - L (no carry between the halves).
+// FP4: two columns per byte, 1.0 = e2m1 0b0010 in the low (even column) or
+// high (odd column) nibble; rows of TC_KCAP / 2 bytes.
+template <bool FP4>
 __global__ void __launch_bounds__(256)
 tc_dense_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut O, int stride16, int bins,
                 const int32_t* __restrict__ ndense, const uint32_t* __restrict__ state) {
+  constexpr int64_t ROWB = FP4 ? TC_KCAP / 2 : TC_KCAP;
   if (tc_infeasible(state)) return;
   const int dwc = ((bins + 15) & ~15) / 16;
   const int64_t items = S.row_begin[S.n] * dwc;
@@ -296,17 +300,25 @@ tc_dense_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut
     const uint4* src = reinterpret_cast<const uint4*>(S.rows[lo] + r * (int64_t)stride16 + c * 16);
     const uint4 v0 = src[0], v1 = src[1];
     const uint32_t vs[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-    uint4* dst = reinterpret_cast<uint4*>(O.out[lo] + r * (int64_t)TC_KCAP) + c;
+    uint8_t* rowp = O.out[lo] + r * ROWB;
     for (int l = 0; l < nd; ++l) {
       const uint32_t bias = (0x8000u - (uint32_t)(l + 1)) * 0x00010001u;
       uint32_t o[4];
 #pragma unroll
       for (int wd = 0; wd < 4; ++wd) {
-        const uint32_t m0 = ((vs[2 * wd] + bias) >> 15) & 0x00010001u;   // bytes 0, 2
+        const uint32_t m0 = ((vs[2 * wd] + bias) >> 15) & 0x00010001u;   // bits 0, 16
         const uint32_t m1 = ((vs[2 * wd + 1] + bias) >> 15) & 0x00010001u;
-        o[wd] = __byte_perm(m0, m1, 0x6420);
+        if constexpr (FP4) {
+          const uint32_t x = (m0 | (m0 >> 12)) & 0x11u, y = (m1 | (m1 >> 12)) & 0x11u;   // bits 0, 4
+          o[wd] = (x | (y << 8)) << 1;                                                     // 16 bits: 4 nibbles
+        } else {
+          o[wd] = __byte_perm(m0, m1, 0x6420);
+        }
       }
-      dst[l * dwc] = make_uint4(o[0], o[1], o[2], o[3]);
+      if constexpr (FP4)
+        reinterpret_cast<uint2*>(rowp)[l * dwc + c] = make_uint2(o[0] | (o[1] << 16), o[2] | (o[3] << 16));
+      else
+        reinterpret_cast<uint4*>(rowp)[l * dwc + c] = make_uint4(o[0], o[1], o[2], o[3]);
     }
   }
 }
@@ -317,10 +329,13 @@ constexpr int TC_BUILD_THREADS = 512;
 // the CTA's rows are taken in batches that give every thread one (row, chunk)
 // item: 16 entries from the column list (L1 / L2), 16 counts gathered from
 // the row, one 16-byte store.
+template <bool FP4>
 __global__ void __launch_bounds__(TC_BUILD_THREADS)
 tc_build_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut O, int stride16, int bins,
                 const uint32_t* __restrict__ collist, const int32_t* __restrict__ kblocks,
                 const int32_t* __restrict__ ndense, const uint32_t* __restrict__ state) {
+  constexpr int64_t ROWB = FP4 ? TC_KCAP / 2 : TC_KCAP;
+  constexpr int KBC = FP4 ? 256 : 128;   // columns per K block
   if (tc_infeasible(state)) return;
   const int64_t R = S.row_begin[S.n];
   const int64_t r0 = blockIdx.x * R / gridDim.x, r1 = (blockIdx.x + 1) * R / gridDim.x;
@@ -335,7 +350,7 @@ tc_build_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut
       side = t;
       q = O.prob[t];
       c0 = ndense[q] * dwc;                 // first listed chunk
-      ns = kblocks[q] * 8 - c0;             // listed + padding chunks per row (may be 0)
+      ns = kblocks[q] * (KBC / 16) - c0;    // listed + padding chunks per row (may be 0)
     }
     if (ns <= 0) {   // every column of this side is in a dense layer
       g = min(r1, S.row_begin[t + 1]);
@@ -357,11 +372,16 @@ tc_build_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           const uint32_t layer = es[b] >> 16;
-          word |= ((layer != 0u && (uint32_t)__ldg(row + (es[b] & 0xffffu)) >= layer) ? 1u : 0u) << (8 * b);
+          const uint32_t bit = (layer != 0u && (uint32_t)__ldg(row + (es[b] & 0xffffu)) >= layer) ? 1u : 0u;
+          word |= FP4 ? (bit << (4 * b + 1)) : (bit << (8 * b));
         }
         o[k] = word;
       }
-      reinterpret_cast<uint4*>(O.out[t] + (rbase + h) * (int64_t)TC_KCAP)[c] = make_uint4(o[0], o[1], o[2], o[3]);
+      uint8_t* rowp = O.out[t] + (rbase + h) * ROWB;
+      if constexpr (FP4)
+        reinterpret_cast<uint2*>(rowp)[c] = make_uint2(o[0] | (o[1] << 16), o[2] | (o[3] << 16));
+      else
+        reinterpret_cast<uint4*>(rowp)[c] = make_uint4(o[0], o[1], o[2], o[3]);
     }
     g += cnt;
   }
@@ -598,22 +618,46 @@ __global__ void f_division_check_kernel(unsigned long long* bad) {
 }
 
 // ------------------------------------------------------------- host ----
-template <class Epi, int EW, int CW>
+template <class Epi, int EW, int CW, bool FP4>
 static sa_status tc_configure() {
-  SA_CUDA(cudaFuncSetAttribute(tc::gemm_kernel<Epi, EW, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               tc::smem_of(EW, CW)));
+  SA_CUDA(cudaFuncSetAttribute(tc::gemm_kernel<Epi, EW, CW, FP4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               tc::smem_of(EW, CW, FP4)));
   return SA_OK;
 }
-template <class Epi, int EW, int CW>
+template <class Epi, int EW, int CW, bool FP4>
 static void tc_gemm(int64_t grid, const tc::Batch& batch, const tc::Maps& maps, int64_t tiles,
                     const KeyMatEpi<EPI_ALL>& epi, cudaStream_t st) {
   Epi k;
   static_assert(sizeof k == sizeof epi, "epilogue layouts");
   std::memcpy(&k, &epi, sizeof k);
-  tc::gemm_kernel<Epi, EW, CW><<<(unsigned)grid, tc::threads_of(EW), tc::smem_of(EW, CW), st>>>(batch, maps, tiles, k);
+  tc::gemm_kernel<Epi, EW, CW, FP4>
+      <<<(unsigned)grid, tc::threads_of(EW), tc::smem_of(EW, CW, FP4), st>>>(batch, maps, tiles, k);
 }
-
-static sa_status tc_encode_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int box_rows);
+// the (epilogue mode, geometry) instantiations a launch can pick
+template <bool FP4>
+static sa_status tc_configure_all() {
+  constexpr int CW_ALL = FP4 ? 16 : 32;
+  sa_status cs = tc_configure<KeyMatEpi<EPI_KEYS>, 16, 16, FP4>();
+  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_KEYS>, 8, CW_ALL, FP4>();
+  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM>, 16, 16, FP4>();
+  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4>();
+  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_ALL>, 8, CW_ALL, FP4>();
+  return cs;
+}
+template <bool FP4>
+static void tc_gemm_mode(int mode, bool keys16, int64_t grid, const tc::Batch& batch, const tc::Maps& maps,
+                         int64_t tiles, const KeyMatEpi<EPI_ALL>& epi, cudaStream_t st) {
+  constexpr int CW_ALL = FP4 ? 16 : 32;
+  // 16 epilogue warps x 16-column chunks (more warps to hide the store / F /
+  // key-term latency, fewer registers each); keys and matrices together
+  // (a rank call that also wants numerators) use 8 warps
+  if (mode == EPI_KEYS && keys16) tc_gemm<KeyMatEpi<EPI_KEYS>, 16, 16, FP4>(grid, batch, maps, tiles, epi, st);
+  else if (mode == EPI_KEYS) tc_gemm<KeyMatEpi<EPI_KEYS>, 8, CW_ALL, FP4>(grid, batch, maps, tiles, epi, st);
+  else if (mode == EPI_NUM) tc_gemm<KeyMatEpi<EPI_NUM>, 16, 16, FP4>(grid, batch, maps, tiles, epi, st);
+  else if ((mode & EPI_KEYS) == 0)
+    tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4>(grid, batch, maps, tiles, epi, st);
+  else tc_gemm<KeyMatEpi<EPI_ALL>, 8, CW_ALL, FP4>(grid, batch, maps, tiles, epi, st);
+}
 
 sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t bins, uint32_t* state,
                     uint32_t* cols_out, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1) {
@@ -628,15 +672,18 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
   if (!configured) {
     SA_CUDA(cudaFuncSetAttribute(tc_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  2 * (TC_LCAP - TC_HREG) * TC_WPL * 4));
-    sa_status cs = tc_configure<KeyMatEpi<EPI_KEYS>, 8, 32>();
-    if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM>, 16, 16>();
-    if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16>();
-    if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_ALL>, 8, 32>();
-    if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_KEYS>, 16, 16>();
+    sa_status cs = tc_configure_all<false>();
+    if (cs == SA_OK) cs = tc_configure_all<true>();
     if (cs != SA_OK) return cs;
     configured = true;
   }
   const int stride16 = 2 * ldw16;
+  static const bool fp4 = [] {   // SA_K2T_FP4=1: packed e2m1 operands, kind::mxf4 (2x MMA rate)
+    const char* e = getenv("SA_K2T_FP4");
+    return e && atoi(e) != 0;
+  }();
+  const int64_t rowb = fp4 ? TC_KCAP / 2 : TC_KCAP;
+  const int kbc = fp4 ? 256 : 128;
   static const bool fpass = [] {
     const char* e = getenv("SA_K2T_FPASS");
     return e && atoi(e) != 0;
@@ -678,19 +725,27 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     const int hx = (int)std::max<int64_t>(1, std::min<int64_t>((R + TC_HIST_ROWS - 1) / TC_HIST_ROWS, 4 * g_num_sms));
     tc_hist_kernel<<<hx, TC_HIST_THREADS, 2 * (TC_LCAP - TC_HREG) * TC_WPL * 4, st>>>(sides, stride16, planes, state);
     SA_LAUNCHED();
-    tc_select_kernel<<<np, 1024, 0, st>>>(sel, planes, bins, collist, kblocks, ndense, state, cols_out);
+    tc_select_kernel<<<np, 1024, 0, st>>>(sel, planes, bins, kbc, collist, kblocks, ndense, state, cols_out);
     SA_LAUNCHED();
     // operand rows: one output per side (its problem's column list)
     uint8_t* side_out[2 * tc::MAXPROB];
     for (int sd = 0; sd < sides.n; ++sd) {
-      uint8_t* o = scratch.alloc<uint8_t>((size_t)side_n[sd] * TC_KCAP);
+      uint8_t* o = scratch.alloc<uint8_t>((size_t)side_n[sd] * rowb);
       if (!o) return fail(SA_E_NOMEM, "scratch allocation of K2T operand rows failed");
       side_out[sd] = outs.out[sd] = o;
     }
     const int bx = (int)std::max<int64_t>(1, std::min<int64_t>(R, 4 * g_num_sms));
-    tc_dense_kernel<<<8 * g_num_sms, 256, 0, st>>>(sides, outs, stride16, bins, ndense, state);
-    SA_LAUNCHED();
-    tc_build_kernel<<<bx, TC_BUILD_THREADS, 0, st>>>(sides, outs, stride16, bins, collist, kblocks, ndense, state);
+    if (fp4) {
+      tc_dense_kernel<true><<<8 * g_num_sms, 256, 0, st>>>(sides, outs, stride16, bins, ndense, state);
+      SA_LAUNCHED();
+      tc_build_kernel<true><<<bx, TC_BUILD_THREADS, 0, st>>>(sides, outs, stride16, bins, collist, kblocks, ndense,
+                                                             state);
+    } else {
+      tc_dense_kernel<false><<<8 * g_num_sms, 256, 0, st>>>(sides, outs, stride16, bins, ndense, state);
+      SA_LAUNCHED();
+      tc_build_kernel<false><<<bx, TC_BUILD_THREADS, 0, st>>>(sides, outs, stride16, bins, collist, kblocks, ndense,
+                                                              state);
+    }
     SA_LAUNCHED();
     // GEMM
     tc::Batch batch{};
@@ -706,15 +761,17 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       T.na = P.na;
       T.nb = P.nb;
       T.sym = P.sym;
-      T.tiles_n = (P.nb + tc::BN - 1) / tc::BN;
+      const int BN = fp4 ? tc::Geo<true>::BN : tc::Geo<false>::BN;
+      T.tiles_n = (P.nb + BN - 1) / BN;
       T.tile_begin = tiles;
       T.kblocks = kblocks + q;
       T.map = q;
-      tiles += tc::problem_tiles(P.na, P.nb, P.sym != 0);
+      tiles += fp4 ? tc::problem_tiles<tc::Geo<true>::BN>(P.na, P.nb, P.sym != 0)
+                   : tc::problem_tiles<tc::Geo<false>::BN>(P.na, P.nb, P.sym != 0);
       const uint8_t* a = side_out[sel.side_a[q]];
       const uint8_t* b = P.sym ? a : side_out[sel.side_b[q]];
-      SA_TRY(tc_encode_map(&maps.m[2 * q], a, P.na, tc::BM));
-      SA_TRY(tc_encode_map(&maps.m[2 * q + 1], b, P.nb, tc::BN));
+      SA_TRY(tc_encode_map(&maps.m[2 * q], a, P.na, tc::BM, rowb));
+      SA_TRY(tc_encode_map(&maps.m[2 * q + 1], b, P.nb, BN, rowb));
       TcEpiProb& E = epi.e[q];
       E.nkA = P.nkA;
       E.nkB = P.nkB;
@@ -746,15 +803,12 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     // 16 epilogue warps x 16-column chunks (more warps to hide the store / F /
     // key-term latency, fewer registers each); keys and matrices together
     // (a rank call that also wants numerators) use 8 warps x 32 columns
-    static const bool keys16 = [] {   // SA_K2T_KEYS16=0: the 8-warp x 32-column key epilogue
+    static const bool keys16 = [] {   // SA_K2T_KEYS16=0: the 8-warp key epilogue
       const char* e = getenv("SA_K2T_KEYS16");
       return !(e && atoi(e) == 0);
     }();
-    if (mode == EPI_KEYS && keys16) tc_gemm<KeyMatEpi<EPI_KEYS>, 16, 16>(grid, batch, maps, tiles, epi, st);
-    else if (mode == EPI_KEYS) tc_gemm<KeyMatEpi<EPI_KEYS>, 8, 32>(grid, batch, maps, tiles, epi, st);
-    else if (mode == EPI_NUM) tc_gemm<KeyMatEpi<EPI_NUM>, 16, 16>(grid, batch, maps, tiles, epi, st);
-    else if ((mode & EPI_KEYS) == 0) tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16>(grid, batch, maps, tiles, epi, st);
-    else tc_gemm<KeyMatEpi<EPI_ALL>, 8, 32>(grid, batch, maps, tiles, epi, st);
+    if (fp4) tc_gemm_mode<true>(mode, keys16, grid, batch, maps, tiles, epi, st);
+    else tc_gemm_mode<false>(mode, keys16, grid, batch, maps, tiles, epi, st);
     SA_LAUNCHED();
     for (int q = 0; q < np; ++q) {
       const MsProblem& P = probs[i0 + q];
@@ -782,11 +836,11 @@ sa_status f_division_selftest(int64_t* mismatches_h) {
   return SA_OK;
 }
 
-static sa_status tc_encode_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int box_rows) {
+static sa_status tc_encode_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int box_rows, int64_t rowb) {
   auto enc = tensor_map_encoder();
   if (!enc) return fail(SA_E_CUDA, "cuTensorMapEncodeTiled is unavailable");
-  const cuuint64_t dims[2] = {(cuuint64_t)TC_KCAP, (cuuint64_t)rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)TC_KCAP};
+  const cuuint64_t dims[2] = {(cuuint64_t)rowb, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)rowb};
   const cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims, strides, box, estr,

@@ -30,14 +30,25 @@ namespace sa {
 namespace tc {
 
 constexpr int BM = 128;          // tile rows (UMMA M)
-constexpr int BN = 256;          // tile columns (UMMA N)
-constexpr int BK = 128;          // bytes (= u8 elements of K) per stage
-constexpr int UK = 32;           // K per tcgen05.mma kind::i8
+constexpr int BK = 128;          // bytes of K per stage (128 u8 columns, or 256 packed fp4 columns)
+constexpr int UKB = 32;          // bytes of K per tcgen05.mma (kind::i8: K = 32; kind::mxf4: K = 64)
 constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK;
-constexpr int B_BYTES = BN * BK;
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int TMEM_COLS = 2 * BN;
+constexpr int TMEM_COLS = 512;
+// Operand format: u8 0/1 columns (kind::i8, s32 accumulators, 128 x 256
+// tiles) or packed e2m1 0/1.0 columns (kind::mxf4, block32 UE8M0 scale factors
+// all 1.0, f32 accumulators -- exact: sums <= 32768 < 2^24 -- twice the MMA
+// rate; 128 x 240 tiles so that two accumulators leave 32 TMEM columns for the
+// scale factors).
+template <bool FP4>
+struct Geo {
+  static constexpr int BN = FP4 ? 240 : 256;               // tile columns (UMMA N)
+  static constexpr int B_BYTES = BN * BK;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;    // multiple of 1024 (SWIZZLE_128B atoms)
+  static constexpr int SF_COL = 2 * BN;                    // first scale-factor TMEM column (FP4)
+  static constexpr int COLS_PER_KB = FP4 ? 256 : 128;      // operand columns per 128-byte K block
+};
+static_assert(Geo<true>::STAGE_BYTES % 1024 == 0 && Geo<false>::STAGE_BYTES % 1024 == 0, "stage alignment");
 // Epilogue geometry (template parameters of gemm_kernel): EW epilogue warps
 // (a multiple of 4: warp w reads TMEM lanes 32 (w % 4) .. and the w / 4-th
 // column slice), CW columns per tcgen05.ld chunk (16 or 32), a padded
@@ -52,8 +63,8 @@ __device__ __forceinline__ int xpose_at(int row, int col) {
   if constexpr (CW == 32) return row * 33 + col;
   else return row * CW + (col ^ (row & (CW - 1)));
 }
-__host__ __device__ constexpr int smem_of(int EW, int CW) {
-  return STAGES * STAGE_BYTES + 1024 + 256 + EW * xpose_words(CW) * 4;
+__host__ __device__ constexpr int smem_of(int EW, int CW, bool FP4) {
+  return STAGES * (FP4 ? Geo<true>::STAGE_BYTES : Geo<false>::STAGE_BYTES) + 1024 + 256 + EW * xpose_words(CW) * 4;
 }
 constexpr int MAXPROB = 16;
 
@@ -106,6 +117,22 @@ __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint3
       "}\n" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+// D[tmem] (+)= (A[smem] x SFA) . (B[smem] x SFB)^T, packed e2m1, UE8M0 scale per 32 K
+__device__ __forceinline__ void mma_mxf4(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc,
+                                         uint32_t sfa, uint32_t sfb) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n"
+      "}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb));
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, uint32_t v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(v)
+               : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s_addr(bar))
                : "memory");
@@ -148,9 +175,14 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   d |= (uint64_t)2 << 61;
   return d;
 }
-// Instruction descriptor: s32 accumulator, u8 x u8, both K-major, M = BM, N = BN.
+// Instruction descriptor: s32 accumulator, u8 x u8, both K-major, M = BM, N = 256.
 __host__ __device__ constexpr uint32_t idesc_i8() {
-  return (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  return (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(Geo<false>::BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+// Block-scaled descriptor: e2m1 x e2m1 (MXF4 format 1), UE8M0 scales (bit 23),
+// scale-factor ids 0, dense K = 64, both K-major, M = BM, N = 240.
+__host__ __device__ constexpr uint32_t idesc_mxf4() {
+  return (1u << 7) | (1u << 10) | ((uint32_t)(Geo<true>::BN >> 3) << 17) | (1u << 23) | ((uint32_t)(BM >> 4) << 24);
 }
 
 // ------------------------------------------------------------ schedule ----
@@ -180,15 +212,6 @@ struct Tile {
   int pi, row0, col0, ra, rb;
 };
 
-// tiles of a problem
-__host__ __device__ inline int64_t problem_tiles(int64_t na, int64_t nb, bool sym) {
-  const int64_t tm = (na + BM - 1) / BM, tn = (nb + BN - 1) / BN;
-  if (!sym) return tm * tn;
-  int64_t t = 0;
-  for (int64_t i = 0; i < tm; ++i) t += tn - i / 2;
-  return t;
-}
-
 // Tile order inside a problem: groups of GROUP (Batch::group) row blocks; in a group, column
 // block by column block, the group's rows inside (column-major).  The ~148
 // tiles in flight then share ~148 / GROUP column blocks of B and GROUP row
@@ -196,12 +219,33 @@ __host__ __device__ inline int64_t problem_tiles(int64_t na, int64_t nb, bool sy
 // L2) instead of sweeping all of B every wave.  Symmetric problems keep the tiles with
 // column block J >= I / 2.
 
-// tiles of rows [0, i1) of a symmetric problem: sum_{i < i1} (tn - floor(i / 2))
-__device__ __forceinline__ int64_t sym_tiles_before(int i1, int tn) {
-  const int64_t h = i1 / 2;   // sum_{i < i1} floor(i / 2) = h (h - 1) + (i1 odd ? h : 0)
-  return (int64_t)i1 * tn - (h * (h - 1) + ((i1 & 1) ? h : 0));
+// sum_{i < n} floor((a i + b) / m)  (the classic floor-sum recursion)
+__host__ __device__ inline int64_t floor_sum(int64_t n, int64_t m, int64_t a, int64_t b) {
+  int64_t ans = 0;
+  while (true) {
+    if (a >= m) { ans += (n - 1) * n / 2 * (a / m); a %= m; }
+    if (b >= m) { ans += n * (b / m); b %= m; }
+    const int64_t y = a * n + b;
+    if (y < m) break;
+    n = y / m;
+    b = y % m;
+    const int64_t t = m; m = a; a = t;
+  }
+  return ans;
+}
+// tiles of rows [0, i1) of a symmetric problem: row block i keeps column
+// blocks j >= floor(i BM / BN) (the blocks holding some column >= a row)
+template <int BN>
+__host__ __device__ inline int64_t sym_tiles_before(int i1, int tn) {
+  return (int64_t)i1 * tn - floor_sum(i1, BN, BM, 0);
+}
+template <int BN>
+__host__ __device__ inline int64_t problem_tiles(int64_t na, int64_t nb, bool sym) {
+  const int64_t tm = (na + BM - 1) / BM, tn = (nb + BN - 1) / BN;
+  return sym ? sym_tiles_before<BN>((int)tm, (int)tn) : tm * tn;
 }
 
+template <int BN>
 __device__ __forceinline__ Tile decode(const Batch& b, int64_t tile) {
   int pi = 0;
   while (pi + 1 < b.n && b.p[pi + 1].tile_begin <= tile) ++pi;
@@ -219,17 +263,18 @@ __device__ __forceinline__ Tile decode(const Batch& b, int64_t tile) {
     tj = (int)(u / rows);
   } else {
     int g0 = 0;
-    while (g0 + GROUP < tm && sym_tiles_before(g0 + GROUP, tn) <= t) g0 += GROUP;
-    int64_t u = t - sym_tiles_before(g0, tn);
+    while (g0 + GROUP < tm && sym_tiles_before<BN>(g0 + GROUP, tn) <= t) g0 += GROUP;
+    int64_t u = t - sym_tiles_before<BN>(g0, tn);
     const int g1 = min(g0 + GROUP, tm);
-    int j = g0 / 2;
-    for (;; ++j) {   // the first few columns hold fewer rows (i <= 2 j + 1)
-      const int cnt = min(g1, 2 * j + 2) - g0;
-      if (cnt == g1 - g0) break;
-      if (u < cnt) break;
+    // column j holds the group's rows i < ceil((j + 1) BN / BM)
+    auto rows_at = [&](int j) { return min(g1, ((j + 1) * BN + BM - 1) / BM) - g0; };
+    int j = (int)((int64_t)g0 * BM / BN);
+    for (;; ++j) {   // the first few columns hold fewer rows
+      const int cnt = rows_at(j);
+      if (cnt == g1 - g0 || u < cnt) break;
       u -= cnt;
     }
-    const int cnt = min(g1, 2 * j + 2) - g0;
+    const int cnt = rows_at(j);
     ti = g0 + (int)(u % cnt);
     tj = j + (int)(u / cnt);
   }
@@ -251,10 +296,12 @@ __device__ __forceinline__ Tile decode(const Batch& b, int64_t tile) {
 //   __device__ void end(State&, const Tile&, int row) const;
 // row = tile row of this thread (0..127), col = first tile column of the chunk,
 // xpose = this warp's 32 x (CW + 1) word shared-memory scratch.
-template <class Epi, int EW, int CW>
+template <class Epi, int EW, int CW, bool FP4>
 __global__ void __launch_bounds__(threads_of(EW), 1)
 gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps maps, int64_t total_tiles, Epi epi) {
-  static_assert(EW % 4 == 0 && (BN / (EW / 4)) % CW == 0, "epilogue geometry");
+  using G = Geo<FP4>;
+  constexpr int BN = G::BN, STAGE_BYTES = G::STAGE_BYTES;
+  static_assert(EW % 4 == 0 && BN % CW == 0, "epilogue geometry");
   constexpr int EPI_WARPS = EW;
   if (epi.skip()) return;
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -285,13 +332,21 @@ gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps ma
   __syncthreads();
   fence_after();
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+  if constexpr (FP4) {
+    // every UE8M0 scale factor = 2^0 (0x7F): columns [SF_COL, 512) of all 128 lanes
+    if (warp < 4)
+      for (int c = G::SF_COL; c < TMEM_COLS; c += 8) tmem_st8(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, 0x7F7F7F7Fu);
+    fence_before();
+    __syncthreads();
+    fence_after();
+  }
 
   if (warp == EPI_WARPS) {
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
       int64_t g = 0;
       for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-        const Tile T = decode(batch, tile);
+        const Tile T = decode<BN>(batch, tile);
         const Problem& P = batch.p[T.pi];
         const int nkb = *reinterpret_cast<const volatile int32_t*>(P.kblocks);
         const CUtensorMap* ma = &maps.m[2 * P.map];
@@ -309,10 +364,11 @@ gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps ma
   } else if (warp == EPI_WARPS + 1) {
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_i8();
+      constexpr uint32_t idesc = FP4 ? idesc_mxf4() : idesc_i8();
+      const uint32_t sfa = tmem_base + (uint32_t)G::SF_COL, sfb = tmem_base + (uint32_t)G::SF_COL + 16u;
       int64_t g = 0, lt = 0;
       for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
-        const Tile T = decode(batch, tile);
+        const Tile T = decode<BN>(batch, tile);
         const Problem& P = batch.p[T.pi];
         const int nkb = *reinterpret_cast<const volatile int32_t*>(P.kblocks);
         const int buf = (int)(lt & 1);
@@ -326,8 +382,11 @@ gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps ma
           const uint32_t sa_ = base_s + slot * STAGE_BYTES;
           const uint64_t da = sw128_desc(sa_), db = sw128_desc(sa_ + A_BYTES);
 #pragma unroll
-          for (int k = 0; k < BK / UK; ++k)
-            mma_i8(d, da + (uint64_t)((k * UK) >> 4), db + (uint64_t)((k * UK) >> 4), idesc, (kb | k) != 0);
+          for (int k = 0; k < BK / UKB; ++k) {
+            const uint64_t off = (uint64_t)((k * UKB) >> 4);
+            if constexpr (FP4) mma_mxf4(d, da + off, db + off, idesc, (kb | k) != 0, sfa, sfb);
+            else mma_i8(d, da + off, db + off, idesc, (kb | k) != 0);
+          }
           mma_commit(&empty[slot]);
         }
         mma_commit(&tfull[buf]);
@@ -338,20 +397,24 @@ gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps ma
     const int quad = warp & 3, part = warp >> 2;
     const int row = quad * 32 + lane;
     uint32_t* xpose = xpose_all + warp * xpose_words(CW);
-    constexpr int SLICE = BN / (EW / 4);   // columns per epilogue warp
+    // columns per epilogue warp: a multiple of CW; the last slice may be shorter
+    constexpr int SLICE = ((BN / (EW / 4) + CW - 1) / CW) * CW;
     typename Epi::State es;
     int64_t lt = 0;
     for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
-      const Tile T = decode(batch, tile);
+      const Tile T = decode<BN>(batch, tile);
       const int buf = (int)(lt & 1);
       bar_wait(&tfull[buf], (uint32_t)((lt >> 1) & 1));
       fence_after();
       epi.begin(es, T, row);
 #pragma unroll 1
-      for (int ch = 0; ch < SLICE / CW; ++ch) {
-        const int col = part * SLICE + ch * CW;
+      for (int col = part * SLICE; col < min(part * SLICE + SLICE, BN); col += CW) {
         uint32_t v[CW];
         tmem_ld<CW>(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + col), v);
+        if constexpr (FP4) {
+#pragma unroll
+          for (int j = 0; j < CW; ++j) v[j] = (uint32_t)__uint_as_float(v[j]);   // exact integer sums
+        }
         epi.template chunk<CW>(es, T, row, col, v, lane, xpose);
       }
       fence_before();

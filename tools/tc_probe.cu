@@ -82,21 +82,21 @@ int main(int argc, char** argv) {
   P.na = M;
   P.nb = Nb;
   P.sym = sym;
-  P.tiles_n = (Nb + BN - 1) / BN;
+  P.tiles_n = (Nb + Geo<false>::BN - 1) / Geo<false>::BN;
   P.tile_begin = 0;
   P.kblocks = dkb;
   P.map = 0;
   Maps maps;
   memset(&maps, 0, sizeof maps);
   make_map(&maps.m[0], dA, M, K, BM);
-  make_map(&maps.m[1], sym ? dA : dB, Nb, K, BN);
-  const int64_t tiles = problem_tiles(M, Nb, sym);
+  make_map(&maps.m[1], sym ? dA : dB, Nb, K, Geo<false>::BN);
+  const int64_t tiles = problem_tiles<Geo<false>::BN>(M, Nb, sym);
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-  CK(cudaFuncSetAttribute(gemm_kernel<WriteEpi, 8, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_of(8, 32)));
+  CK(cudaFuncSetAttribute(gemm_kernel<WriteEpi, 8, 32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_of(8, 32, false)));
   WriteEpi epi{dC, Nb};
   const int grid = (int)(tiles < sms ? tiles : sms);
-  gemm_kernel<WriteEpi, 8, 32><<<grid, threads_of(8), smem_of(8, 32)>>>(batch, maps, tiles, epi);
+  gemm_kernel<WriteEpi, 8, 32, false><<<grid, threads_of(8), smem_of(8, 32, false)>>>(batch, maps, tiles, epi);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   std::vector<int32_t> C((size_t)M * Nb);
@@ -105,7 +105,7 @@ int main(int argc, char** argv) {
   long bad = 0, checked = 0;
   for (int i = 0; i < M; ++i)
     for (int j = 0; j < Nb; ++j) {
-      if (sym && (j / BN) < (i / BM) / 2) continue;   // tile not scheduled
+      if (sym && (j / Geo<false>::BN) < (i / BM) / 2) continue;   // tile not scheduled
       int32_t ref = 0;
       for (int k = 0; k < K; ++k) ref += A[(size_t)i * K + k] * Bh[(size_t)j * K + k];
       ++checked;
@@ -122,13 +122,13 @@ int main(int argc, char** argv) {
   CK(cudaEventCreate(&e1));
   const int reps = 5;
   CK(cudaEventRecord(e0));
-  for (int r = 0; r < reps; ++r) gemm_kernel<WriteEpi, 8, 32><<<grid, threads_of(8), smem_of(8, 32)>>>(batch, maps, tiles, epi);
+  for (int r = 0; r < reps; ++r) gemm_kernel<WriteEpi, 8, 32, false><<<grid, threads_of(8), smem_of(8, 32, false)>>>(batch, maps, tiles, epi);
   CK(cudaEventRecord(e1));
   CK(cudaEventSynchronize(e1));
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, e0, e1));
   ms /= reps;
-  const double ops = 2.0 * tiles * BM * BN * (double)K;
+  const double ops = 2.0 * tiles * BM * Geo<false>::BN * (double)K;
   printf("time %.3f ms, %.1f TOPS (tile ops incl. padding)\n", ms, ops / ms / 1e9);
   return bad ? 2 : 0;
 }
