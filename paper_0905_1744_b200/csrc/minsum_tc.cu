@@ -659,6 +659,21 @@ static void tc_gemm_mode(int mode, bool keys16, int64_t grid, const tc::Batch& b
   else tc_gemm<KeyMatEpi<EPI_ALL>, 8, CW_ALL, FP4>(grid, batch, maps, tiles, epi, st);
 }
 
+static sa_status tc_encode_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int box_rows, int64_t rowb) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return fail(SA_E_CUDA, "cuTensorMapEncodeTiled is unavailable");
+  const cuuint64_t dims[2] = {(cuuint64_t)rowb, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)rowb};
+  const cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SA_E_CUDA, "cuTensorMapEncodeTiled (K2T) failed (%d)", (int)r);
+  return SA_OK;
+}
+
+
 sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t bins, uint32_t* state,
                     uint32_t* cols_out, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1) {
   SA_TRY(ensure_recip_tables_tu(st));
@@ -833,20 +848,6 @@ sa_status f_division_selftest(int64_t* mismatches_h) {
   if (e != cudaSuccess) return fail(SA_E_CUDA, "division self-test launch: %s", cudaGetErrorString(e));
   SA_CUDA(cudaGetLastError());
   *mismatches_h = (int64_t)h;
-  return SA_OK;
-}
-
-static sa_status tc_encode_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int box_rows, int64_t rowb) {
-  auto enc = tensor_map_encoder();
-  if (!enc) return fail(SA_E_CUDA, "cuTensorMapEncodeTiled is unavailable");
-  const cuuint64_t dims[2] = {(cuuint64_t)rowb, (cuuint64_t)rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)rowb};
-  const cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)box_rows};
-  const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims, strides, box, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(SA_E_CUDA, "cuTensorMapEncodeTiled (K2T) failed (%d)", (int)r);
   return SA_OK;
 }
 
