@@ -36,6 +36,22 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(f) <= t for f in sources() + headers() + [__file__])
 
 
+def _deps(src: str, seen=None) -> set:
+    """The source and every local header it includes (transitively)."""
+    import re
+    seen = set() if seen is None else seen
+    if src in seen or not os.path.exists(src):
+        return seen
+    seen.add(src)
+    for inc in re.findall(r'#include\s+"([^"]+)"', open(src).read()):
+        for d in (os.path.dirname(src), os.path.join(ROOT, "include")):
+            f = os.path.normpath(os.path.join(d, inc))
+            if os.path.exists(f):
+                _deps(f, seen)
+                break
+    return seen
+
+
 def _obj(src: str) -> str:
     return os.path.join(os.path.dirname(LIB), "obj", os.path.basename(src) + ".o")
 
@@ -51,11 +67,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
     os.makedirs(os.path.join(os.path.dirname(LIB), "obj"), exist_ok=True)
-    newest_dep = max(os.path.getmtime(f) for f in headers() + [__file__])
-
     def compile_one(src):
         obj = _obj(src)
-        if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(newest_dep, os.path.getmtime(src)):
+        newest = max(os.path.getmtime(f) for f in _deps(src) | {__file__})
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) >= newest:
             return src, None
         r = subprocess.run([NVCC, *_flags(verbose), "-c", src, "-o", obj + ".tmp"], capture_output=True, text=True)
         if r.returncode == 0:

@@ -406,11 +406,27 @@ struct TcEpiProb {
 // re-read from L2.
 __device__ __forceinline__ void st_out(uint16_t* p, uint16_t v) { __stcs(reinterpret_cast<unsigned short*>(p), v); }
 __device__ __forceinline__ void st_out(double* p, double v) { __stcs(p, v); }
-
 // 96-bit (lo, hi) add
 __device__ __forceinline__ void add96(uint64_t& lo, uint32_t& hi, uint64_t blo, uint32_t bhi) {
   lo += blo;
   hi += bhi + ((lo < blo) ? 1u : 0u);
+}
+
+// floor(C 2^64 / D) mod 2^64 (the exact-rank key term) from the
+// D-side reciprocal tables rl + 2^32 rh = r = floor(2^64 / D), e = 2^64 mod D
+// (0 <= C <= D < 2^16):  C r + floor(C e / D).  The quotient x / D of
+// x = C e < 2^32 is taken without a division: floor(x / D) = floor(x (r + 1) / 2^64),
+// because r + 1 - 2^64 / D < 1 and x 2^-64 < 2^-32 < 1 / D keep x (r + 1) / 2^64
+// inside [x / D, floor(x / D) + 1) (e = 0 gives x = 0).  C = D gives 2^64, which
+// wraps to 0 here: the caller adds it to the high word.
+__device__ __forceinline__ uint64_t key_term_lo(uint32_t C, uint32_t rl, uint32_t rh, uint32_t e) {
+  const uint64_t p = (uint64_t)C * rl + ((uint64_t)(C * rh) << 32);
+  const uint32_t x = C * e;
+  const uint64_t p0 = (uint64_t)x * rl;
+  const uint64_t p1 = (uint64_t)x * rh + (p0 >> 32);
+  const uint32_t s = (uint32_t)p0 + x;
+  const uint32_t q = (uint32_t)((p1 + (s < x ? 1ull : 0ull)) >> 32);
+  return p + q;
 }
 
 // MODE: which outputs this instantiation can write (EPI_KEYS | EPI_NUM |
@@ -418,159 +434,291 @@ __device__ __forceinline__ void add96(uint64_t& lo, uint32_t& hi, uint64_t blo, 
 // key path and the matrix path each get their own register allocation.
 enum { EPI_KEYS = 1, EPI_NUM = 2, EPI_SIM = 4, EPI_ALL = 7 };
 
+// Per-tile tables.  Every epilogue warp stages, for each column of its slice,
+// before the accumulator is ready (tc_gemm.cuh):
+//   key entry  {rl, rh, e, nk'}  reciprocal tables of D = nk' (EPI_KEYS)
+//   F entry    {y_lo, y_hi, nk', 0}  y = RN(1 / nk')        (EPI_SIM)
+// with nk' = nk if the column exists and nk > 0, else -1 (tables of 0: r = e
+// = y = 0).  A pair then takes D = min(nk'_row, nk'_col) and the tables of
+// whichever side is smaller; the -1 sentinel makes every term of a missing or
+// empty (n < k, Z4) row or column 0 with no extra test: r = e = 0 gives key
+// term 0, C = D is impossible, y = 0 gives F = 0.  The lanes read the entries
+// of the chunk's columns as shared-memory broadcasts.
 template <int MODE>
 struct KeyMatEpi {
   TcEpiProb e[tc::MAXPROB];
   const uint32_t* state;
 
+  static constexpr bool KEYS = (MODE & EPI_KEYS) != 0;
+  static constexpr bool SIM = (MODE & EPI_SIM) != 0;
+  static constexpr bool MATS = (MODE & (EPI_NUM | EPI_SIM)) != 0;
+  static constexpr int KOFF = 0;
+  static constexpr int YOFF = KEYS ? 16 : 0;
+  static constexpr int TAB_BYTES = (KEYS && SIM) ? 32 : 16;
+  // the per-warp 32 x CW uint16 transpose buffer of the matrix path
+  __host__ __device__ static constexpr int xpose_bytes(int CW) { return MATS ? 64 * CW : 0; }
+
   struct State {
-    uint64_t lo;
+    uint64_t lo;      // row key, 96 bits
     uint32_t hi;
-    int nk_r;
+    int nk;           // nk' of the row (sentinel -1: no row or nk = 0)
+    int nk0;          // nk of the row (0 if none): the diagonal numerator C_ii
     int row_g;
-    double d_r, y_r;   // (double)nk_r and RN(1 / nk_r): F = C / min(nk_r, nk_c) without a division
+    bool rv;          // the row exists
+    uint32_t rl, rh, ek;
+    double y;
   };
 
   __device__ bool skip() const { return tc_infeasible(state); }
 
-  __device__ void begin(State& s, const tc::Tile& T, int row) const {
+  __device__ void begin(State& s, const tc::Tile& T, int row, int lane, int cbeg, int cend, uint8_t* tab) const {
     const TcEpiProb& E = e[T.pi];
     s.lo = 0;
     s.hi = 0;
     s.row_g = T.row0 + row;
-    s.nk_r = row < T.ra ? E.nkA[s.row_g] : -1;
-    if ((MODE & EPI_SIM) && E.sim) {
-      s.d_r = (double)max(s.nk_r, 0);
-      s.y_r = rcp_of(s.nk_r);
+    s.rv = row < T.ra;
+    s.nk0 = s.rv ? E.nkA[s.row_g] : 0;
+    s.nk = s.nk0 > 0 ? s.nk0 : -1;
+    const int dr = s.nk > 0 ? s.nk : 0;
+    if constexpr (KEYS) {
+      const uint64_t r = g_rtab[dr];
+      s.rl = (uint32_t)r;
+      s.rh = (uint32_t)(r >> 32);
+      s.ek = g_etab[dr];
     }
+    if constexpr (SIM) s.y = g_rcp[dr];
+    if constexpr (KEYS || SIM) {
+      for (int c = cbeg + lane; c < cend; c += 32) {
+        const int nkc = c < T.rb ? E.nkB[T.col0 + c] : 0;
+        const int ns = nkc > 0 ? nkc : -1;
+        const int dc = ns > 0 ? ns : 0;
+        uint8_t* ent = tab + (c - cbeg) * TAB_BYTES;
+        if constexpr (KEYS) {
+          const uint64_t r = g_rtab[dc];
+          *reinterpret_cast<uint4*>(ent + KOFF) = make_uint4((uint32_t)r, (uint32_t)(r >> 32), g_etab[dc], (uint32_t)ns);
+        }
+        if constexpr (SIM) {
+          const double y = g_rcp[dc];
+          *reinterpret_cast<uint4*>(ent + YOFF) =
+              make_uint4((uint32_t)__double2loint(y), (uint32_t)__double2hiint(y), (uint32_t)ns, 0u);
+        }
+      }
+    }
+    __syncwarp();
+  }
+
+  // the exact-rank term of pair (row, column entry k), numerator C: 64 low bits + the 2^64 carry
+  __device__ __forceinline__ void fterm(const State& s, const uint4& k, uint32_t C, uint64_t& t, uint32_t& cd) const {
+    const int nkc = (int)k.w;
+    const bool cm = nkc < s.nk;
+    t = key_term_lo(C, cm ? k.x : s.rl, cm ? k.y : s.rh, cm ? k.z : s.ek);
+    cd = ((int)C == min(s.nk, nkc)) ? 1u : 0u;
+  }
+
+  // column sums of 8 columns' terms over the 32 rows of the warp: butterfly
+  // over lane bits 4, 3, 2 (8 -> 1 value per lane), then xor 2, 1; lanes
+  // 4 m hold column m and add it to its key with a 128-bit atomic
+  __device__ __forceinline__ static void colsum8(uint64_t (&tlo)[8], uint32_t (&thi)[8], int lane, sa_key128* keys,
+                                                  int c0, int jbase, int ncols) {
+#pragma unroll
+    for (int sft = 4, half = 16; sft >= 1; sft >>= 1, half >>= 1) {
+      const bool upper = (lane & half) != 0;
+#pragma unroll
+      for (int i = 0; i < sft; ++i) {
+        const uint64_t slo = upper ? tlo[i] : tlo[i + sft];
+        const uint32_t shi = upper ? thi[i] : thi[i + sft];
+        uint64_t klo = upper ? tlo[i + sft] : tlo[i];
+        uint32_t khi = upper ? thi[i + sft] : thi[i];
+        const uint64_t rlo = __shfl_xor_sync(0xffffffffu, slo, half);
+        const uint32_t rhi = __shfl_xor_sync(0xffffffffu, shi, half);
+        add96(klo, khi, rlo, rhi);
+        tlo[i] = klo;
+        thi[i] = khi;
+      }
+    }
+    uint64_t lo = tlo[0];
+    uint32_t hi = thi[0];
+    {
+      uint64_t rlo = __shfl_xor_sync(0xffffffffu, lo, 2);
+      uint32_t rhi = __shfl_xor_sync(0xffffffffu, hi, 2);
+      add96(lo, hi, rlo, rhi);
+      rlo = __shfl_xor_sync(0xffffffffu, lo, 1);
+      rhi = __shfl_xor_sync(0xffffffffu, hi, 1);
+      add96(lo, hi, rlo, rhi);
+    }
+    // lane bits 4,3,2 name the column: 4 * b4 + 2 * b3 + b2
+    const int jc = jbase + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+    if ((lane & 3) == 0 && (lo | hi) && jc < ncols) atomic_add_key(keys + c0 + jc, lo, hi);
   }
 
   // CW columns [col, col + CW) of this thread's row; lanes = 32 consecutive rows.
   template <int CW>
   __device__ void chunk(State& s, const tc::Tile& T, int row, int col, const uint32_t (&v)[CW], int lane,
-                        uint32_t* xpose) const {
+                        const uint8_t* tab, int tj, uint8_t* xp) const {
     static_assert(CW == 16 || CW == 32, "chunk width");
     const TcEpiProb& E = e[T.pi];
     const bool sym = E.sym != 0;
-    const int c0 = T.col0 + col;                          // global column of j = 0
-    const int cl = lane % CW;                             // the column a lane describes
-    const int nk_cl = (col + cl < T.rb) ? E.nkB[c0 + cl] : -1;
-    uint32_t C[CW];
-#pragma unroll
-    for (int j = 0; j < CW; ++j) C[j] = (sym && c0 + j == s.row_g) ? (uint32_t)s.nk_r : v[j];
+    const int c0 = T.col0 + col;                        // global column of j = 0
+    const int wrow0 = s.row_g - lane;                   // the warp's first row
+    const bool upper = !sym || c0 > wrow0 + 31;         // every pair strictly above the diagonal (warp-uniform)
+    const int ncols = min(CW, T.rb - col);              // columns that exist
+    const uint8_t* ent = tab + tj * TAB_BYTES;
+    if (sym && c0 + CW <= wrow0) return;                // every pair below the diagonal: counted by its mirror
 
-    if ((MODE & EPI_KEYS) && E.keyA) {
+    if (KEYS && E.keyA) {
       const bool colsum = sym && E.keyB;
+      if (upper && E.form != SA_RANK_DF) {
+        // ---- fast path: every pair counted for the row (and mirrored), sentinels mask the rest
 #pragma unroll
-      for (int g = 0; g < CW / 8; ++g) {
-        uint64_t tlo[8];
-        uint32_t thi[8];
+        for (int g = 0; g < CW / 8; ++g) {
+          uint64_t tlo[8];
+          uint32_t thi[8];
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          const int j = g * 8 + jj;
-          const int nk_c = __shfl_sync(0xffffffffu, nk_cl, j);
-          const int gc = c0 + j;
-          uint64_t lo = 0;
-          uint32_t hi = 0;
-          if (s.nk_r >= 0 && nk_c >= 0 && (!sym || gc >= s.row_g))
-            key_term_f(E, lo, hi, C[j], (uint32_t)min(s.nk_r, nk_c));
-          add96(s.lo, s.hi, lo, hi);
-          const bool mirror = colsum && gc > s.row_g;
-          tlo[jj] = mirror ? lo : 0ull;
-          thi[jj] = mirror ? hi : 0u;
+          for (int jj = 0; jj < 8; ++jj) {
+            const int j = g * 8 + jj;
+            const uint4 k = *reinterpret_cast<const uint4*>(ent + j * TAB_BYTES + KOFF);
+            fterm(s, k, v[j], tlo[jj], thi[jj]);
+            add96(s.lo, s.hi, tlo[jj], thi[jj]);
+          }
+          if (colsum) colsum8(tlo, thi, lane, E.keyB, c0, g * 8, ncols);
         }
-        if (colsum) {
-          // reduce the 8 column terms over the 32 rows of the warp: butterfly
-          // over lane bits 4, 3, 2 (8 -> 1 value per lane), then xor 2, 1
+      } else {
+        // ---- diagonal chunks and the d^F form: explicit masks
 #pragma unroll
-          for (int sft = 4, half = 16; sft >= 1; sft >>= 1, half >>= 1) {
-            const bool upper = (lane & half) != 0;
+        for (int g = 0; g < CW / 8; ++g) {
+          uint64_t tlo[8];
+          uint32_t thi[8];
 #pragma unroll
-            for (int i = 0; i < sft; ++i) {
-              const uint64_t slo = upper ? tlo[i] : tlo[i + sft];
-              const uint32_t shi = upper ? thi[i] : thi[i + sft];
-              uint64_t klo = upper ? tlo[i + sft] : tlo[i];
-              uint32_t khi = upper ? thi[i + sft] : thi[i];
-              const uint64_t rlo = __shfl_xor_sync(0xffffffffu, slo, half);
-              const uint32_t rhi = __shfl_xor_sync(0xffffffffu, shi, half);
-              add96(klo, khi, rlo, rhi);
-              tlo[i] = klo;
-              thi[i] = khi;
+          for (int jj = 0; jj < 8; ++jj) {
+            const int j = g * 8 + jj;
+            const int gc = c0 + j;
+            const uint4 k = *reinterpret_cast<const uint4*>(ent + j * TAB_BYTES + KOFF);
+            const bool cv = j < ncols;
+            const bool diag = sym && gc == s.row_g;
+            const uint32_t C = diag ? (uint32_t)s.nk0 : v[j];
+            uint64_t lo = 0;
+            uint32_t hi = 0;
+            if (s.rv && cv && (!sym || gc >= s.row_g)) {
+              if (E.form == SA_RANK_DF) {
+                const int nkc0 = max((int)k.w, 0);
+                add_dF_term(lo, hi, C, (uint32_t)min(s.nk0, nkc0), E.delta, E.ln1pd);
+              } else {
+                fterm(s, k, C, lo, hi);
+              }
             }
+            add96(s.lo, s.hi, lo, hi);
+            const bool mirror = sym && gc > s.row_g;
+            tlo[jj] = mirror ? lo : 0ull;
+            thi[jj] = mirror ? hi : 0u;
           }
-          uint64_t lo = tlo[0];
-          uint32_t hi = thi[0];
-          {
-            uint64_t rlo = __shfl_xor_sync(0xffffffffu, lo, 2);
-            uint32_t rhi = __shfl_xor_sync(0xffffffffu, hi, 2);
-            add96(lo, hi, rlo, rhi);
-            rlo = __shfl_xor_sync(0xffffffffu, lo, 1);
-            rhi = __shfl_xor_sync(0xffffffffu, hi, 1);
-            add96(lo, hi, rlo, rhi);
-          }
-          // lane bits 4,3,2 name the column: 4 * b4 + 2 * b3 + b2
-          const int jc = g * 8 + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-          if ((lane & 3) == 0 && (lo | hi) && col + jc < T.rb) atomic_add_key(E.keyB + c0 + jc, lo, hi);
+          if (colsum) colsum8(tlo, thi, lane, E.keyB, c0, g * 8, ncols);
         }
       }
     }
 
-    if ((MODE & (EPI_NUM | EPI_SIM)) && (E.num || E.sim)) {
-      const bool want_sim = (MODE & EPI_SIM) && E.sim;
-      // per-lane column side of D = min(nk_r, nk_c) for the division-free F
-      const double d_cl = (double)max(nk_cl, 0), y_cl = want_sim ? rcp_of(nk_cl) : 0.0;
-      // mirrored half (symmetric): lanes = consecutive rows -> coalesced columns
-      if (sym) {
+    if (MATS && (E.num || E.sim)) {
+      const bool want_num = (MODE & EPI_NUM) && E.num;
+      const bool want_sim = SIM && E.sim;
+      if (upper && ncols == CW) {
+        // ---- fast path.  (1) lanes = rows: F of every pair, the mirrored
+        // element (gc, row) stored with lanes = consecutive rows (coalesced),
+        // C staged in the warp's 32 x CW uint16 transpose buffer (16-byte
+        // units XOR-swizzled by the row: conflict-free both ways).
+        constexpr int Q = CW / 8;                          // 16-byte units per buffer row
+        constexpr int QSH = CW == 16 ? 2 : 1;              // swizzle: unit ^ ((row >> QSH) % Q)
+        {
+          uint32_t w[CW / 2];
+#pragma unroll
+          for (int j = 0; j < CW; ++j) {
+            const uint32_t C = v[j];
+            if (j & 1) w[j >> 1] |= C << 16;
+            else w[j >> 1] = C;
+            if (sym && s.rv) {
+              const int64_t o = (int64_t)(c0 + j) * E.ld + s.row_g;
+              if (want_num) st_out(E.num + o, (uint16_t)C);
+              if (want_sim) {
+                const uint4 k = *reinterpret_cast<const uint4*>(ent + j * TAB_BYTES + YOFF);
+                const int nkc = (int)k.z;
+                const double yc = __hiloint2double((int)k.y, (int)k.x);
+                const int D = min(s.nk, nkc);
+                const double d = __hiloint2double(0x43300000, D) - 4503599627370496.0;
+                st_out(E.sim + o, f_ratio_y(C, d, nkc < s.nk ? yc : s.y));
+              }
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            const int qs = q ^ ((lane >> QSH) & (Q - 1));
+            *reinterpret_cast<uint4*>(xp + lane * (CW * 2) + qs * 16) =
+                make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+          }
+        }
+        __syncwarp();
+        // (2) lanes = columns: the direct row segments (row, c0 ..) from the
+        // buffer, 32 / CW rows per pass, row data by shuffles
+        const int cl = lane % CW;
+        int nkc = -1;
+        double yc = 0.0;
+        if (want_sim) {
+          const uint4 k = *reinterpret_cast<const uint4*>(ent + cl * TAB_BYTES + YOFF);
+          nkc = (int)k.z;
+          yc = __hiloint2double((int)k.y, (int)k.x);
+        }
+        constexpr int RPP = 32 / CW;
+        const int wrow = s.row_g - lane;
+#pragma unroll 4
+        for (int pss = 0; pss < CW; ++pss) {
+          const int i = pss * RPP + lane / CW;              // buffer row = warp row
+          const int nk_i = __shfl_sync(0xffffffffu, s.nk, i);
+          const double y_i = __shfl_sync(0xffffffffu, s.y, i);
+          const bool rv_i = __shfl_sync(0xffffffffu, (int)s.rv, i) != 0;
+          const int qs = (cl >> 3) ^ ((i >> QSH) & (Q - 1));
+          const uint32_t C = *reinterpret_cast<const uint16_t*>(xp + i * (CW * 2) + qs * 16 + (cl & 7) * 2);
+          if (!rv_i) continue;
+          const int64_t o = (int64_t)(wrow + i) * E.ld + c0 + cl;
+          if (want_num) st_out(E.num + o, (uint16_t)C);
+          if (want_sim) {
+            const int D = min(nk_i, nkc);
+            const double d = __hiloint2double(0x43300000, D) - 4503599627370496.0;
+            st_out(E.sim + o, f_ratio_y(C, d, nkc < nk_i ? yc : y_i));
+          }
+        }
+        __syncwarp();
+      } else {
+        // ---- diagonal / ragged chunks: per-element masks
 #pragma unroll
         for (int j = 0; j < CW; ++j) {
-          const int nk_c = __shfl_sync(0xffffffffu, nk_cl, j);
-          const double d_c = __shfl_sync(0xffffffffu, d_cl, j), y_c = __shfl_sync(0xffffffffu, y_cl, j);
           const int gc = c0 + j;
-          if (s.nk_r < 0 || nk_c < 0 || gc <= s.row_g) continue;
-          const int64_t o = (int64_t)gc * E.ld + s.row_g;
-          if (E.num) st_out(E.num + o, (uint16_t)C[j]);
+          if (!s.rv || j >= ncols || (sym && gc < s.row_g)) continue;
+          const bool diag = sym && gc == s.row_g;
+          const uint32_t C = diag ? (uint32_t)s.nk0 : v[j];
+          double F = 0.0;
           if (want_sim) {
-            const bool rmin = s.nk_r <= nk_c;
-            st_out(E.sim + o, f_ratio_y(C[j], rmin ? s.d_r : d_c, rmin ? s.y_r : y_c));
+            const uint4 k = *reinterpret_cast<const uint4*>(ent + j * TAB_BYTES + YOFF);
+            const int nkc = (int)k.z;
+            const double yc = __hiloint2double((int)k.y, (int)k.x);
+            const double y = nkc < s.nk ? yc : s.y;
+            const int D = min(s.nk, nkc);
+            const double d = __hiloint2double(0x43300000, D) - 4503599627370496.0;
+            F = f_ratio_y(C, d, y);
+          }
+          const int64_t od = (int64_t)s.row_g * E.ld + gc;
+          if (want_num) st_out(E.num + od, (uint16_t)C);
+          if (want_sim) st_out(E.sim + od, F);
+          if (sym && !diag) {
+            const int64_t om = (int64_t)gc * E.ld + s.row_g;
+            if (want_num) st_out(E.num + om, (uint16_t)C);
+            if (want_sim) st_out(E.sim + om, F);
           }
         }
       }
-      // direct half through a 32 x CW transpose: lanes = consecutive columns
-      // (32 / CW rows per pass)
-#pragma unroll
-      for (int j = 0; j < CW; ++j) xpose[tc::xpose_at<CW>(lane, j)] = C[j];
-      __syncwarp();
-      const int rbase = s.row_g - lane;
-      const int gc = c0 + cl;
-      constexpr int RPP = 32 / CW;                        // rows per pass
-#pragma unroll 4
-      for (int p = 0; p < 32 / RPP; ++p) {
-        const int i = p * RPP + lane / CW;
-        const int nk_ri = __shfl_sync(0xffffffffu, s.nk_r, i);
-        const double d_ri = __shfl_sync(0xffffffffu, s.d_r, i), y_ri = __shfl_sync(0xffffffffu, s.y_r, i);
-        const int rg = rbase + i;
-        if (nk_ri < 0 || nk_cl < 0 || (sym && gc < rg)) continue;
-        const uint32_t Cv = xpose[tc::xpose_at<CW>(i, cl)];
-        const int64_t o = (int64_t)rg * E.ld + gc;
-        if (E.num) st_out(E.num + o, (uint16_t)Cv);
-        if (want_sim) {
-          const bool rmin = nk_ri <= nk_cl;
-          st_out(E.sim + o, f_ratio_y(Cv, rmin ? d_ri : d_cl, rmin ? y_ri : y_cl));
-        }
-      }
-      __syncwarp();
     }
   }
 
   __device__ void end(State& s, const tc::Tile& T, int row) const {
     const TcEpiProb& E = e[T.pi];
-    if ((MODE & EPI_KEYS) && E.keyA && s.nk_r >= 0 && (s.lo | s.hi)) atomic_add_key(E.keyA + s.row_g, s.lo, s.hi);
+    if (KEYS && E.keyA && s.rv && (s.lo | s.hi)) atomic_add_key(E.keyA + s.row_g, s.lo, s.hi);
     (void)row;
-  }
-
-  __device__ static void key_term_f(const TcEpiProb& E, uint64_t& lo, uint32_t& hi, uint32_t C, uint32_t D) {
-    if (E.form == SA_RANK_DF) add_dF_term(lo, hi, C, D, E.delta, E.ln1pd);
-    else add_term(lo, hi, C, D);
   }
 };
 
@@ -620,8 +768,9 @@ __global__ void f_division_check_kernel(unsigned long long* bad) {
 // ------------------------------------------------------------- host ----
 template <class Epi, int EW, int CW, bool FP4>
 static sa_status tc_configure() {
+  static_assert(tc::smem_of(EW, CW, FP4, Epi::TAB_BYTES, Epi::xpose_bytes(CW)) <= 232448, "shared memory per CTA");
   SA_CUDA(cudaFuncSetAttribute(tc::gemm_kernel<Epi, EW, CW, FP4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               tc::smem_of(EW, CW, FP4)));
+                               tc::smem_of(EW, CW, FP4, Epi::TAB_BYTES, Epi::xpose_bytes(CW))));
   return SA_OK;
 }
 template <class Epi, int EW, int CW, bool FP4>
@@ -631,7 +780,7 @@ static void tc_gemm(int64_t grid, const tc::Batch& batch, const tc::Maps& maps, 
   static_assert(sizeof k == sizeof epi, "epilogue layouts");
   std::memcpy(&k, &epi, sizeof k);
   tc::gemm_kernel<Epi, EW, CW, FP4>
-      <<<(unsigned)grid, tc::threads_of(EW), tc::smem_of(EW, CW, FP4), st>>>(batch, maps, tiles, k);
+      <<<(unsigned)grid, tc::threads_of(EW), tc::smem_of(EW, CW, FP4, Epi::TAB_BYTES, Epi::xpose_bytes(CW)), st>>>(batch, maps, tiles, k);
 }
 // the (epilogue mode, geometry) instantiations a launch can pick
 template <bool FP4>
@@ -641,7 +790,7 @@ static sa_status tc_configure_all() {
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_KEYS>, 8, CW_ALL, FP4>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM>, 16, 16, FP4>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4>();
-  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_ALL>, 8, CW_ALL, FP4>();
+  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_KEYS | EPI_NUM>, 8, CW_ALL, FP4>();
   return cs;
 }
 template <bool FP4>
@@ -656,7 +805,7 @@ static void tc_gemm_mode(int mode, bool keys16, int64_t grid, const tc::Batch& b
   else if (mode == EPI_NUM) tc_gemm<KeyMatEpi<EPI_NUM>, 16, 16, FP4>(grid, batch, maps, tiles, epi, st);
   else if ((mode & EPI_KEYS) == 0)
     tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4>(grid, batch, maps, tiles, epi, st);
-  else tc_gemm<KeyMatEpi<EPI_ALL>, 8, CW_ALL, FP4>(grid, batch, maps, tiles, epi, st);
+  else tc_gemm<KeyMatEpi<EPI_KEYS | EPI_NUM>, 8, CW_ALL, FP4>(grid, batch, maps, tiles, epi, st);   // never with F
 }
 
 static sa_status tc_encode_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int box_rows, int64_t rowb) {
@@ -770,6 +919,11 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     int mode = 0;
     epi.state = state;
     int64_t tiles = 0;
+    // keys and F in one launch would need both column tables: F then goes
+    // through the F pass (numerators in the epilogue, ratio_kernel after)
+    bool any_keys = false;
+    for (int q = 0; q < np; ++q) any_keys = any_keys || probs[i0 + q].keyA;
+    const bool fpass_here = fpass || any_keys;
     for (int q = 0; q < np; ++q) {
       const MsProblem& P = probs[i0 + q];
       tc::Problem& T = batch.p[q];
@@ -795,8 +949,8 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       // S5's F: in the tensor-core epilogue (default), or (SA_K2T_FPASS=1) numerators
       // there and F by ratio_kernel after
       E.num = P.num;
-      E.sim = fpass ? nullptr : P.sim;
-      if (fpass && P.sim && !P.num) {
+      E.sim = fpass_here ? nullptr : P.sim;
+      if (fpass_here && P.sim && !P.num) {
         E.num = scratch.alloc<uint16_t>((size_t)P.na * P.ld);
         if (!E.num) return fail(SA_E_NOMEM, "scratch allocation of K2T numerators failed");
       }
@@ -827,7 +981,7 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     SA_LAUNCHED();
     for (int q = 0; q < np; ++q) {
       const MsProblem& P = probs[i0 + q];
-      if (fpass && P.sim) SA_TRY(ratio_launch(epi.e[q].num, P.nkA, P.nkB, P.na, P.nb, P.ld, P.sim, st, state));
+      if (fpass_here && P.sim) SA_TRY(ratio_launch(epi.e[q].num, P.nkA, P.nkB, P.na, P.nb, P.ld, P.sim, st, state));
     }
     i0 = i1;
   }

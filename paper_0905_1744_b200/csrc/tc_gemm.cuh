@@ -51,20 +51,17 @@ struct Geo {
 static_assert(Geo<true>::STAGE_BYTES % 1024 == 0 && Geo<false>::STAGE_BYTES % 1024 == 0, "stage alignment");
 // Epilogue geometry (template parameters of gemm_kernel): EW epilogue warps
 // (a multiple of 4: warp w reads TMEM lanes 32 (w % 4) .. and the w / 4-th
-// column slice), CW columns per tcgen05.ld chunk (16 or 32), a padded
-// 32 x CW transpose buffer per epilogue warp.
+// column slice of SLICE columns), CW columns per tcgen05.ld chunk (16 or 32).
+// Each epilogue warp owns TB bytes of shared memory per slice column
+// (Epi::TAB_BYTES: the per-tile column tables the epilogue stages before the
+// accumulator is ready) plus XB scratch bytes (Epi::xpose_bytes(CW)).
 __host__ __device__ constexpr int threads_of(int EW) { return (EW + 2) * 32; }
-// 32 x 32 chunks: rows padded to 33 words; 32 x 16 chunks: unpadded rows,
-// columns XOR-swizzled by the row (xpose_at) -- keeps the 16-warp layout
-// inside the 227 KB shared-memory limit.
-__host__ __device__ constexpr int xpose_words(int CW) { return CW == 32 ? 32 * 33 : 32 * CW; }
-template <int CW>
-__device__ __forceinline__ int xpose_at(int row, int col) {
-  if constexpr (CW == 32) return row * 33 + col;
-  else return row * CW + (col ^ (row & (CW - 1)));
+__host__ __device__ constexpr int slice_of(int EW, int CW, bool FP4) {
+  return (((FP4 ? 240 : 256) / (EW / 4) + CW - 1) / CW) * CW;
 }
-__host__ __device__ constexpr int smem_of(int EW, int CW, bool FP4) {
-  return STAGES * (FP4 ? Geo<true>::STAGE_BYTES : Geo<false>::STAGE_BYTES) + 1024 + 256 + EW * xpose_words(CW) * 4;
+__host__ __device__ constexpr int smem_of(int EW, int CW, bool FP4, int TB, int XB) {
+  return STAGES * (FP4 ? Geo<true>::STAGE_BYTES : Geo<false>::STAGE_BYTES) + 1024 + 256 +
+         EW * (slice_of(EW, CW, FP4) * TB + XB);
 }
 constexpr int MAXPROB = 16;
 
@@ -291,11 +288,16 @@ __device__ __forceinline__ Tile decode(const Batch& b, int64_t tile) {
 // Epi (const, a kernel parameter) must provide a per-thread `State` and
 //   __device__ bool skip() const;                                  // device-side dispatch guard
 //   __device__ void begin(State&, const Tile&, int row) const;     // per thread, per tile
+//   static constexpr int TAB_BYTES;                                // table bytes per slice column
+//   __device__ void begin(State&, const Tile&, int row, int lane, int cbeg, int cend,
+//                         uint8_t* tab) const;                       // before the accumulator wait
 //   template <int CW> __device__ void chunk(State&, const Tile&, int row, int col, const uint32_t (&v)[CW],
-//                         int lane, uint32_t* xpose) const;        // all 32 lanes, converged
+//                         int lane, const uint8_t* tab, int tj, uint8_t* xp) const;   // all lanes, converged
 //   __device__ void end(State&, const Tile&, int row) const;
-// row = tile row of this thread (0..127), col = first tile column of the chunk,
-// xpose = this warp's 32 x (CW + 1) word shared-memory scratch.
+// row = tile row of this thread (0..127), [cbeg, cend) = the warp's column
+// slice of the tile, col = first tile column of the chunk, tab = the warp's
+// table (TAB_BYTES x SLICE bytes, 16-byte aligned), tj = col - cbeg, xp = the
+// warp's xpose_bytes(CW) scratch.
 template <class Epi, int EW, int CW, bool FP4>
 __global__ void __launch_bounds__(threads_of(EW), 1)
 gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps maps, int64_t total_tiles, Epi epi) {
@@ -313,7 +315,7 @@ gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps ma
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint32_t* xpose_all = reinterpret_cast<uint32_t*>(smem + STAGES * STAGE_BYTES + 256);
+  uint8_t* tab_all = smem + STAGES * STAGE_BYTES + 256;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == EPI_WARPS && lane == 0) {
@@ -396,26 +398,29 @@ gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps ma
     // ------------------------------------------------ epilogue warps
     const int quad = warp & 3, part = warp >> 2;
     const int row = quad * 32 + lane;
-    uint32_t* xpose = xpose_all + warp * xpose_words(CW);
-    // columns per epilogue warp: a multiple of CW; the last slice may be shorter
-    constexpr int SLICE = ((BN / (EW / 4) + CW - 1) / CW) * CW;
+    constexpr int SLICE = slice_of(EW, CW, FP4);
+    constexpr int XB = Epi::xpose_bytes(CW);
+    uint8_t* tab = tab_all + warp * (SLICE * Epi::TAB_BYTES + XB);
+    uint8_t* xp = tab + SLICE * Epi::TAB_BYTES;
+    const int cbeg = part * SLICE, cend = min(cbeg + SLICE, BN);
     typename Epi::State es;
     int64_t lt = 0;
     for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
       const Tile T = decode<BN>(batch, tile);
       const int buf = (int)(lt & 1);
+      epi.begin(es, T, row, lane, cbeg, cend, tab);   // row state and column tables while the MMA runs
       bar_wait(&tfull[buf], (uint32_t)((lt >> 1) & 1));
       fence_after();
-      epi.begin(es, T, row);
 #pragma unroll 1
-      for (int col = part * SLICE; col < min(part * SLICE + SLICE, BN); col += CW) {
+      for (int col = cbeg; col < cend; col += CW) {
         uint32_t v[CW];
         tmem_ld<CW>(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + col), v);
         if constexpr (FP4) {
+          // exact integer-valued f32 sums (< 2^23): add 2^23, keep the mantissa
 #pragma unroll
-          for (int j = 0; j < CW; ++j) v[j] = (uint32_t)__uint_as_float(v[j]);   // exact integer sums
+          for (int j = 0; j < CW; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + 8388608.0f) & 0x7FFFFFu;
         }
-        epi.template chunk<CW>(es, T, row, col, v, lane, xpose);
+        epi.template chunk<CW>(es, T, row, col, v, lane, tab, col - cbeg, xp);
       }
       fence_before();
       __syncwarp();

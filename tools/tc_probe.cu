@@ -22,10 +22,13 @@ struct WriteEpi {
   int32_t* C;
   int64_t ldc;
   struct State {};
+  static constexpr int TAB_BYTES = 16;
+  __host__ __device__ static constexpr int xpose_bytes(int) { return 0; }
   __device__ bool skip() const { return false; }
-  __device__ void begin(State&, const Tile&, int) const {}
+  __device__ void begin(State&, const Tile&, int, int, int, int, uint8_t*) const {}
   template <int CW>
-  __device__ void chunk(State&, const Tile& T, int row, int col, const uint32_t (&v)[CW], int, uint32_t*) const {
+  __device__ void chunk(State&, const Tile& T, int row, int col, const uint32_t (&v)[CW], int, const uint8_t*,
+                        int, uint8_t*) const {
     if (row >= T.ra) return;
     const int pi = T.pi;
     int32_t* out = C + (int64_t)pi * 0 + (int64_t)(T.row0 + row) * ldc + T.col0 + col;
@@ -93,10 +96,10 @@ int main(int argc, char** argv) {
   const int64_t tiles = problem_tiles<Geo<false>::BN>(M, Nb, sym);
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-  CK(cudaFuncSetAttribute(gemm_kernel<WriteEpi, 8, 32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_of(8, 32, false)));
+  CK(cudaFuncSetAttribute(gemm_kernel<WriteEpi, 8, 32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_of(8, 32, false, 16, 0)));
   WriteEpi epi{dC, Nb};
   const int grid = (int)(tiles < sms ? tiles : sms);
-  gemm_kernel<WriteEpi, 8, 32, false><<<grid, threads_of(8), smem_of(8, 32, false)>>>(batch, maps, tiles, epi);
+  gemm_kernel<WriteEpi, 8, 32, false><<<grid, threads_of(8), smem_of(8, 32, false, 16, 0)>>>(batch, maps, tiles, epi);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   std::vector<int32_t> C((size_t)M * Nb);
@@ -122,7 +125,7 @@ int main(int argc, char** argv) {
   CK(cudaEventCreate(&e1));
   const int reps = 5;
   CK(cudaEventRecord(e0));
-  for (int r = 0; r < reps; ++r) gemm_kernel<WriteEpi, 8, 32, false><<<grid, threads_of(8), smem_of(8, 32, false)>>>(batch, maps, tiles, epi);
+  for (int r = 0; r < reps; ++r) gemm_kernel<WriteEpi, 8, 32, false><<<grid, threads_of(8), smem_of(8, 32, false, 16, 0)>>>(batch, maps, tiles, epi);
   CK(cudaEventRecord(e1));
   CK(cudaEventSynchronize(e1));
   float ms = 0;
