@@ -285,6 +285,7 @@ def main():
         "partition_S2a_to_S4": part_ms,
         "S1_received": med(lambda ev, ph: ev["S4"].elapsed_time(ev["S1b"])),
         "S5": s5_ms,
+        "S5_gemm": med(lambda ev, ph: ph["gemm"]),
     }
     part_ms_max = max_over_ranks(part_ms)
     s5_ms_max = max_over_ranks(s5_ms)
@@ -301,29 +302,43 @@ def main():
         # K2T: the S5 buckets as exact 0/1 threshold-layer
         # contractions on the tensor cores; algorithmic work = 2 K'_b ops per
         # pair (K'_b = kept layer columns of bucket b, read back after the timed
-        # region by re-running each bucket once) against the u8 tensor peak.
+        # region by re-running each bucket once) against the tensor peak of the
+        # operand format, over the GEMM kernel's own CUDA-event time (median
+        # over the timed steps, SA_PHASE_GEMM); the whole S5 phase (operand
+        # build + GEMM) is reported beside it.
         nz = [(b, row, n_b) for b, row, n_b in out.buckets if n_b > 0]
-        B.sa_bucket_similarity_batch(ctx, out.bucket_profiles, out.bucket_nkmers,
-                                     [r for _, r, _ in out.buckets] + [sum(n for _, _, n in out.buckets)],
-                                     hp.bins, numerators=out.numerators, similarity=out.similarity)
+        rb_s5 = [r for _, r, _ in out.buckets] + [sum(n for _, _, n in out.buckets)]
+        B.sa_bucket_similarity_batch(ctx, out.bucket_profiles, out.bucket_nkmers, rb_s5, hp.bins,
+                                     numerators=out.numerators, similarity=out.similarity)
         kcols = dict(zip([b for b, _, _ in nz], ctx.tc_columns()))
+        operand = ctx.tc_operand()
         ops = sum(2.0 * kcols[b] * int(sizes[b]) * (int(sizes[b]) - 1) / 2 for b in kcols)
         bf16 = float(peaks.get("bf16_tflops", 1590.0))
-        peak = 2.0 * bf16 * 1e12          # u8 dense = 2 x bf16 dense (4.5 / 2.25 PF nominal)
-        achieved = ops / (s5_ms / 1e3)
+        ratio = 4.0 if operand == "e2m1" else 2.0   # nominal dense 9 (fp4) / 4.5 (int8) vs 2.25 (bf16) PF
+        peak = ratio * bf16 * 1e12
+        gemm_ms = phases["S5_gemm"]
+        achieved = ops / (gemm_ms / 1e3)
         tpath = os.path.join(ROOT, "profiles", "k2t_traffic.json")
         if os.path.exists(tpath):
             with open(tpath) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
-        roof = {"bound": "tensor", "kernel": "tc::gemm_kernel<KeyMatEpi> (K2T, S5 bucket matrices)",
-                "engine": engine, "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TOP/s",
+                tj = json.load(f)
+            if tj.get("operand", "u8") == operand:
+                traffic = tj.get("dram_bytes_per_launch")
+        roof = {"bound": "tensor", "kernel": f"tc::gemm_kernel<KeyMatEpi<NUM|SIM>> (K2T, {operand} operands, "
+                                             f"S5 bucket matrices, one launch per step)",
+                "engine": engine, "operand": operand,
+                "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TOP/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "peak_source": (f"{peak_src} bf16_tflops {bf16:.1f} (burst, MEASURED_PEAKS.json) x 2 = u8 dense "
-                                f"(nominal 4.5 / 2.25 PF ratio)"),
+                "kernel_ms": gemm_ms,
+                "peak_source": (f"{peak_src} bf16_tflops {bf16:.1f} (burst, MEASURED_PEAKS.json) x {ratio:.0f} = "
+                                f"{'e2m1 (kind::mxf4)' if operand == 'e2m1' else 'u8 (kind::i8)'} dense "
+                                f"(nominal {'9' if operand == 'e2m1' else '4.5'} / 2.25 PF ratio)"),
                 "algorithmic": (f"2 K'_b ops per pair, K'_b = kept threshold-layer columns "
-                                f"{[kcols[b] for b in sorted(kcols)]} x {my_s5_pairs} pairs / S5 phase CUDA-event "
-                                f"time (includes the operand build kernels)"),
-                "binops_per_s_equiv": my_s5_pairs * EPS_BINS / (s5_ms / 1e3) / 1e12}
+                                f"{[kcols[b] for b in sorted(kcols)]} x {my_s5_pairs} pairs / the GEMM kernel's "
+                                f"CUDA-event time"),
+                "phase_achieved": ops / (s5_ms / 1e3) / 1e12,
+                "phase_frac": ops / (s5_ms / 1e3) / peak,
+                "binops_per_s_equiv": my_s5_pairs * EPS_BINS / (gemm_ms / 1e3) / 1e12}
     else:
         per_clk = BINOPS_PER_SM_CLK[engine]
         peak_binops = per_clk * nsm * sm_mhz_peak * 1e6
@@ -412,7 +427,9 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None,
-            "dtype": {"tc": "u8 (0/1 threshold layers, s32 accumulate)", "u8": "u8"}.get(engine, "u16"),
+            "dtype": (("e2m1 (0/1 threshold layers, f32 accumulate, exact)" if ctx.tc_operand() == "e2m1"
+                       else "u8 (0/1 threshold layers, s32 accumulate)") if engine == "tc"
+                      else {"u8": "u8"}.get(engine, "u16")),
             "data": "synthetic (seeded star-phylogeny protein families, sa_synth)",
             "config": {"workload": workload_desc(cfg), "N": ds.n, "p": cfg.p,
                        "samples_per_block": cfg.samples_per_block, "k": cfg.k, "alphabet": cfg.alphabet,

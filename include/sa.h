@@ -101,7 +101,8 @@ enum {
   SA_PHASE_S3 = 4,       /* block sort, regular samples, pivots, bucket assign  */
   SA_PHASE_S5 = 5,       /* last sa_bucket_similarity min-sum launch            */
   SA_PHASE_RANK = 6,     /* last sa_kmer_rank min-sum launch                    */
-  SA_PHASE_COUNT = 7
+  SA_PHASE_GEMM = 7,     /* the tensor-core GEMM kernel alone of the last K2T launch */
+  SA_PHASE_COUNT = 8
 };
 sa_status sa_ctx_set_timing(sa_ctx* ctx, int enable);
 /* Operand encoding of the last min-sum launch on this context:
@@ -126,6 +127,11 @@ int32_t sa_ctx_tc_columns(const sa_ctx* ctx, int32_t* cols_h, int32_t max);
  * with IEEE round-to-nearest division for every 0 <= C <= D <= 65535 on
  * `cuda_device` and returns the number of mismatches (expected 0). */
 sa_status sa_selftest_f_division(int32_t cuda_device, int64_t* mismatches_h);
+/* K2T operand format of this library: 1 = packed e2m1 0/1.0
+ * columns on tcgen05 kind::mxf4 (default), 0 = u8 0/1 columns on kind::i8
+ * (environment SA_K2T_FP4=0); -1 when the context has not launched K2T.
+ * Both are exact. */
+int sa_ctx_tc_operand(const sa_ctx* ctx);
 sa_status sa_ctx_phase_ms(sa_ctx* ctx, float* ms_h /* [SA_PHASE_COUNT] */);
 
 /* Rank form used by sa_kmer_rank and sa_partition on this context.
@@ -259,11 +265,16 @@ sa_status sa_bucket_similarity(sa_ctx* ctx, const uint16_t* profiles, const int3
  * sa_redistribute produces: buckets contiguous, members ascending by global
  * id); its outputs are numerators_h[b] / similarity_h[b] (host arrays of
  * device pointers, each [n_b][n_b]; the arrays and any entry are nullable).
+ * ld_h (host, nullable): row stride in elements of bucket b's matrices,
+ * ld_h[b] >= n_b (NULL: n_b, dense); the columns [n_b, ld_h[b]) are not
+ * written.  A multiple of 16 makes every row start on a 32-byte sector, so
+ * the epilogue's stores are whole sectors (no partial-sector merges in L2).
  * Empty buckets are skipped.  SA_E_INVAL: nbuckets < 0, row_begin_h not
- * non-decreasing from 0, bad bins, NULL profiles / nkmers with rows. */
+ * non-decreasing from 0, bad bins, NULL profiles / nkmers with rows,
+ * ld_h[b] < n_b. */
 sa_status sa_bucket_similarity_batch(sa_ctx* ctx, int32_t nbuckets, const uint16_t* profiles, const int32_t* nkmers,
                                      const int64_t* row_begin_h, int32_t bins, uint16_t* const* numerators_h,
-                                     double* const* similarity_h, void* stream);
+                                     double* const* similarity_h, const int64_t* ld_h, void* stream);
 
 #ifdef __cplusplus
 }

@@ -21,12 +21,12 @@ LIB_PATH = os.path.join(_PKG, "lib", "libsa.so")
 SA_OK, SA_E_INVAL, SA_E_RANGE, SA_E_CUDA, SA_E_COMM, SA_E_NOMEM, SA_E_STATE = range(7)
 STATUS_NAMES = {0: "SA_OK", 1: "SA_E_INVAL", 2: "SA_E_RANGE", 3: "SA_E_CUDA", 4: "SA_E_COMM",
                 5: "SA_E_NOMEM", 6: "SA_E_STATE"}
-PHASES = ["S2a", "S2b", "S2c", "S2d", "S3", "S5", "rank"]
+PHASES = ["S2a", "S2b", "S2c", "S2d", "S3", "S5", "rank", "gemm"]
 
 EXPORTED = ["sa_ctx_create", "sa_ctx_attach_comm", "sa_ctx_destroy", "sa_last_error", "sa_launch_count",
             "sa_ctx_set_timing", "sa_ctx_phase_ms", "sa_profile_stride", "sa_kmer_profiles", "sa_kmer_rank",
             "sa_partition", "sa_redistribute", "sa_bucket_similarity", "sa_exact_rank_compare", "sa_ctx_engine",
-            "sa_ctx_set_rank_form", "sa_ctx_tc_columns", "sa_selftest_f_division",
+            "sa_ctx_set_rank_form", "sa_ctx_tc_columns", "sa_ctx_tc_operand", "sa_selftest_f_division",
             "sa_bucket_similarity_batch"]
 SA_RANK_F, SA_RANK_DF = 0, 1
 
@@ -96,10 +96,12 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "sa_bucket_similarity": (ctypes.c_int, [P, P, P, I32, I32, P, P, VP]),
         "sa_bucket_similarity_batch": (ctypes.c_int, [P, I32, P, P, ctypes.POINTER(ctypes.c_int64), I32,
                                                       ctypes.POINTER(ctypes.c_void_p),
-                                                      ctypes.POINTER(ctypes.c_void_p), VP]),
+                                                      ctypes.POINTER(ctypes.c_void_p),
+                                                      ctypes.POINTER(ctypes.c_int64), VP]),
         "sa_exact_rank_compare": (ctypes.c_int, [P, I32, P, I32, P, I32]),
         "sa_ctx_engine": (ctypes.c_int, [P]),
         "sa_ctx_tc_columns": (ctypes.c_int32, [P, P, ctypes.c_int32]),
+        "sa_ctx_tc_operand": (ctypes.c_int, [P]),
         "sa_selftest_f_division": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(ctypes.c_int64)]),
         "sa_ctx_set_rank_form": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_double]),
     }
@@ -191,6 +193,10 @@ class Context:
     def engine(self) -> str:
         """Operand encoding of the last min-sum launch ('u16', 'u8', 'u16imad')."""
         return {0: "u16", 1: "u8", 2: "u16imad", 4: "tc"}.get(int(load_library().sa_ctx_engine(self.handle)), "none")
+
+    def tc_operand(self) -> str:
+        """K2T operand format: 'e2m1' (kind::mxf4, default) or 'u8' (kind::i8); 'none' before any K2T call."""
+        return {0: "u8", 1: "e2m1"}.get(int(load_library().sa_ctx_tc_operand(self.handle)), "none")
 
     def tc_columns(self) -> list[int]:
         """K2T only: kept threshold-layer columns K' of each problem of the last
@@ -364,28 +370,53 @@ def sa_bucket_similarity(ctx: Context, profiles, nkmers, bins: int = 8000, want_
     return numerators, similarity
 
 
+def padded_matrix(n: int, dtype, device, ld_align: int = 1):
+    """An n x n view (row stride ld = n rounded up to ld_align) of an n x ld
+    allocation: the padded layout sa_bucket_similarity_batch writes when
+    given ld (whole 32-byte store sectors for ld_align = 16)."""
+    ld = -(-n // ld_align) * ld_align
+    return torch.empty((n, ld), dtype=dtype, device=device)[:, :n]
+
+
+def _row_stride(t, n):
+    if t is None:
+        return None
+    if t.dim() != 2 or t.shape[0] != n or t.shape[1] != n or t.stride(1) != 1 or t.stride(0) < n:
+        raise ValueError("bucket matrix must be n x n with unit column stride")
+    return t.stride(0)
+
+
 def sa_bucket_similarity_batch(ctx: Context, profiles, nkmers, row_begin, bins: int = 8000,
                                want_numerators: bool = True, want_similarity: bool = True,
-                               numerators=None, similarity=None, stream=None):
+                               numerators=None, similarity=None, stream=None, ld_align: int = 1):
     """S5 over several buckets in one call: bucket b = rows [row_begin[b],
     row_begin[b+1]).  Returns (list of numerators | None, list of similarity | None),
-    one entry per bucket (None for empty buckets or when not wanted)."""
+    one entry per bucket (None for empty buckets or when not wanted).  Given or
+    allocated matrices may be padded n x n views (row stride >= n, see
+    padded_matrix; both of a bucket must share the stride)."""
     _dev(profiles, torch.uint16, "profiles")
     _dev(nkmers, torch.int32, "nkmers")
     nb = len(row_begin) - 1
     dev = nkmers.device
     sizes = [int(row_begin[b + 1]) - int(row_begin[b]) for b in range(nb)]
     if numerators is None:
-        numerators = [torch.empty((n, n), dtype=torch.uint16, device=dev) if want_numerators and n else None
+        numerators = [padded_matrix(n, torch.uint16, dev, ld_align) if want_numerators and n else None
                       for n in sizes]
     if similarity is None:
-        similarity = [torch.empty((n, n), dtype=torch.float64, device=dev) if want_similarity and n else None
+        similarity = [padded_matrix(n, torch.float64, dev, ld_align) if want_similarity and n else None
                       for n in sizes]
+    lds = []
+    for n, t_num, t_sim in zip(sizes, numerators, similarity):
+        a, b_ = _row_stride(t_num, n), _row_stride(t_sim, n)
+        if a is not None and b_ is not None and a != b_:
+            raise ValueError("numerators and similarity of a bucket must share the row stride")
+        lds.append(a if a is not None else (b_ if b_ is not None else n))
     rb = (ctypes.c_int64 * (nb + 1))(*[int(x) for x in row_begin])
+    ldh = (ctypes.c_int64 * max(nb, 1))(*lds)
     nums = (ctypes.c_void_p * max(nb, 1))(*[(t.data_ptr() if t is not None else None) for t in numerators])
     sims = (ctypes.c_void_p * max(nb, 1))(*[(t.data_ptr() if t is not None else None) for t in similarity])
     _check(load_library().sa_bucket_similarity_batch(ctx.handle, nb, _ptr(profiles), _ptr(nkmers), rb, bins,
-                                                     nums, sims, _stream(stream)))
+                                                     nums, sims, ldh, _stream(stream)))
     return numerators, similarity
 
 

@@ -171,6 +171,9 @@ static sa_status prepare_ops(sa_ctx* c, Scratch& scratch, const uint16_t* A16, i
   return SA_OK;
 }
 
+static inline cudaEvent_t ev_begin(sa_ctx* c, int ph);
+static inline cudaEvent_t ev_end(sa_ctx* c, int ph);
+
 // Enqueue the problems (A / B pointers given into the u16 operands).
 static sa_status launch_ops(sa_ctx* c, const EngineOps& E, const std::vector<MsProblem>& probs16, cudaStream_t st,
                             cudaEvent_t ev0, cudaEvent_t ev1) {
@@ -182,7 +185,8 @@ static sa_status launch_ops(sa_ctx* c, const EngineOps& E, const std::vector<MsP
   SA_CUDA(cudaMemsetAsync(E.guard + 2, E.tc ? 1 : 0, sizeof(uint32_t), st));
   if (E.tc) {
     c->last_tc_probs = (int)probs16.size();
-    SA_TRY(tc_launch(probs16, E.a16.ldw, E.bins, E.guard, E.guard + SA_TC_COLS_AT, st, nullptr, nullptr));
+    SA_TRY(tc_launch(probs16, E.a16.ldw, E.bins, E.guard, E.guard + SA_TC_COLS_AT, st, ev_begin(c, SA_PHASE_GEMM),
+                     ev_end(c, SA_PHASE_GEMM)));
     for (const auto& cv : E.conv)
       SA_TRY(to_u8_launch(cv.p16, cv.n, stride_u16(E.bins), E.bins, cv.p8, stride_u8(E.bins), E.guard, st, true));
   }
@@ -308,6 +312,11 @@ int sa_ctx_engine(const sa_ctx* ctx) {
   }
   if (ctx->hpinned[2] && !ctx->hpinned[1]) return ENC_TC;
   return ctx->hpinned[0] <= 255 ? ENC_U8_SAD : ENC_U16_MIN;
+}
+
+int sa_ctx_tc_operand(const sa_ctx* ctx) {
+  if (!ctx || !ctx->last_tc) return -1;
+  return tc_fp4_operands() ? 1 : 0;
 }
 
 int32_t sa_ctx_tc_columns(const sa_ctx* ctx, int32_t* cols_h, int32_t max) {
@@ -1035,7 +1044,7 @@ sa_status sa_bucket_similarity(sa_ctx* ctx, const uint16_t* profiles, const int3
 
 sa_status sa_bucket_similarity_batch(sa_ctx* ctx, int32_t nbuckets, const uint16_t* profiles, const int32_t* nkmers,
                                      const int64_t* row_begin_h, int32_t bins, uint16_t* const* numerators_h,
-                                     double* const* similarity_h, void* stream) {
+                                     double* const* similarity_h, const int64_t* ld_h, void* stream) {
   g_err.clear();
   if (!ctx) return fail(SA_E_INVAL, "ctx is NULL");
   if (nbuckets < 0 || bins < 1 || bins > 65536) return fail(SA_E_INVAL, "bad nbuckets / bins");
@@ -1045,6 +1054,7 @@ sa_status sa_bucket_similarity_batch(sa_ctx* ctx, int32_t nbuckets, const uint16
   for (int b = 0; b < nbuckets; ++b) {
     if (row_begin_h[b + 1] < row_begin_h[b]) return fail(SA_E_INVAL, "row_begin_h must be non-decreasing");
     if (row_begin_h[b + 1] - row_begin_h[b] > INT32_MAX) return fail(SA_E_INVAL, "bucket too large");
+    if (ld_h && ld_h[b] < row_begin_h[b + 1] - row_begin_h[b]) return fail(SA_E_INVAL, "ld_h[b] < bucket size");
   }
   const int64_t n = row_begin_h[nbuckets];
   if (n == 0) return SA_OK;
@@ -1065,7 +1075,7 @@ sa_status sa_bucket_similarity_batch(sa_ctx* ctx, int32_t nbuckets, const uint16
     pr.sym = 1;
     pr.num = numerators_h ? numerators_h[b] : nullptr;
     pr.sim = similarity_h ? similarity_h[b] : nullptr;
-    pr.ld = nb;
+    pr.ld = ld_h ? ld_h[b] : nb;
     probs.push_back(pr);
   }
   SA_TRY(launch_ops(ctx, E, probs, st, ev_begin(ctx, SA_PHASE_S5), ev_end(ctx, SA_PHASE_S5)));

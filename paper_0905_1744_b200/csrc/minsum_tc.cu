@@ -429,6 +429,12 @@ __device__ __forceinline__ uint64_t key_term_lo(uint32_t C, uint32_t rl, uint32_
   return p + q;
 }
 
+// the d^F term out of line: its log keeps registers the F-form fast path needs
+__device__ __noinline__ void dF_term_outlined(uint64_t& lo, uint32_t& hi, uint32_t C, uint32_t D, double delta,
+                                              double ln1pd) {
+  add_dF_term(lo, hi, C, D, delta, ln1pd);
+}
+
 // MODE: which outputs this instantiation can write (EPI_KEYS | EPI_NUM |
 // EPI_SIM); a launch picks the smallest one covering its problems, so the
 // key path and the matrix path each get their own register allocation.
@@ -601,7 +607,7 @@ struct KeyMatEpi {
             if (s.rv && cv && (!sym || gc >= s.row_g)) {
               if (E.form == SA_RANK_DF) {
                 const int nkc0 = max((int)k.w, 0);
-                add_dF_term(lo, hi, C, (uint32_t)min(s.nk0, nkc0), E.delta, E.ln1pd);
+                dF_term_outlined(lo, hi, C, (uint32_t)min(s.nk0, nkc0), E.delta, E.ln1pd);
               } else {
                 fterm(s, k, C, lo, hi);
               }
@@ -616,33 +622,39 @@ struct KeyMatEpi {
       }
     }
 
-    if (MATS && (E.num || E.sim)) {
-      const bool want_num = (MODE & EPI_NUM) && E.num;
-      const bool want_sim = SIM && E.sim;
-      if (upper && ncols == CW) {
-        // ---- fast path.  (1) lanes = rows: F of every pair, the mirrored
-        // element (gc, row) stored with lanes = consecutive rows (coalesced),
-        // C staged in the warp's 32 x CW uint16 transpose buffer (16-byte
-        // units XOR-swizzled by the row: conflict-free both ways).
+    if constexpr (MATS) {
+      // the host sets num (sim) on every problem of a launch whose MODE has NUM (SIM)
+      constexpr bool want_num = (MODE & EPI_NUM) != 0;
+      constexpr bool want_sim = SIM;
+      const bool rows_all = wrow0 + 32 <= T.row0 + T.ra;   // warp-uniform
+      if (upper && ncols == CW && rows_all) {
+        // ---- fast path (all 32 rows and CW columns exist, no diagonal).
+        // (1) lanes = rows: F of every pair; the mirrored element (gc, row)
+        // with lanes = consecutive rows (coalesced); C staged in the warp's
+        // 32 x CW uint16 transpose buffer (16-byte units XOR-swizzled by the
+        // row: conflict-free both ways).
         constexpr int Q = CW / 8;                          // 16-byte units per buffer row
         constexpr int QSH = CW == 16 ? 2 : 1;              // swizzle: unit ^ ((row >> QSH) % Q)
+        const int64_t ld = E.ld;
+        uint16_t* const num = E.num;
+        double* const sim = E.sim;
         {
+          const int64_t om = (int64_t)c0 * ld + s.row_g;
           uint32_t w[CW / 2];
 #pragma unroll
           for (int j = 0; j < CW; ++j) {
             const uint32_t C = v[j];
             if (j & 1) w[j >> 1] |= C << 16;
             else w[j >> 1] = C;
-            if (sym && s.rv) {
-              const int64_t o = (int64_t)(c0 + j) * E.ld + s.row_g;
-              if (want_num) st_out(E.num + o, (uint16_t)C);
-              if (want_sim) {
+            if (sym) {
+              if constexpr (want_num) st_out(num + om + j * ld, (uint16_t)C);
+              if constexpr (want_sim) {
                 const uint4 k = *reinterpret_cast<const uint4*>(ent + j * TAB_BYTES + YOFF);
                 const int nkc = (int)k.z;
                 const double yc = __hiloint2double((int)k.y, (int)k.x);
                 const int D = min(s.nk, nkc);
                 const double d = __hiloint2double(0x43300000, D) - 4503599627370496.0;
-                st_out(E.sim + o, f_ratio_y(C, d, nkc < s.nk ? yc : s.y));
+                st_out(sim + om + j * ld, f_ratio_y(C, d, nkc < s.nk ? yc : s.y));
               }
             }
           }
@@ -659,28 +671,26 @@ struct KeyMatEpi {
         const int cl = lane % CW;
         int nkc = -1;
         double yc = 0.0;
-        if (want_sim) {
+        if constexpr (want_sim) {
           const uint4 k = *reinterpret_cast<const uint4*>(ent + cl * TAB_BYTES + YOFF);
           nkc = (int)k.z;
           yc = __hiloint2double((int)k.y, (int)k.x);
         }
         constexpr int RPP = 32 / CW;
-        const int wrow = s.row_g - lane;
+        const int64_t od = (int64_t)(wrow0 + lane / CW) * ld + c0 + cl;
 #pragma unroll 4
         for (int pss = 0; pss < CW; ++pss) {
           const int i = pss * RPP + lane / CW;              // buffer row = warp row
-          const int nk_i = __shfl_sync(0xffffffffu, s.nk, i);
-          const double y_i = __shfl_sync(0xffffffffu, s.y, i);
-          const bool rv_i = __shfl_sync(0xffffffffu, (int)s.rv, i) != 0;
           const int qs = (cl >> 3) ^ ((i >> QSH) & (Q - 1));
           const uint32_t C = *reinterpret_cast<const uint16_t*>(xp + i * (CW * 2) + qs * 16 + (cl & 7) * 2);
-          if (!rv_i) continue;
-          const int64_t o = (int64_t)(wrow + i) * E.ld + c0 + cl;
-          if (want_num) st_out(E.num + o, (uint16_t)C);
-          if (want_sim) {
+          const int64_t o = od + (int64_t)(pss * RPP) * ld;
+          if constexpr (want_num) st_out(num + o, (uint16_t)C);
+          if constexpr (want_sim) {
+            const int nk_i = __shfl_sync(0xffffffffu, s.nk, i);
+            const double y_i = __shfl_sync(0xffffffffu, s.y, i);
             const int D = min(nk_i, nkc);
             const double d = __hiloint2double(0x43300000, D) - 4503599627370496.0;
-            st_out(E.sim + o, f_ratio_y(C, d, nkc < nk_i ? yc : y_i));
+            st_out(sim + o, f_ratio_y(C, d, nkc < nk_i ? yc : y_i));
           }
         }
         __syncwarp();
@@ -789,6 +799,7 @@ static sa_status tc_configure_all() {
   sa_status cs = tc_configure<KeyMatEpi<EPI_KEYS>, 16, 16, FP4>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_KEYS>, 8, CW_ALL, FP4>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM>, 16, 16, FP4>();
+  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_SIM>, 16, 16, FP4>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_KEYS | EPI_NUM>, 8, CW_ALL, FP4>();
   return cs;
@@ -803,6 +814,7 @@ static void tc_gemm_mode(int mode, bool keys16, int64_t grid, const tc::Batch& b
   if (mode == EPI_KEYS && keys16) tc_gemm<KeyMatEpi<EPI_KEYS>, 16, 16, FP4>(grid, batch, maps, tiles, epi, st);
   else if (mode == EPI_KEYS) tc_gemm<KeyMatEpi<EPI_KEYS>, 8, CW_ALL, FP4>(grid, batch, maps, tiles, epi, st);
   else if (mode == EPI_NUM) tc_gemm<KeyMatEpi<EPI_NUM>, 16, 16, FP4>(grid, batch, maps, tiles, epi, st);
+  else if (mode == EPI_SIM) tc_gemm<KeyMatEpi<EPI_SIM>, 16, 16, FP4>(grid, batch, maps, tiles, epi, st);
   else if ((mode & EPI_KEYS) == 0)
     tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4>(grid, batch, maps, tiles, epi, st);
   else tc_gemm<KeyMatEpi<EPI_KEYS | EPI_NUM>, 8, CW_ALL, FP4>(grid, batch, maps, tiles, epi, st);   // never with F
@@ -842,10 +854,7 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     configured = true;
   }
   const int stride16 = 2 * ldw16;
-  static const bool fp4 = [] {   // SA_K2T_FP4=1: packed e2m1 operands, kind::mxf4 (2x MMA rate)
-    const char* e = getenv("SA_K2T_FP4");
-    return e && atoi(e) != 0;
-  }();
+  const bool fp4 = tc_fp4_operands();
   const int64_t rowb = fp4 ? TC_KCAP / 2 : TC_KCAP;
   const int kbc = fp4 ? 256 : 128;
   static const bool fpass = [] {
@@ -855,7 +864,6 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
   std::vector<MsProblem> probs;
   for (const auto& p : probs_in)
     if (p.na > 0 && p.nb > 0) probs.push_back(p);
-  if (ev0) SA_CUDA(cudaEventRecord(ev0, st));
   size_t i0 = 0;
   while (i0 < probs.size()) {
     const size_t i1 = std::min(probs.size(), i0 + (size_t)tc::MAXPROB);
@@ -961,6 +969,17 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       E.sym = P.sym;
       mode |= (P.keyA ? EPI_KEYS : 0) | (E.num ? EPI_NUM : 0) | (E.sim ? EPI_SIM : 0);
     }
+    // every problem of the launch gets every output its MODE writes (the
+    // epilogue's fast paths test no pointer): scratch for a problem that did
+    // not ask for one (only in mixed batches)
+    for (int q = 0; q < np; ++q) {
+      TcEpiProb& E = epi.e[q];
+      const MsProblem& P = probs[i0 + q];
+      if ((mode & EPI_NUM) && !E.num) E.num = scratch.alloc<uint16_t>((size_t)P.na * P.ld);
+      if ((mode & EPI_SIM) && !E.sim) E.sim = scratch.alloc<double>((size_t)P.na * P.ld);
+      if (((mode & EPI_NUM) && !E.num) || ((mode & EPI_SIM) && !E.sim))
+        return fail(SA_E_NOMEM, "scratch allocation of K2T output matrices failed");
+    }
     batch.n = np;
     static const int group = [] {   // SA_K2T_GROUP: row blocks per group of the tile order
       const char* e = getenv("SA_K2T_GROUP");
@@ -968,6 +987,16 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       return g >= 1 && g <= 64 ? g : 16;
     }();
     batch.group = group;
+    static const int evict_last = [] {   // SA_K2T_EVICT_LAST=0: operand loads without the L2 policy
+      const char* e = getenv("SA_K2T_EVICT_LAST");
+      return e ? atoi(e) : 1;
+    }();
+    batch.evict_last = evict_last;
+    static const int debug = [] {
+      const char* e = getenv("SA_K2T_DEBUG");
+      return e ? atoi(e) : 0;
+    }();
+    batch.debug = debug;
     const int64_t grid = tiles < g_num_sms ? tiles : g_num_sms;
     // 16 epilogue warps x 16-column chunks (more warps to hide the store / F /
     // key-term latency, fewer registers each); keys and matrices together
@@ -976,17 +1005,29 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       const char* e = getenv("SA_K2T_KEYS16");
       return !(e && atoi(e) == 0);
     }();
+    if (ev0) SA_CUDA(cudaEventRecord(ev0, st));   // the GEMM kernel alone (SA_PHASE_GEMM)
     if (fp4) tc_gemm_mode<true>(mode, keys16, grid, batch, maps, tiles, epi, st);
     else tc_gemm_mode<false>(mode, keys16, grid, batch, maps, tiles, epi, st);
     SA_LAUNCHED();
+    if (ev1) SA_CUDA(cudaEventRecord(ev1, st));
     for (int q = 0; q < np; ++q) {
       const MsProblem& P = probs[i0 + q];
       if (fpass_here && P.sim) SA_TRY(ratio_launch(epi.e[q].num, P.nkA, P.nkB, P.na, P.nb, P.ld, P.sim, st, state));
     }
     i0 = i1;
   }
-  if (ev1) SA_CUDA(cudaEventRecord(ev1, st));
   return SA_OK;
+}
+
+// Operand format of K2T: packed e2m1 0/1.0 columns on kind::mxf4 (default: twice
+// the kind::i8 MMA rate, half the operand bytes; exact, tc_gemm.cuh) or u8 0/1
+// columns on kind::i8 (SA_K2T_FP4=0).
+bool tc_fp4_operands() {
+  static const bool fp4 = [] {
+    const char* e = getenv("SA_K2T_FP4");
+    return !(e && atoi(e) == 0);
+  }();
+  return fp4;
 }
 
 sa_status f_division_selftest(int64_t* mismatches_h) {

@@ -95,6 +95,21 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int
           "r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(s_addr(bar))
       : "memory");
 }
+// the same with an L2 eviction-priority policy (createpolicy): operand rows are
+// re-read by many tiles, the output matrices stream past them
+__device__ __forceinline__ void tma_2d_hint(uint32_t dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(s_addr(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t cols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_addr(slot)), "r"(cols));
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -199,7 +214,9 @@ struct Problem {
 struct Batch {
   Problem p[MAXPROB];
   int n;
-  int group;   // GROUP: row blocks per group of the tile order (below)
+  int group;        // GROUP: row blocks per group of the tile order (below)
+  int evict_last;   // operand loads with an L2 evict-last policy
+  int debug;        // experiments only (SA_K2T_DEBUG): 1 no MMA, 2 no TMA loads, 4 no epilogue work
 };
 struct alignas(64) Maps {
   CUtensorMap m[2 * MAXPROB];
@@ -346,6 +363,8 @@ gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps ma
   if (warp == EPI_WARPS) {
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
+      const uint64_t pol = policy_evict_last();
+      const bool hint = batch.evict_last != 0;
       int64_t g = 0;
       for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
         const Tile T = decode<BN>(batch, tile);
@@ -356,10 +375,19 @@ gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps ma
         for (int kb = 0; kb < nkb; ++kb, ++g) {
           const int slot = (int)(g % STAGES);
           if (g >= STAGES) bar_wait(&empty[slot], (uint32_t)(((g / STAGES) - 1) & 1));
+          if (batch.debug & 2) {
+            bar_arrive(&full[slot]);
+            continue;
+          }
           bar_arrive_tx(&full[slot], STAGE_BYTES);
           const uint32_t dst = base_s + slot * STAGE_BYTES;
-          tma_2d(dst, ma, kb * BK, T.row0, &full[slot]);
-          tma_2d(dst + A_BYTES, mb, kb * BK, T.col0, &full[slot]);
+          if (hint) {
+            tma_2d_hint(dst, ma, kb * BK, T.row0, &full[slot], pol);
+            tma_2d_hint(dst + A_BYTES, mb, kb * BK, T.col0, &full[slot], pol);
+          } else {
+            tma_2d(dst, ma, kb * BK, T.row0, &full[slot]);
+            tma_2d(dst + A_BYTES, mb, kb * BK, T.col0, &full[slot]);
+          }
         }
       }
     }
@@ -385,6 +413,7 @@ gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps ma
           const uint64_t da = sw128_desc(sa_), db = sw128_desc(sa_ + A_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / UKB; ++k) {
+            if (batch.debug & 1) break;
             const uint64_t off = (uint64_t)((k * UKB) >> 4);
             if constexpr (FP4) mma_mxf4(d, da + off, db + off, idesc, (kb | k) != 0, sfa, sfb);
             else mma_i8(d, da + off, db + off, idesc, (kb | k) != 0);
@@ -412,7 +441,7 @@ gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps ma
       bar_wait(&tfull[buf], (uint32_t)((lt >> 1) & 1));
       fence_after();
 #pragma unroll 1
-      for (int col = cbeg; col < cend; col += CW) {
+      for (int col = cbeg; col < ((batch.debug & 4) ? cbeg : cend); col += CW) {
         uint32_t v[CW];
         tmem_ld<CW>(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + col), v);
         if constexpr (FP4) {

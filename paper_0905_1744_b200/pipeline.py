@@ -54,7 +54,7 @@ class HotPath:
     when the bucket sizes repeat (the bench re-runs the same workload)."""
 
     def __init__(self, ctx: B.Context, p: int, samples_per_block: int, k: int = 3, alphabet: int = 20,
-                 want_numerators: bool = True, want_similarity: bool = True):
+                 want_numerators: bool = True, want_similarity: bool = True, ld_align: int = 16):
         self.ctx = ctx
         self.p = p
         self.kb = samples_per_block
@@ -63,14 +63,16 @@ class HotPath:
         self.bins = alphabet ** k
         self.want_num = want_numerators
         self.want_sim = want_similarity
+        self.ld_align = ld_align   # row stride of the batch path's bucket matrices (sa.h)
         self._out_cache: dict = {}
 
-    def _outputs(self, b: int, n: int, dev):
-        key = (b, n)
+    def _outputs(self, b: int, n: int, dev, a: int = 1):
+        key = (b, n, a)
         if key not in self._out_cache:
             self._out_cache = {kk: v for kk, v in self._out_cache.items() if kk[0] != b}
-            num = torch.empty((n, n), dtype=torch.uint16, device=dev) if self.want_num else None
-            sim = torch.empty((n, n), dtype=torch.float64, device=dev) if self.want_sim else None
+            # a > 1: padded rows (stride a multiple of a): whole-sector stores in S5 (sa.h)
+            num = B.padded_matrix(n, torch.uint16, dev, a) if self.want_num else None
+            sim = B.padded_matrix(n, torch.float64, dev, a) if self.want_sim else None
             self._out_cache[key] = (num, sim)
         return self._out_cache[key]
 
@@ -104,7 +106,8 @@ class HotPath:
         row = 0
         for b in owned:
             n_b = int(part.counts[:, b].sum())
-            num, sim = self._outputs(b, n_b, offsets.device) if n_b > 0 else (None, None)
+            a = self.ld_align if on_bucket is None else 1   # the per-bucket call writes dense n x n
+            num, sim = self._outputs(b, n_b, offsets.device, a) if n_b > 0 else (None, None)
             res.buckets.append((b, row, n_b))
             res.numerators.append(num)
             res.similarity.append(sim)

@@ -160,17 +160,28 @@ def test_f_division_free_is_ieee_rn(ctx):
     assert B.selftest_f_division(0) == 0
 
 
+@pytest.mark.parametrize("ld_align", [1, 16])
 @pytest.mark.parametrize("sizes", [[0, 300, 1, 129, 0, 257], [2, 0, 0, 3]])
-def test_bucket_similarity_batch(ctx, engine, sizes):
+def test_bucket_similarity_batch(ctx, engine, sizes, ld_align):
     """sa_bucket_similarity_batch: every bucket of a ragged batch (empty ones
-    included) equals the oracle's bucket matrices, in one engine launch."""
+    included) equals the oracle's bucket matrices, in one engine launch; with
+    padded rows (ld = n rounded up to 16) the padding columns stay untouched."""
     n = sum(sizes)
     ds = _rand_set(4242 + n, n, 0, 420, dup=3)
     res, offs = to_dev(ds)
     P, nk = B.sa_kmer_profiles(ctx, res, offs)
     Po, nko = kmer.profiles(ds.residues, ds.offsets)
     rb = np.concatenate([[0], np.cumsum(sizes)])
-    nums, sims = B.sa_bucket_similarity_batch(ctx, P, nk, rb)
+    nums_in = [B.padded_matrix(sz, torch.uint16, "cuda", ld_align) if sz else None for sz in sizes]
+    sims_in = [B.padded_matrix(sz, torch.float64, "cuda", ld_align) if sz else None for sz in sizes]
+    for t in nums_in + sims_in:
+        if t is not None:
+            t.as_strided((t.shape[0], t.stride(0)), (t.stride(0), 1)).fill_(7)
+    nums, sims = B.sa_bucket_similarity_batch(ctx, P, nk, rb, numerators=nums_in, similarity=sims_in)
+    for t in nums + sims:
+        if t is not None and t.stride(0) > t.shape[1]:
+            pad = t.as_strided((t.shape[0], t.stride(0)), (t.stride(0), 1))[:, t.shape[1]:]
+            assert bool((pad == 7).all()), "padding columns written"
     if n > 1:
         assert ctx.engine() == ENGINE_NAME[engine]
     for b, sz in enumerate(sizes):
