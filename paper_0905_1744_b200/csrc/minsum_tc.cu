@@ -74,9 +74,54 @@ __device__ __forceinline__ uint32_t layer_mask(const uint32_t (&v)[16], uint32_t
   return m;
 }
 
+// Row outputs of the operand build (declared here: the histogram pass also
+// writes the first dense layers, below).
+struct TcOut {
+  uint8_t* out[2 * tc::MAXPROB];
+  int prob[2 * tc::MAXPROB];
+};
+
+// 32 layer-mask bits (bin i of the thread's word -> bit i) as operand columns:
+// FP4: 16 bytes, column i = nibble i (e2m1 1.0 = 0b0010); u8: 32 bytes of 0/1.
+template <bool FP4>
+__device__ __forceinline__ void store_mask_columns(uint8_t* dst, uint32_t m, int ncols) {
+  if constexpr (FP4) {
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t x = (m >> (8 * k)) & 0xffu;                // 8 bits -> 8 nibbles
+      x = (x | (x << 12)) & 0x000F000Fu;
+      x = (x | (x << 6)) & 0x03030303u;
+      x = (x | (x << 3)) & 0x11111111u;
+      o[k] = x << 1;
+    }
+    // 8-byte stores: a dense layer of dw (a multiple of 16) columns is a multiple of 8 bytes
+    *reinterpret_cast<uint2*>(dst) = make_uint2(o[0], o[1]);
+    if (ncols >= 32) *reinterpret_cast<uint2*>(dst + 8) = make_uint2(o[2], o[3]);
+  } else {
+    uint32_t o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = (((m >> (4 * k)) & 0xfu) * 0x00204081u) & 0x01010101u;   // 4 bits -> 4 bytes
+    *reinterpret_cast<uint4*>(dst) = make_uint4(o[0], o[1], o[2], o[3]);
+    if (ncols >= 32) *reinterpret_cast<uint4*>(dst + 16) = make_uint4(o[4], o[5], o[6], o[7]);
+  }
+}
+
+// The first TC_SPEC dense layers are written by the histogram pass itself
+// (every bin of the layer, in bin order: the layout the column selection
+// gives a dense layer), so the profile rows are read once for both: the
+// selection later keeps nd dense layers; tc_dense_kernel adds layers
+// TC_SPEC + 1 .. nd when nd > TC_SPEC, and tc_build_kernel overwrites the
+// columns from nd * dw on when nd < TC_SPEC.
+constexpr int TC_SPEC = 2;
+
+template <bool FP4>
 __global__ void __launch_bounds__(TC_HIST_THREADS)
-tc_hist_kernel(const __grid_constant__ TcSides S, int stride16, uint32_t* __restrict__ planes,
-               uint32_t* __restrict__ state) {
+tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut O, int stride16, int bins,
+               uint32_t* __restrict__ planes, uint32_t* __restrict__ state) {
+  constexpr int64_t ROWB = FP4 ? TC_KCAP / 2 : TC_KCAP;
+  const int dw = (bins + 15) & ~15;                      // columns per dense layer
+  const int64_t layer_bytes = FP4 ? dw / 2 : dw;
   extern __shared__ uint32_t deep[];   // [2][TC_LCAP - TC_HREG][TC_WPL], word w owned by thread w
   constexpr int ND = TC_LCAP - TC_HREG;
   const int w = threadIdx.x;
@@ -140,10 +185,13 @@ tc_hist_kernel(const __grid_constant__ TcSides S, int stride16, uint32_t* __rest
         for (int i = 1; i < 16; ++i) vm = __vmaxu2(vm, v[i]);
         const uint32_t vmax = max(vm & 0xffffu, vm >> 16);
         mx = max(mx, vmax);
+        const bool in_cols = w * 32 < dw;
+        uint8_t* orow = O.out[t] + (g - S.row_begin[t] + h) * ROWB + (FP4 ? w * 16 : w * 32);
 #pragma unroll
         for (int l = 0; l < TC_HREG; ++l) {
-          if ((uint32_t)l >= vmax) break;
-          const uint32_t m = layer_mask(v, (uint32_t)(l + 1) * 0x00010001u);
+          const uint32_t m = (uint32_t)l < vmax ? layer_mask(v, (uint32_t)(l + 1) * 0x00010001u) : 0u;
+          if (l < TC_SPEC && h < cnt && in_cols) store_mask_columns<FP4>(orow + l * layer_bytes, m, dw - w * 32);
+          if ((uint32_t)l >= vmax && l >= TC_SPEC) break;
           s2[l] |= s1[l] & m;
           s1[l] |= m;
         }
@@ -265,10 +313,11 @@ tc_select_kernel(const __grid_constant__ TcSel sel, const uint32_t* __restrict__
 // (two 16-byte loads) and writes one 16-byte chunk per dense layer; listed
 // (sparse) columns: 16 entries per chunk, the counts gathered from the row
 // (L1 / L2).
-struct TcOut {
-  uint8_t* out[2 * tc::MAXPROB];
-  int prob[2 * tc::MAXPROB];
-};
+__device__ __forceinline__ int TcOutProbs(const TcOut& O, int nsides) {
+  int n = 0;
+  for (int sd = 0; sd < nsides; ++sd) n = max(n, O.prob[sd] + 1);
+  return n;
+}
 
 // Dense layers: one thread per (row, 16-bin chunk) of every side, all dense
 // layers of that chunk from one 32-byte load.  Counts are <= TC_LCAP here (the
@@ -282,6 +331,9 @@ tc_dense_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut
                 const int32_t* __restrict__ ndense, const uint32_t* __restrict__ state) {
   constexpr int64_t ROWB = FP4 ? TC_KCAP / 2 : TC_KCAP;
   if (tc_infeasible(state)) return;
+  int ndmax = 0;   // no problem keeps more dense layers than the histogram pass wrote: nothing to do
+  for (int q = 0; q < TcOutProbs(O, S.n); ++q) ndmax = max(ndmax, ndense[q]);
+  if (ndmax <= TC_SPEC) return;
   const int dwc = ((bins + 15) & ~15) / 16;
   const int64_t items = S.row_begin[S.n] * dwc;
   for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items;
@@ -295,13 +347,13 @@ tc_dense_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut
       else hi = mid - 1;
     }
     const int nd = ndense[O.prob[lo]];
-    if (nd == 0) continue;
+    if (nd <= TC_SPEC) continue;
     const int64_t r = g - S.row_begin[lo];
     const uint4* src = reinterpret_cast<const uint4*>(S.rows[lo] + r * (int64_t)stride16 + c * 16);
     const uint4 v0 = src[0], v1 = src[1];
     const uint32_t vs[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
     uint8_t* rowp = O.out[lo] + r * ROWB;
-    for (int l = 0; l < nd; ++l) {
+    for (int l = TC_SPEC; l < nd; ++l) {   // layers 1 .. TC_SPEC: written by tc_hist_kernel
       const uint32_t bias = (0x8000u - (uint32_t)(l + 1)) * 0x00010001u;
       uint32_t o[4];
 #pragma unroll
@@ -846,7 +898,9 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
   }
   static bool configured = false;
   if (!configured) {
-    SA_CUDA(cudaFuncSetAttribute(tc_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SA_CUDA(cudaFuncSetAttribute(tc_hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 2 * (TC_LCAP - TC_HREG) * TC_WPL * 4));
+    SA_CUDA(cudaFuncSetAttribute(tc_hist_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  2 * (TC_LCAP - TC_HREG) * TC_WPL * 4));
     sa_status cs = tc_configure_all<false>();
     if (cs == SA_OK) cs = tc_configure_all<true>();
@@ -894,11 +948,6 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     SA_ALLOC(ndense, int32_t, np);
     SA_CUDA(cudaMemsetAsync(planes, 0, (size_t)sides.n * 2 * TC_PLANE * 4, st));
     const int64_t R = sides.row_begin[sides.n];
-    const int hx = (int)std::max<int64_t>(1, std::min<int64_t>((R + TC_HIST_ROWS - 1) / TC_HIST_ROWS, 4 * g_num_sms));
-    tc_hist_kernel<<<hx, TC_HIST_THREADS, 2 * (TC_LCAP - TC_HREG) * TC_WPL * 4, st>>>(sides, stride16, planes, state);
-    SA_LAUNCHED();
-    tc_select_kernel<<<np, 1024, 0, st>>>(sel, planes, bins, kbc, collist, kblocks, ndense, state, cols_out);
-    SA_LAUNCHED();
     // operand rows: one output per side (its problem's column list)
     uint8_t* side_out[2 * tc::MAXPROB];
     for (int sd = 0; sd < sides.n; ++sd) {
@@ -906,6 +955,13 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       if (!o) return fail(SA_E_NOMEM, "scratch allocation of K2T operand rows failed");
       side_out[sd] = outs.out[sd] = o;
     }
+    const int hx = (int)std::max<int64_t>(1, std::min<int64_t>((R + TC_HIST_ROWS - 1) / TC_HIST_ROWS, 4 * g_num_sms));
+    const int hsm = 2 * (TC_LCAP - TC_HREG) * TC_WPL * 4;
+    if (fp4) tc_hist_kernel<true><<<hx, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state);
+    else tc_hist_kernel<false><<<hx, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state);
+    SA_LAUNCHED();
+    tc_select_kernel<<<np, 1024, 0, st>>>(sel, planes, bins, kbc, collist, kblocks, ndense, state, cols_out);
+    SA_LAUNCHED();
     const int bx = (int)std::max<int64_t>(1, std::min<int64_t>(R, 4 * g_num_sms));
     if (fp4) {
       tc_dense_kernel<true><<<8 * g_num_sms, 256, 0, st>>>(sides, outs, stride16, bins, ndense, state);
