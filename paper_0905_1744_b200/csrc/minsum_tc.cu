@@ -513,8 +513,12 @@ struct KeyMatEpi {
   static constexpr int KOFF = 0;
   static constexpr int YOFF = KEYS ? 16 : 0;
   static constexpr int TAB_BYTES = (KEYS && SIM) ? 32 : 16;
-  // the per-warp 32 x CW uint16 transpose buffer of the matrix path
-  __host__ __device__ static constexpr int xpose_bytes(int CW) { return MATS ? 64 * CW : 0; }
+  // the per-warp 32 x CW uint16 transpose buffer of the matrix path, plus (F
+  // with the e2m1 stage sizes, where it fits) a 32-row {y, d} table
+  __host__ __device__ static constexpr bool row_table(bool FP4) { return SIM && FP4; }
+  __host__ __device__ static constexpr int xpose_bytes(int CW, bool FP4) {
+    return (MATS ? 64 * CW : 0) + (row_table(FP4) ? 32 * 16 : 0);
+  }
 
   struct State {
     uint64_t lo;      // row key, 96 bits
@@ -524,7 +528,7 @@ struct KeyMatEpi {
     int row_g;
     bool rv;          // the row exists
     uint32_t rl, rh, ek;
-    double y;
+    double y, d;      // RN(1 / nk') and nk' as doubles (0 for the sentinel)
   };
 
   __device__ bool skip() const { return tc_infeasible(state); }
@@ -544,7 +548,10 @@ struct KeyMatEpi {
       s.rh = (uint32_t)(r >> 32);
       s.ek = g_etab[dr];
     }
-    if constexpr (SIM) s.y = g_rcp[dr];
+    if constexpr (SIM) {
+      s.y = g_rcp[dr];
+      s.d = (double)dr;
+    }
     if constexpr (KEYS || SIM) {
       for (int c = cbeg + lane; c < cend; c += 32) {
         const int nkc = c < T.rb ? E.nkB[T.col0 + c] : 0;
@@ -556,13 +563,22 @@ struct KeyMatEpi {
           *reinterpret_cast<uint4*>(ent + KOFF) = make_uint4((uint32_t)r, (uint32_t)(r >> 32), g_etab[dc], (uint32_t)ns);
         }
         if constexpr (SIM) {
-          const double y = g_rcp[dc];
-          *reinterpret_cast<uint4*>(ent + YOFF) =
-              make_uint4((uint32_t)__double2loint(y), (uint32_t)__double2hiint(y), (uint32_t)ns, 0u);
+          const double y = g_rcp[dc], d = (double)dc;
+          *reinterpret_cast<double2*>(ent + YOFF) = make_double2(y, d);
         }
       }
     }
     __syncwarp();
+  }
+
+  // F = C / D (reading Z19, division-free) with D = min(nk'_row, nk'_col)
+  // taken by comparing the reciprocals: y_c > y_r <=> nk'_c < nk'_r for
+  // nk' >= 1 (RN(1/D) is strictly decreasing over D < 2^16); a sentinel side
+  // (y = d = 0) meets C = 0 (an empty or missing row / column: zero profile or
+  // TMA zero fill), and C = 0 gives +0 whatever side is taken.
+  __device__ __forceinline__ static double fsel(uint32_t C, double yr, double dr, double yc, double dc) {
+    const bool col = yc > yr;
+    return f_ratio_y(C, col ? dc : dr, col ? yc : yr);
   }
 
   // the exact-rank term of pair (row, column entry k), numerator C: 64 low bits + the 2^64 carry
@@ -610,7 +626,7 @@ struct KeyMatEpi {
   }
 
   // CW columns [col, col + CW) of this thread's row; lanes = 32 consecutive rows.
-  template <int CW>
+  template <int CW, bool FP4>
   __device__ void chunk(State& s, const tc::Tile& T, int row, int col, const uint32_t (&v)[CW], int lane,
                         const uint8_t* tab, int tj, uint8_t* xp) const {
     static_assert(CW == 16 || CW == 32, "chunk width");
@@ -621,6 +637,12 @@ struct KeyMatEpi {
     const bool upper = !sym || c0 > wrow0 + 31;         // every pair strictly above the diagonal (warp-uniform)
     const int ncols = min(CW, T.rb - col);              // columns that exist
     const uint8_t* ent = tab + tj * TAB_BYTES;
+    if constexpr (row_table(FP4)) {
+      if (tj == 0) {                                    // the warp's rows' {y, d}, once per tile
+        reinterpret_cast<double2*>(xp + 64 * CW)[lane] = make_double2(s.y, s.d);
+        __syncwarp();
+      }
+    }
     if (sym && c0 + CW <= wrow0) return;                // every pair below the diagonal: counted by its mirror
 
     if (KEYS && E.keyA) {
@@ -675,103 +697,110 @@ struct KeyMatEpi {
     }
 
     if constexpr (MATS) {
-      // the host sets num (sim) on every problem of a launch whose MODE has NUM (SIM)
-      constexpr bool want_num = (MODE & EPI_NUM) != 0;
-      constexpr bool want_sim = SIM;
-      const bool rows_all = wrow0 + 32 <= T.row0 + T.ra;   // warp-uniform
-      if (upper && ncols == CW && rows_all) {
-        // ---- fast path (all 32 rows and CW columns exist, no diagonal).
-        // (1) lanes = rows: F of every pair; the mirrored element (gc, row)
-        // with lanes = consecutive rows (coalesced); C staged in the warp's
-        // 32 x CW uint16 transpose buffer (16-byte units XOR-swizzled by the
-        // row: conflict-free both ways).
-        constexpr int Q = CW / 8;                          // 16-byte units per buffer row
-        constexpr int QSH = CW == 16 ? 2 : 1;              // swizzle: unit ^ ((row >> QSH) % Q)
-        const int64_t ld = E.ld;
-        uint16_t* const num = E.num;
-        double* const sim = E.sim;
-        {
-          const int64_t om = (int64_t)c0 * ld + s.row_g;
-          uint32_t w[CW / 2];
-#pragma unroll
-          for (int j = 0; j < CW; ++j) {
-            const uint32_t C = v[j];
-            if (j & 1) w[j >> 1] |= C << 16;
-            else w[j >> 1] = C;
-            if (sym) {
-              if constexpr (want_num) st_out(num + om + j * ld, (uint16_t)C);
-              if constexpr (want_sim) {
-                const uint4 k = *reinterpret_cast<const uint4*>(ent + j * TAB_BYTES + YOFF);
-                const int nkc = (int)k.z;
-                const double yc = __hiloint2double((int)k.y, (int)k.x);
-                const int D = min(s.nk, nkc);
-                const double d = __hiloint2double(0x43300000, D) - 4503599627370496.0;
-                st_out(sim + om + j * ld, f_ratio_y(C, d, nkc < s.nk ? yc : s.y));
-              }
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < Q; ++q) {
-            const int qs = q ^ ((lane >> QSH) & (Q - 1));
-            *reinterpret_cast<uint4*>(xp + lane * (CW * 2) + qs * 16) =
-                make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
-          }
-        }
-        __syncwarp();
-        // (2) lanes = columns: the direct row segments (row, c0 ..) from the
-        // buffer, 32 / CW rows per pass, row data by shuffles
-        const int cl = lane % CW;
-        int nkc = -1;
-        double yc = 0.0;
-        if constexpr (want_sim) {
-          const uint4 k = *reinterpret_cast<const uint4*>(ent + cl * TAB_BYTES + YOFF);
-          nkc = (int)k.z;
-          yc = __hiloint2double((int)k.y, (int)k.x);
-        }
-        constexpr int RPP = 32 / CW;
-        const int64_t od = (int64_t)(wrow0 + lane / CW) * ld + c0 + cl;
-#pragma unroll 4
-        for (int pss = 0; pss < CW; ++pss) {
-          const int i = pss * RPP + lane / CW;              // buffer row = warp row
-          const int qs = (cl >> 3) ^ ((i >> QSH) & (Q - 1));
-          const uint32_t C = *reinterpret_cast<const uint16_t*>(xp + i * (CW * 2) + qs * 16 + (cl & 7) * 2);
-          const int64_t o = od + (int64_t)(pss * RPP) * ld;
-          if constexpr (want_num) st_out(num + o, (uint16_t)C);
-          if constexpr (want_sim) {
-            const int nk_i = __shfl_sync(0xffffffffu, s.nk, i);
-            const double y_i = __shfl_sync(0xffffffffu, s.y, i);
-            const int D = min(nk_i, nkc);
-            const double d = __hiloint2double(0x43300000, D) - 4503599627370496.0;
-            st_out(sim + o, f_ratio_y(C, d, nkc < nk_i ? yc : y_i));
-          }
-        }
-        __syncwarp();
-      } else {
-        // ---- diagonal / ragged chunks: per-element masks
+      if (sym) mats<true, CW, FP4>(s, E, T, col, c0, wrow0, upper, ncols, v, lane, ent, tj, xp);
+      else mats<false, CW, FP4>(s, E, T, col, c0, wrow0, upper, ncols, v, lane, ent, tj, xp);
+    }
+  }
+
+  // the numerator / F matrices of a chunk (the host sets num (sim) on every
+  // problem of a launch whose MODE has NUM (SIM))
+  template <bool SYM, int CW, bool FP4>
+  __device__ __forceinline__ void mats(State& s, const TcEpiProb& E, const tc::Tile& T, int col, int c0, int wrow0,
+                                       bool upper, int ncols, const uint32_t (&v)[CW], int lane, const uint8_t* ent,
+                                       int tj, uint8_t* xp) const {
+    constexpr bool want_num = (MODE & EPI_NUM) != 0;
+    constexpr bool want_sim = SIM;
+    constexpr bool RT = row_table(FP4);
+    const bool rows_all = wrow0 + 32 <= T.row0 + T.ra;   // warp-uniform
+    const double2* rtab = reinterpret_cast<const double2*>(xp + 64 * CW);   // written by chunk() at tj = 0
+    if (upper && ncols == CW && rows_all) {
+      // ---- fast path (all 32 rows and CW columns exist, no diagonal).
+      // (1) lanes = rows: F of every pair; the mirrored element (gc, row)
+      // with lanes = consecutive rows (coalesced); C staged in the warp's
+      // 32 x CW uint16 transpose buffer (16-byte units XOR-swizzled by the
+      // row: conflict-free both ways).  Element offsets fit 32 bits (n_b ld < 2^31).
+      constexpr int Q = CW / 8;                          // 16-byte units per buffer row
+      constexpr int QSH = CW == 16 ? 2 : 1;              // swizzle: unit ^ ((row >> QSH) % Q)
+      const int ld = (int)E.ld;
+      uint16_t* const num = E.num;
+      double* const sim = E.sim;
+      {
+        uint32_t w[CW / 2];
+        int om = c0 * ld + s.row_g;
 #pragma unroll
         for (int j = 0; j < CW; ++j) {
-          const int gc = c0 + j;
-          if (!s.rv || j >= ncols || (sym && gc < s.row_g)) continue;
-          const bool diag = sym && gc == s.row_g;
-          const uint32_t C = diag ? (uint32_t)s.nk0 : v[j];
-          double F = 0.0;
-          if (want_sim) {
-            const uint4 k = *reinterpret_cast<const uint4*>(ent + j * TAB_BYTES + YOFF);
-            const int nkc = (int)k.z;
-            const double yc = __hiloint2double((int)k.y, (int)k.x);
-            const double y = nkc < s.nk ? yc : s.y;
-            const int D = min(s.nk, nkc);
-            const double d = __hiloint2double(0x43300000, D) - 4503599627370496.0;
-            F = f_ratio_y(C, d, y);
+          const uint32_t C = v[j];
+          if (j & 1) w[j >> 1] |= C << 16;
+          else w[j >> 1] = C;
+          if constexpr (SYM) {
+            if constexpr (want_num) st_out(num + om, (uint16_t)C);
+            if constexpr (want_sim) {
+              const double2 yd = *reinterpret_cast<const double2*>(ent + j * TAB_BYTES + YOFF);
+              st_out(sim + om, fsel(C, s.y, s.d, yd.x, yd.y));
+            }
           }
-          const int64_t od = (int64_t)s.row_g * E.ld + gc;
-          if (want_num) st_out(E.num + od, (uint16_t)C);
-          if (want_sim) st_out(E.sim + od, F);
-          if (sym && !diag) {
-            const int64_t om = (int64_t)gc * E.ld + s.row_g;
-            if (want_num) st_out(E.num + om, (uint16_t)C);
-            if (want_sim) st_out(E.sim + om, F);
+          om += ld;
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int qs = q ^ ((lane >> QSH) & (Q - 1));
+          *reinterpret_cast<uint4*>(xp + lane * (CW * 2) + qs * 16) =
+              make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+        }
+      }
+      __syncwarp();
+      // (2) lanes = columns: the direct row segments (row, c0 ..) from the
+      // buffer, 32 / CW rows per pass; row data from the row table (or shuffles)
+      const int cl = lane % CW;
+      double yc = 0.0, dc = 0.0;
+      if constexpr (want_sim) {
+        const double2 yd = *reinterpret_cast<const double2*>(ent + cl * TAB_BYTES + YOFF);
+        yc = yd.x;
+        dc = yd.y;
+      }
+      constexpr int RPP = 32 / CW;
+      int od = (wrow0 + lane / CW) * ld + c0 + cl;
+#pragma unroll
+      for (int pss = 0; pss < CW; ++pss) {
+        const int i = pss * RPP + lane / CW;              // buffer row = warp row
+        const int qs = (cl >> 3) ^ ((i >> QSH) & (Q - 1));
+        const uint32_t C = *reinterpret_cast<const uint16_t*>(xp + i * (CW * 2) + qs * 16 + (cl & 7) * 2);
+        if constexpr (want_num) st_out(num + od, (uint16_t)C);
+        if constexpr (want_sim) {
+          double y_i, d_i;
+          if constexpr (RT) {
+            const double2 r = rtab[i];
+            y_i = r.x;
+            d_i = r.y;
+          } else {
+            y_i = __shfl_sync(0xffffffffu, s.y, i);
+            d_i = __shfl_sync(0xffffffffu, s.d, i);
           }
+          st_out(sim + od, fsel(C, y_i, d_i, yc, dc));
+        }
+        od += RPP * ld;
+      }
+      __syncwarp();
+    } else {
+      // ---- diagonal / ragged chunks: per-element masks
+#pragma unroll
+      for (int j = 0; j < CW; ++j) {
+        const int gc = c0 + j;
+        if (!s.rv || j >= ncols || (SYM && gc < s.row_g)) continue;
+        const bool diag = SYM && gc == s.row_g;
+        const uint32_t C = diag ? (uint32_t)s.nk0 : v[j];
+        double F = 0.0;
+        if constexpr (want_sim) {
+          const double2 yd = *reinterpret_cast<const double2*>(ent + j * TAB_BYTES + YOFF);
+          F = fsel(C, s.y, s.d, yd.x, yd.y);
+        }
+        const int64_t od = (int64_t)s.row_g * E.ld + gc;
+        if constexpr (want_num) st_out(E.num + od, (uint16_t)C);
+        if constexpr (want_sim) st_out(E.sim + od, F);
+        if (SYM && !diag) {
+          const int64_t om = (int64_t)gc * E.ld + s.row_g;
+          if constexpr (want_num) st_out(E.num + om, (uint16_t)C);
+          if constexpr (want_sim) st_out(E.sim + om, F);
         }
       }
     }
@@ -830,9 +859,9 @@ __global__ void f_division_check_kernel(unsigned long long* bad) {
 // ------------------------------------------------------------- host ----
 template <class Epi, int EW, int CW, bool FP4>
 static sa_status tc_configure() {
-  static_assert(tc::smem_of(EW, CW, FP4, Epi::TAB_BYTES, Epi::xpose_bytes(CW)) <= 232448, "shared memory per CTA");
+  static_assert(tc::smem_of(EW, CW, FP4, Epi::TAB_BYTES, Epi::xpose_bytes(CW, FP4)) <= 232448, "shared memory per CTA");
   SA_CUDA(cudaFuncSetAttribute(tc::gemm_kernel<Epi, EW, CW, FP4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               tc::smem_of(EW, CW, FP4, Epi::TAB_BYTES, Epi::xpose_bytes(CW))));
+                               tc::smem_of(EW, CW, FP4, Epi::TAB_BYTES, Epi::xpose_bytes(CW, FP4))));
   return SA_OK;
 }
 template <class Epi, int EW, int CW, bool FP4>
@@ -842,7 +871,7 @@ static void tc_gemm(int64_t grid, const tc::Batch& batch, const tc::Maps& maps, 
   static_assert(sizeof k == sizeof epi, "epilogue layouts");
   std::memcpy(&k, &epi, sizeof k);
   tc::gemm_kernel<Epi, EW, CW, FP4>
-      <<<(unsigned)grid, tc::threads_of(EW), tc::smem_of(EW, CW, FP4, Epi::TAB_BYTES, Epi::xpose_bytes(CW)), st>>>(batch, maps, tiles, k);
+      <<<(unsigned)grid, tc::threads_of(EW), tc::smem_of(EW, CW, FP4, Epi::TAB_BYTES, Epi::xpose_bytes(CW, FP4)), st>>>(batch, maps, tiles, k);
 }
 // the (epilogue mode, geometry) instantiations a launch can pick
 template <bool FP4>

@@ -54,7 +54,7 @@ static_assert(Geo<true>::STAGE_BYTES % 1024 == 0 && Geo<false>::STAGE_BYTES % 10
 // column slice of SLICE columns), CW columns per tcgen05.ld chunk (16 or 32).
 // Each epilogue warp owns TB bytes of shared memory per slice column
 // (Epi::TAB_BYTES: the per-tile column tables the epilogue stages before the
-// accumulator is ready) plus XB scratch bytes (Epi::xpose_bytes(CW)).
+// accumulator is ready) plus XB scratch bytes (Epi::xpose_bytes(CW, FP4)).
 __host__ __device__ constexpr int threads_of(int EW) { return (EW + 2) * 32; }
 __host__ __device__ constexpr int slice_of(int EW, int CW, bool FP4) {
   return (((FP4 ? 240 : 256) / (EW / 4) + CW - 1) / CW) * CW;
@@ -308,7 +308,7 @@ __device__ __forceinline__ Tile decode(const Batch& b, int64_t tile) {
 //   static constexpr int TAB_BYTES;                                // table bytes per slice column
 //   __device__ void begin(State&, const Tile&, int row, int lane, int cbeg, int cend,
 //                         uint8_t* tab) const;                       // before the accumulator wait
-//   template <int CW> __device__ void chunk(State&, const Tile&, int row, int col, const uint32_t (&v)[CW],
+//   template <int CW, bool FP4> __device__ void chunk(State&, const Tile&, int row, int col, const uint32_t (&v)[CW],
 //                         int lane, const uint8_t* tab, int tj, uint8_t* xp) const;   // all lanes, converged
 //   __device__ void end(State&, const Tile&, int row) const;
 // row = tile row of this thread (0..127), [cbeg, cend) = the warp's column
@@ -428,7 +428,7 @@ gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps ma
     const int quad = warp & 3, part = warp >> 2;
     const int row = quad * 32 + lane;
     constexpr int SLICE = slice_of(EW, CW, FP4);
-    constexpr int XB = Epi::xpose_bytes(CW);
+    constexpr int XB = Epi::xpose_bytes(CW, FP4);
     uint8_t* tab = tab_all + warp * (SLICE * Epi::TAB_BYTES + XB);
     uint8_t* xp = tab + SLICE * Epi::TAB_BYTES;
     const int cbeg = part * SLICE, cend = min(cbeg + SLICE, BN);
@@ -449,7 +449,7 @@ gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps ma
 #pragma unroll
           for (int j = 0; j < CW; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + 8388608.0f) & 0x7FFFFFu;
         }
-        epi.template chunk<CW>(es, T, row, col, v, lane, tab, col - cbeg, xp);
+        epi.template chunk<CW, FP4>(es, T, row, col, v, lane, tab, col - cbeg, xp);
       }
       fence_before();
       __syncwarp();
