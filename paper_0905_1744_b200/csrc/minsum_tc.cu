@@ -458,6 +458,12 @@ struct TcEpiProb {
 // re-read from L2.
 __device__ __forceinline__ void st_out(uint16_t* p, uint16_t v) { __stcs(reinterpret_cast<unsigned short*>(p), v); }
 __device__ __forceinline__ void st_out(double* p, double v) { __stcs(p, v); }
+__device__ __forceinline__ void st_out_if(bool on, uint16_t* p, uint16_t v) {
+  if (on) st_out(p, v);
+}
+__device__ __forceinline__ void st_out_if(bool on, double* p, double v) {
+  if (on) st_out(p, v);
+}
 // 96-bit (lo, hi) add
 __device__ __forceinline__ void add96(uint64_t& lo, uint32_t& hi, uint64_t blo, uint32_t bhi) {
   lo += blo;
@@ -506,6 +512,7 @@ template <int MODE>
 struct KeyMatEpi {
   TcEpiProb e[tc::MAXPROB];
   const uint32_t* state;
+  int dbg;   // experiments only (SA_K2T_DEBUG bit 8: matrix stores skipped)
 
   static constexpr bool KEYS = (MODE & EPI_KEYS) != 0;
   static constexpr bool SIM = (MODE & EPI_SIM) != 0;
@@ -515,9 +522,19 @@ struct KeyMatEpi {
   static constexpr int TAB_BYTES = (KEYS && SIM) ? 32 : 16;
   // the per-warp 32 x CW uint16 transpose buffer of the matrix path, plus (F
   // with the e2m1 stage sizes, where it fits) a 32-row {y, d} table
-  __host__ __device__ static constexpr bool row_table(bool FP4) { return SIM && FP4; }
-  __host__ __device__ static constexpr int xpose_bytes(int CW, bool FP4) {
-    return (MATS ? 64 * CW : 0) + (row_table(FP4) ? 32 * 16 : 0);
+  //   CTA pairs (CG = 2, small stages): F itself goes through a 32 x CW fp64
+  //   transpose buffer, so each F is computed once (f_transposed);
+  //   one CTA (CG = 1): F is recomputed in the transposed pass, with a
+  //   32-row {y, d} table where it fits (e2m1 stage sizes).
+  __host__ __device__ static constexpr bool f_transposed(int CW, int CG) {
+    // measured slower (its 4 KB per warp costs the CTA pair a pipeline stage): off
+    return false && SIM && CG == 2 && CW == 16;
+  }
+  __host__ __device__ static constexpr bool row_table(bool FP4, int CW, int CG) {
+    return SIM && FP4 && !f_transposed(CW, CG);
+  }
+  __host__ __device__ static constexpr int xpose_bytes(int CW, bool FP4, int CG) {
+    return (MATS ? 64 * CW : 0) + (f_transposed(CW, CG) ? 32 * CW * 8 : 0) + (row_table(FP4, CW, CG) ? 32 * 16 : 0);
   }
 
   struct State {
@@ -626,7 +643,7 @@ struct KeyMatEpi {
   }
 
   // CW columns [col, col + CW) of this thread's row; lanes = 32 consecutive rows.
-  template <int CW, bool FP4>
+  template <int CW, bool FP4, int CG>
   __device__ void chunk(State& s, const tc::Tile& T, int row, int col, const uint32_t (&v)[CW], int lane,
                         const uint8_t* tab, int tj, uint8_t* xp) const {
     static_assert(CW == 16 || CW == 32, "chunk width");
@@ -637,7 +654,7 @@ struct KeyMatEpi {
     const bool upper = !sym || c0 > wrow0 + 31;         // every pair strictly above the diagonal (warp-uniform)
     const int ncols = min(CW, T.rb - col);              // columns that exist
     const uint8_t* ent = tab + tj * TAB_BYTES;
-    if constexpr (row_table(FP4)) {
+    if constexpr (row_table(FP4, CW, CG)) {
       if (tj == 0) {                                    // the warp's rows' {y, d}, once per tile
         reinterpret_cast<double2*>(xp + 64 * CW)[lane] = make_double2(s.y, s.d);
         __syncwarp();
@@ -697,23 +714,25 @@ struct KeyMatEpi {
     }
 
     if constexpr (MATS) {
-      if (sym) mats<true, CW, FP4>(s, E, T, col, c0, wrow0, upper, ncols, v, lane, ent, tj, xp);
-      else mats<false, CW, FP4>(s, E, T, col, c0, wrow0, upper, ncols, v, lane, ent, tj, xp);
+      if (sym) mats<true, CW, FP4, CG>(s, E, T, col, c0, wrow0, upper, ncols, v, lane, ent, tj, xp);
+      else mats<false, CW, FP4, CG>(s, E, T, col, c0, wrow0, upper, ncols, v, lane, ent, tj, xp);
     }
   }
 
   // the numerator / F matrices of a chunk (the host sets num (sim) on every
   // problem of a launch whose MODE has NUM (SIM))
-  template <bool SYM, int CW, bool FP4>
+  template <bool SYM, int CW, bool FP4, int CG>
   __device__ __forceinline__ void mats(State& s, const TcEpiProb& E, const tc::Tile& T, int col, int c0, int wrow0,
                                        bool upper, int ncols, const uint32_t (&v)[CW], int lane, const uint8_t* ent,
                                        int tj, uint8_t* xp) const {
     constexpr bool want_num = (MODE & EPI_NUM) != 0;
     constexpr bool want_sim = SIM;
-    constexpr bool RT = row_table(FP4);
+    constexpr bool RT = row_table(FP4, CW, CG);
+    constexpr bool FT = f_transposed(CW, CG);
     const bool rows_all = wrow0 + 32 <= T.row0 + T.ra;   // warp-uniform
     const double2* rtab = reinterpret_cast<const double2*>(xp + 64 * CW);   // written by chunk() at tj = 0
     if (upper && ncols == CW && rows_all) {
+      const bool stores = (dbg & 8) == 0;
       // ---- fast path (all 32 rows and CW columns exist, no diagonal).
       // (1) lanes = rows: F of every pair; the mirrored element (gc, row)
       // with lanes = consecutive rows (coalesced); C staged in the warp's
@@ -724,20 +743,32 @@ struct KeyMatEpi {
       const int ld = (int)E.ld;
       uint16_t* const num = E.num;
       double* const sim = E.sim;
+      // F transpose buffer (FT): 32 rows x CW doubles, 16-byte unit u of row r
+      // at unit u ^ (r & 7) (conflict-free STS.128 by rows and LDS.64 by columns)
+      uint8_t* const fb = xp + 64 * CW;
       {
         uint32_t w[CW / 2];
         int om = c0 * ld + s.row_g;
+        double Fp = 0.0;
 #pragma unroll
         for (int j = 0; j < CW; ++j) {
           const uint32_t C = v[j];
           if (j & 1) w[j >> 1] |= C << 16;
           else w[j >> 1] = C;
+          double F = 0.0;
+          if constexpr (want_sim && (SYM || FT)) {
+            const double2 yd = *reinterpret_cast<const double2*>(ent + j * TAB_BYTES + YOFF);
+            F = fsel(C, s.y, s.d, yd.x, yd.y);
+          }
           if constexpr (SYM) {
-            if constexpr (want_num) st_out(num + om, (uint16_t)C);
-            if constexpr (want_sim) {
-              const double2 yd = *reinterpret_cast<const double2*>(ent + j * TAB_BYTES + YOFF);
-              st_out(sim + om, fsel(C, s.y, s.d, yd.x, yd.y));
-            }
+            if constexpr (want_num) st_out_if(stores, num + om, (uint16_t)C);
+            if constexpr (want_sim) st_out_if(stores, sim + om, F);
+          }
+          if constexpr (FT) {
+            if (j & 1)
+              *reinterpret_cast<double2*>(fb + lane * (CW * 8) + (((j >> 1) ^ (lane & 7)) * 16)) = make_double2(Fp, F);
+            else
+              Fp = F;
           }
           om += ld;
         }
@@ -753,7 +784,7 @@ struct KeyMatEpi {
       // buffer, 32 / CW rows per pass; row data from the row table (or shuffles)
       const int cl = lane % CW;
       double yc = 0.0, dc = 0.0;
-      if constexpr (want_sim) {
+      if constexpr (want_sim && !FT) {
         const double2 yd = *reinterpret_cast<const double2*>(ent + cl * TAB_BYTES + YOFF);
         yc = yd.x;
         dc = yd.y;
@@ -765,8 +796,11 @@ struct KeyMatEpi {
         const int i = pss * RPP + lane / CW;              // buffer row = warp row
         const int qs = (cl >> 3) ^ ((i >> QSH) & (Q - 1));
         const uint32_t C = *reinterpret_cast<const uint16_t*>(xp + i * (CW * 2) + qs * 16 + (cl & 7) * 2);
-        if constexpr (want_num) st_out(num + od, (uint16_t)C);
-        if constexpr (want_sim) {
+        if constexpr (want_num) st_out_if(stores, num + od, (uint16_t)C);
+        if constexpr (want_sim && FT) {
+          st_out_if(stores, sim + od, *reinterpret_cast<const double*>(fb + i * (CW * 8) + (((cl >> 1) ^ (i & 7)) * 16) +
+                                                             (cl & 1) * 8));
+        } else if constexpr (want_sim) {
           double y_i, d_i;
           if constexpr (RT) {
             const double2 r = rtab[i];
@@ -776,7 +810,7 @@ struct KeyMatEpi {
             y_i = __shfl_sync(0xffffffffu, s.y, i);
             d_i = __shfl_sync(0xffffffffu, s.d, i);
           }
-          st_out(sim + od, fsel(C, y_i, d_i, yc, dc));
+          st_out_if(stores, sim + od, fsel(C, y_i, d_i, yc, dc));
         }
         od += RPP * ld;
       }
@@ -857,48 +891,69 @@ __global__ void f_division_check_kernel(unsigned long long* bad) {
 }
 
 // ------------------------------------------------------------- host ----
-template <class Epi, int EW, int CW, bool FP4>
+template <class Epi, int EW, int CW, bool FP4, int CG>
 static sa_status tc_configure() {
-  static_assert(tc::smem_of(EW, CW, FP4, Epi::TAB_BYTES, Epi::xpose_bytes(CW, FP4)) <= 232448, "shared memory per CTA");
-  SA_CUDA(cudaFuncSetAttribute(tc::gemm_kernel<Epi, EW, CW, FP4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               tc::smem_of(EW, CW, FP4, Epi::TAB_BYTES, Epi::xpose_bytes(CW, FP4))));
+  if constexpr (CG == 1) {
+    static_assert(tc::smem_of(EW, CW, FP4, Epi::TAB_BYTES, Epi::xpose_bytes(CW, FP4, 1)) <= 232448, "shared memory");
+    SA_CUDA(cudaFuncSetAttribute(tc::gemm_kernel<Epi, EW, CW, FP4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tc::smem_of(EW, CW, FP4, Epi::TAB_BYTES, Epi::xpose_bytes(CW, FP4, 1))));
+  } else {
+    static_assert(tc::smem2_of(EW, CW, FP4, Epi::TAB_BYTES, Epi::xpose_bytes(CW, FP4, 2)) <= 232448, "shared memory");
+    SA_CUDA(cudaFuncSetAttribute(tc::gemm2_kernel<Epi, EW, CW, FP4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tc::smem2_of(EW, CW, FP4, Epi::TAB_BYTES, Epi::xpose_bytes(CW, FP4, 2))));
+  }
   return SA_OK;
 }
-template <class Epi, int EW, int CW, bool FP4>
+template <class Epi, int EW, int CW, bool FP4, int CG>
 static void tc_gemm(int64_t grid, const tc::Batch& batch, const tc::Maps& maps, int64_t tiles,
                     const KeyMatEpi<EPI_ALL>& epi, cudaStream_t st) {
   Epi k;
   static_assert(sizeof k == sizeof epi, "epilogue layouts");
   std::memcpy(&k, &epi, sizeof k);
-  tc::gemm_kernel<Epi, EW, CW, FP4>
-      <<<(unsigned)grid, tc::threads_of(EW), tc::smem_of(EW, CW, FP4, Epi::TAB_BYTES, Epi::xpose_bytes(CW, FP4)), st>>>(batch, maps, tiles, k);
+  if constexpr (CG == 1)
+    tc::gemm_kernel<Epi, EW, CW, FP4><<<(unsigned)grid, tc::threads_of(EW),
+                                         tc::smem_of(EW, CW, FP4, Epi::TAB_BYTES, Epi::xpose_bytes(CW, FP4, 1)), st>>>(
+        batch, maps, tiles, k);
+  else
+    tc::gemm2_kernel<Epi, EW, CW, FP4><<<(unsigned)grid, tc::threads_of(EW),
+                                          tc::smem2_of(EW, CW, FP4, Epi::TAB_BYTES, Epi::xpose_bytes(CW, FP4, 2)), st>>>(
+        batch, maps, tiles, k);
 }
 // the (epilogue mode, geometry) instantiations a launch can pick
-template <bool FP4>
+template <bool FP4, int CG>
 static sa_status tc_configure_all() {
   constexpr int CW_ALL = FP4 ? 16 : 32;
-  sa_status cs = tc_configure<KeyMatEpi<EPI_KEYS>, 16, 16, FP4>();
-  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_KEYS>, 8, CW_ALL, FP4>();
-  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM>, 16, 16, FP4>();
-  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_SIM>, 16, 16, FP4>();
-  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4>();
-  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_KEYS | EPI_NUM>, 8, CW_ALL, FP4>();
+  sa_status cs = tc_configure<KeyMatEpi<EPI_KEYS>, 16, 16, FP4, CG>();
+  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_KEYS>, 8, CW_ALL, FP4, CG>();
+  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM>, 16, 16, FP4, CG>();
+  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_SIM>, 16, 16, FP4, CG>();
+  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4, CG>();
+  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_KEYS | EPI_NUM>, 8, CW_ALL, FP4, CG>();
   return cs;
 }
-template <bool FP4>
+template <bool FP4, int CG>
 static void tc_gemm_mode(int mode, bool keys16, int64_t grid, const tc::Batch& batch, const tc::Maps& maps,
                          int64_t tiles, const KeyMatEpi<EPI_ALL>& epi, cudaStream_t st) {
   constexpr int CW_ALL = FP4 ? 16 : 32;
   // 16 epilogue warps x 16-column chunks (more warps to hide the store / F /
   // key-term latency, fewer registers each); keys and matrices together
   // (a rank call that also wants numerators) use 8 warps
-  if (mode == EPI_KEYS && keys16) tc_gemm<KeyMatEpi<EPI_KEYS>, 16, 16, FP4>(grid, batch, maps, tiles, epi, st);
-  else if (mode == EPI_KEYS) tc_gemm<KeyMatEpi<EPI_KEYS>, 8, CW_ALL, FP4>(grid, batch, maps, tiles, epi, st);
-  else if (mode == EPI_NUM) tc_gemm<KeyMatEpi<EPI_NUM>, 16, 16, FP4>(grid, batch, maps, tiles, epi, st);
-  else if (mode == EPI_SIM) tc_gemm<KeyMatEpi<EPI_SIM>, 16, 16, FP4>(grid, batch, maps, tiles, epi, st);
+  if (mode == EPI_KEYS && keys16) tc_gemm<KeyMatEpi<EPI_KEYS>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
+  else if (mode == EPI_KEYS) tc_gemm<KeyMatEpi<EPI_KEYS>, 8, CW_ALL, FP4, CG>(grid, batch, maps, tiles, epi, st);
+  else if (mode == EPI_NUM) tc_gemm<KeyMatEpi<EPI_NUM>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
+  else if (mode == EPI_SIM) tc_gemm<KeyMatEpi<EPI_SIM>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
   else if ((mode & EPI_KEYS) == 0)
-    tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4>(grid, batch, maps, tiles, epi, st);
-  else tc_gemm<KeyMatEpi<EPI_KEYS | EPI_NUM>, 8, CW_ALL, FP4>(grid, batch, maps, tiles, epi, st);   // never with F
+    tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
+  else tc_gemm<KeyMatEpi<EPI_KEYS | EPI_NUM>, 8, CW_ALL, FP4, CG>(grid, batch, maps, tiles, epi, st);   // never with F
+}
+
+// CTA pairs (tcgen05 cta_group::2, tc_gemm.cuh) unless SA_K2T_PAIR=0
+static bool tc_pairs() {
+  static const bool on = [] {
+    const char* e = getenv("SA_K2T_PAIR");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
 }
 
 static sa_status tc_encode_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int box_rows, int64_t rowb) {
@@ -931,13 +986,16 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
                                  2 * (TC_LCAP - TC_HREG) * TC_WPL * 4));
     SA_CUDA(cudaFuncSetAttribute(tc_hist_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  2 * (TC_LCAP - TC_HREG) * TC_WPL * 4));
-    sa_status cs = tc_configure_all<false>();
-    if (cs == SA_OK) cs = tc_configure_all<true>();
+    sa_status cs = tc_configure_all<false, 1>();
+    if (cs == SA_OK) cs = tc_configure_all<true, 1>();
+    if (cs == SA_OK) cs = tc_configure_all<false, 2>();
+    if (cs == SA_OK) cs = tc_configure_all<true, 2>();
     if (cs != SA_OK) return cs;
     configured = true;
   }
   const int stride16 = 2 * ldw16;
   const bool fp4 = tc_fp4_operands();
+  const bool pairs = tc_pairs();
   const int64_t rowb = fp4 ? TC_KCAP / 2 : TC_KCAP;
   const int kbc = fp4 ? 256 : 128;
   static const bool fpass = [] {
@@ -1008,9 +1066,14 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     tc::Batch batch{};
     tc::Maps maps;
     std::memset(&maps, 0, sizeof maps);
+    static const int debug = [] {   // SA_K2T_DEBUG: component switches for experiments (tc_gemm.cuh, KeyMatEpi)
+      const char* e = getenv("SA_K2T_DEBUG");
+      return e ? atoi(e) : 0;
+    }();
     KeyMatEpi<EPI_ALL> epi{};
     int mode = 0;
     epi.state = state;
+    epi.dbg = debug;
     int64_t tiles = 0;
     // keys and F in one launch would need both column tables: F then goes
     // through the F pass (numerators in the epilogue, ratio_kernel after)
@@ -1028,12 +1091,16 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       T.tile_begin = tiles;
       T.kblocks = kblocks + q;
       T.map = q;
-      tiles += fp4 ? tc::problem_tiles<tc::Geo<true>::BN>(P.na, P.nb, P.sym != 0)
-                   : tc::problem_tiles<tc::Geo<false>::BN>(P.na, P.nb, P.sym != 0);
+      if (pairs)
+        tiles += fp4 ? tc::problem_tiles<tc::Geo<true>::BN, tc::TBM2>(P.na, P.nb, P.sym != 0)
+                     : tc::problem_tiles<tc::Geo<false>::BN, tc::TBM2>(P.na, P.nb, P.sym != 0);
+      else
+        tiles += fp4 ? tc::problem_tiles<tc::Geo<true>::BN>(P.na, P.nb, P.sym != 0)
+                     : tc::problem_tiles<tc::Geo<false>::BN>(P.na, P.nb, P.sym != 0);
       const uint8_t* a = side_out[sel.side_a[q]];
       const uint8_t* b = P.sym ? a : side_out[sel.side_b[q]];
       SA_TRY(tc_encode_map(&maps.m[2 * q], a, P.na, tc::BM, rowb));
-      SA_TRY(tc_encode_map(&maps.m[2 * q + 1], b, P.nb, BN, rowb));
+      SA_TRY(tc_encode_map(&maps.m[2 * q + 1], b, P.nb, pairs ? BN / 2 : BN, rowb));
       TcEpiProb& E = epi.e[q];
       E.nkA = P.nkA;
       E.nkB = P.nkB;
@@ -1077,12 +1144,8 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       return e ? atoi(e) : 1;
     }();
     batch.evict_last = evict_last;
-    static const int debug = [] {
-      const char* e = getenv("SA_K2T_DEBUG");
-      return e ? atoi(e) : 0;
-    }();
     batch.debug = debug;
-    const int64_t grid = tiles < g_num_sms ? tiles : g_num_sms;
+    const int64_t grid = pairs ? 2 * std::min<int64_t>(tiles, g_num_sms / 2) : std::min<int64_t>(tiles, g_num_sms);
     // 16 epilogue warps x 16-column chunks (more warps to hide the store / F /
     // key-term latency, fewer registers each); keys and matrices together
     // (a rank call that also wants numerators) use 8 warps x 32 columns
@@ -1091,8 +1154,13 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       return !(e && atoi(e) == 0);
     }();
     if (ev0) SA_CUDA(cudaEventRecord(ev0, st));   // the GEMM kernel alone (SA_PHASE_GEMM)
-    if (fp4) tc_gemm_mode<true>(mode, keys16, grid, batch, maps, tiles, epi, st);
-    else tc_gemm_mode<false>(mode, keys16, grid, batch, maps, tiles, epi, st);
+    if (pairs) {
+      if (fp4) tc_gemm_mode<true, 2>(mode, keys16, grid, batch, maps, tiles, epi, st);
+      else tc_gemm_mode<false, 2>(mode, keys16, grid, batch, maps, tiles, epi, st);
+    } else {
+      if (fp4) tc_gemm_mode<true, 1>(mode, keys16, grid, batch, maps, tiles, epi, st);
+      else tc_gemm_mode<false, 1>(mode, keys16, grid, batch, maps, tiles, epi, st);
+    }
     SA_LAUNCHED();
     if (ev1) SA_CUDA(cudaEventRecord(ev1, st));
     for (int q = 0; q < np; ++q) {

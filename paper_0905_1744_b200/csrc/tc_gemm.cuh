@@ -54,7 +54,7 @@ static_assert(Geo<true>::STAGE_BYTES % 1024 == 0 && Geo<false>::STAGE_BYTES % 10
 // column slice of SLICE columns), CW columns per tcgen05.ld chunk (16 or 32).
 // Each epilogue warp owns TB bytes of shared memory per slice column
 // (Epi::TAB_BYTES: the per-tile column tables the epilogue stages before the
-// accumulator is ready) plus XB scratch bytes (Epi::xpose_bytes(CW, FP4)).
+// accumulator is ready) plus XB scratch bytes (Epi::xpose_bytes(CW, FP4, CG)).
 __host__ __device__ constexpr int threads_of(int EW) { return (EW + 2) * 32; }
 __host__ __device__ constexpr int slice_of(int EW, int CW, bool FP4) {
   return (((FP4 ? 240 : 256) / (EW / 4) + CW - 1) / CW) * CW;
@@ -249,23 +249,24 @@ __host__ __device__ inline int64_t floor_sum(int64_t n, int64_t m, int64_t a, in
 }
 // tiles of rows [0, i1) of a symmetric problem: row block i keeps column
 // blocks j >= floor(i BM / BN) (the blocks holding some column >= a row)
-template <int BN>
+// (TBM = tile rows: 128, or 256 for a CTA pair)
+template <int BN, int TBM = BM>
 __host__ __device__ inline int64_t sym_tiles_before(int i1, int tn) {
-  return (int64_t)i1 * tn - floor_sum(i1, BN, BM, 0);
+  return (int64_t)i1 * tn - floor_sum(i1, BN, TBM, 0);
 }
-template <int BN>
+template <int BN, int TBM = BM>
 __host__ __device__ inline int64_t problem_tiles(int64_t na, int64_t nb, bool sym) {
-  const int64_t tm = (na + BM - 1) / BM, tn = (nb + BN - 1) / BN;
-  return sym ? sym_tiles_before<BN>((int)tm, (int)tn) : tm * tn;
+  const int64_t tm = (na + TBM - 1) / TBM, tn = (nb + BN - 1) / BN;
+  return sym ? sym_tiles_before<BN, TBM>((int)tm, (int)tn) : tm * tn;
 }
 
-template <int BN>
+template <int BN, int TBM = BM>
 __device__ __forceinline__ Tile decode(const Batch& b, int64_t tile) {
   int pi = 0;
   while (pi + 1 < b.n && b.p[pi + 1].tile_begin <= tile) ++pi;
   const Problem& P = b.p[pi];
   int64_t t = tile - P.tile_begin;
-  const int tm = (P.na + BM - 1) / BM, tn = P.tiles_n;
+  const int tm = (P.na + TBM - 1) / TBM, tn = P.tiles_n;
   const int GROUP = b.group;
   int ti, tj;
   if (!P.sym) {
@@ -277,12 +278,12 @@ __device__ __forceinline__ Tile decode(const Batch& b, int64_t tile) {
     tj = (int)(u / rows);
   } else {
     int g0 = 0;
-    while (g0 + GROUP < tm && sym_tiles_before<BN>(g0 + GROUP, tn) <= t) g0 += GROUP;
-    int64_t u = t - sym_tiles_before<BN>(g0, tn);
+    while (g0 + GROUP < tm && sym_tiles_before<BN, TBM>(g0 + GROUP, tn) <= t) g0 += GROUP;
+    int64_t u = t - sym_tiles_before<BN, TBM>(g0, tn);
     const int g1 = min(g0 + GROUP, tm);
     // column j holds the group's rows i < ceil((j + 1) BN / BM)
-    auto rows_at = [&](int j) { return min(g1, ((j + 1) * BN + BM - 1) / BM) - g0; };
-    int j = (int)((int64_t)g0 * BM / BN);
+    auto rows_at = [&](int j) { return min(g1, ((j + 1) * BN + TBM - 1) / TBM) - g0; };
+    int j = (int)((int64_t)g0 * TBM / BN);
     for (;; ++j) {   // the first few columns hold fewer rows
       const int cnt = rows_at(j);
       if (cnt == g1 - g0 || u < cnt) break;
@@ -294,9 +295,9 @@ __device__ __forceinline__ Tile decode(const Batch& b, int64_t tile) {
   }
   Tile T;
   T.pi = pi;
-  T.row0 = ti * BM;
+  T.row0 = ti * TBM;
   T.col0 = tj * BN;
-  T.ra = min(BM, P.na - T.row0);
+  T.ra = min(TBM, P.na - T.row0);
   T.rb = min(BN, P.nb - T.col0);
   return T;
 }
@@ -308,7 +309,7 @@ __device__ __forceinline__ Tile decode(const Batch& b, int64_t tile) {
 //   static constexpr int TAB_BYTES;                                // table bytes per slice column
 //   __device__ void begin(State&, const Tile&, int row, int lane, int cbeg, int cend,
 //                         uint8_t* tab) const;                       // before the accumulator wait
-//   template <int CW, bool FP4> __device__ void chunk(State&, const Tile&, int row, int col, const uint32_t (&v)[CW],
+//   template <int CW, bool FP4, int CG> __device__ void chunk(State&, const Tile&, int row, int col, const uint32_t (&v)[CW],
 //                         int lane, const uint8_t* tab, int tj, uint8_t* xp) const;   // all lanes, converged
 //   __device__ void end(State&, const Tile&, int row) const;
 // row = tile row of this thread (0..127), [cbeg, cend) = the warp's column
@@ -428,7 +429,7 @@ gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps ma
     const int quad = warp & 3, part = warp >> 2;
     const int row = quad * 32 + lane;
     constexpr int SLICE = slice_of(EW, CW, FP4);
-    constexpr int XB = Epi::xpose_bytes(CW, FP4);
+    constexpr int XB = Epi::xpose_bytes(CW, FP4, 1);
     uint8_t* tab = tab_all + warp * (SLICE * Epi::TAB_BYTES + XB);
     uint8_t* xp = tab + SLICE * Epi::TAB_BYTES;
     const int cbeg = part * SLICE, cend = min(cbeg + SLICE, BN);
@@ -449,7 +450,7 @@ gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps ma
 #pragma unroll
           for (int j = 0; j < CW; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + 8388608.0f) & 0x7FFFFFu;
         }
-        epi.template chunk<CW, FP4>(es, T, row, col, v, lane, tab, col - cbeg, xp);
+        epi.template chunk<CW, FP4, 1>(es, T, row, col, v, lane, tab, col - cbeg, xp);
       }
       fence_before();
       __syncwarp();
@@ -461,6 +462,271 @@ gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps ma
   __syncthreads();
   fence_after();
   if (warp == EPI_WARPS + 1) tmem_dealloc(tmem_base, TMEM_COLS);
+}
+
+
+// ============================================================ CTA pair ====
+// The same contraction with tcgen05.mma.cta_group::2 on a CTA pair (a
+// cluster of 2 CTAs on the two SMs of a TPC): one MMA instruction computes a
+// 256 x BN tile, each CTA holding 128 rows of A and BN / 2 rows of B in its
+// own shared memory and its own 128 x BN accumulator in its own TMEM.  Each
+// SM therefore streams 128 + BN / 2 operand rows per tile instead of
+// 128 + BN -- a third less L2 -> SM traffic for the same tensor work -- and
+// a stage is 31 (32) KB, so more stages fit.
+//   both CTAs, warp EW lane 0: TMA loads of the CTA's A rows / B half into
+//     its own stage slot, completing on the LEADER's full barrier (the
+//     .cta_group::2 form; the leader alone posts expect_tx for both halves);
+//   leader, warp EW+1 lane 0: waits full, issues 4 x tcgen05.mma.cta_group::2
+//     per stage, commits (multicast to both CTAs) the stage's empty barriers
+//     and, per tile, the accumulator's tfull barriers;
+//   both CTAs, warps 0..EW-1: the epilogue on the CTA's own 128 rows; each
+//     warp releases the accumulator on the leader's tempty barrier (2 EW
+//     arrivals per tile, the peer's through its cluster address).
+template <bool FP4>
+struct Geo2 {
+  static constexpr int BN = Geo<FP4>::BN;                 // tile columns (UMMA N, split over the pair)
+  static constexpr int BNH = BN / 2;                      // B rows per CTA
+  static constexpr int B_BYTES = BNH * BK;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // per CTA
+  static constexpr int SF_COL = 2 * BN;
+};
+static_assert(Geo2<true>::STAGE_BYTES % 1024 == 0 && Geo2<false>::STAGE_BYTES % 1024 == 0, "stage alignment");
+constexpr int TBM2 = 2 * BM;   // pair-tile rows
+
+__host__ __device__ constexpr int stages2_of(int EW, int CW, bool FP4, int TB, int XB) {
+  return (232448 - 1024 - 512 - EW * (slice_of(EW, CW, FP4) * TB + XB)) /
+                     (FP4 ? Geo2<true>::STAGE_BYTES : Geo2<false>::STAGE_BYTES) > 8
+             ? 8
+             : (232448 - 1024 - 512 - EW * (slice_of(EW, CW, FP4) * TB + XB)) /
+                   (FP4 ? Geo2<true>::STAGE_BYTES : Geo2<false>::STAGE_BYTES);
+}
+__host__ __device__ constexpr int smem2_of(int EW, int CW, bool FP4, int TB, int XB) {
+  return stages2_of(EW, CW, FP4, TB, XB) * (FP4 ? Geo2<true>::STAGE_BYTES : Geo2<false>::STAGE_BYTES) + 1024 + 512 +
+         EW * (slice_of(EW, CW, FP4) * TB + XB);
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void bar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// TMA load into this CTA's shared memory, completing on the leader CTA's barrier
+__device__ __forceinline__ void tma_2d_pair(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t leader_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_alloc2(uint32_t* slot, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_addr(slot)), "r"(cols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols));
+}
+__device__ __forceinline__ void mma2_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma2_mxf4(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc,
+                                          uint32_t sfa, uint32_t sfb) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n"
+      "}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb));
+}
+// arrive on barrier `bar` (same offset) in both CTAs of the pair when the issued MMAs complete
+__device__ __forceinline__ void mma_commit2(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          s_addr(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+// instruction descriptors with M = 256 (the pair)
+__host__ __device__ constexpr uint32_t idesc2_i8() {
+  return (2u << 4) | ((uint32_t)(Geo<false>::BN >> 3) << 17) | ((uint32_t)(TBM2 >> 4) << 24);
+}
+__host__ __device__ constexpr uint32_t idesc2_mxf4() {
+  return (1u << 7) | (1u << 10) | ((uint32_t)(Geo<true>::BN >> 3) << 17) | (1u << 23) | ((uint32_t)(TBM2 >> 4) << 24);
+}
+
+template <class Epi, int EW, int CW, bool FP4>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(threads_of(EW), 1)
+gemm2_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps maps, int64_t total_tiles, Epi epi) {
+  using G = Geo2<FP4>;
+  constexpr int BN = G::BN, BNH = G::BNH, STAGE_BYTES = G::STAGE_BYTES;
+  constexpr int XB = Epi::xpose_bytes(CW, FP4, 2);
+  constexpr int NST = stages2_of(EW, CW, FP4, Epi::TAB_BYTES, XB);
+  static_assert(NST >= 3, "CTA-pair stages");
+  static_assert(EW % 4 == 0 && BN % CW == 0, "epilogue geometry");
+  constexpr int EPI_WARPS = EW;
+  if (epi.skip()) return;   // uniform over the grid (device state word)
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const uint32_t raw_s = s_addr(smem_raw);
+  const uint32_t base_s = (raw_s + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (base_s - raw_s);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * STAGE_BYTES);
+  uint64_t* empty = full + NST;
+  uint64_t* tfull = empty + NST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint8_t* tab_all = smem + NST * STAGE_BYTES + 512;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int64_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (warp == EPI_WARPS && lane == 0) {
+    for (int s = 0; s < NST; ++s) {
+      bar_init(&full[s], 1);
+      bar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      bar_init(&tfull[b], 1);
+      bar_init(&tempty[b], 2 * EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == EPI_WARPS + 1) tmem_alloc2(tmem_slot, TMEM_COLS);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+  if constexpr (FP4) {
+    if (warp < 4)
+      for (int c = G::SF_COL; c < TMEM_COLS; c += 8)
+        tmem_st8(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, 0x7F7F7F7Fu);
+    fence_before();
+  }
+  cluster_sync_all();   // barriers initialised and scale factors written in both CTAs
+  fence_after();
+
+  if (warp == EPI_WARPS) {
+    // ------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      const uint32_t full0_leader = map_to_rank(s_addr(&full[0]), 0);   // the leader's full barriers
+      const bool no_tma = (batch.debug & 2) != 0;
+      uint32_t g = 0;
+      for (int64_t tile = pair; tile < total_tiles; tile += npairs) {
+        const Tile T = decode<BN, TBM2>(batch, tile);
+        const Problem& P = batch.p[T.pi];
+        const int nkb = *reinterpret_cast<const volatile int32_t*>(P.kblocks);
+        const CUtensorMap* ma = &maps.m[2 * P.map];
+        const CUtensorMap* mb = &maps.m[2 * P.map + 1];
+        const int arow = T.row0 + (int)rank * BM, brow = T.col0 + (int)rank * BNH;
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const uint32_t slot = g % NST;
+          if (g >= (uint32_t)NST) bar_wait(&empty[slot], ((g / NST) - 1) & 1u);
+          if (no_tma) {
+            if (leader) bar_arrive(&full[slot]);
+            continue;
+          }
+          if (leader) bar_arrive_tx(&full[slot], 2 * STAGE_BYTES);
+          const uint32_t dst = base_s + slot * STAGE_BYTES;
+          const uint32_t fb = full0_leader + slot * 8u;
+          tma_2d_pair(dst, ma, kb * BK, arow, fb);
+          tma_2d_pair(dst + A_BYTES, mb, kb * BK, brow, fb);
+        }
+      }
+    }
+  } else if (warp == EPI_WARPS + 1) {
+    // ------------------------------------------------ MMA issuer (leader)
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = FP4 ? idesc2_mxf4() : idesc2_i8();
+      const uint32_t sfa = tmem_base + (uint32_t)G::SF_COL, sfb = tmem_base + (uint32_t)G::SF_COL + 16u;
+      const bool no_mma = (batch.debug & 1) != 0;
+      uint32_t g = 0, lt = 0;
+      for (int64_t tile = pair; tile < total_tiles; tile += npairs, ++lt) {
+        const Tile T = decode<BN, TBM2>(batch, tile);
+        const Problem& P = batch.p[T.pi];
+        const int nkb = *reinterpret_cast<const volatile int32_t*>(P.kblocks);
+        const uint32_t buf = lt & 1u;
+        if (lt >= 2) bar_wait(&tempty[buf], ((lt >> 1) - 1) & 1u);
+        fence_after();
+        const uint32_t d = tmem_base + buf * (uint32_t)BN;
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const uint32_t slot = g % NST;
+          bar_wait(&full[slot], (g / NST) & 1u);
+          fence_after();
+          const uint32_t sa_ = base_s + slot * STAGE_BYTES;
+          const uint64_t da = sw128_desc(sa_), db = sw128_desc(sa_ + A_BYTES);
+          if (!no_mma) {
+#pragma unroll
+            for (int k = 0; k < BK / UKB; ++k) {
+              const uint64_t off = (uint64_t)((k * UKB) >> 4);
+              if constexpr (FP4) mma2_mxf4(d, da + off, db + off, idesc, (kb | k) != 0, sfa, sfb);
+              else mma2_i8(d, da + off, db + off, idesc, (kb | k) != 0);
+            }
+          }
+          mma_commit2(&empty[slot]);
+        }
+        mma_commit2(&tfull[buf]);
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue warps (both CTAs)
+    const int quad = warp & 3, part = warp >> 2;
+    const int row = quad * 32 + lane;
+    constexpr int SLICE = slice_of(EW, CW, FP4);
+    uint8_t* tab = tab_all + warp * (SLICE * Epi::TAB_BYTES + XB);
+    uint8_t* xp = tab + SLICE * Epi::TAB_BYTES;
+    const int cbeg = part * SLICE, cend = min(cbeg + SLICE, BN);
+    const uint32_t tempty_leader = map_to_rank(s_addr(&tempty[0]), 0);
+    const bool no_epi = (batch.debug & 4) != 0;
+    typename Epi::State es;
+    uint32_t lt = 0;
+    for (int64_t tile = pair; tile < total_tiles; tile += npairs, ++lt) {
+      Tile T = decode<BN, TBM2>(batch, tile);
+      T.row0 += (int)rank * BM;                        // this CTA's half of the pair tile
+      T.ra = max(0, min(BM, T.ra - (int)rank * BM));
+      const uint32_t buf = lt & 1u;
+      epi.begin(es, T, row, lane, cbeg, cend, tab);
+      bar_wait(&tfull[buf], (lt >> 1) & 1u);
+      fence_after();
+#pragma unroll 1
+      for (int col = cbeg; col < (no_epi ? cbeg : cend); col += CW) {
+        uint32_t v[CW];
+        tmem_ld<CW>(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + col), v);
+        if constexpr (FP4) {
+#pragma unroll
+          for (int j = 0; j < CW; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + 8388608.0f) & 0x7FFFFFu;
+        }
+        epi.template chunk<CW, FP4, 2>(es, T, row, col, v, lane, tab, col - cbeg, xp);
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) bar_arrive_cluster(tempty_leader + buf * 8u);
+      epi.end(es, T, row);
+    }
+  }
+  fence_before();
+  __syncthreads();
+  cluster_sync_all();   // no CTA leaves while its peer may still signal its barriers
+  fence_after();
+  if (warp == EPI_WARPS + 1) tmem_dealloc2(tmem_base, TMEM_COLS);
 }
 
 }  // namespace tc

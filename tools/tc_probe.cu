@@ -23,10 +23,10 @@ struct WriteEpi {
   int64_t ldc;
   struct State {};
   static constexpr int TAB_BYTES = 16;
-  __host__ __device__ static constexpr int xpose_bytes(int, bool) { return 0; }
+  __host__ __device__ static constexpr int xpose_bytes(int, bool, int) { return 0; }
   __device__ bool skip() const { return false; }
   __device__ void begin(State&, const Tile&, int, int, int, int, uint8_t*) const {}
-  template <int CW, bool FP4>
+  template <int CW, bool FP4, int CG>
   __device__ void chunk(State&, const Tile& T, int row, int col, const uint32_t (&v)[CW], int, const uint8_t*,
                         int, uint8_t*) const {
     if (row >= T.ra) return;
