@@ -458,11 +458,16 @@ struct TcEpiProb {
 // re-read from L2.
 __device__ __forceinline__ void st_out(uint16_t* p, uint16_t v) { __stcs(reinterpret_cast<unsigned short*>(p), v); }
 __device__ __forceinline__ void st_out(double* p, double v) { __stcs(p, v); }
-__device__ __forceinline__ void st_out_if(bool on, uint16_t* p, uint16_t v) {
-  if (on) st_out(p, v);
+// experiment flavours (SA_K2T_DEBUG): 8 skip, 16 plain st.global, 32 st.global.L1::no_allocate, else .cs
+__device__ __forceinline__ void st_out_if(int fl, uint16_t* p, uint16_t v) {
+  if (fl == 0) st_out(p, v);
+  else if (fl == 16) *p = v;
+  else if (fl == 32) asm volatile("st.global.L1::no_allocate.b16 [%0], %1;" ::"l"(p), "h"(v) : "memory");
 }
-__device__ __forceinline__ void st_out_if(bool on, double* p, double v) {
-  if (on) st_out(p, v);
+__device__ __forceinline__ void st_out_if(int fl, double* p, double v) {
+  if (fl == 0) st_out(p, v);
+  else if (fl == 16) *p = v;
+  else if (fl == 32) asm volatile("st.global.L1::no_allocate.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 // 96-bit (lo, hi) add
 __device__ __forceinline__ void add96(uint64_t& lo, uint32_t& hi, uint64_t blo, uint32_t bhi) {
@@ -732,7 +737,7 @@ struct KeyMatEpi {
     const bool rows_all = wrow0 + 32 <= T.row0 + T.ra;   // warp-uniform
     const double2* rtab = reinterpret_cast<const double2*>(xp + 64 * CW);   // written by chunk() at tj = 0
     if (upper && ncols == CW && rows_all) {
-      const bool stores = (dbg & 8) == 0;
+      const int stores = dbg & 56;
       // ---- fast path (all 32 rows and CW columns exist, no diagonal).
       // (1) lanes = rows: F of every pair; the mirrored element (gc, row)
       // with lanes = consecutive rows (coalesced); C staged in the warp's
