@@ -316,7 +316,7 @@ int sa_ctx_engine(const sa_ctx* ctx) {
 
 int sa_ctx_tc_operand(const sa_ctx* ctx) {
   if (!ctx || !ctx->last_tc) return -1;
-  return tc_fp4_operands() ? 1 : 0;
+  return tc_last_fp4() ? 1 : 0;
 }
 
 int32_t sa_ctx_tc_columns(const sa_ctx* ctx, int32_t* cols_h, int32_t max) {

@@ -131,7 +131,8 @@ sa_status to_u8_launch(const uint16_t* p16, int64_t n, int32_t stride16, int32_t
 // cols_out[i] (device, nullable) = kept layer columns K' of problem i (i < SA_TC_COLS_MAX).
 constexpr int TC_MAX_BINS = 8192;
 sa_status f_division_selftest(int64_t* mismatches_h);
-bool tc_fp4_operands();   // K2T operand format: true = packed e2m1 (kind::mxf4), false = u8 (kind::i8)
+bool tc_fp4_operands();   // K2T operand format for the next launch: true = packed e2m1 (kind::mxf4), false = u8
+bool tc_last_fp4();       // the format of the last K2T launch
 // sim[i][j] = num[i][j] / min(nkA[i], nkB[j]) (fp64, IEEE RN; 0 when the min is 0), row stride ld.
 sa_status ratio_launch(const uint16_t* num, const int32_t* nkA, const int32_t* nkB, int64_t na, int64_t nb,
                        int64_t ld, double* sim, cudaStream_t st, const uint32_t* state = nullptr);

@@ -29,6 +29,7 @@
 //                    uint16 C / fp64 F matrices (mirrored for symmetric).
 // When a launch is infeasible every K2T kernel returns at once and the
 // guarded SAD / u16 engines (minsum.cu) run instead: exact in every case.
+#include <atomic>
 #include <cstring>
 
 #include "common.cuh"
@@ -952,14 +953,15 @@ static void tc_gemm_mode(int mode, bool keys16, int64_t grid, const tc::Batch& b
   else tc_gemm<KeyMatEpi<EPI_KEYS | EPI_NUM>, 8, CW_ALL, FP4, CG>(grid, batch, maps, tiles, epi, st);   // never with F
 }
 
-// CTA pairs (tcgen05 cta_group::2, tc_gemm.cuh) unless SA_K2T_PAIR=0
-static bool tc_pairs() {
-  static const bool on = [] {
-    const char* e = getenv("SA_K2T_PAIR");
-    return !(e && atoi(e) == 0);
-  }();
-  return on;
+// Format / pair switches are read at every launch (a test can switch them);
+// g_last_fp4 = the format of the last K2T launch in this process (sa_ctx_tc_operand).
+static bool env_on(const char* name, bool dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) != 0 : dflt;
 }
+static std::atomic<int> g_last_fp4{1};
+// CTA pairs (tcgen05 cta_group::2, tc_gemm.cuh) unless SA_K2T_PAIR=0
+static bool tc_pairs() { return env_on("SA_K2T_PAIR", true); }
 
 static sa_status tc_encode_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int box_rows, int64_t rowb) {
   auto enc = tensor_map_encoder();
@@ -1001,6 +1003,7 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
   const int stride16 = 2 * ldw16;
   const bool fp4 = tc_fp4_operands();
   const bool pairs = tc_pairs();
+  g_last_fp4.store(fp4 ? 1 : 0);
   const int64_t rowb = fp4 ? TC_KCAP / 2 : TC_KCAP;
   const int kbc = fp4 ? 256 : 128;
   static const bool fpass = [] {
@@ -1180,13 +1183,8 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
 // Operand format of K2T: packed e2m1 0/1.0 columns on kind::mxf4 (default: twice
 // the kind::i8 MMA rate, half the operand bytes; exact, tc_gemm.cuh) or u8 0/1
 // columns on kind::i8 (SA_K2T_FP4=0).
-bool tc_fp4_operands() {
-  static const bool fp4 = [] {
-    const char* e = getenv("SA_K2T_FP4");
-    return !(e && atoi(e) == 0);
-  }();
-  return fp4;
-}
+bool tc_fp4_operands() { return env_on("SA_K2T_FP4", true); }
+bool tc_last_fp4() { return g_last_fp4.load() != 0; }
 
 sa_status f_division_selftest(int64_t* mismatches_h) {
   SA_TRY(ensure_recip_tables_tu(0));

@@ -232,22 +232,30 @@ def test_tc_falls_back_on_column_overflow(ctx, monkeypatch):
     assert np.array_equal(sim.cpu().numpy(), Fo)
 
 
+@pytest.mark.parametrize("fp4,pair", [(1, 1), (1, 0), (0, 1), (0, 0)])
 @pytest.mark.parametrize("n,hi,dup", [(600, 420, 0), (531, 3000, 40), (129, 60, 0), (256, 700, 9)])
-def test_tc_layers_random(ctx, monkeypatch, n, hi, dup):
-    """K2T against the oracle on ragged sets that span several 128 x 256 tiles,
-    with repeated 3-mers (several threshold layers) and duplicate rows; keys of
-    the self-pool (symmetric: row + mirrored column sums) and of a rectangular
-    pool, numerators and F."""
+def test_tc_layers_random(ctx, monkeypatch, n, hi, dup, fp4, pair):
+    """K2T against the oracle on ragged sets that span several tiles (and a
+    ragged CTA-pair half), with repeated 3-mers (several threshold layers) and
+    duplicate rows; keys of the self-pool (symmetric: row + mirrored column
+    sums) and of a rectangular pool, numerators and F; every operand format
+    (e2m1 kind::mxf4 / u8 kind::i8) with and without CTA pairs (cta_group::2)."""
     monkeypatch.setenv("SA_ENGINE", "auto")
+    monkeypatch.setenv("SA_K2T_FP4", str(fp4))
+    monkeypatch.setenv("SA_K2T_PAIR", str(pair))
     ds = _rand_set(9000 + n, n, 0, hi, dup=dup)
     res, offs = to_dev(ds)
     P, nk = B.sa_kmer_profiles(ctx, res, offs)
     Po, nko = kmer.profiles(ds.residues, ds.offsets)
     num, sim = B.sa_bucket_similarity(ctx, P, nk)
     assert ctx.engine() == "tc"
+    assert ctx.tc_operand() == ("e2m1" if fp4 else "u8")
     Co, Fo = partition.bucket_similarity(Po, nko, np.arange(n))
     assert np.array_equal(num.cpu().numpy(), Co)
     assert np.array_equal(sim.cpu().numpy(), Fo)
+    nums, sims = B.sa_bucket_similarity_batch(ctx, P, nk, [0, n], ld_align=16)   # padded rows
+    assert np.array_equal(nums[0].cpu().numpy(), Co)
+    assert np.array_equal(sims[0].cpu().numpy(), Fo)
     D = kmer.denominator_matrix(nko, nko)
     keys, _, _ = B.sa_kmer_rank(ctx, P, nk, P, nk)
     assert ctx.engine() == "tc"
