@@ -176,7 +176,7 @@ static inline cudaEvent_t ev_end(sa_ctx* c, int ph);
 
 // Enqueue the problems (A / B pointers given into the u16 operands).
 static sa_status launch_ops(sa_ctx* c, const EngineOps& E, const std::vector<MsProblem>& probs16, cudaStream_t st,
-                            cudaEvent_t ev0, cudaEvent_t ev1) {
+                            cudaEvent_t ev0, cudaEvent_t ev1, TcCarry* keep = nullptr, const TcCarry* use = nullptr) {
   c->last_enc = E.mode;
   c->last_tc = E.tc;
   c->last_tc_probs = 0;
@@ -186,7 +186,7 @@ static sa_status launch_ops(sa_ctx* c, const EngineOps& E, const std::vector<MsP
   if (E.tc) {
     c->last_tc_probs = (int)probs16.size();
     SA_TRY(tc_launch(probs16, E.a16.ldw, E.bins, E.guard, E.guard + SA_TC_COLS_AT, st, ev_begin(c, SA_PHASE_GEMM),
-                     ev_end(c, SA_PHASE_GEMM)));
+                     ev_end(c, SA_PHASE_GEMM), keep, use));
     for (const auto& cv : E.conv)
       SA_TRY(to_u8_launch(cv.p16, cv.n, stride_u16(E.bins), E.bins, cv.p8, stride_u8(E.bins), E.guard, st, true));
   }
@@ -541,6 +541,11 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
   EngineOps E;
   SA_TRY(prepare_ops(c, scratch, a.prof, n, a.prof, n, a.stride, true, &E, st));
 
+  // K2T operand rows built for S2a's blocks are reused by S2d's query side
+  // (the same rows: first dense layers and seen-once planes carried over)
+  TcCarry carry;
+  carry.scratch = &scratch;
+
   // ---- S2a: local rank of every member against its own block
   SA_TRY(rec(ev_begin(c, SA_PHASE_S2A), st));
   {
@@ -557,7 +562,7 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
       apply_form(c, pr);
       probs.push_back(pr);
     }
-    SA_TRY(launch_ops(c, E, probs, st, nullptr, nullptr));
+    SA_TRY(launch_ops(c, E, probs, st, nullptr, nullptr, &carry));
   }
   SA_TRY(rec(ev_end(c, SA_PHASE_S2A), st));
 
@@ -601,7 +606,7 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
     pr.sym = 0;
     pr.keyA = gkey;
     apply_form(c, pr);
-    SA_TRY(launch_ops(c, E2, {pr}, st, nullptr, nullptr));
+    SA_TRY(launch_ops(c, E2, {pr}, st, nullptr, nullptr, nullptr, &carry));
   }
   SA_TRY(rec(ev_end(c, SA_PHASE_S2D), st));
 

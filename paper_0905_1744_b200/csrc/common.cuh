@@ -139,8 +139,24 @@ sa_status ratio_launch(const uint16_t* num, const int32_t* nkA, const int32_t* n
 constexpr int SA_DCOUNT_WORDS = 256;   // ctx->dcount: [0..3] guard words, [16..80) K2T column counts
 constexpr int SA_TC_COLS_AT = 16;
 constexpr int SA_TC_COLS_MAX = 64;
+// Operand rows carried from one K2T launch to the next on the same u16 rows
+// (sa_partition: S2a's blocks -> S2d's query side): the rows with their first
+// dense layers already written and the OR of their seen-once planes.  The
+// memory belongs to the caller's Scratch (it must outlive both launches).
+struct TcCarry {
+  Scratch* scratch = nullptr;        // where a keeping launch allocates (nullptr: nothing kept)
+  bool valid = false;
+  const uint32_t* src = nullptr;     // first u16 row they were built from
+  int64_t nrows = 0;
+  bool fp4 = false;
+  uint8_t* rows = nullptr;           // [nrows][row bytes]
+  uint32_t* seen1 = nullptr;         // seen-once planes (one plane, all layers)
+  int32_t* ndense = nullptr;         // [np] dense layers each problem of the building launch kept
+  int np = 0;
+};
 sa_status tc_launch(const std::vector<MsProblem>& probs, int ldw16, int32_t bins, uint32_t* state,
-                    uint32_t* cols_out, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1);
+                    uint32_t* cols_out, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1,
+                    TcCarry* keep = nullptr, const TcCarry* use = nullptr);
 sa_status ensure_recip_tables(cudaStream_t st);
 
 // ------------------------------------------------------ profiles (K1) --

@@ -119,7 +119,7 @@ constexpr int TC_SPEC = 2;
 template <bool FP4>
 __global__ void __launch_bounds__(TC_HIST_THREADS)
 tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut O, int stride16, int bins,
-               uint32_t* __restrict__ planes, uint32_t* __restrict__ state) {
+               uint32_t* __restrict__ planes, uint32_t* __restrict__ state, int64_t hist_from) {
   constexpr int64_t ROWB = FP4 ? TC_KCAP / 2 : TC_KCAP;
   const int dw = (bins + 15) & ~15;                      // columns per dense layer
   const int64_t layer_bytes = FP4 ? dw / 2 : dw;
@@ -128,8 +128,9 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
   const int w = threadIdx.x;
   const bool active = w * 32 < stride16;
   for (int l = 0; l < 2 * ND; ++l) deep[l * TC_WPL + w] = 0u;
-  const int64_t R = S.row_begin[S.n];
-  const int64_t r0 = blockIdx.x * R / gridDim.x, r1 = (blockIdx.x + 1) * R / gridDim.x;
+  // rows [hist_from, R): a carried side (TcCarry) comes first and is skipped
+  const int64_t R = S.row_begin[S.n] - hist_from;
+  const int64_t r0 = hist_from + blockIdx.x * R / gridDim.x, r1 = hist_from + (blockIdx.x + 1) * R / gridDim.x;
   uint32_t s1[TC_HREG], s2[TC_HREG];
 #pragma unroll
   for (int l = 0; l < TC_HREG; ++l) s1[l] = s2[l] = 0u;
@@ -212,6 +213,18 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((w & 31) == 0 && mx) atomicMax(&state[0], mx);
+}
+
+// OR of the seen-once planes of sides [0, nsides) (the carried query side of a
+// later rectangular launch: a column can contribute if any of its rows reaches it)
+__global__ void tc_or_planes_kernel(const uint32_t* __restrict__ planes, int nsides, uint32_t* __restrict__ out,
+                                    const uint32_t* __restrict__ state) {
+  if (tc_infeasible(state)) return;
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < TC_PLANE; w += gridDim.x * blockDim.x) {
+    uint32_t m = 0;
+    for (int sd = 0; sd < nsides; ++sd) m |= planes[(int64_t)sd * 2 * TC_PLANE + w];
+    out[w] = m;
+  }
 }
 
 // ------------------------------------------------------ column select ----
@@ -329,12 +342,17 @@ __device__ __forceinline__ int TcOutProbs(const TcOut& O, int nsides) {
 template <bool FP4>
 __global__ void __launch_bounds__(256)
 tc_dense_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut O, int stride16, int bins,
-                const int32_t* __restrict__ ndense, const uint32_t* __restrict__ state) {
+                const int32_t* __restrict__ ndense, const uint32_t* __restrict__ state,
+                const int32_t* __restrict__ carry_nd, int carry_np) {
   constexpr int64_t ROWB = FP4 ? TC_KCAP / 2 : TC_KCAP;
   if (tc_infeasible(state)) return;
   int ndmax = 0;   // no problem keeps more dense layers than the histogram pass wrote: nothing to do
   for (int q = 0; q < TcOutProbs(O, S.n); ++q) ndmax = max(ndmax, ndense[q]);
-  if (ndmax <= TC_SPEC) return;
+  // a carried side 0 (TcCarry) holds the layers below min(TC_SPEC, nd of every
+  // problem of the launch that built it): its build overwrote the rest
+  int cfrom = TC_SPEC;
+  for (int q = 0; q < carry_np; ++q) cfrom = min(cfrom, carry_nd[q]);
+  if (ndmax <= TC_SPEC && !(carry_np > 0 && cfrom < ndense[O.prob[0]])) return;
   const int dwc = ((bins + 15) & ~15) / 16;
   const int64_t items = S.row_begin[S.n] * dwc;
   for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items;
@@ -348,13 +366,14 @@ tc_dense_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut
       else hi = mid - 1;
     }
     const int nd = ndense[O.prob[lo]];
-    if (nd <= TC_SPEC) continue;
+    const int lfrom = (carry_np > 0 && lo == 0) ? cfrom : TC_SPEC;
+    if (nd <= lfrom) continue;
     const int64_t r = g - S.row_begin[lo];
     const uint4* src = reinterpret_cast<const uint4*>(S.rows[lo] + r * (int64_t)stride16 + c * 16);
     const uint4 v0 = src[0], v1 = src[1];
     const uint32_t vs[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
     uint8_t* rowp = O.out[lo] + r * ROWB;
-    for (int l = TC_SPEC; l < nd; ++l) {   // layers 1 .. TC_SPEC: written by tc_hist_kernel
+    for (int l = lfrom; l < nd; ++l) {   // layers 1 .. TC_SPEC: written by tc_hist_kernel
       const uint32_t bias = (0x8000u - (uint32_t)(l + 1)) * 0x00010001u;
       uint32_t o[4];
 #pragma unroll
@@ -979,7 +998,8 @@ static sa_status tc_encode_map(CUtensorMap* m, const uint8_t* base, int64_t rows
 
 
 sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t bins, uint32_t* state,
-                    uint32_t* cols_out, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1) {
+                    uint32_t* cols_out, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1, TcCarry* keep,
+                    const TcCarry* use) {
   SA_TRY(ensure_recip_tables_tu(st));
   static int g_num_sms = 0;
   if (g_num_sms == 0) {
@@ -1040,31 +1060,65 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     SA_ALLOC(planes, uint32_t, (size_t)sides.n * 2 * TC_PLANE);
     SA_ALLOC(collist, uint32_t, (size_t)np * TC_KCAP);
     SA_ALLOC(kblocks, int32_t, np);
-    SA_ALLOC(ndense, int32_t, np);
+    int32_t* ndense = (keep && keep->scratch && i0 == 0) ? keep->scratch->alloc<int32_t>(np) : scratch.alloc<int32_t>(np);
+    if (!ndense) return fail(SA_E_NOMEM, "scratch allocation of K2T dense-layer counts failed");
     SA_CUDA(cudaMemsetAsync(planes, 0, (size_t)sides.n * 2 * TC_PLANE * 4, st));
     const int64_t R = sides.row_begin[sides.n];
-    // operand rows: one output per side (its problem's column list)
+    // operand rows: one output per side (its problem's column list).  A
+    // keeping launch (S2a) puts all its sides (contiguous source rows) in one
+    // buffer of the caller's scratch; a launch given a carry whose rows are
+    // its first side (S2d's queries) reuses rows, dense layers and planes.
+    const bool carried = use && use->valid && use->fp4 == fp4 && np == 1 && sides.n >= 1 &&
+                         reinterpret_cast<const uint32_t*>(sides.rows[0]) == use->src && side_n[0] == use->nrows;
+    bool keeping = keep && keep->scratch && i0 == 0 && probs.size() <= (size_t)tc::MAXPROB;
+    for (int sd = 1; keeping && sd < sides.n; ++sd)
+      keeping = sides.rows[sd] == sides.rows[0] + (sides.row_begin[sd] - sides.row_begin[0]) * (int64_t)stride16;
     uint8_t* side_out[2 * tc::MAXPROB];
+    uint8_t* kept = keeping ? keep->scratch->alloc<uint8_t>((size_t)R * rowb) : nullptr;
+    if (keeping && !kept) return fail(SA_E_NOMEM, "scratch allocation of K2T operand rows failed");
     for (int sd = 0; sd < sides.n; ++sd) {
-      uint8_t* o = scratch.alloc<uint8_t>((size_t)side_n[sd] * rowb);
+      uint8_t* o = nullptr;
+      if (carried && sd == 0) o = use->rows;
+      else if (kept) o = kept + sides.row_begin[sd] * rowb;
+      else o = scratch.alloc<uint8_t>((size_t)side_n[sd] * rowb);
       if (!o) return fail(SA_E_NOMEM, "scratch allocation of K2T operand rows failed");
       side_out[sd] = outs.out[sd] = o;
     }
-    const int hx = (int)std::max<int64_t>(1, std::min<int64_t>((R + TC_HIST_ROWS - 1) / TC_HIST_ROWS, 4 * g_num_sms));
+    if (carried)
+      SA_CUDA(cudaMemcpyAsync(planes, use->seen1, TC_PLANE * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+    const int64_t hfrom = carried ? sides.row_begin[1] : 0;
+    const int hx = (int)std::max<int64_t>(
+        1, std::min<int64_t>((R - hfrom + TC_HIST_ROWS - 1) / TC_HIST_ROWS, 4 * g_num_sms));
     const int hsm = 2 * (TC_LCAP - TC_HREG) * TC_WPL * 4;
-    if (fp4) tc_hist_kernel<true><<<hx, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state);
-    else tc_hist_kernel<false><<<hx, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state);
+    if (fp4) tc_hist_kernel<true><<<hx, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, hfrom);
+    else tc_hist_kernel<false><<<hx, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, hfrom);
     SA_LAUNCHED();
+    if (kept) {
+      uint32_t* s1 = keep->scratch->alloc<uint32_t>(TC_PLANE);
+      if (!s1) return fail(SA_E_NOMEM, "scratch allocation of K2T planes failed");
+      tc_or_planes_kernel<<<TC_PLANE / 256, 256, 0, st>>>(planes, sides.n, s1, state);
+      SA_LAUNCHED();
+      keep->valid = true;
+      keep->src = reinterpret_cast<const uint32_t*>(sides.rows[0]);
+      keep->nrows = R;
+      keep->fp4 = fp4;
+      keep->rows = kept;
+      keep->seen1 = s1;
+      keep->ndense = ndense;
+      keep->np = np;
+    }
     tc_select_kernel<<<np, 1024, 0, st>>>(sel, planes, bins, kbc, collist, kblocks, ndense, state, cols_out);
     SA_LAUNCHED();
     const int bx = (int)std::max<int64_t>(1, std::min<int64_t>(R, 4 * g_num_sms));
+    const int32_t* cnd = carried ? use->ndense : nullptr;
+    const int cnp = carried ? use->np : 0;
     if (fp4) {
-      tc_dense_kernel<true><<<8 * g_num_sms, 256, 0, st>>>(sides, outs, stride16, bins, ndense, state);
+      tc_dense_kernel<true><<<8 * g_num_sms, 256, 0, st>>>(sides, outs, stride16, bins, ndense, state, cnd, cnp);
       SA_LAUNCHED();
       tc_build_kernel<true><<<bx, TC_BUILD_THREADS, 0, st>>>(sides, outs, stride16, bins, collist, kblocks, ndense,
                                                              state);
     } else {
-      tc_dense_kernel<false><<<8 * g_num_sms, 256, 0, st>>>(sides, outs, stride16, bins, ndense, state);
+      tc_dense_kernel<false><<<8 * g_num_sms, 256, 0, st>>>(sides, outs, stride16, bins, ndense, state, cnd, cnp);
       SA_LAUNCHED();
       tc_build_kernel<false><<<bx, TC_BUILD_THREADS, 0, st>>>(sides, outs, stride16, bins, collist, kblocks, ndense,
                                                               state);
