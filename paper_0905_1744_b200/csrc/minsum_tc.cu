@@ -949,26 +949,32 @@ template <bool FP4, int CG>
 static sa_status tc_configure_all() {
   constexpr int CW_ALL = FP4 ? 16 : 32;
   sa_status cs = tc_configure<KeyMatEpi<EPI_KEYS>, 16, 16, FP4, CG>();
+  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_KEYS>, 12, 16, FP4, CG>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_KEYS>, 8, CW_ALL, FP4, CG>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM>, 16, 16, FP4, CG>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_SIM>, 16, 16, FP4, CG>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4, CG>();
+  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 8, 16, FP4, CG>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_KEYS | EPI_NUM>, 8, CW_ALL, FP4, CG>();
   return cs;
 }
 template <bool FP4, int CG>
-static void tc_gemm_mode(int mode, bool keys16, int64_t grid, const tc::Batch& batch, const tc::Maps& maps,
+static void tc_gemm_mode(int mode, int keysw, bool mats16, int64_t grid, const tc::Batch& batch, const tc::Maps& maps,
                          int64_t tiles, const KeyMatEpi<EPI_ALL>& epi, cudaStream_t st) {
   constexpr int CW_ALL = FP4 ? 16 : 32;
   // 16 epilogue warps x 16-column chunks (more warps to hide the store / F /
   // key-term latency, fewer registers each); keys and matrices together
   // (a rank call that also wants numerators) use 8 warps
-  if (mode == EPI_KEYS && keys16) tc_gemm<KeyMatEpi<EPI_KEYS>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
+  if (mode == EPI_KEYS && keysw == 16) tc_gemm<KeyMatEpi<EPI_KEYS>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
+  else if (mode == EPI_KEYS && keysw == 12)
+    tc_gemm<KeyMatEpi<EPI_KEYS>, 12, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
   else if (mode == EPI_KEYS) tc_gemm<KeyMatEpi<EPI_KEYS>, 8, CW_ALL, FP4, CG>(grid, batch, maps, tiles, epi, st);
   else if (mode == EPI_NUM) tc_gemm<KeyMatEpi<EPI_NUM>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
   else if (mode == EPI_SIM) tc_gemm<KeyMatEpi<EPI_SIM>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
-  else if ((mode & EPI_KEYS) == 0)
+  else if ((mode & EPI_KEYS) == 0 && mats16)
     tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
+  else if ((mode & EPI_KEYS) == 0)
+    tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 8, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
   else tc_gemm<KeyMatEpi<EPI_KEYS | EPI_NUM>, 8, CW_ALL, FP4, CG>(grid, batch, maps, tiles, epi, st);   // never with F
 }
 
@@ -1211,17 +1217,22 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     // 16 epilogue warps x 16-column chunks (more warps to hide the store / F /
     // key-term latency, fewer registers each); keys and matrices together
     // (a rank call that also wants numerators) use 8 warps x 32 columns
-    static const bool keys16 = [] {   // SA_K2T_KEYS16=0: the 8-warp key epilogue
-      const char* e = getenv("SA_K2T_KEYS16");
-      return !(e && atoi(e) == 0);
+    // epilogue warps (16 or 8) of the key and matrix instantiations (read per launch)
+    // (8 key warps: fewer epilogue warps competing with the MMA / TMA warps for
+    // issue slots; the matrix epilogue needs its 16 to keep up with the stores)
+    const int keysw = [] {
+      const char* e = getenv("SA_K2T_KEYSW");
+      const int w = e ? atoi(e) : 8;
+      return w == 12 || w == 16 ? w : 8;
     }();
+    const bool mats16 = env_on("SA_K2T_MATS16", true);
     if (ev0) SA_CUDA(cudaEventRecord(ev0, st));   // the GEMM kernel alone (SA_PHASE_GEMM)
     if (pairs) {
-      if (fp4) tc_gemm_mode<true, 2>(mode, keys16, grid, batch, maps, tiles, epi, st);
-      else tc_gemm_mode<false, 2>(mode, keys16, grid, batch, maps, tiles, epi, st);
+      if (fp4) tc_gemm_mode<true, 2>(mode, keysw, mats16, grid, batch, maps, tiles, epi, st);
+      else tc_gemm_mode<false, 2>(mode, keysw, mats16, grid, batch, maps, tiles, epi, st);
     } else {
-      if (fp4) tc_gemm_mode<true, 1>(mode, keys16, grid, batch, maps, tiles, epi, st);
-      else tc_gemm_mode<false, 1>(mode, keys16, grid, batch, maps, tiles, epi, st);
+      if (fp4) tc_gemm_mode<true, 1>(mode, keysw, mats16, grid, batch, maps, tiles, epi, st);
+      else tc_gemm_mode<false, 1>(mode, keysw, mats16, grid, batch, maps, tiles, epi, st);
     }
     SA_LAUNCHED();
     if (ev1) SA_CUDA(cudaEventRecord(ev1, st));
