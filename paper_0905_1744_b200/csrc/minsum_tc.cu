@@ -622,6 +622,11 @@ struct KeyMatEpi {
     const bool col = yc > yr;
     return f_ratio_y(C, col ? dc : dr, col ? yc : yr);
   }
+  // experiment (SA_K2T_DEBUG bit 64): a stand-in for F with no fp64 arithmetic
+  __device__ __forceinline__ double fsel_dbg(uint32_t C, double yr, double dr, double yc, double dc) const {
+    if (dbg & 64) return __hiloint2double((int)(C ^ __double2hiint(yc)), (int)C);
+    return fsel(C, yr, dr, yc, dc);
+  }
 
   // the exact-rank term of pair (row, column entry k), numerator C: 64 low bits + the 2^64 carry
   __device__ __forceinline__ void fterm(const State& s, const uint4& k, uint32_t C, uint64_t& t, uint32_t& cd) const {
@@ -783,7 +788,7 @@ struct KeyMatEpi {
           double F = 0.0;
           if constexpr (want_sim && (SYM || FT)) {
             const double2 yd = *reinterpret_cast<const double2*>(ent + j * TAB_BYTES + YOFF);
-            F = fsel(C, s.y, s.d, yd.x, yd.y);
+            F = fsel_dbg(C, s.y, s.d, yd.x, yd.y);
           }
           if constexpr (SYM) {
             if constexpr (want_num) st_out_if(stores, num + om, (uint16_t)C);
@@ -835,7 +840,7 @@ struct KeyMatEpi {
             y_i = __shfl_sync(0xffffffffu, s.y, i);
             d_i = __shfl_sync(0xffffffffu, s.d, i);
           }
-          st_out_if(stores, sim + od, fsel(C, y_i, d_i, yc, dc));
+          st_out_if(stores, sim + od, fsel_dbg(C, y_i, d_i, yc, dc));
         }
         od += RPP * ld;
       }

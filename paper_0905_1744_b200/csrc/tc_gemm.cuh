@@ -505,6 +505,20 @@ __host__ __device__ constexpr int smem2_of(int EW, int CW, bool FP4, int TB, int
          EW * (slice_of(EW, CW, FP4) * TB + XB);
 }
 
+// one lane of a converged warp (elect.sync): the warp-wide role loops keep
+// their descriptors / coordinates warp-uniform (uniform registers), and only
+// the elected lane issues the single-thread TMA / MMA / commit instructions
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "elect.sync _|P, 0xffffffff;\n"
+      "selp.b32 %0, 1, 0, P;\n"
+      "}\n"
+      : "=r"(p));
+  return p != 0;
+}
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -628,8 +642,8 @@ gemm2_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps m
   fence_after();
 
   if (warp == EPI_WARPS) {
-    // ------------------------------------------------ TMA producer (both CTAs)
-    if (lane == 0) {
+    // ------------------------------------------------ TMA producer (both CTAs, whole warp)
+    {
       const uint32_t full0_leader = map_to_rank(s_addr(&full[0]), 0);   // the leader's full barriers
       const bool no_tma = (batch.debug & 2) != 0;
       uint32_t g = 0;
@@ -640,24 +654,31 @@ gemm2_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps m
         const CUtensorMap* ma = &maps.m[2 * P.map];
         const CUtensorMap* mb = &maps.m[2 * P.map + 1];
         const int arow = T.row0 + (int)rank * BM, brow = T.col0 + (int)rank * BNH;
+        uint32_t slot = g % NST, phase = (g / NST) & 1u;
         for (int kb = 0; kb < nkb; ++kb, ++g) {
-          const uint32_t slot = g % NST;
-          if (g >= (uint32_t)NST) bar_wait(&empty[slot], ((g / NST) - 1) & 1u);
-          if (no_tma) {
-            if (leader) bar_arrive(&full[slot]);
-            continue;
+          if (g >= (uint32_t)NST) bar_wait(&empty[slot], phase ^ 1u);
+          if (elect_one()) {
+            if (no_tma) {
+              if (leader) bar_arrive(&full[slot]);
+            } else {
+              if (leader) bar_arrive_tx(&full[slot], 2 * STAGE_BYTES);
+              const uint32_t dst = base_s + slot * STAGE_BYTES;
+              const uint32_t fb = full0_leader + slot * 8u;
+              tma_2d_pair(dst, ma, kb * BK, arow, fb);
+              tma_2d_pair(dst + A_BYTES, mb, kb * BK, brow, fb);
+            }
           }
-          if (leader) bar_arrive_tx(&full[slot], 2 * STAGE_BYTES);
-          const uint32_t dst = base_s + slot * STAGE_BYTES;
-          const uint32_t fb = full0_leader + slot * 8u;
-          tma_2d_pair(dst, ma, kb * BK, arow, fb);
-          tma_2d_pair(dst + A_BYTES, mb, kb * BK, brow, fb);
+          __syncwarp();
+          if (++slot == (uint32_t)NST) {
+            slot = 0;
+            phase ^= 1u;
+          }
         }
       }
     }
   } else if (warp == EPI_WARPS + 1) {
-    // ------------------------------------------------ MMA issuer (leader)
-    if (leader && lane == 0) {
+    // ------------------------------------------------ MMA issuer (leader CTA, whole warp)
+    if (leader) {
       constexpr uint32_t idesc = FP4 ? idesc2_mxf4() : idesc2_i8();
       const uint32_t sfa = tmem_base + (uint32_t)G::SF_COL, sfb = tmem_base + (uint32_t)G::SF_COL + 16u;
       const bool no_mma = (batch.debug & 1) != 0;
@@ -670,23 +691,31 @@ gemm2_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps m
         if (lt >= 2) bar_wait(&tempty[buf], ((lt >> 1) - 1) & 1u);
         fence_after();
         const uint32_t d = tmem_base + buf * (uint32_t)BN;
+        uint32_t slot = g % NST, phase = (g / NST) & 1u;
         for (int kb = 0; kb < nkb; ++kb, ++g) {
-          const uint32_t slot = g % NST;
-          bar_wait(&full[slot], (g / NST) & 1u);
+          bar_wait(&full[slot], phase);
           fence_after();
           const uint32_t sa_ = base_s + slot * STAGE_BYTES;
           const uint64_t da = sw128_desc(sa_), db = sw128_desc(sa_ + A_BYTES);
-          if (!no_mma) {
+          if (elect_one()) {
+            if (!no_mma) {
 #pragma unroll
-            for (int k = 0; k < BK / UKB; ++k) {
-              const uint64_t off = (uint64_t)((k * UKB) >> 4);
-              if constexpr (FP4) mma2_mxf4(d, da + off, db + off, idesc, (kb | k) != 0, sfa, sfb);
-              else mma2_i8(d, da + off, db + off, idesc, (kb | k) != 0);
+              for (int k = 0; k < BK / UKB; ++k) {
+                const uint64_t off = (uint64_t)((k * UKB) >> 4);
+                if constexpr (FP4) mma2_mxf4(d, da + off, db + off, idesc, (kb | k) != 0, sfa, sfb);
+                else mma2_i8(d, da + off, db + off, idesc, (kb | k) != 0);
+              }
             }
+            mma_commit2(&empty[slot]);
           }
-          mma_commit2(&empty[slot]);
+          __syncwarp();
+          if (++slot == (uint32_t)NST) {
+            slot = 0;
+            phase ^= 1u;
+          }
         }
-        mma_commit2(&tfull[buf]);
+        if (elect_one()) mma_commit2(&tfull[buf]);
+        __syncwarp();
       }
     }
   } else {
