@@ -551,15 +551,17 @@ struct KeyMatEpi {
   //   transpose buffer, so each F is computed once (f_transposed);
   //   one CTA (CG = 1): F is recomputed in the transposed pass, with a
   //   32-row {y, d} table where it fits (e2m1 stage sizes).
-  __host__ __device__ static constexpr bool f_transposed(int CW, int CG) {
-    // measured slower (its 4 KB per warp costs the CTA pair a pipeline stage): off
-    return false && SIM && CG == 2 && CW == 16;
-  }
+  //   CTA pairs (CG = 2, 31 KB stages): F computed once per pair and staged
+  //   half a chunk at a time (32 rows x 8 doubles) for 16-byte direct stores
+  //   (vec_direct; rows padded to a multiple of 16, else the path below);
+  //   otherwise F is recomputed in the transposed pass, with a 32-row {y, d}
+  //   table where it fits (e2m1 stage sizes).
+  __host__ __device__ static constexpr bool vec_direct(int CW, int CG) { return SIM && CG == 2 && CW == 16; }
   __host__ __device__ static constexpr bool row_table(bool FP4, int CW, int CG) {
-    return SIM && FP4 && !f_transposed(CW, CG);
+    return SIM && FP4 && !vec_direct(CW, CG);
   }
   __host__ __device__ static constexpr int xpose_bytes(int CW, bool FP4, int CG) {
-    return (MATS ? 64 * CW : 0) + (f_transposed(CW, CG) ? 32 * CW * 8 : 0) + (row_table(FP4, CW, CG) ? 32 * 16 : 0);
+    return (MATS ? 64 * CW : 0) + (vec_direct(CW, CG) ? 32 * 8 * 8 : 0) + (row_table(FP4, CW, CG) ? 32 * 16 : 0);
   }
 
   struct State {
@@ -749,6 +751,71 @@ struct KeyMatEpi {
     }
   }
 
+  // Fast path with vector direct stores (vec_direct; 16 columns, rows padded
+  // to a multiple of 16 elements): lanes = rows compute every F once, store
+  // the mirrored elements (lanes = consecutive rows: coalesced) and stage F
+  // half a chunk at a time in a 32 x 8 fp64 buffer (16-byte unit u of row r
+  // at u ^ ((r >> 1) & 3): conflict-free both ways) and C in the 32 x 16
+  // uint16 buffer; the direct row segments then leave as 16-byte stores
+  // (4 lanes per 64-byte F row segment, 2 per 32-byte C segment).
+  template <bool SYM>
+  __device__ __forceinline__ void fast_vec(const State& s, const TcEpiProb& E, int c0, int wrow0,
+                                           const uint32_t (&v)[16], int lane, const uint8_t* ent, uint8_t* xp,
+                                           int stores) const {
+    constexpr bool want_num = (MODE & EPI_NUM) != 0;
+    const int ld = (int)E.ld;
+    uint16_t* const num = E.num;
+    double* const sim = E.sim;
+    uint8_t* const fb = xp + 64 * 16;
+    const bool vst = stores != 8;
+    uint32_t w[8];
+    int om = c0 * ld + s.row_g;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double Fp = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        const int j = h * 8 + jj;
+        const uint32_t C = v[j];
+        if (j & 1) w[j >> 1] |= C << 16;
+        else w[j >> 1] = C;
+        const double2 yd = *reinterpret_cast<const double2*>(ent + j * TAB_BYTES + YOFF);
+        const double F = fsel_dbg(C, s.y, s.d, yd.x, yd.y);
+        if constexpr (SYM) {
+          if constexpr (want_num) st_out_if(stores, num + om, (uint16_t)C);
+          st_out_if(stores, sim + om, F);
+        }
+        om += ld;
+        if (jj & 1)
+          *reinterpret_cast<double2*>(fb + lane * 64 + (((jj >> 1) ^ ((lane >> 1) & 3)) * 16)) = make_double2(Fp, F);
+        else
+          Fp = F;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int rho = (lane >> 2) + 8 * k, u = lane & 3;
+        const double2 f2 = *reinterpret_cast<const double2*>(fb + rho * 64 + ((u ^ ((rho >> 1) & 3)) * 16));
+        if (vst) __stcs(reinterpret_cast<double2*>(sim + (wrow0 + rho) * ld + c0 + h * 8 + u * 2), f2);
+      }
+      __syncwarp();
+    }
+    if constexpr (want_num) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        *reinterpret_cast<uint4*>(xp + lane * 32 + ((q ^ ((lane >> 2) & 1)) * 16)) =
+            make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int rho = (lane >> 1) + 16 * k, u = lane & 1;
+        const uint4 c8 = *reinterpret_cast<const uint4*>(xp + rho * 32 + ((u ^ ((rho >> 2) & 1)) * 16));
+        if (vst) __stcs(reinterpret_cast<uint4*>(num + (wrow0 + rho) * ld + c0 + u * 8), c8);
+      }
+      __syncwarp();
+    }
+  }
+
   // the numerator / F matrices of a chunk (the host sets num (sim) on every
   // problem of a launch whose MODE has NUM (SIM))
   template <bool SYM, int CW, bool FP4, int CG>
@@ -758,7 +825,7 @@ struct KeyMatEpi {
     constexpr bool want_num = (MODE & EPI_NUM) != 0;
     constexpr bool want_sim = SIM;
     constexpr bool RT = row_table(FP4, CW, CG);
-    constexpr bool FT = f_transposed(CW, CG);
+    constexpr bool VD = vec_direct(CW, CG);
     const bool rows_all = wrow0 + 32 <= T.row0 + T.ra;   // warp-uniform
     const double2* rtab = reinterpret_cast<const double2*>(xp + 64 * CW);   // written by chunk() at tj = 0
     if (upper && ncols == CW && rows_all) {
@@ -773,32 +840,26 @@ struct KeyMatEpi {
       const int ld = (int)E.ld;
       uint16_t* const num = E.num;
       double* const sim = E.sim;
-      // F transpose buffer (FT): 32 rows x CW doubles, 16-byte unit u of row r
-      // at unit u ^ (r & 7) (conflict-free STS.128 by rows and LDS.64 by columns)
-      uint8_t* const fb = xp + 64 * CW;
+      if constexpr (VD) {
+        if ((ld & 15) == 0) {
+          fast_vec<SYM>(s, E, c0, wrow0, v, lane, ent, xp, stores);
+          return;
+        }
+      }
       {
         uint32_t w[CW / 2];
         int om = c0 * ld + s.row_g;
-        double Fp = 0.0;
 #pragma unroll
         for (int j = 0; j < CW; ++j) {
           const uint32_t C = v[j];
           if (j & 1) w[j >> 1] |= C << 16;
           else w[j >> 1] = C;
-          double F = 0.0;
-          if constexpr (want_sim && (SYM || FT)) {
-            const double2 yd = *reinterpret_cast<const double2*>(ent + j * TAB_BYTES + YOFF);
-            F = fsel_dbg(C, s.y, s.d, yd.x, yd.y);
-          }
           if constexpr (SYM) {
             if constexpr (want_num) st_out_if(stores, num + om, (uint16_t)C);
-            if constexpr (want_sim) st_out_if(stores, sim + om, F);
-          }
-          if constexpr (FT) {
-            if (j & 1)
-              *reinterpret_cast<double2*>(fb + lane * (CW * 8) + (((j >> 1) ^ (lane & 7)) * 16)) = make_double2(Fp, F);
-            else
-              Fp = F;
+            if constexpr (want_sim) {
+              const double2 yd = *reinterpret_cast<const double2*>(ent + j * TAB_BYTES + YOFF);
+              st_out_if(stores, sim + om, fsel_dbg(C, s.y, s.d, yd.x, yd.y));
+            }
           }
           om += ld;
         }
@@ -814,7 +875,7 @@ struct KeyMatEpi {
       // buffer, 32 / CW rows per pass; row data from the row table (or shuffles)
       const int cl = lane % CW;
       double yc = 0.0, dc = 0.0;
-      if constexpr (want_sim && !FT) {
+      if constexpr (want_sim) {
         const double2 yd = *reinterpret_cast<const double2*>(ent + cl * TAB_BYTES + YOFF);
         yc = yd.x;
         dc = yd.y;
@@ -827,10 +888,7 @@ struct KeyMatEpi {
         const int qs = (cl >> 3) ^ ((i >> QSH) & (Q - 1));
         const uint32_t C = *reinterpret_cast<const uint16_t*>(xp + i * (CW * 2) + qs * 16 + (cl & 7) * 2);
         if constexpr (want_num) st_out_if(stores, num + od, (uint16_t)C);
-        if constexpr (want_sim && FT) {
-          st_out_if(stores, sim + od, *reinterpret_cast<const double*>(fb + i * (CW * 8) + (((cl >> 1) ^ (i & 7)) * 16) +
-                                                             (cl & 1) * 8));
-        } else if constexpr (want_sim) {
+        if constexpr (want_sim) {
           double y_i, d_i;
           if constexpr (RT) {
             const double2 r = rtab[i];
