@@ -7,6 +7,8 @@
 // by at least the pool size.  Every kernel that orders also
 // flags the items whose order the keys do not certify, so the host can resolve
 // them exactly (sa_partition's exact path).
+#include <cstring>
+
 #include "common.cuh"
 
 namespace sa {
@@ -145,21 +147,204 @@ bucket_sort_kernel(const sa_key128* __restrict__ keys, const int64_t* __restrict
   if (near) atomicAdd(amb_count, near);
 }
 
+// The same exact segment sort spread over the whole GPU (the one-CTA-per-
+// segment kernel above leaves 140 of 148 SMs idle on p = 8 blocks): five
+// grid-wide passes over all items of all segments -- (1) d_i = RN(key_i) and
+// per-segment [min, max] (warp-reduced atomics on the doubles' bit patterns,
+// which order like the non-negative doubles), (2) bucket_i and per-segment
+// bucket counts, (3) one CTA per segment scans its counts, (4) bucket lists,
+// (5) position inside the bucket by exact (key, gid) compares, then the
+// uncertified-neighbour count over the sorted order.
+constexpr int SS_NB = 16384;   // buckets per segment at most (w / 2 when smaller)
+
+__device__ __forceinline__ int seg_of(const SegSpec& sp, int nseg, int64_t i) {
+  int s = 0;
+  while (s + 1 < nseg && sp.begin(s + 1) <= i) ++s;
+  return s;
+}
+
+__global__ void ss_minmax_kernel(const sa_key128* __restrict__ keys, SegSpec sp, int nseg, int64_t total,
+                                 double* __restrict__ dv, unsigned long long* __restrict__ mm) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool in = i < total;
+  const int s = in ? seg_of(sp, nseg, i) : -1;
+  double d = 0.0;
+  if (in) {
+    d = key_to_double(keys[i]);
+    dv[i] = d;
+  }
+  unsigned long long lo = in ? (unsigned long long)__double_as_longlong(d) : ~0ull;
+  unsigned long long hi = in ? lo : 0ull;
+  const int s0 = __shfl_sync(0xffffffffu, s, 0);
+  if (__all_sync(0xffffffffu, s == s0 || s < 0)) {   // warp inside one segment: reduce first
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0 && s0 >= 0) {
+      atomicMin(&mm[2 * s0], lo);
+      atomicMax(&mm[2 * s0 + 1], hi);
+    }
+  } else if (in) {
+    atomicMin(&mm[2 * s], lo);
+    atomicMax(&mm[2 * s + 1], hi);
+  }
+}
+
+__device__ __forceinline__ void seg_scale(const SegSpec& sp, int s, const unsigned long long* mm, int& nb,
+                                          double& mn, double& scale) {
+  const int64_t w = sp.begin(s + 1) - sp.begin(s);
+  const int64_t want = w / 2 < 1 ? 1 : w / 2;
+  nb = (int)(want < SS_NB ? want : SS_NB);
+  mn = __longlong_as_double((long long)mm[2 * s]);
+  const double mx = __longlong_as_double((long long)mm[2 * s + 1]);
+  scale = mx > mn ? (double)nb / (mx - mn) : 0.0;
+}
+
+__global__ void ss_bucket_kernel(SegSpec sp, int nseg, int64_t total, const double* __restrict__ dv,
+                                 const unsigned long long* __restrict__ mm, int32_t* __restrict__ bkt,
+                                 int32_t* __restrict__ cnt) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int s = seg_of(sp, nseg, i);
+  int nb;
+  double mn, scale;
+  seg_scale(sp, s, mm, nb, mn, scale);
+  int bk = (int)((dv[i] - mn) * scale);
+  bk = min(max(bk, 0), nb - 1);
+  bkt[i] = bk;
+  atomicAdd(&cnt[(int64_t)s * (SS_NB + 1) + bk], 1);
+}
+
+// one CTA per segment: exclusive scan of its bucket counts -> start (in place) and fill
+__global__ void __launch_bounds__(1024) ss_scan_kernel(SegSpec sp, const unsigned long long* __restrict__ mm,
+                                                       int32_t* __restrict__ cnt, int32_t* __restrict__ fill) {
+  __shared__ int32_t part[1024];
+  const int s = blockIdx.x, tid = threadIdx.x;
+  int nb;
+  double mn, scale;
+  seg_scale(sp, s, mm, nb, mn, scale);
+  int32_t* c = cnt + (int64_t)s * (SS_NB + 1);
+  int32_t* f = fill + (int64_t)s * SS_NB;
+  constexpr int PER = SS_NB / 1024;
+  int loc[PER], sum = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int t = tid * PER + q;
+    loc[q] = t < nb ? c[t] : 0;
+    sum += loc[q];
+  }
+  part[tid] = sum;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const int v = tid >= o ? part[tid - o] : 0;
+    __syncthreads();
+    part[tid] += v;
+    __syncthreads();
+  }
+  int run = part[tid] - sum;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int t = tid * PER + q;
+    if (t < nb) {
+      c[t] = run;
+      f[t] = run;
+    }
+    run += loc[q];
+  }
+  if (tid == 0) c[nb] = (int)(sp.begin(s + 1) - sp.begin(s));
+}
+
+__global__ void ss_fill_kernel(SegSpec sp, int nseg, int64_t total, const int32_t* __restrict__ bkt,
+                               int32_t* __restrict__ fill, int32_t* __restrict__ list) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int s = seg_of(sp, nseg, i);
+  const int64_t b = sp.begin(s);
+  const int slot = atomicAdd(&fill[(int64_t)s * SS_NB + bkt[i]], 1);
+  list[b + slot] = (int32_t)(i - b);
+}
+
+__global__ void ss_rank_kernel(const sa_key128* __restrict__ keys, const int64_t* __restrict__ gids, int64_t gid0,
+                               SegSpec sp, int nseg, int64_t total, const int32_t* __restrict__ bkt,
+                               const int32_t* __restrict__ cnt, const int32_t* __restrict__ list,
+                               int32_t* __restrict__ order_out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int s = seg_of(sp, nseg, i);
+  const int64_t b = sp.begin(s);
+  auto gid = [&](int64_t x) { return gids ? gids[x] : gid0 + x; };
+  const int32_t* c = cnt + (int64_t)s * (SS_NB + 1);
+  const int bk = bkt[i];
+  const sa_key128 ki = keys[i];
+  const int64_t gi = gid(i);
+  int r = 0;
+  for (int t = c[bk]; t < c[bk + 1]; ++t) {
+    const int64_t j = b + list[b + t];
+    r += (j != i && key_lt(keys[j], gid(j), ki, gi)) ? 1 : 0;
+  }
+  order_out[b + c[bk] + r] = (int32_t)(i - b);
+}
+
+__global__ void ss_near_kernel(const sa_key128* __restrict__ keys, SegSpec sp, int nseg, int64_t total,
+                               int64_t window, const int32_t* __restrict__ order, uint32_t* __restrict__ amb_count) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  bool near = false;
+  if (t < total) {
+    const int s = seg_of(sp, nseg, t);
+    const int64_t b = sp.begin(s);
+    if (t + 1 < sp.begin(s + 1)) near = key_near(keys[b + order[t]], keys[b + order[t + 1]], window);
+  }
+  const uint32_t m = __ballot_sync(0xffffffffu, near);
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(amb_count, (uint32_t)__popc(m));
+}
+
 sa_status segsort_launch_impl(const sa_key128* keys, const int64_t* gids, int64_t gid0, SegSpec sp, int nseg,
                               int64_t total, int64_t window, int32_t* order_out, uint32_t* amb_count,
                               cudaStream_t st) {
   if (nseg <= 0 || total <= 0) return SA_OK;
-  void* scratch = nullptr;
-  SA_CUDA(cudaMallocAsync(&scratch, (size_t)total * 8, st));
-  int32_t* bkt = static_cast<int32_t*>(scratch);
-  int32_t* list = bkt + total;
-  // segment s covers [sp.begin(s), sp.begin(s + 1)) of these arrays (indices relative to sp.begin(0) = 0)
-  bucket_sort_kernel<<<(unsigned)nseg, BS_THREADS, 0, st>>>(keys, gids, gid0, sp, window, order_out, bkt, list,
-                                                            amb_count);
-  const cudaError_t le = cudaGetLastError();
-  count_launch();
-  cudaFreeAsync(scratch, st);
-  if (le != cudaSuccess) return fail(SA_E_CUDA, "bucket_sort_kernel launch: %s", cudaGetErrorString(le));
+  static const bool one_cta = [] {   // SA_SEGSORT=cta: the one-CTA-per-segment kernel
+    const char* e = getenv("SA_SEGSORT");
+    return e && !strcmp(e, "cta");
+  }();
+  if (one_cta) {
+    void* scratch = nullptr;
+    SA_CUDA(cudaMallocAsync(&scratch, (size_t)total * 8, st));
+    int32_t* bkt = static_cast<int32_t*>(scratch);
+    int32_t* list = bkt + total;
+    bucket_sort_kernel<<<(unsigned)nseg, BS_THREADS, 0, st>>>(keys, gids, gid0, sp, window, order_out, bkt, list,
+                                                              amb_count);
+    const cudaError_t le = cudaGetLastError();
+    count_launch();
+    cudaFreeAsync(scratch, st);
+    if (le != cudaSuccess) return fail(SA_E_CUDA, "bucket_sort_kernel launch: %s", cudaGetErrorString(le));
+    return SA_OK;
+  }
+  Scratch scratch(st);
+  SA_ALLOC(dv, double, total);
+  SA_ALLOC(bkt, int32_t, total);
+  SA_ALLOC(list, int32_t, total);
+  SA_ALLOC(mm, unsigned long long, 2 * nseg);
+  SA_ALLOC(cnt, int32_t, (size_t)nseg * (SS_NB + 1));
+  SA_ALLOC(fill, int32_t, (size_t)nseg * SS_NB);
+  SA_CUDA(cudaMemsetAsync(cnt, 0, (size_t)nseg * (SS_NB + 1) * sizeof(int32_t), st));
+  // [min, max] init: min = all ones (above every double's bits), max = 0
+  SA_CUDA(cudaMemsetAsync(mm, 0, 2 * nseg * sizeof(unsigned long long), st));
+  for (int s = 0; s < nseg; ++s)
+    SA_CUDA(cudaMemsetAsync(mm + 2 * s, 0xff, sizeof(unsigned long long), st));
+  const unsigned g = (unsigned)((total + 255) / 256);
+  ss_minmax_kernel<<<g, 256, 0, st>>>(keys, sp, nseg, total, dv, mm);
+  SA_LAUNCHED();
+  ss_bucket_kernel<<<g, 256, 0, st>>>(sp, nseg, total, dv, mm, bkt, cnt);
+  SA_LAUNCHED();
+  ss_scan_kernel<<<nseg, 1024, 0, st>>>(sp, mm, cnt, fill);
+  SA_LAUNCHED();
+  ss_fill_kernel<<<g, 256, 0, st>>>(sp, nseg, total, bkt, fill, list);
+  SA_LAUNCHED();
+  ss_rank_kernel<<<g, 256, 0, st>>>(keys, gids, gid0, sp, nseg, total, bkt, cnt, list, order_out);
+  SA_LAUNCHED();
+  ss_near_kernel<<<g, 256, 0, st>>>(keys, sp, nseg, total, window, order_out, amb_count);
+  SA_LAUNCHED();
   return SA_OK;
 }
 
