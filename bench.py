@@ -368,16 +368,23 @@ def main():
                 h_out[k] = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
             return h_out[k]
 
+        d_packed = {}
+
         def on_bucket(b, num, sim):
-            # bucket b's numerators go to the host on a copy stream while the
-            # next bucket computes
+            # bucket b's numerator matrix, packed to its upper triangle (the
+            # whole symmetric content, sa_pack_upper_u16), goes to the host on
+            # a copy stream while the next bucket computes
             if num is None:
                 return
+            n_b = num.shape[0]
+            if b not in d_packed or d_packed[b].numel() != n_b * (n_b + 1) // 2:
+                d_packed[b] = torch.empty(n_b * (n_b + 1) // 2, dtype=torch.uint16, device=dev)
+            pk = B.sa_pack_upper_u16(ctx, num, d_packed[b], stream=st)
             ev = torch.cuda.Event()
             ev.record(st)
             copy_st.wait_event(ev)
             with torch.cuda.stream(copy_st):
-                pinned(f"num{b}", num.view(torch.int16)).copy_(num.view(torch.int16), non_blocking=True)
+                pinned(f"num{b}", pk.view(torch.int16)).copy_(pk.view(torch.int16), non_blocking=True)
 
         def d2h_tail(o):
             nb = 0
@@ -386,7 +393,7 @@ def main():
                 nb += t.numel() * t.element_size()
             for num in o.numerators:
                 if num is not None:
-                    nb += num.numel() * 2
+                    nb += num.shape[0] * (num.shape[0] + 1) // 2 * 2
             st.wait_stream(copy_st)          # the step ends when every result is on the host
             return nb
 
@@ -411,7 +418,8 @@ def main():
         e2e = {"value": pairs * args.steps / (e2e_ms / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(res_h.numel() + offs_h.numel() * 8),
                "d2h_bytes_per_step": int(d2h_bytes), "ms_per_step": e2e_ms / args.steps,
-               "results_copied": "bucket_of, received member ids, uint16 numerator matrices of owned buckets"}
+               "results_copied": ("bucket_of, received member ids, and every owned bucket's symmetric uint16 "
+                                  "numerator matrix as its packed upper triangle (sa_pack_upper_u16)")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -276,6 +276,15 @@ sa_status sa_bucket_similarity_batch(sa_ctx* ctx, int32_t nbuckets, const uint16
                                      const int64_t* row_begin_h, int32_t bins, uint16_t* const* numerators_h,
                                      double* const* similarity_h, const int64_t* ld_h, void* stream);
 
+/* Packed upper triangle (diagonal included) of a symmetric n x n uint16
+ * matrix with row stride ld >= n: row i's columns i..n-1 at packed offset
+ * i*n - i*(i-1)/2, n(n+1)/2 elements in all -- the complete content of a
+ * bucket's numerator matrix in half the bytes (the end-to-end bench moves
+ * these to the host).  Device pointers; enqueued on `stream`.  SA_E_INVAL:
+ * n < 0, ld < n, NULL pointers with n > 0. */
+sa_status sa_pack_upper_u16(sa_ctx* ctx, const uint16_t* matrix, int32_t n, int64_t ld, uint16_t* packed,
+                            void* stream);
+
 #ifdef __cplusplus
 }
 #endif

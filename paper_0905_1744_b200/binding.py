@@ -27,7 +27,7 @@ EXPORTED = ["sa_ctx_create", "sa_ctx_attach_comm", "sa_ctx_destroy", "sa_last_er
             "sa_ctx_set_timing", "sa_ctx_phase_ms", "sa_profile_stride", "sa_kmer_profiles", "sa_kmer_rank",
             "sa_partition", "sa_redistribute", "sa_bucket_similarity", "sa_exact_rank_compare", "sa_ctx_engine",
             "sa_ctx_set_rank_form", "sa_ctx_tc_columns", "sa_ctx_tc_operand", "sa_selftest_f_division",
-            "sa_bucket_similarity_batch"]
+            "sa_bucket_similarity_batch", "sa_pack_upper_u16"]
 SA_RANK_F, SA_RANK_DF = 0, 1
 
 
@@ -99,6 +99,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                                       ctypes.POINTER(ctypes.c_void_p),
                                                       ctypes.POINTER(ctypes.c_int64), VP]),
         "sa_exact_rank_compare": (ctypes.c_int, [P, I32, P, I32, P, I32]),
+        "sa_pack_upper_u16": (ctypes.c_int, [P, P, I32, ctypes.c_int64, P, VP]),
         "sa_ctx_engine": (ctypes.c_int, [P]),
         "sa_ctx_tc_columns": (ctypes.c_int32, [P, P, ctypes.c_int32]),
         "sa_ctx_tc_operand": (ctypes.c_int, [P]),
@@ -418,6 +419,22 @@ def sa_bucket_similarity_batch(ctx: Context, profiles, nkmers, row_begin, bins: 
     _check(load_library().sa_bucket_similarity_batch(ctx.handle, nb, _ptr(profiles), _ptr(nkmers), rb, bins,
                                                      nums, sims, ldh, _stream(stream)))
     return numerators, similarity
+
+
+def sa_pack_upper_u16(ctx: Context, matrix: torch.Tensor, packed: torch.Tensor | None = None, stream=None):
+    """Packed upper triangle (diagonal included) of a symmetric n x n uint16
+    matrix (n x n view with any row stride >= n): row i's columns i..n-1 at
+    i*n - i*(i-1)/2; returns the n(n+1)/2 uint16 device tensor (sa.h)."""
+    if matrix.dtype != torch.uint16 or not matrix.is_cuda or matrix.dim() != 2 or matrix.shape[0] != matrix.shape[1]:
+        raise ValueError("matrix must be an n x n uint16 CUDA tensor")
+    if matrix.stride(1) != 1:
+        raise ValueError("matrix rows must be contiguous")
+    n = matrix.shape[0]
+    if packed is None:
+        packed = torch.empty(n * (n + 1) // 2, dtype=torch.uint16, device=matrix.device)
+    _check(load_library().sa_pack_upper_u16(ctx.handle, ctypes.c_void_p(matrix.data_ptr()), n, matrix.stride(0),
+                                            _ptr(packed), _stream(stream)))
+    return packed
 
 
 # ------------------------------------------------------- communicator -----

@@ -171,6 +171,15 @@ static sa_status prepare_ops(sa_ctx* c, Scratch& scratch, const uint16_t* A16, i
   return SA_OK;
 }
 
+// packed upper triangle: one CTA per row, coalesced row-segment copy
+__global__ void pack_upper_kernel(const uint16_t* __restrict__ m, int32_t n, int64_t ld, uint16_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const uint16_t* src = m + i * ld;
+    uint16_t* dst = out + i * (int64_t)n - i * (i - 1) / 2 - i;   // = i*n - i*(i+1)/2, then column j at + j
+    for (int64_t j = i + threadIdx.x; j < n; j += blockDim.x) dst[j] = src[j];
+  }
+}
+
 static inline cudaEvent_t ev_begin(sa_ctx* c, int ph);
 static inline cudaEvent_t ev_end(sa_ctx* c, int ph);
 
@@ -1044,6 +1053,19 @@ sa_status sa_bucket_similarity(sa_ctx* ctx, const uint16_t* profiles, const int3
   pr.sim = similarity;
   pr.ld = n;
   SA_TRY(launch_ops(ctx, E, {pr}, st, ev_begin(ctx, SA_PHASE_S5), ev_end(ctx, SA_PHASE_S5)));
+  return SA_OK;
+}
+
+sa_status sa_pack_upper_u16(sa_ctx* ctx, const uint16_t* matrix, int32_t n, int64_t ld, uint16_t* packed,
+                            void* stream) {
+  g_err.clear();
+  if (!ctx) return fail(SA_E_INVAL, "ctx is NULL");
+  if (n < 0 || ld < n) return fail(SA_E_INVAL, "bad n / ld");
+  if (n == 0) return SA_OK;
+  if (!matrix || !packed) return fail(SA_E_INVAL, "NULL required pointer");
+  SA_CUDA(cudaSetDevice(ctx->device));
+  pack_upper_kernel<<<(unsigned)std::min<int64_t>(n, 148 * 16), 256, 0, (cudaStream_t)stream>>>(matrix, n, ld, packed);
+  SA_LAUNCHED();
   return SA_OK;
 }
 

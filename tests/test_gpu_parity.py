@@ -193,6 +193,24 @@ def test_bucket_similarity_batch(ctx, engine, sizes, ld_align):
         assert np.array_equal(sims[b].cpu().numpy(), Fo)
 
 
+@pytest.mark.parametrize("n,ld_align", [(0, 1), (1, 1), (257, 1), (300, 16)])
+def test_pack_upper_u16(ctx, n, ld_align):
+    """sa_pack_upper_u16: the packed upper triangle (diagonal included) of a
+    bucket numerator matrix equals the row-major triu of the oracle's matrix."""
+    ds = _rand_set(77 + n, n, 0, 420, dup=2) if n else None
+    if n == 0:
+        m = torch.empty((0, 0), dtype=torch.uint16, device="cuda")
+        assert B.sa_pack_upper_u16(ctx, m).numel() == 0
+        return
+    res, offs = to_dev(ds)
+    P, nk = B.sa_kmer_profiles(ctx, res, offs)
+    Po, nko = kmer.profiles(ds.residues, ds.offsets)
+    nums, _ = B.sa_bucket_similarity_batch(ctx, P, nk, [0, n], want_similarity=False, ld_align=ld_align)
+    packed = B.sa_pack_upper_u16(ctx, nums[0]).cpu().numpy()
+    Co, _ = partition.bucket_similarity(Po, nko, np.arange(n))
+    assert np.array_equal(packed, Co[np.triu_indices(n)])
+
+
 def test_tc_falls_back_on_deep_counts(ctx, monkeypatch):
     """K2T tracks 32 threshold layers: a bin count of 33..255 must hand the call
     to the uint8 SAD engine on the device, exactly."""
