@@ -1018,11 +1018,13 @@ static sa_status tc_configure_all() {
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_SIM>, 16, 16, FP4, CG>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4, CG>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 8, 16, FP4, CG>();
+  if constexpr (CG == 2)   // 20 epilogue warps fit beside the CTA pair's stages only
+    if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 20, 16, FP4, CG>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_KEYS | EPI_NUM>, 8, CW_ALL, FP4, CG>();
   return cs;
 }
 template <bool FP4, int CG>
-static void tc_gemm_mode(int mode, int keysw, bool mats16, int64_t grid, const tc::Batch& batch, const tc::Maps& maps,
+static void tc_gemm_mode(int mode, int keysw, int matsw, int64_t grid, const tc::Batch& batch, const tc::Maps& maps,
                          int64_t tiles, const KeyMatEpi<EPI_ALL>& epi, cudaStream_t st) {
   constexpr int CW_ALL = FP4 ? 16 : 32;
   // 16 epilogue warps x 16-column chunks (more warps to hide the store / F /
@@ -1034,7 +1036,9 @@ static void tc_gemm_mode(int mode, int keysw, bool mats16, int64_t grid, const t
   else if (mode == EPI_KEYS) tc_gemm<KeyMatEpi<EPI_KEYS>, 8, CW_ALL, FP4, CG>(grid, batch, maps, tiles, epi, st);
   else if (mode == EPI_NUM) tc_gemm<KeyMatEpi<EPI_NUM>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
   else if (mode == EPI_SIM) tc_gemm<KeyMatEpi<EPI_SIM>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
-  else if ((mode & EPI_KEYS) == 0 && mats16)
+  else if ((mode & EPI_KEYS) == 0 && matsw == 20 && CG == 2) {
+    if constexpr (CG == 2) tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 20, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
+  } else if ((mode & EPI_KEYS) == 0 && matsw != 8)
     tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
   else if ((mode & EPI_KEYS) == 0)
     tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 8, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
@@ -1288,14 +1292,18 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       const int w = e ? atoi(e) : 8;
       return w == 12 || w == 16 ? w : 8;
     }();
-    const bool mats16 = env_on("SA_K2T_MATS16", true);
+    const int matsw = [] {
+      const char* e = getenv("SA_K2T_MATSW");
+      const int w = e ? atoi(e) : 16;
+      return w == 8 || w == 20 ? w : 16;
+    }();
     if (ev0) SA_CUDA(cudaEventRecord(ev0, st));   // the GEMM kernel alone (SA_PHASE_GEMM)
     if (pairs) {
-      if (fp4) tc_gemm_mode<true, 2>(mode, keysw, mats16, grid, batch, maps, tiles, epi, st);
-      else tc_gemm_mode<false, 2>(mode, keysw, mats16, grid, batch, maps, tiles, epi, st);
+      if (fp4) tc_gemm_mode<true, 2>(mode, keysw, matsw, grid, batch, maps, tiles, epi, st);
+      else tc_gemm_mode<false, 2>(mode, keysw, matsw, grid, batch, maps, tiles, epi, st);
     } else {
-      if (fp4) tc_gemm_mode<true, 1>(mode, keysw, mats16, grid, batch, maps, tiles, epi, st);
-      else tc_gemm_mode<false, 1>(mode, keysw, mats16, grid, batch, maps, tiles, epi, st);
+      if (fp4) tc_gemm_mode<true, 1>(mode, keysw, matsw, grid, batch, maps, tiles, epi, st);
+      else tc_gemm_mode<false, 1>(mode, keysw, matsw, grid, batch, maps, tiles, epi, st);
     }
     SA_LAUNCHED();
     if (ev1) SA_CUDA(cudaEventRecord(ev1, st));

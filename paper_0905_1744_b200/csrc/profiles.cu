@@ -15,7 +15,7 @@ namespace sa {
 __global__ void __launch_bounds__(256)
 profiles_kernel(const uint8_t* __restrict__ res, const int64_t* __restrict__ offs, int32_t n, int32_t k,
                 int32_t alphabet, int32_t stride, uint16_t* __restrict__ out, int32_t* __restrict__ nk_out,
-                uint32_t* __restrict__ err) {
+                uint32_t* __restrict__ err, int cs) {
   extern __shared__ __align__(16) uint32_t hist[];   // stride / 2 words
   const int words = stride >> 1;
   const int vec = words >> 2;                         // uint4 per row (stride % 64 == 0)
@@ -47,7 +47,11 @@ profiles_kernel(const uint8_t* __restrict__ res, const int64_t* __restrict__ off
     }
     __syncthreads();
     uint4* o4 = reinterpret_cast<uint4*>(out + s * (int64_t)stride);
-    for (int v = threadIdx.x; v < vec; v += blockDim.x) o4[v] = h4[v];
+    if (cs) {
+      for (int v = threadIdx.x; v < vec; v += blockDim.x) __stcs(o4 + v, h4[v]);
+    } else {
+      for (int v = threadIdx.x; v < vec; v += blockDim.x) o4[v] = h4[v];
+    }
     __syncthreads();
   }
 }
@@ -67,9 +71,13 @@ sa_status profiles_launch(const uint8_t* residues, const int64_t* offsets, int32
   SA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   SA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, profiles_kernel, 256, smem));
   if (per_sm < 1) per_sm = 1;
+  static const int cs = [] {   // streaming (evict-first) row stores unless SA_PROF_CS=0
+    const char* e = getenv("SA_PROF_CS");
+    return e ? atoi(e) : 1;
+  }();
   const int64_t grid = (int64_t)sms * per_sm;
   profiles_kernel<<<(unsigned)(n < grid ? n : grid), 256, smem, st>>>(residues, offsets, n, k, alphabet, stride, out,
-                                                                     nk, err_flag);
+                                                                     nk, err_flag, cs);
   SA_LAUNCHED();
   return SA_OK;
 }
