@@ -457,15 +457,43 @@ bucket_hist_kernel(const int32_t* __restrict__ bucket_of, int n, int p, int32_t*
   for (int b = threadIdx.x; b < p; b += blockDim.x) hist[(int64_t)blockIdx.x * p + b] = hs[b];
 }
 
-// exclusive offsets, bucket-major then chunk: base[c][b]
-__global__ void bucket_scan_kernel(const int32_t* __restrict__ hist, int nchunk, int p, int64_t* __restrict__ base) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  int64_t run = 0;
-  for (int b = 0; b < p; ++b)
-    for (int c = 0; c < nchunk; ++c) {
-      base[(int64_t)c * p + b] = run;
-      run += hist[(int64_t)c * p + b];
+// exclusive offsets, bucket-major then chunk: base[c][b] (one CTA: block scans
+// of 4096-entry tiles of the (b, c) sequence, carried from tile to tile)
+__global__ void __launch_bounds__(1024) bucket_scan_kernel(const int32_t* __restrict__ hist, int nchunk, int p,
+                                                           int64_t* __restrict__ base) {
+  __shared__ int64_t part[1024];
+  __shared__ int64_t carry;
+  const int tid = threadIdx.x;
+  const int64_t total = (int64_t)nchunk * p;
+  if (tid == 0) carry = 0;
+  __syncthreads();
+  for (int64_t t0 = 0; t0 < total; t0 += 4096) {
+    int64_t loc[4], sum = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t k = t0 + tid * 4 + q;   // k = b * nchunk + c
+      loc[q] = k < total ? hist[(k % nchunk) * p + k / nchunk] : 0;
+      sum += loc[q];
     }
+    part[tid] = sum;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+      const int64_t v = tid >= o ? part[tid - o] : 0;
+      __syncthreads();
+      part[tid] += v;
+      __syncthreads();
+    }
+    int64_t run = carry + part[tid] - sum;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t k = t0 + tid * 4 + q;
+      if (k < total) base[(k % nchunk) * p + k / nchunk] = run;
+      run += loc[q];
+    }
+    __syncthreads();
+    if (tid == 1023) carry = run;
+    __syncthreads();
+  }
 }
 
 __global__ void __launch_bounds__(256)
@@ -688,7 +716,7 @@ sa_status bucket_perm_launch(const int32_t* bucket_of, int n, int p, int32_t* hi
   const int nchunk = (int)cdiv(n, 256);
   bucket_hist_kernel<<<nchunk, 256, p * sizeof(int32_t), st>>>(bucket_of, n, p, hist);
   SA_LAUNCHED();
-  bucket_scan_kernel<<<1, 32, 0, st>>>(hist, nchunk, p, base);
+  bucket_scan_kernel<<<1, 1024, 0, st>>>(hist, nchunk, p, base);
   SA_LAUNCHED();
   bucket_scatter_kernel<<<nchunk, 256, 8 * p * sizeof(int32_t), st>>>(bucket_of, n, p, base, perm);
   SA_LAUNCHED();
