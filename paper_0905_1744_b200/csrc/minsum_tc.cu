@@ -1018,8 +1018,10 @@ static sa_status tc_configure_all() {
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_SIM>, 16, 16, FP4, CG>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4, CG>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 8, 16, FP4, CG>();
-  if constexpr (CG == 2)   // 20 epilogue warps fit beside the CTA pair's stages only
+  if constexpr (CG == 2) {   // 12 / 20 epilogue warps: CTA pairs only
     if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 20, 16, FP4, CG>();
+    if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 12, 16, FP4, CG>();
+  }
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_KEYS | EPI_NUM>, 8, CW_ALL, FP4, CG>();
   return cs;
 }
@@ -1036,8 +1038,11 @@ static void tc_gemm_mode(int mode, int keysw, int matsw, int64_t grid, const tc:
   else if (mode == EPI_KEYS) tc_gemm<KeyMatEpi<EPI_KEYS>, 8, CW_ALL, FP4, CG>(grid, batch, maps, tiles, epi, st);
   else if (mode == EPI_NUM) tc_gemm<KeyMatEpi<EPI_NUM>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
   else if (mode == EPI_SIM) tc_gemm<KeyMatEpi<EPI_SIM>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
-  else if ((mode & EPI_KEYS) == 0 && matsw == 20 && CG == 2) {
-    if constexpr (CG == 2) tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 20, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
+  else if ((mode & EPI_KEYS) == 0 && (matsw == 20 || matsw == 12) && CG == 2) {
+    if constexpr (CG == 2) {
+      if (matsw == 20) tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 20, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
+      else tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 12, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
+    }
   } else if ((mode & EPI_KEYS) == 0 && matsw != 8)
     tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
   else if ((mode & EPI_KEYS) == 0)
@@ -1294,8 +1299,8 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     }();
     const int matsw = [] {
       const char* e = getenv("SA_K2T_MATSW");
-      const int w = e ? atoi(e) : 16;
-      return w == 8 || w == 20 ? w : 16;
+      const int w = e ? atoi(e) : 12;   // CTA pairs: 12 (one CTA: 12 is not built, 16 runs)
+      return w == 8 || w == 12 || w == 20 ? w : 16;
     }();
     if (ev0) SA_CUDA(cudaEventRecord(ev0, st));   // the GEMM kernel alone (SA_PHASE_GEMM)
     if (pairs) {
