@@ -1279,9 +1279,12 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       return g >= 1 && g <= 64 ? g : 16;
     }();
     batch.group = group;
-    static const int evict_last = [] {   // SA_K2T_EVICT_LAST=0: operand loads without the L2 policy
+    // SA_K2T_EVICT_LAST=1: operand loads with an L2 evict-last policy (measured:
+    // no faster, and more DRAM reads for the S5 launch, whose output streams
+    // through L2 -- off by default)
+    static const int evict_last = [] {
       const char* e = getenv("SA_K2T_EVICT_LAST");
-      return e ? atoi(e) : 1;
+      return e ? atoi(e) : 0;
     }();
     batch.evict_last = evict_last;
     batch.debug = debug;

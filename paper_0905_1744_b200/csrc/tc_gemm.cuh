@@ -548,6 +548,15 @@ __device__ __forceinline__ void tma_2d_pair(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(leader_bar)
       : "memory");
 }
+// the same with an L2 eviction-priority policy
+__device__ __forceinline__ void tma_2d_pair_hint(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                                 uint32_t leader_bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(leader_bar), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_alloc2(uint32_t* slot, uint32_t cols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_addr(slot)), "r"(cols));
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
@@ -646,6 +655,8 @@ gemm2_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps m
     {
       const uint32_t full0_leader = map_to_rank(s_addr(&full[0]), 0);   // the leader's full barriers
       const bool no_tma = (batch.debug & 2) != 0;
+      const bool hint = batch.evict_last != 0;
+      const uint64_t pol = policy_evict_last();
       uint32_t g = 0;
       for (int64_t tile = pair; tile < total_tiles; tile += npairs) {
         const Tile T = decode<BN, TBM2>(batch, tile);
@@ -664,8 +675,13 @@ gemm2_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps m
               if (leader) bar_arrive_tx(&full[slot], 2 * STAGE_BYTES);
               const uint32_t dst = base_s + slot * STAGE_BYTES;
               const uint32_t fb = full0_leader + slot * 8u;
-              tma_2d_pair(dst, ma, kb * BK, arow, fb);
-              tma_2d_pair(dst + A_BYTES, mb, kb * BK, brow, fb);
+              if (hint) {
+                tma_2d_pair_hint(dst, ma, kb * BK, arow, fb, pol);
+                tma_2d_pair_hint(dst + A_BYTES, mb, kb * BK, brow, fb, pol);
+              } else {
+                tma_2d_pair(dst, ma, kb * BK, arow, fb);
+                tma_2d_pair(dst + A_BYTES, mb, kb * BK, brow, fb);
+              }
             }
           }
           __syncwarp();
