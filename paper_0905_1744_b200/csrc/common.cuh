@@ -153,6 +153,7 @@ struct TcCarry {
   uint32_t* seen1 = nullptr;         // seen-once planes (one plane, all layers)
   int32_t* ndense = nullptr;         // [np] dense layers each problem of the building launch kept
   int np = 0;
+  uint32_t* masks = nullptr;         // [nrows][2][256] layer-2 / layer-3 masks (minsum_tc.cu TcMasks)
 };
 sa_status tc_launch(const std::vector<MsProblem>& probs, int ldw16, int32_t bins, uint32_t* state,
                     uint32_t* cols_out, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1,

@@ -82,6 +82,21 @@ struct TcOut {
   int prob[2 * tc::MAXPROB];
 };
 
+// Per row, the histogram pass also stores its layer-2 and layer-3 masks
+// ([c >= 2], [c >= 3]: 2 x 256 words, 2 KB, coalesced); the build then reads
+// the listed layer-2 / layer-3 columns from them instead of gathering counts
+// from the 16 KB profile row (one 32-byte DRAM sector per gathered count).
+// Rows [0, split) of a launch with a carried side use the carry's masks.
+constexpr int TC_MW = TC_WPL;   // mask words per layer
+struct TcMasks {
+  uint32_t* own;                // rows [split, R): row g at own + (g - split) * 2 * TC_MW
+  const uint32_t* carried;      // rows [0, split)
+  int64_t split;
+  __device__ __forceinline__ const uint32_t* row(int64_t g) const {
+    return g < split ? carried + g * 2 * TC_MW : own + (g - split) * 2 * TC_MW;
+  }
+};
+
 // 32 layer-mask bits (bin i of the thread's word -> bit i) as operand columns:
 // FP4: 16 bytes, column i = nibble i (e2m1 1.0 = 0b0010); u8: 32 bytes of 0/1.
 template <bool FP4>
@@ -119,7 +134,7 @@ constexpr int TC_SPEC = 2;
 template <bool FP4>
 __global__ void __launch_bounds__(TC_HIST_THREADS)
 tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut O, int stride16, int bins,
-               uint32_t* __restrict__ planes, uint32_t* __restrict__ state, int64_t hist_from) {
+               uint32_t* __restrict__ planes, uint32_t* __restrict__ state, int64_t hist_from, TcMasks mk) {
   constexpr int64_t ROWB = FP4 ? TC_KCAP / 2 : TC_KCAP;
   const int dw = (bins + 15) & ~15;                      // columns per dense layer
   const int64_t layer_bytes = FP4 ? dw / 2 : dw;
@@ -189,13 +204,20 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
         mx = max(mx, vmax);
         const bool in_cols = w * 32 < dw;
         uint8_t* orow = O.out[t] + (g - S.row_begin[t] + h) * ROWB + (FP4 ? w * 16 : w * 32);
+        uint32_t m23[2] = {0u, 0u};   // [c >= 2], [c >= 3] of the thread's 32 bins
 #pragma unroll
         for (int l = 0; l < TC_HREG; ++l) {
           const uint32_t m = (uint32_t)l < vmax ? layer_mask(v, (uint32_t)(l + 1) * 0x00010001u) : 0u;
           if (l < TC_SPEC && h < cnt && in_cols) store_mask_columns<FP4>(orow + l * layer_bytes, m, dw - w * 32);
-          if ((uint32_t)l >= vmax && l >= TC_SPEC) break;
+          if (l == 1 || l == 2) m23[l - 1] = m;
+          if ((uint32_t)l >= vmax && l >= TC_SPEC + 1) break;
           s2[l] |= s1[l] & m;
           s1[l] |= m;
+        }
+        if (h < cnt) {
+          uint32_t* mr = mk.own + (g + h - hist_from) * 2 * TC_MW;
+          mr[w] = m23[0];
+          mr[TC_MW + w] = m23[1];
         }
         const int top = (int)min(vmax, (uint32_t)TC_LCAP);
         for (int l = TC_HREG; l < top; ++l) {
@@ -405,7 +427,7 @@ template <bool FP4>
 __global__ void __launch_bounds__(TC_BUILD_THREADS)
 tc_build_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut O, int stride16, int bins,
                 const uint32_t* __restrict__ collist, const int32_t* __restrict__ kblocks,
-                const int32_t* __restrict__ ndense, const uint32_t* __restrict__ state) {
+                const int32_t* __restrict__ ndense, const uint32_t* __restrict__ state, TcMasks mk) {
   constexpr int64_t ROWB = FP4 ? TC_KCAP / 2 : TC_KCAP;
   constexpr int KBC = FP4 ? 256 : 128;   // columns per K block
   if (tc_infeasible(state)) return;
@@ -435,6 +457,7 @@ tc_build_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut
     for (int item = tid; item < cnt * ns; item += TC_BUILD_THREADS) {
       const int h = item / ns, c = c0 + item % ns;
       const uint16_t* row = S.rows[t] + (rbase + h) * (int64_t)stride16;
+      const uint32_t* mrow = mk.row(g + h);
       uint32_t o[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -443,8 +466,12 @@ tc_build_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut
         uint32_t word = 0;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-          const uint32_t layer = es[b] >> 16;
-          const uint32_t bit = (layer != 0u && (uint32_t)__ldg(row + (es[b] & 0xffffu)) >= layer) ? 1u : 0u;
+          const uint32_t layer = es[b] >> 16, bin = es[b] & 0xffffu;
+          uint32_t bit;
+          if (layer == 2u || layer == 3u)   // from the row's layer mask
+            bit = (__ldg(mrow + (layer - 2u) * TC_MW + (bin >> 5)) >> (bin & 31u)) & 1u;
+          else
+            bit = (layer != 0u && (uint32_t)__ldg(row + bin) >= layer) ? 1u : 0u;
           word |= FP4 ? (bit << (4 * b + 1)) : (bit << (8 * b));
         }
         o[k] = word;
@@ -1165,11 +1192,20 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     if (carried)
       SA_CUDA(cudaMemcpyAsync(planes, use->seen1, TC_PLANE * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
     const int64_t hfrom = carried ? sides.row_begin[1] : 0;
+    // layer-2/3 masks of the rows this launch's histogram pass covers (a keeping
+    // launch's live in the caller's scratch, for the next launch's carried side)
+    TcMasks mk{};
+    mk.split = hfrom;
+    mk.carried = carried ? use->masks : nullptr;
+    mk.own = (kept ? keep->scratch : &scratch)->alloc<uint32_t>((size_t)(R - hfrom) * 2 * TC_MW);
+    if (!mk.own) return fail(SA_E_NOMEM, "scratch allocation of K2T layer masks failed");
     const int hx = (int)std::max<int64_t>(
         1, std::min<int64_t>((R - hfrom + TC_HIST_ROWS - 1) / TC_HIST_ROWS, 4 * g_num_sms));
     const int hsm = 2 * (TC_LCAP - TC_HREG) * TC_WPL * 4;
-    if (fp4) tc_hist_kernel<true><<<hx, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, hfrom);
-    else tc_hist_kernel<false><<<hx, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, hfrom);
+    if (fp4)
+      tc_hist_kernel<true><<<hx, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, hfrom, mk);
+    else
+      tc_hist_kernel<false><<<hx, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, hfrom, mk);
     SA_LAUNCHED();
     if (kept) {
       uint32_t* s1 = keep->scratch->alloc<uint32_t>(TC_PLANE);
@@ -1184,6 +1220,7 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       keep->seen1 = s1;
       keep->ndense = ndense;
       keep->np = np;
+      keep->masks = mk.own;
     }
     tc_select_kernel<<<np, 1024, 0, st>>>(sel, planes, bins, kbc, collist, kblocks, ndense, state, cols_out);
     SA_LAUNCHED();
@@ -1194,12 +1231,12 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       tc_dense_kernel<true><<<8 * g_num_sms, 256, 0, st>>>(sides, outs, stride16, bins, ndense, state, cnd, cnp);
       SA_LAUNCHED();
       tc_build_kernel<true><<<bx, TC_BUILD_THREADS, 0, st>>>(sides, outs, stride16, bins, collist, kblocks, ndense,
-                                                             state);
+                                                             state, mk);
     } else {
       tc_dense_kernel<false><<<8 * g_num_sms, 256, 0, st>>>(sides, outs, stride16, bins, ndense, state, cnd, cnp);
       SA_LAUNCHED();
       tc_build_kernel<false><<<bx, TC_BUILD_THREADS, 0, st>>>(sides, outs, stride16, bins, collist, kblocks, ndense,
-                                                              state);
+                                                              state, mk);
     }
     SA_LAUNCHED();
     // GEMM
