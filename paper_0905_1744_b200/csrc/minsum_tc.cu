@@ -648,7 +648,10 @@ struct KeyMatEpi {
   // (y = d = 0) meets C = 0 (an empty or missing row / column: zero profile or
   // TMA zero fill), and C = 0 gives +0 whatever side is taken.
   __device__ __forceinline__ static double fsel(uint32_t C, double yr, double dr, double yc, double dc) {
-    const bool col = yc > yr;
+    // y > 0 (or the +0 sentinel) order like their bit patterns; distinct D < 2^16
+    // differ in the high word (relative gap 1/D > 2^-20), so an integer compare
+    // of the high words (ALU pipe) decides yc > yr
+    const bool col = __double2hiint(yc) > __double2hiint(yr);
     return f_ratio_y(C, col ? dc : dr, col ? yc : yr);
   }
   // experiment (SA_K2T_DEBUG bit 64): a stand-in for F with no fp64 arithmetic
