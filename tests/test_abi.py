@@ -113,3 +113,14 @@ def test_exchange_plan_host_logic():
     assert B.recv_sizes(counts, nbytes, 4, 2, 0) == (6, 600)
     assert B.recv_sizes(counts, nbytes, 4, 2, 1) == (6, 600)
     assert B.recv_sizes(counts[:1], nbytes[:1], 4, 1, 0) == (6, 600)
+
+
+def test_host_checked_arguments_without_a_device(lib):
+    """Argument errors are host-checked before any CUDA call (SA_E_INVAL with
+    no GPU present); sa_last_error names the problem."""
+    import ctypes
+    # NULL context
+    assert lib.sa_pack_upper_u16(None, None, 4, 4, None, None) == B.SA_E_INVAL
+    assert b"ctx" in lib.sa_last_error()
+    assert lib.sa_bucket_similarity_batch(None, 1, None, None, None, 8000, None, None, None, None) == B.SA_E_INVAL
+    assert lib.sa_ctx_tc_operand(None) == -1
