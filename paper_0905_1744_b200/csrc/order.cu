@@ -303,10 +303,8 @@ sa_status segsort_launch_impl(const sa_key128* keys, const int64_t* gids, int64_
                               int64_t total, int64_t window, int32_t* order_out, uint32_t* amb_count,
                               cudaStream_t st) {
   if (nseg <= 0 || total <= 0) return SA_OK;
-  static const bool one_cta = [] {   // SA_SEGSORT=cta: the one-CTA-per-segment kernel
-    const char* e = getenv("SA_SEGSORT");
-    return e && !strcmp(e, "cta");
-  }();
+  const char* env = getenv("SA_SEGSORT");   // SA_SEGSORT=cta: the one-CTA-per-segment kernel (read per call)
+  const bool one_cta = env && !strcmp(env, "cta");
   if (one_cta) {
     void* scratch = nullptr;
     SA_CUDA(cudaMallocAsync(&scratch, (size_t)total * 8, st));

@@ -349,6 +349,19 @@ def test_partition_matches_golden(ctx, monkeypatch, c, eng):
     assert part.exact_fallbacks == 0      # synthetic data has no uncertified comparisons
 
 
+@pytest.mark.parametrize("segsort", ["grid", "cta"])
+def test_partition_segment_sorts_agree(ctx, monkeypatch, segsort):
+    """Both exact segment sorts (grid-wide passes, default; one CTA per block,
+    SA_SEGSORT=cta) give the oracle's partition of config 2."""
+    monkeypatch.setenv("SA_SEGSORT", segsort)
+    g, meta = load_golden(2)
+    ds, P, nk, part = _partition_g1(ctx, 2)
+    d = part.debug
+    assert np.array_equal(d["local_order"].cpu().numpy(), g["local_order"])
+    assert np.array_equal(d["global_order"].cpu().numpy(), g["global_order"])
+    assert np.array_equal(part.bucket_of.cpu().numpy(), g["bucket_of"])
+
+
 def test_partition_invariants_any_size(ctx):
     """Properties that hold at any size: permutation, the
     regular-sampling bound 2N/p, pivot boundaries respected."""
