@@ -249,6 +249,26 @@ __global__ void tc_or_planes_kernel(const uint32_t* __restrict__ planes, int nsi
   }
 }
 
+// Per-row epilogue info (TcEpiProb kinfo / yinfo) of every row of every side.
+struct TcNk {
+  const int32_t* nk[2 * tc::MAXPROB];
+};
+__global__ void tc_info_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcNk N,
+                               uint4* __restrict__ kinfo, double2* __restrict__ yinfo, const uint32_t* __restrict__ state) {
+  if (tc_infeasible(state)) return;
+  const int64_t R = S.row_begin[S.n];
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < R; g += (int64_t)gridDim.x * blockDim.x) {
+    int t = 0;
+    while (g >= S.row_begin[t + 1]) ++t;
+    const int nk = N.nk[t][g - S.row_begin[t]];
+    const int ns = nk > 0 ? nk : -1;
+    const int d = ns > 0 ? ns : 0;
+    const uint64_t r = g_rtab[d];
+    kinfo[g] = make_uint4((uint32_t)r, (uint32_t)(r >> 32), g_etab[d], (uint32_t)ns);
+    yinfo[g] = make_double2(g_rcp[d], (double)d);
+  }
+}
+
 // ------------------------------------------------------ column select ----
 struct TcSel {
   int side_a[tc::MAXPROB], side_b[tc::MAXPROB];   // side_b = -1: symmetric
@@ -490,6 +510,13 @@ tc_build_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut
 struct TcEpiProb {
   const int32_t* nkA;
   const int32_t* nkB;
+  // per row of each side, precomputed by tc_info_kernel (one 16-byte load in
+  // the epilogue instead of nk -> dependent table gathers): keys {rl, rh, e, nk'},
+  // F {RN(1/nk'), nk'} (nk' = nk if > 0, else -1 with zero tables)
+  const uint4* kinfoA;
+  const uint4* kinfoB;
+  const double2* yinfoA;
+  const double2* yinfoB;
   sa_key128* keyA;
   sa_key128* keyB;
   uint16_t* num;
@@ -612,31 +639,26 @@ struct KeyMatEpi {
     s.rv = row < T.ra;
     s.nk0 = s.rv ? E.nkA[s.row_g] : 0;
     s.nk = s.nk0 > 0 ? s.nk0 : -1;
-    const int dr = s.nk > 0 ? s.nk : 0;
     if constexpr (KEYS) {
-      const uint64_t r = g_rtab[dr];
-      s.rl = (uint32_t)r;
-      s.rh = (uint32_t)(r >> 32);
-      s.ek = g_etab[dr];
+      const uint4 k = s.rv ? __ldg(E.kinfoA + s.row_g) : make_uint4(0u, 0u, 0u, 0xffffffffu);
+      s.rl = k.x;
+      s.rh = k.y;
+      s.ek = k.z;
     }
     if constexpr (SIM) {
-      s.y = g_rcp[dr];
-      s.d = (double)dr;
+      const double2 yd = s.rv ? __ldg(E.yinfoA + s.row_g) : make_double2(0.0, 0.0);
+      s.y = yd.x;
+      s.d = yd.y;
     }
     if constexpr (KEYS || SIM) {
       for (int c = cbeg + lane; c < cend; c += 32) {
-        const int nkc = c < T.rb ? E.nkB[T.col0 + c] : 0;
-        const int ns = nkc > 0 ? nkc : -1;
-        const int dc = ns > 0 ? ns : 0;
+        const bool cv = c < T.rb;
         uint8_t* ent = tab + (c - cbeg) * TAB_BYTES;
-        if constexpr (KEYS) {
-          const uint64_t r = g_rtab[dc];
-          *reinterpret_cast<uint4*>(ent + KOFF) = make_uint4((uint32_t)r, (uint32_t)(r >> 32), g_etab[dc], (uint32_t)ns);
-        }
-        if constexpr (SIM) {
-          const double y = g_rcp[dc], d = (double)dc;
-          *reinterpret_cast<double2*>(ent + YOFF) = make_double2(y, d);
-        }
+        if constexpr (KEYS)
+          *reinterpret_cast<uint4*>(ent + KOFF) =
+              cv ? __ldg(E.kinfoB + T.col0 + c) : make_uint4(0u, 0u, 0u, 0xffffffffu);
+        if constexpr (SIM)
+          *reinterpret_cast<double2*>(ent + YOFF) = cv ? __ldg(E.yinfoB + T.col0 + c) : make_double2(0.0, 0.0);
       }
     }
     __syncwarp();
@@ -1160,10 +1182,13 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       side_n.push_back(n);
       return sides.n++;
     };
+    TcNk sides_nk{};
     for (int q = 0; q < np; ++q) {
       const MsProblem& P = probs[i0 + q];
       sel.side_a[q] = add_side(P.A, P.na, q);
+      sides_nk.nk[sel.side_a[q]] = P.nkA;
       sel.side_b[q] = P.sym ? -1 : add_side(P.B, P.nb, q);
+      if (!P.sym) sides_nk.nk[sel.side_b[q]] = P.nkB;
     }
     SA_ALLOC(planes, uint32_t, (size_t)sides.n * 2 * TC_PLANE);
     SA_ALLOC(collist, uint32_t, (size_t)np * TC_KCAP);
@@ -1227,6 +1252,12 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     }
     tc_select_kernel<<<np, 1024, 0, st>>>(sel, planes, bins, kbc, collist, kblocks, ndense, state, cols_out);
     SA_LAUNCHED();
+    uint4* kinfo = scratch.alloc<uint4>((size_t)R);
+    double2* yinfo = scratch.alloc<double2>((size_t)R);
+    if (!kinfo || !yinfo) return fail(SA_E_NOMEM, "scratch allocation of K2T row info failed");
+    tc_info_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((R + 255) / 256, 4 * g_num_sms)), 256, 0, st>>>(
+        sides, sides_nk, kinfo, yinfo, state);
+    SA_LAUNCHED();
     const int bx = (int)std::max<int64_t>(1, std::min<int64_t>(R, 4 * g_num_sms));
     const int32_t* cnd = carried ? use->ndense : nullptr;
     const int cnp = carried ? use->np : 0;
@@ -1284,6 +1315,14 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       TcEpiProb& E = epi.e[q];
       E.nkA = P.nkA;
       E.nkB = P.nkB;
+      {
+        const int64_t ra = sides.row_begin[sel.side_a[q]];
+        const int64_t rb = sides.row_begin[P.sym ? sel.side_a[q] : sel.side_b[q]];
+        E.kinfoA = kinfo + ra;
+        E.kinfoB = kinfo + rb;
+        E.yinfoA = yinfo + ra;
+        E.yinfoB = yinfo + rb;
+      }
       E.keyA = P.keyA;
       E.keyB = P.sym ? P.keyB : nullptr;
       // S5's F: in the tensor-core epilogue (default), or (SA_K2T_FPASS=1) numerators
