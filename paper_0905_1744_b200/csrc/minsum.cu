@@ -670,7 +670,10 @@ sa_status to_u8_launch(const uint16_t* p16, int64_t n, int32_t stride16, int32_t
   if (n <= 0) return SA_OK;
   const int64_t work = n * (stride8 / 8);
   const int64_t blocks = (work + 255) / 256;
-  to_u8_kernel<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, st>>>(p16, n, stride16, p8, stride8, maxc, guarded);
+  // a guarded conversion (the K2T fallback's rows) usually returns at once:
+  // a small grid keeps that cheap (it strides over the rows when it does run)
+  const int64_t cap = guarded ? 148 * 2 : 148 * 16;
+  to_u8_kernel<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, st>>>(p16, n, stride16, p8, stride8, maxc, guarded);
   SA_LAUNCHED();
   return SA_OK;
 }
