@@ -19,10 +19,11 @@ profiles_kernel(const uint8_t* __restrict__ res, const int64_t* __restrict__ off
   extern __shared__ __align__(16) uint32_t hist[];   // stride / 2 words
   const int words = stride >> 1;
   const int vec = words >> 2;                         // uint4 per row (stride % 64 == 0)
+  uint4* h4 = reinterpret_cast<uint4*>(hist);
+  for (int v = threadIdx.x; v < vec; v += blockDim.x) h4[v] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  // the copy-out of each row zeroes the histogram for the next one
   for (int64_t s = blockIdx.x; s < n; s += gridDim.x) {
-    uint4* h4 = reinterpret_cast<uint4*>(hist);
-    for (int v = threadIdx.x; v < vec; v += blockDim.x) h4[v] = make_uint4(0, 0, 0, 0);
-    __syncthreads();
     const int64_t b = offs[s], e = offs[s + 1];
     const int64_t len = e - b;
     const int64_t nk = len >= k ? len - k + 1 : 0;
@@ -48,9 +49,15 @@ profiles_kernel(const uint8_t* __restrict__ res, const int64_t* __restrict__ off
     __syncthreads();
     uint4* o4 = reinterpret_cast<uint4*>(out + s * (int64_t)stride);
     if (cs) {
-      for (int v = threadIdx.x; v < vec; v += blockDim.x) __stcs(o4 + v, h4[v]);
+      for (int v = threadIdx.x; v < vec; v += blockDim.x) {
+        __stcs(o4 + v, h4[v]);
+        h4[v] = make_uint4(0, 0, 0, 0);
+      }
     } else {
-      for (int v = threadIdx.x; v < vec; v += blockDim.x) o4[v] = h4[v];
+      for (int v = threadIdx.x; v < vec; v += blockDim.x) {
+        o4[v] = h4[v];
+        h4[v] = make_uint4(0, 0, 0, 0);
+      }
     }
     __syncthreads();
   }
