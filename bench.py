@@ -361,7 +361,8 @@ def main():
     e2e = None
     if not args.no_e2e:
         h_out = {}
-        copy_st = torch.cuda.Stream(device=dev)
+        # two copy streams, alternating by bucket: two copy engines share the PCIe link
+        copy_sts = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
 
         def pinned(k, t):
             if k not in h_out or h_out[k].shape != t.shape:
@@ -382,6 +383,7 @@ def main():
             pk = B.sa_pack_upper_u16(ctx, num, d_packed[b], stream=st)
             ev = torch.cuda.Event()
             ev.record(st)
+            copy_st = copy_sts[b % 2]
             copy_st.wait_event(ev)
             with torch.cuda.stream(copy_st):
                 pinned(f"num{b}", pk.view(torch.int16)).copy_(pk.view(torch.int16), non_blocking=True)
@@ -394,7 +396,8 @@ def main():
             for num in o.numerators:
                 if num is not None:
                     nb += num.shape[0] * (num.shape[0] + 1) // 2 * 2
-            st.wait_stream(copy_st)          # the step ends when every result is on the host
+            for cs in copy_sts:
+                st.wait_stream(cs)           # the step ends when every result is on the host
             return nb
 
         res_dd = torch.empty_like(res_d)
