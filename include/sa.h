@@ -276,6 +276,20 @@ sa_status sa_bucket_similarity_batch(sa_ctx* ctx, int32_t nbuckets, const uint16
                                      const int64_t* row_begin_h, int32_t bins, uint16_t* const* numerators_h,
                                      double* const* similarity_h, const int64_t* ld_h, void* stream);
 
+/* --------------------------------------------- N4: bucket guide tree ----- */
+/* The guide tree the underlying MSA builds from a bucket's similarity matrix
+ * (SPEC build_guide_tree S:277-285): UPGMA on
+ * d = 1 - F (readings T1-T3): n - 1 merges of the active pair
+ * (a, b), a < b, of largest F, ties to the smallest (a, b); a cluster's id is
+ * its smallest member; F(ab, c) = (n_a F_ac + n_b F_bc) / (n_a + n_b) with
+ * IEEE round-to-nearest on every operation; merge height (1 - F_ab) / 2.
+ * Inputs: similarity [n][ld] (device, row-major, symmetric; the diagonal is
+ * ignored).  Outputs (device): merges [n-1][2] (a, b), heights [n-1], in
+ * merge order (n = 1: nothing written).  One CTA runs the merges (they are
+ * sequential); O(n^2) work.  SA_E_INVAL: n < 1, ld < n, NULL pointers. */
+sa_status sa_guide_tree(sa_ctx* ctx, const double* similarity, int32_t n, int64_t ld, int32_t* merges,
+                        double* heights, void* stream);
+
 /* Packed upper triangle (diagonal included) of a symmetric n x n uint16
  * matrix with row stride ld >= n: row i's columns i..n-1 at packed offset
  * i*n - i*(i-1)/2, n(n+1)/2 elements in all -- the complete content of a

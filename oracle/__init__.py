@@ -22,5 +22,7 @@ Pins (tests/test_oracle.py, ``-m "not gpu"``):
   * partition.*                        -- SPEC position / pivot / bucket
     examples, closed-form partitions of identical sequences, two-cluster
     purity, permutation and 2N/p invariants.
+  * tree.upgma (N4)                    -- SPEC guide-tree examples, the tie
+    rule on all-tied matrices, scipy average-linkage heights, monotone heights.
 No oracle function is "parity unpinned".
 """

@@ -27,7 +27,7 @@ EXPORTED = ["sa_ctx_create", "sa_ctx_attach_comm", "sa_ctx_destroy", "sa_last_er
             "sa_ctx_set_timing", "sa_ctx_phase_ms", "sa_profile_stride", "sa_kmer_profiles", "sa_kmer_rank",
             "sa_partition", "sa_redistribute", "sa_bucket_similarity", "sa_exact_rank_compare", "sa_ctx_engine",
             "sa_ctx_set_rank_form", "sa_ctx_tc_columns", "sa_ctx_tc_operand", "sa_selftest_f_division",
-            "sa_bucket_similarity_batch", "sa_pack_upper_u16"]
+            "sa_bucket_similarity_batch", "sa_pack_upper_u16", "sa_guide_tree"]
 SA_RANK_F, SA_RANK_DF = 0, 1
 
 
@@ -100,6 +100,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                                       ctypes.POINTER(ctypes.c_int64), VP]),
         "sa_exact_rank_compare": (ctypes.c_int, [P, I32, P, I32, P, I32]),
         "sa_pack_upper_u16": (ctypes.c_int, [P, P, I32, ctypes.c_int64, P, VP]),
+        "sa_guide_tree": (ctypes.c_int, [P, P, I32, ctypes.c_int64, P, P, VP]),
         "sa_ctx_engine": (ctypes.c_int, [P]),
         "sa_ctx_tc_columns": (ctypes.c_int32, [P, P, ctypes.c_int32]),
         "sa_ctx_tc_operand": (ctypes.c_int, [P]),
@@ -419,6 +420,21 @@ def sa_bucket_similarity_batch(ctx: Context, profiles, nkmers, row_begin, bins: 
     _check(load_library().sa_bucket_similarity_batch(ctx.handle, nb, _ptr(profiles), _ptr(nkmers), rb, bins,
                                                      nums, sims, ldh, _stream(stream)))
     return numerators, similarity
+
+
+def sa_guide_tree(ctx: Context, similarity: torch.Tensor, stream=None):
+    """N4: UPGMA guide tree of a bucket's similarity matrix (n x n fp64 view,
+    any row stride >= n).  Returns (merges int32 [n-1][2], heights f64 [n-1])
+    on the device (sa.h)."""
+    if similarity.dtype != torch.float64 or not similarity.is_cuda or similarity.dim() != 2 \
+            or similarity.shape[0] != similarity.shape[1] or similarity.stride(1) != 1:
+        raise ValueError("similarity must be an n x n float64 CUDA tensor with contiguous rows")
+    n = similarity.shape[0]
+    merges = torch.empty((max(n - 1, 0), 2), dtype=torch.int32, device=similarity.device)
+    heights = torch.empty(max(n - 1, 0), dtype=torch.float64, device=similarity.device)
+    _check(load_library().sa_guide_tree(ctx.handle, ctypes.c_void_p(similarity.data_ptr()), n, similarity.stride(0),
+                                        _ptr(merges), _ptr(heights), _stream(stream)))
+    return merges, heights
 
 
 def sa_pack_upper_u16(ctx: Context, matrix: torch.Tensor, packed: torch.Tensor | None = None, stream=None):

@@ -1056,6 +1056,17 @@ sa_status sa_bucket_similarity(sa_ctx* ctx, const uint16_t* profiles, const int3
   return SA_OK;
 }
 
+sa_status sa_guide_tree(sa_ctx* ctx, const double* similarity, int32_t n, int64_t ld, int32_t* merges,
+                        double* heights, void* stream) {
+  g_err.clear();
+  if (!ctx) return fail(SA_E_INVAL, "ctx is NULL");
+  if (n < 1 || ld < n) return fail(SA_E_INVAL, "bad n / ld");
+  if (n == 1) return SA_OK;
+  if (!similarity || !merges || !heights) return fail(SA_E_INVAL, "NULL required pointer");
+  SA_CUDA(cudaSetDevice(ctx->device));
+  return upgma_launch(similarity, n, ld, merges, heights, (cudaStream_t)stream);
+}
+
 sa_status sa_pack_upper_u16(sa_ctx* ctx, const uint16_t* matrix, int32_t n, int64_t ld, uint16_t* packed,
                             void* stream) {
   g_err.clear();

@@ -211,6 +211,48 @@ def test_pack_upper_u16(ctx, n, ld_align):
     assert np.array_equal(packed, Co[np.triu_indices(n)])
 
 
+@pytest.mark.parametrize("n,seed,ties", [(1, 0, False), (2, 1, False), (3, 2, False), (57, 3, False),
+                                         (300, 4, False), (64, 5, True)])
+def test_guide_tree_matches_oracle(ctx, n, seed, ties):
+    """N4: sa_guide_tree on a bucket's S5 similarity matrix (random sets,
+    duplicates -> exactly tied similarities) equals the oracle's UPGMA merge
+    for merge and height for height (bit-exact fp64)."""
+    from oracle import tree
+    ds = _rand_set(600 + seed, n, 0, 420, dup=(n // 3 if ties else 0))
+    res, offs = to_dev(ds)
+    P, nk = B.sa_kmer_profiles(ctx, res, offs)
+    _, sims = B.sa_bucket_similarity_batch(ctx, P, nk, [0, n], want_numerators=False, ld_align=16)
+    merges, heights = B.sa_guide_tree(ctx, sims[0])
+    Po, nko = kmer.profiles(ds.residues, ds.offsets)
+    _, Fo = partition.bucket_similarity(Po, nko, np.arange(n))
+    mo, ho = tree.upgma(Fo)
+    assert np.array_equal(merges.cpu().numpy().astype(np.int64), mo)
+    assert np.array_equal(heights.cpu().numpy(), ho)
+
+
+def test_guide_tree_on_a_config_bucket(ctx):
+    """N4 on config 1's largest bucket after the full partition; the oracle
+    side takes that bucket's members from the oracle's golden partition and
+    its F from the oracle's own profiles."""
+    from oracle import tree
+    g, _ = load_golden(1)
+    ds = generate(CONFIGS[1])
+    res, offs = to_dev(ds)
+    hp = HotPath(ctx, CONFIGS[1].p, CONFIGS[1].samples_per_block)
+    out = hp.step(res, offs, ds.n, 0)
+    sizes = [nb for _, _, nb in out.buckets]
+    b = int(np.argmax(sizes))
+    merges, heights = B.sa_guide_tree(ctx, out.similarity[b])
+    members = np.flatnonzero(g["bucket_of"] == b)
+    assert len(members) == sizes[b]
+    Po, nko = kmer.profiles(ds.residues, ds.offsets)
+    _, Fo = partition.bucket_similarity(Po, nko, members)
+    mo, ho = tree.upgma(Fo)
+    assert np.array_equal(merges.cpu().numpy().astype(np.int64), mo)
+    assert np.array_equal(heights.cpu().numpy(), ho)
+    assert np.all(np.diff(ho) >= 0)
+
+
 def test_tc_falls_back_on_deep_counts(ctx, monkeypatch):
     """K2T tracks 32 threshold layers: a bin count of 33..255 must hand the call
     to the uint8 SAD engine on the device, exactly."""

@@ -376,3 +376,53 @@ def test_dF_partition_closed_form_and_invariants():
     allm = np.concatenate(r.buckets)
     assert np.array_equal(np.sort(allm), np.arange(ds.n))
     assert max(len(b) for b in r.buckets) <= 2 * ds.n / 4
+
+
+# ------------------------------------------------------------ N4 tree ------
+from oracle import tree  # noqa: E402
+
+
+def test_upgma_spec_examples():
+    """SPEC build_guide_tree examples, with d = 1 - F (reading T1):
+    one sequence -> no merge; two -> one merge at half their distance; three
+    with d(A,B) < d(A,C) = d(B,C) -> (A, B) merged first."""
+    m, h = tree.upgma(np.ones((1, 1)))
+    assert m.shape == (0, 2) and h.shape == (0,)
+    F2 = np.array([[1.0, 0.3], [0.3, 1.0]])
+    m, h = tree.upgma(F2)
+    assert m.tolist() == [[0, 1]] and h[0] == (1.0 - 0.3) / 2.0
+    F3 = np.array([[1.0, 0.8, 0.2], [0.8, 1.0, 0.2], [0.2, 0.2, 1.0]])
+    m, h = tree.upgma(F3)
+    assert m.tolist() == [[0, 1], [0, 2]]
+    assert h.tolist() == [(1 - 0.8) / 2, (1 - 0.2) / 2]
+
+
+def test_upgma_ties_take_the_smallest_pair():
+    """All off-diagonal similarities equal: every average stays equal, so the
+    tie rule alone orders the merges: (0,1), (0,2), (0,3), ..."""
+    n = 6
+    F = np.full((n, n), 0.25)
+    np.fill_diagonal(F, 1.0)
+    m, h = tree.upgma(F)
+    assert m.tolist() == [[0, j] for j in range(1, n)]
+    assert np.all(h == 0.375)
+
+
+def test_upgma_matches_scipy_average_linkage():
+    """UPGMA = average linkage: on tie-free random symmetric matrices the merge
+    heights equal scipy's average-linkage heights on d = 1 - F (a library
+    routine), and they never decrease."""
+    from scipy.cluster.hierarchy import linkage
+    from scipy.spatial.distance import squareform
+    rng = np.random.default_rng(5)
+    for n in (3, 7, 40):
+        A = rng.random((n, n))
+        F = (A + A.T) / 2
+        np.fill_diagonal(F, 1.0)
+        m, h = tree.upgma(F)
+        D = 1.0 - F
+        np.fill_diagonal(D, 0.0)
+        Z = linkage(squareform(D, checks=False), method="average")
+        assert np.allclose(h, Z[:, 2] / 2.0, rtol=0, atol=1e-12)
+        assert np.all(np.diff(h) >= -1e-15)
+        assert len(set(m[:, 1].tolist())) == n - 1 and np.all(m[:, 0] < m[:, 1])
