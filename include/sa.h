@@ -11,7 +11,10 @@
  *   S2  k-mer rank vs a pool (Eq. 1 averaged)     sa_kmer_rank (S2a/S2d inside sa_partition)
  *   S3  rank-based sample-sort partition          sa_partition
  *   S4  all-to-all redistribution                 sa_redistribute
- *   S5  all-pairs similarity inside a bucket      sa_bucket_similarity
+ *   S5  all-pairs similarity inside a bucket      sa_bucket_similarity (_batch)
+ * and, past the hot path:
+ *   N4  the bucket's guide tree (UPGMA)           sa_guide_tree
+ *   result transfer: packed symmetric matrices    sa_pack_upper_u16
  *
  * Conventions for every call:
  *   - pointers are DEVICE pointers unless the name ends in _h (host);
