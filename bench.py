@@ -324,10 +324,10 @@ def main():
                 tj = json.load(f)
             if tj.get("operand", "u8") == operand:
                 traffic = tj.get("dram_bytes_per_launch")
-        pairs = os.environ.get("SA_K2T_PAIR", "1") != "0"
+        cta_pairs = os.environ.get("SA_K2T_PAIR", "1") != "0"
         roof = {"bound": "tensor",
-                "kernel": (f"tc::{'gemm2_kernel' if pairs else 'gemm_kernel'}<KeyMatEpi<NUM|SIM>> (K2T, "
-                           f"{'tcgen05 cta_group::2 CTA pairs' if pairs else 'one CTA per tile'}, {operand} operands, "
+                "kernel": (f"tc::{'gemm2_kernel' if cta_pairs else 'gemm_kernel'}<KeyMatEpi<NUM|SIM>> (K2T, "
+                           f"{'tcgen05 cta_group::2 CTA pairs' if cta_pairs else 'one CTA per tile'}, {operand} operands, "
                            f"S5 bucket matrices, one launch per step)"),
                 "engine": engine, "operand": operand,
                 "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TOP/s",
