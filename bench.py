@@ -14,7 +14,8 @@ value   = k-mer similarity sequence-pairs evaluated per second by the whole job
           of K device-timed steps, inputs resident in HBM;
 e2e     = the same through the public API with the step's inputs copied from
           pinned host memory and its results (buckets, member ids, uint16
-          numerator matrices) copied back inside the timed region;
+          numerator matrices) copied back inside the timed region (consecutive
+          steps pipelined: step t+1 computes while step t's results copy);
 roofline= the dominant kernel over the S5 launches: K2T (tensor-core threshold
           layers, default) in TOP/s against the u8 tensor peak (DESIGN.md
           §4b), or K2 (SAD / u16 fallback) in bin-ops/s against the derived
@@ -372,7 +373,11 @@ def main():
                 h_out[k] = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
             return h_out[k]
 
-        d_packed = {}
+        # packed triangles double-buffered by step parity: step t + 1's S1-S4
+        # (and its buckets' S5) overlap step t's copies; a buffer is reused
+        # only after the copy that read it two steps earlier has finished
+        d_packed, copied = {}, {}
+        parity = [0]
 
         def on_bucket(b, num, sim):
             # bucket b's numerator matrix, packed to its upper triangle (the
@@ -381,17 +386,22 @@ def main():
             if num is None:
                 return
             n_b = num.shape[0]
-            if b not in d_packed or d_packed[b].numel() != n_b * (n_b + 1) // 2:
-                d_packed[b] = torch.empty(n_b * (n_b + 1) // 2, dtype=torch.uint16, device=dev)
-            pk = B.sa_pack_upper_u16(ctx, num, d_packed[b], stream=st)
+            key = (parity[0], b)
+            if key not in d_packed or d_packed[key].numel() != n_b * (n_b + 1) // 2:
+                d_packed[key] = torch.empty(n_b * (n_b + 1) // 2, dtype=torch.uint16, device=dev)
+            if key in copied:
+                st.wait_event(copied[key])
+            pk = B.sa_pack_upper_u16(ctx, num, d_packed[key], stream=st)
             ev = torch.cuda.Event()
             ev.record(st)
             copy_st = copy_sts[b % 2]
             copy_st.wait_event(ev)
             with torch.cuda.stream(copy_st):
                 pinned(f"num{b}", pk.view(torch.int16)).copy_(pk.view(torch.int16), non_blocking=True)
+                copied[key] = torch.cuda.Event()
+                copied[key].record(copy_st)
 
-        def d2h_tail(o):
+        def d2h_tail(o, last: bool):
             nb = 0
             for k, t in (("bucket_of", o.part.bucket_of), ("gid", o.recv_global_idx)):
                 pinned(k, t).copy_(t, non_blocking=True)
@@ -399,25 +409,28 @@ def main():
             for num in o.numerators:
                 if num is not None:
                     nb += num.shape[0] * (num.shape[0] + 1) // 2 * 2
-            for cs in copy_sts:
-                st.wait_stream(cs)           # the step ends when every result is on the host
+            parity[0] ^= 1
+            if last:
+                for cs in copy_sts:
+                    st.wait_stream(cs)       # the run ends when every step's results are on the host
             return nb
 
         res_dd = torch.empty_like(res_d)
         offs_dd = torch.empty_like(offs_d)
-        o = hp.step(res_d, offs_d, ds.n, first, on_bucket=on_bucket)   # allocate pinned buffers untimed
-        d2h_tail(o)
+        for _ in range(2):   # allocate both parities' buffers and the pinned host buffers untimed
+            o = hp.step(res_d, offs_d, ds.n, first, on_bucket=on_bucket)
+            d2h_tail(o, last=True)
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(st)
         d2h_bytes = 0
-        for _ in range(args.steps):
+        for i in range(args.steps):
             res_dd.copy_(res_h, non_blocking=True)
             offs_dd.copy_(offs_h, non_blocking=True)
             o = hp.step(res_dd, offs_dd, ds.n, first, on_bucket=on_bucket)
-            d2h_bytes = d2h_tail(o)
+            d2h_bytes = d2h_tail(o, last=i == args.steps - 1)
         f1.record(st)
         torch.cuda.synchronize()
         e2e_ms = max_over_ranks(f0.elapsed_time(f1))
@@ -425,7 +438,8 @@ def main():
                "h2d_bytes_per_step": int(res_h.numel() + offs_h.numel() * 8),
                "d2h_bytes_per_step": int(d2h_bytes), "ms_per_step": e2e_ms / args.steps,
                "results_copied": ("bucket_of, received member ids, and every owned bucket's symmetric uint16 "
-                                  "numerator matrix as its packed upper triangle (sa_pack_upper_u16)")}
+                                  "numerator matrix as its packed upper triangle (sa_pack_upper_u16)"),
+               "overlap": "steps pipelined: step t+1 computes while step t's triangles copy (double-buffered)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
