@@ -1283,6 +1283,7 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     }();
     KeyMatEpi<EPI_ALL> epi{};
     int mode = 0;
+    bool all_sym = true;
     epi.state = state;
     epi.dbg = debug;
     int64_t tiles = 0;
@@ -1339,6 +1340,7 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       E.ln1pd = P.ln1pd;
       E.sym = P.sym;
       mode |= (P.keyA ? EPI_KEYS : 0) | (E.num ? EPI_NUM : 0) | (E.sim ? EPI_SIM : 0);
+      all_sym = all_sym && P.sym;
     }
     // every problem of the launch gets every output its MODE writes (the
     // epilogue's fast paths test no pointer): scratch for a problem that did
@@ -1354,10 +1356,21 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     batch.n = np;
     static const int group = [] {   // SA_K2T_GROUP: row blocks per group of the tile order
       const char* e = getenv("SA_K2T_GROUP");
-      const int g = e ? atoi(e) : 16;
-      return g >= 1 && g <= 64 ? g : 16;
+      const int g = e ? atoi(e) : 12;
+      return g >= 1 && g <= 1024 ? g : 12;
     }();
-    batch.group = group;
+    // SA_K2T_GROUP_KEYS: the same for a keys-only launch of symmetric problems
+    // (S2a's blocks), default one group per problem (column-major over the
+    // triangle: the whole A side stays in L2, nothing else streams through it).
+    // Measured on config 4 (scripts/gpu_group_sweep.sh): S2a 3.75 -> 3.64 ms
+    // with one group, while S2d and S5 (12.5 GB of output through L2) lose
+    // with large groups and gain a little at 12 (S5 GEMM 4.80 -> 4.74 ms).
+    static const int group_keys = [] {
+      const char* e = getenv("SA_K2T_GROUP_KEYS");
+      const int g = e ? atoi(e) : 1 << 20;
+      return g >= 1 ? g : 1 << 20;
+    }();
+    batch.group = (mode == EPI_KEYS && all_sym) ? group_keys : group;
     // SA_K2T_EVICT_LAST=1: operand loads with an L2 evict-last policy (measured:
     // no faster, and more DRAM reads for the S5 launch, whose output streams
     // through L2 -- off by default)

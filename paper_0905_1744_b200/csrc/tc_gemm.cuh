@@ -229,7 +229,7 @@ struct Tile {
 // Tile order inside a problem: groups of GROUP (Batch::group) row blocks; in a group, column
 // block by column block, the group's rows inside (column-major).  The ~148
 // tiles in flight then share ~148 / GROUP column blocks of B and GROUP row
-// blocks of A (config 4 bucket, GROUP = 16: ~38 MB + 34 MB, inside the 126 MB
+// blocks of A (config 4 bucket, GROUP = 12: ~38 MB + 25 MB, inside the 126 MB
 // L2) instead of sweeping all of B every wave.  Symmetric problems keep the tiles with
 // column block J >= I / 2.
 
