@@ -1371,12 +1371,15 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       return g >= 1 ? g : 1 << 20;
     }();
     batch.group = (mode == EPI_KEYS && all_sym) ? group_keys : group;
-    // SA_K2T_EVICT_LAST=1: operand loads with an L2 evict-last policy (measured:
-    // no faster, and more DRAM reads for the S5 launch, whose output streams
-    // through L2 -- off by default)
+    // SA_K2T_EVICT_LAST: operand L2 policies (tc::side_policy bits: 1 / 2 the
+    // A / B side evict_last, 4 / 8 evict_first, 0 no hint).  Default 1: the
+    // group's A row band, re-read by every column block of the group, is kept
+    // over the output stream (scripts/gpu_policy_sweep.sh, config 4: S5 GEMM
+    // 4.75 -> 4.73 ms; any evict_first side is slower, up to +0.56 ms).
+    // The one-CTA kernel applies evict_last to both sides for any non-zero value.
     static const int evict_last = [] {
       const char* e = getenv("SA_K2T_EVICT_LAST");
-      return e ? atoi(e) : 0;
+      return e ? atoi(e) : 1;
     }();
     batch.evict_last = evict_last;
     batch.debug = debug;

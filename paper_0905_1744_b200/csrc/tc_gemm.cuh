@@ -110,6 +110,23 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// Batch::evict_last bits -> the policy of one operand side (A: shift 0, B: shift 1):
+// bit 0/1 evict_last, bit 2/3 evict_first, else evict_normal
+__device__ __forceinline__ uint64_t side_policy(int bits, int shift) {
+  if (bits & (1 << shift)) return policy_evict_last();
+  if (bits & (4 << shift)) return policy_evict_first();
+  return policy_evict_normal();
+}
 __device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t cols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_addr(slot)), "r"(cols));
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -215,7 +232,7 @@ struct Batch {
   Problem p[MAXPROB];
   int n;
   int group;        // GROUP: row blocks per group of the tile order (below)
-  int evict_last;   // operand loads with an L2 evict-last policy
+  int evict_last;   // operand L2 policies (side_policy bits; 0: no hint)
   int debug;        // experiments only (SA_K2T_DEBUG): 1 no MMA, 2 no TMA loads, 4 no epilogue work
 };
 struct alignas(64) Maps {
@@ -656,7 +673,7 @@ gemm2_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps m
       const uint32_t full0_leader = map_to_rank(s_addr(&full[0]), 0);   // the leader's full barriers
       const bool no_tma = (batch.debug & 2) != 0;
       const bool hint = batch.evict_last != 0;
-      const uint64_t pol = policy_evict_last();
+      const uint64_t pol_a = side_policy(batch.evict_last, 0), pol_b = side_policy(batch.evict_last, 1);
       uint32_t g = 0;
       for (int64_t tile = pair; tile < total_tiles; tile += npairs) {
         const Tile T = decode<BN, TBM2>(batch, tile);
@@ -676,8 +693,8 @@ gemm2_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps m
               const uint32_t dst = base_s + slot * STAGE_BYTES;
               const uint32_t fb = full0_leader + slot * 8u;
               if (hint) {
-                tma_2d_pair_hint(dst, ma, kb * BK, arow, fb, pol);
-                tma_2d_pair_hint(dst + A_BYTES, mb, kb * BK, brow, fb, pol);
+                tma_2d_pair_hint(dst, ma, kb * BK, arow, fb, pol_a);
+                tma_2d_pair_hint(dst + A_BYTES, mb, kb * BK, brow, fb, pol_b);
               } else {
                 tma_2d_pair(dst, ma, kb * BK, arow, fb);
                 tma_2d_pair(dst + A_BYTES, mb, kb * BK, brow, fb);
