@@ -402,10 +402,17 @@ def main():
                 copied[key].record(copy_st)
 
         def d2h_tail(o, last: bool):
+            # on a copy stream too: a device-to-host copy on the step's stream
+            # would hold the next step's kernels behind the copy engine's queue
             nb = 0
-            for k, t in (("bucket_of", o.part.bucket_of), ("gid", o.recv_global_idx)):
-                pinned(k, t).copy_(t, non_blocking=True)
-                nb += t.numel() * t.element_size()
+            ev = torch.cuda.Event()
+            ev.record(st)
+            copy_sts[0].wait_event(ev)
+            with torch.cuda.stream(copy_sts[0]):
+                for k, t in (("bucket_of", o.part.bucket_of), ("gid", o.recv_global_idx)):
+                    t.record_stream(copy_sts[0])   # not reused by the allocator before the copy ran
+                    pinned(k, t).copy_(t, non_blocking=True)
+                    nb += t.numel() * t.element_size()
             for num in o.numerators:
                 if num is not None:
                     nb += num.shape[0] * (num.shape[0] + 1) // 2 * 2

@@ -258,7 +258,9 @@ sa_status sa_ctx_create(int cuda_device, sa_ctx** out) {
   sa_ctx* c = new sa_ctx();
   c->device = cuda_device;
   if (cudaMalloc(&c->dcount, SA_DCOUNT_WORDS * 4) != cudaSuccess ||
-      cudaHostAlloc(&c->hpinned, SA_DCOUNT_WORDS * 4, cudaHostAllocDefault) != cudaSuccess) {
+      cudaHostAlloc(&c->hpinned, SA_DCOUNT_WORDS * 4, cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc(&c->hstage, SA_STAGE_BYTES, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+      cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->dstage), c->hstage, 0) != cudaSuccess) {
     cudaGetLastError();
     delete c;
     return fail(SA_E_NOMEM, "context allocation failed");
@@ -296,6 +298,7 @@ sa_status sa_ctx_destroy(sa_ctx* ctx) {
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
   if (ctx->dcount) cudaFree(ctx->dcount);
   if (ctx->hpinned) cudaFreeHost(ctx->hpinned);
+  if (ctx->hstage) cudaFreeHost(ctx->hstage);
   delete ctx;
   return SA_OK;
 }
@@ -494,10 +497,32 @@ static sa_status resolve_segments(sa_ctx* c, const sa_key128* keys_d, int32_t* o
   return SA_OK;
 }
 
-static sa_status read_u32(const uint32_t* d, uint32_t* h, cudaStream_t st) {
-  SA_CUDA(cudaMemcpyAsync(h, d, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+// Small device -> host readback on the hot path: one kernel copies the bytes
+// into the context's mapped pinned staging buffer (stores over PCIe, no copy
+// engine), then the stream is synchronised.  A cudaMemcpyAsync would queue on
+// the device-to-host copy engine behind whatever large copies the caller has
+// in flight on other streams (measured: a 4-byte read waits 23 ms behind
+// 1.25 GB of result copies, tools/dma_probe.py).
+__global__ void stage_copy_kernel(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, int64_t bytes) {
+  for (int64_t i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+}
+
+static sa_status d2h_small(sa_ctx* c, void* h, const void* d, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return SA_OK;
+  if (bytes > (size_t)SA_STAGE_BYTES) {
+    SA_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, st));
+    SA_CUDA(cudaStreamSynchronize(st));
+    return SA_OK;
+  }
+  stage_copy_kernel<<<1, 256, 0, st>>>(c->dstage, static_cast<const uint8_t*>(d), (int64_t)bytes);
+  SA_LAUNCHED();
   SA_CUDA(cudaStreamSynchronize(st));
+  std::memcpy(h, c->hstage, bytes);
   return SA_OK;
+}
+
+static sa_status read_u32(sa_ctx* c, const uint32_t* d, uint32_t* h, cudaStream_t st) {
+  return d2h_small(c, h, d, sizeof(uint32_t), st);
 }
 
 struct PartArgs {
@@ -581,7 +606,7 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
                            amb_cnt + 0, st));
   if (exact) {
     uint32_t h = 0;
-    SA_TRY(read_u32(amb_cnt + 0, &h, st));
+    SA_TRY(read_u32(c, amb_cnt + 0, &h, st));
     if (h)
       SA_TRY(resolve_segments(c, lkey, lorder, n, a.N, a.p, q0, a.first, pb, wmax, a.prof, a.nk, a.stride, true,
                               nullptr, nullptr, 0, resolved, st));
@@ -625,7 +650,7 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
                            amb_cnt + 1, st));
   if (exact) {
     uint32_t h = 0;
-    SA_TRY(read_u32(amb_cnt + 1, &h, st));
+    SA_TRY(read_u32(c, amb_cnt + 1, &h, st));
     if (h)
       SA_TRY(resolve_segments(c, gkey, gorder, n, a.N, a.p, q0, a.first, pb, s_all, a.prof, a.nk, a.stride, false,
                               s_prof, s_nk, s_all, resolved, st));
@@ -688,7 +713,7 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
                          amb_cnt + 3, counts_d, counts_d + a.p, st));
     if (exact) {
       uint32_t h = 0;
-      SA_TRY(read_u32(amb_cnt + 3, &h, st));
+      SA_TRY(read_u32(c, amb_cnt + 3, &h, st));
       if (h) {
         // re-decide every item whose comparison with a pivot is uncertified
         std::vector<sa_pivot> piv(a.p - 1);
@@ -762,8 +787,7 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
   SA_CUDA(cudaMemcpyAsync(xrec + 2 * a.p, amb_cnt, 4 * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
   SA_TRY(comm_allgather(c, xrec, xall, (int64_t)recw * 8, st));
   std::vector<int64_t> xh((size_t)recw * G);
-  SA_CUDA(cudaMemcpyAsync(xh.data(), xall, xh.size() * 8, cudaMemcpyDeviceToHost, st));
-  SA_CUDA(cudaStreamSynchronize(st));
+  SA_TRY(d2h_small(c, xh.data(), xall, xh.size() * 8, st));
   int64_t amb_total = 0;
   for (int g = 0; g < G; ++g) {
     uint32_t cnt4[4];
@@ -850,9 +874,8 @@ sa_status sa_kmer_profiles(sa_ctx* ctx, const uint8_t* residues, const int64_t* 
   SA_ALLOC(err, uint32_t, 1);
   SA_CUDA(cudaMemsetAsync(err, 0, 4, st));
   SA_TRY(profiles_launch(residues, offsets, n, k, alphabet, profile_stride((int32_t)bins), profiles, nkmers, err, st));
-  SA_CUDA(cudaMemcpyAsync(ctx->hpinned, err, 4, cudaMemcpyDeviceToHost, st));
-  SA_CUDA(cudaStreamSynchronize(st));
-  const uint32_t h = *ctx->hpinned;
+  uint32_t h = 0;
+  SA_TRY(d2h_small(ctx, &h, err, 4, st));
   if (h & ERR_RESIDUE) return fail(SA_E_RANGE, "residue outside the alphabet (code >= %d)", alphabet);
   if (h & ERR_NK) return fail(SA_E_RANGE, "a sequence has more than 65535 k-mers (uint16 counts)");
   return SA_OK;

@@ -138,6 +138,7 @@ bool tc_last_fp4();       // the format of the last K2T launch
 // sim[i][j] = num[i][j] / min(nkA[i], nkB[j]) (fp64, IEEE RN; 0 when the min is 0), row stride ld.
 sa_status ratio_launch(const uint16_t* num, const int32_t* nkA, const int32_t* nkB, int64_t na, int64_t nb,
                        int64_t ld, double* sim, cudaStream_t st, const uint32_t* state = nullptr);
+constexpr int SA_STAGE_BYTES = 1 << 16;   // ctx->hstage: mapped pinned staging for d2h_small
 constexpr int SA_DCOUNT_WORDS = 256;   // ctx->dcount: [0..3] guard words, [16..80) K2T column counts
 constexpr int SA_TC_COLS_AT = 16;
 constexpr int SA_TC_COLS_MAX = 64;
@@ -210,4 +211,9 @@ struct sa_ctx {
   double delta = 0.02;
   uint32_t* dcount = nullptr;   // device: largest count of the last auto-dispatched call
   uint32_t* hpinned = nullptr;  // pinned host word for small readbacks
+  // mapped pinned staging for the hot path's small readbacks (d2h_small): a
+  // kernel stores into it over PCIe, so the read never queues on the copy
+  // engine behind a caller's large device-to-host copies
+  uint8_t* hstage = nullptr;
+  uint8_t* dstage = nullptr;
 };
