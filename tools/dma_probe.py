@@ -1,3 +1,8 @@
+"""Does a small device->host copy on one stream wait behind large
+device->host copies queued on another stream?  (It does: the copy engine
+serves them in submission order.)  Prints the host-observed latency of a
+64-byte read behind 8 x 156 MB of queued copies, and of a kernel on the same
+stream for comparison (the first trial includes warm-up)."""
 import time, torch
 CH = 156 << 20
 dev = [torch.empty(CH, dtype=torch.uint8, device="cuda") for _ in range(8)]
