@@ -86,14 +86,19 @@ struct TcOut {
 // ([c >= 2], [c >= 3]: 2 x 256 words, 2 KB, coalesced); the build then reads
 // the listed layer-2 / layer-3 columns from them instead of gathering counts
 // from the 16 KB profile row (one 32-byte DRAM sector per gathered count).
+// After them, 8 summary words: bit j of word w is set when one of bins
+// [1024 w + 32 j, + 32) reaches count 4, so the build skips the profile read
+// of a listed layer >= 4 column whose 32-bin word has no count >= 4 (most).
 // Rows [0, split) of a launch with a carried side use the carry's masks.
 constexpr int TC_MW = TC_WPL;   // mask words per layer
+constexpr int TC_MDEEP = 2 * TC_MW;        // offset of the count >= 4 summary words
+constexpr int TC_MROW = 2 * TC_MW + 8;     // words per row
 struct TcMasks {
-  uint32_t* own;                // rows [split, R): row g at own + (g - split) * 2 * TC_MW
+  uint32_t* own;                // rows [split, R): row g at own + (g - split) * TC_MROW
   const uint32_t* carried;      // rows [0, split)
   int64_t split;
   __device__ __forceinline__ const uint32_t* row(int64_t g) const {
-    return g < split ? carried + g * 2 * TC_MW : own + (g - split) * 2 * TC_MW;
+    return g < split ? carried + g * TC_MROW : own + (g - split) * TC_MROW;
   }
 };
 
@@ -179,6 +184,9 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
       side = t;
     }
     const int cnt = (int)min((int64_t)TC_HIST_ROWS, min(r1, S.row_begin[t + 1]) - g);
+    bool deep4[TC_HIST_ROWS];
+#pragma unroll
+    for (int h = 0; h < TC_HIST_ROWS; ++h) deep4[h] = false;
     if (active) {
       uint4 raw[TC_HIST_ROWS][4];
       const uint16_t* base = S.rows[t] + (g - S.row_begin[t]) * (int64_t)stride16 + w * 32;
@@ -202,6 +210,7 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
         for (int i = 1; i < 16; ++i) vm = __vmaxu2(vm, v[i]);
         const uint32_t vmax = max(vm & 0xffffu, vm >> 16);
         mx = max(mx, vmax);
+        deep4[h] = vmax >= 4u;
         const bool in_cols = w * 32 < dw;
         uint8_t* orow = O.out[t] + (g - S.row_begin[t] + h) * ROWB + (FP4 ? w * 16 : w * 32);
         uint32_t m23[2] = {0u, 0u};   // [c >= 2], [c >= 3] of the thread's 32 bins
@@ -215,7 +224,7 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
           s1[l] |= m;
         }
         if (h < cnt) {
-          uint32_t* mr = mk.own + (g + h - hist_from) * 2 * TC_MW;
+          uint32_t* mr = mk.own + (g + h - hist_from) * TC_MROW;
           mr[w] = m23[0];
           mr[TC_MW + w] = m23[1];
         }
@@ -228,6 +237,12 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
           deepest = max(deepest, l - TC_HREG + 1);
         }
       }
+    }
+    // the row's count >= 4 summary: one word per warp (all lanes take part)
+#pragma unroll
+    for (int h = 0; h < TC_HIST_ROWS; ++h) {
+      const uint32_t b4 = __ballot_sync(0xffffffffu, deep4[h]);
+      if ((w & 31) == 0 && h < cnt) mk.own[(g + h - hist_from) * TC_MROW + TC_MDEEP + (w >> 5)] = b4;
     }
     g += cnt;
   }
@@ -490,6 +505,8 @@ tc_build_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut
           uint32_t bit;
           if (layer == 2u || layer == 3u)   // from the row's layer mask
             bit = (__ldg(mrow + (layer - 2u) * TC_MW + (bin >> 5)) >> (bin & 31u)) & 1u;
+          else if (layer >= 4u && !((__ldg(mrow + TC_MDEEP + (bin >> 10)) >> ((bin >> 5) & 31u)) & 1u))
+            bit = 0u;                       // no count >= 4 in the bin's 32-bin word
           else
             bit = (layer != 0u && (uint32_t)__ldg(row + bin) >= layer) ? 1u : 0u;
           word |= FP4 ? (bit << (4 * b + 1)) : (bit << (8 * b));
@@ -1225,7 +1242,7 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     TcMasks mk{};
     mk.split = hfrom;
     mk.carried = carried ? use->masks : nullptr;
-    mk.own = (kept ? keep->scratch : &scratch)->alloc<uint32_t>((size_t)(R - hfrom) * 2 * TC_MW);
+    mk.own = (kept ? keep->scratch : &scratch)->alloc<uint32_t>((size_t)(R - hfrom) * TC_MROW);
     if (!mk.own) return fail(SA_E_NOMEM, "scratch allocation of K2T layer masks failed");
     const int hx = (int)std::max<int64_t>(
         1, std::min<int64_t>((R - hfrom + TC_HIST_ROWS - 1) / TC_HIST_ROWS, 4 * g_num_sms));
