@@ -63,6 +63,62 @@ profiles_kernel(const uint8_t* __restrict__ res, const int64_t* __restrict__ off
   }
 }
 
+// The same with the row copy-out as an asynchronous bulk copy (TMA engine,
+// cp.async.bulk shared -> global) from one of two shared-memory histograms:
+// the CTA counts row s + grid into the other buffer while row s streams out.
+// Before a buffer is zeroed and reused, the bulk store issued from it two
+// rows earlier must have finished reading it (wait_group.read 1).
+__global__ void __launch_bounds__(256)
+profiles_bulk_kernel(const uint8_t* __restrict__ res, const int64_t* __restrict__ offs, int32_t n, int32_t k,
+                     int32_t alphabet, int32_t stride, uint16_t* __restrict__ out, int32_t* __restrict__ nk_out,
+                     uint32_t* __restrict__ err) {
+  extern __shared__ __align__(128) uint32_t hist2[];   // 2 x stride / 2 words
+  const int words = stride >> 1;
+  const int vec = words >> 2;
+  const uint32_t row_bytes = (uint32_t)stride * 2u;
+  int buf = 0;
+  for (int64_t s = blockIdx.x; s < n; s += gridDim.x, buf ^= 1) {
+    uint32_t* hist = hist2 + buf * words;
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncthreads();
+    uint4* h4 = reinterpret_cast<uint4*>(hist);
+    for (int v = threadIdx.x; v < vec; v += blockDim.x) h4[v] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    const int64_t b = offs[s], e = offs[s + 1];
+    const int64_t len = e - b;
+    const int64_t nk = len >= k ? len - k + 1 : 0;
+    const uint8_t* x = res + b;
+    uint32_t bad = 0;
+    for (int64_t u = threadIdx.x; u < len; u += blockDim.x)
+      if (x[u] >= alphabet) bad = 1;
+    for (int64_t u = threadIdx.x; u < nk; u += blockDim.x) {
+      uint32_t id = 0;
+      bool ok = true;
+      for (int t = 0; t < k; ++t) {
+        const uint32_t r = x[u + t];
+        ok &= r < (uint32_t)alphabet;
+        id = id * (uint32_t)alphabet + r;
+      }
+      if (ok) atomicAdd(&hist[id >> 1], 1u << ((id & 1u) << 4));
+    }
+    if (bad) atomicOr(err, ERR_RESIDUE);
+    if (threadIdx.x == 0) {
+      if (nk > 65535) atomicOr(err, ERR_NK);
+      nk_out[s] = (int32_t)nk;
+    }
+    // the histogram's generic-proxy writes before the async-proxy read
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t src = (uint32_t)__cvta_generic_to_shared(hist);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+                   "cp.async.bulk.commit_group;"
+                   :: "l"(out + s * (int64_t)stride), "r"(src), "r"(row_bytes) : "memory");
+    }
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 sa_status profiles_launch(const uint8_t* residues, const int64_t* offsets, int32_t n, int32_t k,
                           int32_t alphabet, int32_t stride, uint16_t* out, int32_t* nk, uint32_t* err_flag,
                           cudaStream_t st) {
@@ -82,6 +138,25 @@ sa_status profiles_launch(const uint8_t* residues, const int64_t* offsets, int32
     const char* e = getenv("SA_PROF_CS");
     return e ? atoi(e) : 1;
   }();
+  static const int bulk = [] {   // SA_PROF_BULK=0: thread stores instead of bulk copies
+    const char* e = getenv("SA_PROF_BULK");
+    return e ? atoi(e) : 1;
+  }();
+  if (bulk && 2 * smem <= 227 * 1024) {   // two row buffers fit (bins <= 58 112)
+    static int configured_bulk = 0;
+    if (2 * smem > 48 * 1024 && 2 * smem > configured_bulk) {
+      SA_CUDA(cudaFuncSetAttribute(profiles_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * smem));
+      configured_bulk = 2 * smem;
+    }
+    int per_sm_b = 0;
+    SA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_b, profiles_bulk_kernel, 256, 2 * smem));
+    if (per_sm_b < 1) per_sm_b = 1;
+    const int64_t gb = (int64_t)sms * per_sm_b;
+    profiles_bulk_kernel<<<(unsigned)(n < gb ? n : gb), 256, 2 * smem, st>>>(residues, offsets, n, k, alphabet, stride,
+                                                                          out, nk, err_flag);
+    SA_LAUNCHED();
+    return SA_OK;
+  }
   const int64_t grid = (int64_t)sms * per_sm;
   profiles_kernel<<<(unsigned)(n < grid ? n : grid), 256, smem, st>>>(residues, offsets, n, k, alphabet, stride, out,
                                                                      nk, err_flag, cs);
