@@ -7,7 +7,9 @@
 // carries into its neighbour: a count is <= nk <= 65535, checked), then the
 // whole row -- including the zero padding up to the 64-bin row stride -- is
 // streamed to HBM with 16-byte vector stores.  The kernel is bound by that
-// 16 KB-per-sequence write (K1).
+// 16 KB-per-sequence write (K1).  profiles_bulk_kernel (the
+// default) hands that write to the TMA engine as one bulk copy per row and
+// counts the next sequence into a second buffer meanwhile.
 #include "common.cuh"
 
 namespace sa {
