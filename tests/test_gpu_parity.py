@@ -57,8 +57,10 @@ def test_profiles_configs(ctx, c):
     assert np.array_equal(nk.cpu().numpy(), nko)
 
 
-@pytest.mark.parametrize("alphabet,k", [(20, 3), (4, 3), (2, 5), (20, 1), (3, 2)])
+@pytest.mark.parametrize("alphabet,k", [(20, 3), (4, 3), (2, 5), (20, 1), (3, 2), (4, 8)])
 def test_profiles_small_alphabets_ragged(ctx, alphabet, k):
+    """(4, 8): 65 536 bins, too many for two shared-memory rows -- the
+    thread-store profiles_kernel runs instead of the bulk-copy one."""
     ds = _rand_set(alphabet * 10 + k, 77, 0, 60, alphabet)
     res, offs = to_dev(ds)
     P, nk = B.sa_kmer_profiles(ctx, res, offs, k=k, alphabet=alphabet)
