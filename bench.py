@@ -13,13 +13,15 @@ value   = k-mer similarity sequence-pairs evaluated per second by the whole job
           (S2a + S2d + S5 pairs, SURVEY §8(d) accounting) / max-over-ranks time
           of K device-timed steps, inputs resident in HBM;
 e2e     = the same through the public API with the step's inputs copied from
-          pinned host memory and its results (buckets, member ids, uint16
-          numerator matrices) copied back inside the timed region (consecutive
+          pinned host memory and its results (buckets, member ids, every
+          bucket's uint16 numerator and fp64 similarity matrices as packed
+          upper triangles) copied back inside the timed region (consecutive
           steps pipelined: step t+1 computes while step t's results copy);
-roofline= the dominant kernel over the S5 launches: K2T (tensor-core threshold
-          layers, default) in TOP/s against the u8 tensor peak (DESIGN.md
-          §4b), or K2 (SAD / u16 fallback) in bin-ops/s against the derived
-          integer-pipe peak (DESIGN.md §4);
+          e2e.numerators_only = the same without the fp64 matrices;
+roofline= the dominant kernel (the S5 GEMM): the method's work (2 x 8000 ops
+          per pair, Eq. 1) against the e2m1 tensor peak, and its algorithmic
+          HBM bytes (full C + F output, operand rows once) against the copy
+          bandwidth; `bound` is the binding one (DESIGN.md §7);
 cpu_baseline = the CPU oracle (oracle/, as it stands) on a bounded sample of
           the same workload, on the host's cores (rank 0, N = 1 only).
 """
@@ -241,6 +243,7 @@ def main():
     for _ in range(args.warmup):
         out = hp.step(res_d, offs_d, ds.n, first)
     torch.cuda.synchronize()
+    ctx.set_timing(True)   # clears the phase history: it now holds the timed steps only
 
     # ------------------------------------------------ device-timed steps
     per_step = []
@@ -253,16 +256,20 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     for _ in range(args.steps):
+        # no host synchronisation inside the timed region: libsa only records
+        # its phase events; they are read after the region (phase_history)
         ev = {k: torch.cuda.Event(enable_timing=True) for k in names}
         out = hp.step(res_d, offs_d, ds.n, first, events=ev)
-        ph = ctx.phase_ms()
-        per_step.append((ev, ph))
+        per_step.append(ev)
     e1.record(st)
     torch.cuda.synchronize()
     launches = B.sa_launch_count() - launches0
     barrier()
     clk = clocks.stop()
     total_ms = max_over_ranks(e0.elapsed_time(e1))
+    hist = {k: ctx.phase_history(k)[-args.steps:] for k in B.PHASES}
+    per_step = [(ev, {k: (hist[k][i] if i < len(hist[k]) else 0.0) for k in B.PHASES})
+                for i, ev in enumerate(per_step[-len(hist["S2a"]):] if hist["S2a"] else per_step)]
 
     # pair accounting; bucket sizes are known on every rank
     bounds = [q * ds.n // cfg.p for q in range(cfg.p + 1)]
@@ -286,7 +293,9 @@ def main():
         "partition_S2a_to_S4": part_ms,
         "S1_received": med(lambda ev, ph: ev["S4"].elapsed_time(ev["S1b"])),
         "S5": s5_ms,
-        "S5_gemm": med(lambda ev, ph: ph["gemm"]),
+        "S5_gemm": med(lambda ev, ph: ph["gemm_S5"]),
+        "S2a_gemm": med(lambda ev, ph: ph["gemm_S2a"]),
+        "S2d_gemm": med(lambda ev, ph: ph["gemm_S2d"]),
     }
     part_ms_max = max_over_ranks(part_ms)
     s5_ms_max = max_over_ranks(s5_ms)
@@ -300,49 +309,66 @@ def main():
     my_s5_pairs = sum(int(sizes[b]) * (int(sizes[b]) - 1) // 2 for b in own)
     traffic = None
     if engine == "tc":
-        # K2T: the S5 buckets as exact 0/1 threshold-layer
-        # contractions on the tensor cores; algorithmic work = 2 K'_b ops per
-        # pair (K'_b = kept layer columns of bucket b, read back after the timed
-        # region by re-running each bucket once) against the tensor peak of the
-        # operand format, over the GEMM kernel's own CUDA-event time (median
-        # over the timed steps, SA_PHASE_GEMM); the whole S5 phase (operand
-        # build + GEMM) is reported beside it.
+        # K2T: the S5 buckets as exact 0/1 contractions on the
+        # tensor cores.  The roofline counts the METHOD's work, not the
+        # implementation's contraction: Eq. 1 is EPS_BINS = 8000 min-accumulate
+        # bin-ops per pair, each one e2m1 multiply-add (2 ops) -- so
+        # 2 * 8000 * pairs ops -- against the e2m1 tensor peak; the kernel must
+        # also write the full symmetric C (uint16) and F (fp64) of every bucket
+        # and read each bucket's operand rows once: that HBM floor is the other
+        # roofline.  `bound` is whichever floor is larger (the binding one);
+        # both fractions are reported, and the implementation's own contraction
+        # length K' (kept threshold-layer columns) as a secondary figure.
         nz = [(b, row, n_b) for b, row, n_b in out.buckets if n_b > 0]
         rb_s5 = [r for _, r, _ in out.buckets] + [sum(n for _, _, n in out.buckets)]
         B.sa_bucket_similarity_batch(ctx, out.bucket_profiles, out.bucket_nkmers, rb_s5, hp.bins,
                                      numerators=out.numerators, similarity=out.similarity)
         kcols = dict(zip([b for b, _, _ in nz], ctx.tc_columns()))
         operand = ctx.tc_operand()
-        ops = sum(2.0 * kcols[b] * int(sizes[b]) * (int(sizes[b]) - 1) / 2 for b in kcols)
+        gemm_ms = phases["S5_gemm"]
         bf16 = float(peaks.get("bf16_tflops", 1590.0))
         ratio = 4.0 if operand == "e2m1" else 2.0   # nominal dense 9 (fp4) / 4.5 (int8) vs 2.25 (bf16) PF
-        peak = ratio * bf16 * 1e12
-        gemm_ms = phases["S5_gemm"]
-        achieved = ops / (gemm_ms / 1e3)
+        peak_t = ratio * bf16 * 1e12
+        ops_method = 2.0 * EPS_BINS * my_s5_pairs
+        ops_kprime = sum(2.0 * kcols[b] * int(sizes[b]) * (int(sizes[b]) - 1) / 2 for b in kcols)
+        hbm = float(peaks.get("hbm_gbs", 6551.0)) * 1e9
+        out_bytes = sum(int(sizes[b]) ** 2 * ((2 if hp.want_num else 0) + (8 if hp.want_sim else 0)) for b in own)
+        opnd_bytes = sum(int(sizes[b]) * (EPS_BINS // 2 if operand == "e2m1" else EPS_BINS) for b in own)
+        bytes_alg = out_bytes + opnd_bytes
+        t_tensor = ops_method / peak_t
+        t_hbm = bytes_alg / hbm
         tpath = os.path.join(ROOT, "profiles", "k2t_traffic.json")
+        ncu_note = None
         if os.path.exists(tpath):
             with open(tpath) as f:
                 tj = json.load(f)
             if tj.get("operand", "u8") == operand:
                 traffic = tj.get("dram_bytes_per_launch")
+                ncu_note = {k: tj[k] for k in ("tensor_active_pct", "source", "round") if k in tj}
         cta_pairs = os.environ.get("SA_K2T_PAIR", "1") != "0"
-        roof = {"bound": "tensor",
-                "kernel": (f"tc::{'gemm2_kernel' if cta_pairs else 'gemm_kernel'}<KeyMatEpi<NUM|SIM>> (K2T, "
-                           f"{'tcgen05 cta_group::2 CTA pairs' if cta_pairs else 'one CTA per tile'}, {operand} operands, "
-                           f"S5 bucket matrices, one launch per step)"),
-                "engine": engine, "operand": operand,
-                "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TOP/s",
-                "frac": achieved / peak, "traffic": traffic,
-                "kernel_ms": gemm_ms,
-                "peak_source": (f"{peak_src} bf16_tflops {bf16:.1f} (burst, MEASURED_PEAKS.json) x {ratio:.0f} = "
-                                f"{'e2m1 (kind::mxf4)' if operand == 'e2m1' else 'u8 (kind::i8)'} dense "
-                                f"(nominal {'9' if operand == 'e2m1' else '4.5'} / 2.25 PF ratio)"),
-                "algorithmic": (f"2 K'_b ops per pair, K'_b = kept threshold-layer columns "
-                                f"{[kcols[b] for b in sorted(kcols)]} x {my_s5_pairs} pairs / the GEMM kernel's "
-                                f"CUDA-event time"),
-                "phase_achieved": ops / (s5_ms / 1e3) / 1e12,
-                "phase_frac": ops / (s5_ms / 1e3) / peak,
-                "binops_per_s_equiv": my_s5_pairs * EPS_BINS / (gemm_ms / 1e3) / 1e12}
+        kernel = (f"tc::{'gemm2_kernel' if cta_pairs else 'gemm_kernel'}<KeyMatEpi<NUM|SIM>> (K2T, "
+                  f"{'tcgen05 cta_group::2 CTA pairs' if cta_pairs else 'one CTA per tile'}, {operand} operands, "
+                  f"S5 bucket matrices, one launch per step)")
+        common = {"kernel": kernel, "engine": engine, "operand": operand, "kernel_ms": gemm_ms, "traffic": traffic,
+                  "frac_tensor_method": t_tensor * 1e3 / gemm_ms, "frac_hbm": t_hbm * 1e3 / gemm_ms,
+                  "frac_tensor_kprime": ops_kprime / peak_t * 1e3 / gemm_ms,
+                  "kprime": [kcols[b] for b in sorted(kcols)],
+                  "tensor_peak_source": (f"{peak_src} bf16_tflops {bf16:.1f} (burst, MEASURED_PEAKS.json) x "
+                                         f"{ratio:.0f} = {'e2m1 (kind::mxf4)' if operand == 'e2m1' else 'u8 (kind::i8)'}"
+                                         f" dense (nominal {'9' if operand == 'e2m1' else '4.5'} / 2.25 PF ratio)"),
+                  "hbm_peak_source": f"{peak_src} hbm_gbs {hbm / 1e9:.1f} (MEASURED_PEAKS.json copy bandwidth)",
+                  "algorithmic": (f"tensor: 2 x {EPS_BINS} ops per pair (Eq. 1 bins) x {my_s5_pairs} pairs; "
+                                  f"hbm: full symmetric C (2 B) + F (8 B) per ordered pair "
+                                  f"({out_bytes / 1e9:.3f} GB) + each bucket's e2m1 layer-1 operand rows once "
+                                  f"({opnd_bytes / 1e9:.3f} GB); over the GEMM kernel's CUDA-event time "
+                                  f"(median of the timed steps)"),
+                  "phase_frac_tensor_method": t_tensor * 1e3 / s5_ms, "ncu": ncu_note}
+        if t_hbm >= t_tensor:
+            roof = {"bound": "hbm", "achieved": bytes_alg / (gemm_ms / 1e3) / 1e9, "peak": hbm / 1e9,
+                    "unit": "GB/s", "frac": t_hbm * 1e3 / gemm_ms, **common}
+        else:
+            roof = {"bound": "tensor", "achieved": ops_method / (gemm_ms / 1e3) / 1e12, "peak": peak_t / 1e12,
+                    "unit": "TOP/s", "frac": t_tensor * 1e3 / gemm_ms, **common}
     else:
         per_clk = BINOPS_PER_SM_CLK[engine]
         peak_binops = per_clk * nsm * sm_mhz_peak * 1e6
@@ -362,14 +388,19 @@ def main():
                 "algorithmic": f"{EPS_BINS} bin-ops per pair x {my_s5_pairs} pairs / S5 CUDA-event time"}
 
     # --------------------------------------------- end-to-end (host buffers)
-    e2e = None
-    if not args.no_e2e:
+    def run_e2e(with_sim: bool):
+        """K steps through the public API with host buffers: each step's
+        residues are copied from pinned host memory, and its results -- bucket
+        ids, received member ids, every owned bucket's numerator matrix and
+        (with_sim) its fp64 similarity matrix, each as its packed upper
+        triangle (the whole symmetric content) -- are copied back to pinned
+        host memory inside the timed region."""
         h_out = {}
         # two copy streams, alternating by bucket: two copy engines share the PCIe link
         copy_sts = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
 
         def pinned(k, t):
-            if k not in h_out or h_out[k].shape != t.shape:
+            if k not in h_out or h_out[k].shape != t.shape or h_out[k].dtype != t.dtype:
                 h_out[k] = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
             return h_out[k]
 
@@ -379,27 +410,30 @@ def main():
         d_packed, copied = {}, {}
         parity = [0]
 
-        def on_bucket(b, num, sim):
-            # bucket b's numerator matrix, packed to its upper triangle (the
-            # whole symmetric content, sa_pack_upper_u16), goes to the host on
-            # a copy stream while the next bucket computes
-            if num is None:
-                return
-            n_b = num.shape[0]
-            key = (parity[0], b)
+        def ship(kind, b, mat, pack_fn, dtype):
+            n_b = mat.shape[0]
+            key = (parity[0], kind, b)
             if key not in d_packed or d_packed[key].numel() != n_b * (n_b + 1) // 2:
-                d_packed[key] = torch.empty(n_b * (n_b + 1) // 2, dtype=torch.uint16, device=dev)
+                d_packed[key] = torch.empty(n_b * (n_b + 1) // 2, dtype=dtype, device=dev)
             if key in copied:
                 st.wait_event(copied[key])
-            pk = B.sa_pack_upper_u16(ctx, num, d_packed[key], stream=st)
+            pk = pack_fn(ctx, mat, d_packed[key], stream=st)
             ev = torch.cuda.Event()
             ev.record(st)
             copy_st = copy_sts[b % 2]
             copy_st.wait_event(ev)
             with torch.cuda.stream(copy_st):
-                pinned(f"num{b}", pk.view(torch.int16)).copy_(pk.view(torch.int16), non_blocking=True)
+                src = pk.view(torch.int16) if dtype == torch.uint16 else pk
+                pinned(f"{kind}{b}", src).copy_(src, non_blocking=True)
                 copied[key] = torch.cuda.Event()
                 copied[key].record(copy_st)
+
+        def on_bucket(b, num, sim):
+            # bucket b's matrices go to the host on a copy stream while the next bucket computes
+            if num is not None:
+                ship("num", b, num, B.sa_pack_upper_u16, torch.uint16)
+            if with_sim and sim is not None:
+                ship("sim", b, sim, B.sa_pack_upper_f64, torch.float64)
 
         def d2h_tail(o, last: bool):
             # on a copy stream too: a device-to-host copy on the step's stream
@@ -413,9 +447,11 @@ def main():
                     t.record_stream(copy_sts[0])   # not reused by the allocator before the copy ran
                     pinned(k, t).copy_(t, non_blocking=True)
                     nb += t.numel() * t.element_size()
-            for num in o.numerators:
+            for num, sim in zip(o.numerators, o.similarity):
                 if num is not None:
                     nb += num.shape[0] * (num.shape[0] + 1) // 2 * 2
+                if with_sim and sim is not None:
+                    nb += sim.shape[0] * (sim.shape[0] + 1) // 2 * 8
             parity[0] ^= 1
             if last:
                 for cs in copy_sts:
@@ -441,15 +477,24 @@ def main():
         f1.record(st)
         torch.cuda.synchronize()
         e2e_ms = max_over_ranks(f0.elapsed_time(f1))
-        e2e = {"value": pairs * args.steps / (e2e_ms / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(res_h.numel() + offs_h.numel() * 8),
-               "d2h_bytes_per_step": int(d2h_bytes), "ms_per_step": e2e_ms / args.steps,
-               "results_copied": ("bucket_of, received member ids, and every owned bucket's symmetric uint16 "
-                                  "numerator matrix as its packed upper triangle (sa_pack_upper_u16)"),
-               "overlap": "steps pipelined: step t+1 computes while step t's triangles copy (double-buffered)"}
+        del d_packed, h_out
+        what = ("bucket_of, received member ids, and every owned bucket's symmetric uint16 numerator matrix "
+                + ("and fp64 similarity matrix, each " if with_sim else "") +
+                "as its packed upper triangle (sa_pack_upper_u16" + (" / _f64)" if with_sim else ")"))
+        return {"value": pairs * args.steps / (e2e_ms / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": int(res_h.numel() + offs_h.numel() * 8),
+                "d2h_bytes_per_step": int(d2h_bytes), "ms_per_step": e2e_ms / args.steps,
+                "results_copied": what,
+                "overlap": "steps pipelined: step t+1 computes while step t's triangles copy (double-buffered)"}
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(with_sim=hp.want_sim)
+        if hp.want_sim:
+            e2e["numerators_only"] = run_e2e(with_sim=False)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         from oracle import kmer
         workers = kmer.default_workers()
         cp, cs, kb = cpu_oracle_sample(ds, cfg, args.cpu_sample_n, workers)

@@ -14,7 +14,7 @@
  *   S5  all-pairs similarity inside a bucket      sa_bucket_similarity (_batch)
  * and, past the hot path:
  *   N4  the bucket's guide tree (UPGMA)           sa_guide_tree
- *   result transfer: packed symmetric matrices    sa_pack_upper_u16
+ *   result transfer: packed symmetric matrices    sa_pack_upper_u16 / _f64
  *
  * Conventions for every call:
  *   - pointers are DEVICE pointers unless the name ends in _h (host);
@@ -93,9 +93,14 @@ const char* sa_last_error(void);
 /* Number of libsa kernels launched through this process since load. */
 int64_t sa_launch_count(void);
 /* When enabled, libsa records CUDA events around its phases on the call's
- * stream; sa_ctx_phase_ms returns the durations of the last sa_partition /
- * sa_bucket_similarity / sa_kmer_rank calls (host-blocking: syncs on the
- * recorded events).  Phases: see SA_PHASE_*. */
+ * stream (cudaEventRecord only: recording never blocks the host).  The last
+ * SA_PHASE_RING occurrences of every phase are kept, so a caller can run many
+ * steps and read every step's phase times afterwards:
+ *   sa_ctx_phase_ms       durations of the most recent occurrence of each phase;
+ *   sa_ctx_phase_history  durations of the kept occurrences of one phase,
+ *                         oldest first.
+ * Both are host-blocking (they synchronise on the recorded events); call them
+ * outside timed regions.  sa_ctx_set_timing clears the history. */
 enum {
   SA_PHASE_S2A = 0,      /* local rank (min-sum engine, all local blocks)      */
   SA_PHASE_S2B = 1,      /* local block sort + sample pick                      */
@@ -104,10 +109,17 @@ enum {
   SA_PHASE_S3 = 4,       /* block sort, regular samples, pivots, bucket assign  */
   SA_PHASE_S5 = 5,       /* last sa_bucket_similarity min-sum launch            */
   SA_PHASE_RANK = 6,     /* last sa_kmer_rank min-sum launch                    */
-  SA_PHASE_GEMM = 7,     /* the tensor-core GEMM kernel alone of the last K2T launch */
-  SA_PHASE_COUNT = 8
+  SA_PHASE_GEMM = 7,     /* the tensor-core GEMM kernel alone of the last K2T launch (any call) */
+  SA_PHASE_GEMM_S2A = 8, /* ... of sa_partition's S2a launch                    */
+  SA_PHASE_GEMM_S2D = 9, /* ... of sa_partition's S2d launch                    */
+  SA_PHASE_GEMM_S5 = 10, /* ... of an sa_bucket_similarity(_batch) launch       */
+  SA_PHASE_COUNT = 11
 };
+enum { SA_PHASE_RING = 64 };
 sa_status sa_ctx_set_timing(sa_ctx* ctx, int enable);
+/* ms_h[i] for i < min(max, kept occurrences); returns how many were written
+ * (0 when the phase never ran, -1 on a CUDA error or bad argument). */
+int32_t sa_ctx_phase_history(sa_ctx* ctx, int32_t phase, float* ms_h, int32_t max);
 /* Operand encoding of the last min-sum launch on this context:
  * 0 = uint16 counts (VIMNMX.U16x2 min + add; any count), 1 = uint8 counts
  * (C = (nk_a + nk_b - sum|a-b|)/2 with VABSDIFF4.U8.ACC; used when every
@@ -301,6 +313,8 @@ sa_status sa_guide_tree(sa_ctx* ctx, const double* similarity, int32_t n, int64_
  * n < 0, ld < n, NULL pointers with n > 0. */
 sa_status sa_pack_upper_u16(sa_ctx* ctx, const uint16_t* matrix, int32_t n, int64_t ld, uint16_t* packed,
                             void* stream);
+/* The same for a symmetric fp64 similarity matrix (S5's F): n(n+1)/2 doubles. */
+sa_status sa_pack_upper_f64(sa_ctx* ctx, const double* matrix, int32_t n, int64_t ld, double* packed, void* stream);
 
 #ifdef __cplusplus
 }

@@ -21,13 +21,15 @@ LIB_PATH = os.path.join(_PKG, "lib", "libsa.so")
 SA_OK, SA_E_INVAL, SA_E_RANGE, SA_E_CUDA, SA_E_COMM, SA_E_NOMEM, SA_E_STATE = range(7)
 STATUS_NAMES = {0: "SA_OK", 1: "SA_E_INVAL", 2: "SA_E_RANGE", 3: "SA_E_CUDA", 4: "SA_E_COMM",
                 5: "SA_E_NOMEM", 6: "SA_E_STATE"}
-PHASES = ["S2a", "S2b", "S2c", "S2d", "S3", "S5", "rank", "gemm"]
+PHASES = ["S2a", "S2b", "S2c", "S2d", "S3", "S5", "rank", "gemm", "gemm_S2a", "gemm_S2d", "gemm_S5"]
+PHASE_RING = 64
 
 EXPORTED = ["sa_ctx_create", "sa_ctx_attach_comm", "sa_ctx_destroy", "sa_last_error", "sa_launch_count",
             "sa_ctx_set_timing", "sa_ctx_phase_ms", "sa_profile_stride", "sa_kmer_profiles", "sa_kmer_rank",
             "sa_partition", "sa_redistribute", "sa_bucket_similarity", "sa_exact_rank_compare", "sa_ctx_engine",
             "sa_ctx_set_rank_form", "sa_ctx_tc_columns", "sa_ctx_tc_operand", "sa_selftest_f_division",
-            "sa_bucket_similarity_batch", "sa_pack_upper_u16", "sa_guide_tree"]
+            "sa_bucket_similarity_batch", "sa_pack_upper_u16", "sa_pack_upper_f64", "sa_guide_tree",
+            "sa_ctx_phase_history"]
 SA_RANK_F, SA_RANK_DF = 0, 1
 
 
@@ -100,6 +102,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                                       ctypes.POINTER(ctypes.c_int64), VP]),
         "sa_exact_rank_compare": (ctypes.c_int, [P, I32, P, I32, P, I32]),
         "sa_pack_upper_u16": (ctypes.c_int, [P, P, I32, ctypes.c_int64, P, VP]),
+        "sa_pack_upper_f64": (ctypes.c_int, [P, P, I32, ctypes.c_int64, P, VP]),
+        "sa_ctx_phase_history": (ctypes.c_int32, [P, ctypes.c_int32, ctypes.POINTER(ctypes.c_float), ctypes.c_int32]),
         "sa_guide_tree": (ctypes.c_int, [P, P, I32, ctypes.c_int64, P, P, VP]),
         "sa_ctx_engine": (ctypes.c_int, [P]),
         "sa_ctx_tc_columns": (ctypes.c_int32, [P, P, ctypes.c_int32]),
@@ -220,6 +224,15 @@ class Context:
         arr = (ctypes.c_float * len(PHASES))()
         _check(load_library().sa_ctx_phase_ms(self.handle, arr))
         return {k: float(arr[i]) for i, k in enumerate(PHASES)}
+
+    def phase_history(self, phase: str) -> list[float]:
+        """Durations (ms) of the kept occurrences of one phase, oldest first
+        (sa_ctx_phase_history; host-blocking -- call outside timed regions)."""
+        arr = (ctypes.c_float * PHASE_RING)()
+        n = int(load_library().sa_ctx_phase_history(self.handle, PHASES.index(phase), arr, PHASE_RING))
+        if n < 0:
+            raise SaError(SA_E_CUDA, "sa_ctx_phase_history failed")
+        return [float(arr[i]) for i in range(n)]
 
 
 # ------------------------------------------------------------- S1 .. S5 ----
@@ -437,20 +450,29 @@ def sa_guide_tree(ctx: Context, similarity: torch.Tensor, stream=None):
     return merges, heights
 
 
-def sa_pack_upper_u16(ctx: Context, matrix: torch.Tensor, packed: torch.Tensor | None = None, stream=None):
-    """Packed upper triangle (diagonal included) of a symmetric n x n uint16
-    matrix (n x n view with any row stride >= n): row i's columns i..n-1 at
-    i*n - i*(i-1)/2; returns the n(n+1)/2 uint16 device tensor (sa.h)."""
-    if matrix.dtype != torch.uint16 or not matrix.is_cuda or matrix.dim() != 2 or matrix.shape[0] != matrix.shape[1]:
-        raise ValueError("matrix must be an n x n uint16 CUDA tensor")
+def _pack_upper(fn: str, dtype, ctx: Context, matrix: torch.Tensor, packed: torch.Tensor | None, stream):
+    if matrix.dtype != dtype or not matrix.is_cuda or matrix.dim() != 2 or matrix.shape[0] != matrix.shape[1]:
+        raise ValueError(f"matrix must be an n x n {dtype} CUDA tensor")
     if matrix.stride(1) != 1:
         raise ValueError("matrix rows must be contiguous")
     n = matrix.shape[0]
     if packed is None:
-        packed = torch.empty(n * (n + 1) // 2, dtype=torch.uint16, device=matrix.device)
-    _check(load_library().sa_pack_upper_u16(ctx.handle, ctypes.c_void_p(matrix.data_ptr()), n, matrix.stride(0),
-                                            _ptr(packed), _stream(stream)))
+        packed = torch.empty(n * (n + 1) // 2, dtype=dtype, device=matrix.device)
+    _check(getattr(load_library(), fn)(ctx.handle, ctypes.c_void_p(matrix.data_ptr()), n, matrix.stride(0),
+                                       _ptr(packed), _stream(stream)))
     return packed
+
+
+def sa_pack_upper_u16(ctx: Context, matrix: torch.Tensor, packed: torch.Tensor | None = None, stream=None):
+    """Packed upper triangle (diagonal included) of a symmetric n x n uint16
+    matrix (n x n view with any row stride >= n): row i's columns i..n-1 at
+    i*n - i*(i-1)/2; returns the n(n+1)/2 uint16 device tensor (sa.h)."""
+    return _pack_upper("sa_pack_upper_u16", torch.uint16, ctx, matrix, packed, stream)
+
+
+def sa_pack_upper_f64(ctx: Context, matrix: torch.Tensor, packed: torch.Tensor | None = None, stream=None):
+    """The same for a symmetric fp64 similarity matrix (sa.h)."""
+    return _pack_upper("sa_pack_upper_f64", torch.float64, ctx, matrix, packed, stream)
 
 
 # ------------------------------------------------------- communicator -----

@@ -172,10 +172,11 @@ static sa_status prepare_ops(sa_ctx* c, Scratch& scratch, const uint16_t* A16, i
 }
 
 // packed upper triangle: one CTA per row, coalesced row-segment copy
-__global__ void pack_upper_kernel(const uint16_t* __restrict__ m, int32_t n, int64_t ld, uint16_t* __restrict__ out) {
+template <class T>
+__global__ void pack_upper_kernel(const T* __restrict__ m, int32_t n, int64_t ld, T* __restrict__ out) {
   for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
-    const uint16_t* src = m + i * ld;
-    uint16_t* dst = out + i * (int64_t)n - i * (i - 1) / 2 - i;   // = i*n - i*(i+1)/2, then column j at + j
+    const T* src = m + i * ld;
+    T* dst = out + i * (int64_t)n - i * (i - 1) / 2 - i;   // = i*n - i*(i+1)/2, then column j at + j
     for (int64_t j = i + threadIdx.x; j < n; j += blockDim.x) dst[j] = src[j];
   }
 }
@@ -185,7 +186,8 @@ static inline cudaEvent_t ev_end(sa_ctx* c, int ph);
 
 // Enqueue the problems (A / B pointers given into the u16 operands).
 static sa_status launch_ops(sa_ctx* c, const EngineOps& E, const std::vector<MsProblem>& probs16, cudaStream_t st,
-                            cudaEvent_t ev0, cudaEvent_t ev1, TcCarry* keep = nullptr, const TcCarry* use = nullptr) {
+                            cudaEvent_t ev0, cudaEvent_t ev1, int gemm_phase, TcCarry* keep = nullptr,
+                            const TcCarry* use = nullptr) {
   c->last_enc = E.mode;
   c->last_tc = E.tc;
   c->last_tc_probs = 0;
@@ -194,8 +196,10 @@ static sa_status launch_ops(sa_ctx* c, const EngineOps& E, const std::vector<MsP
   SA_CUDA(cudaMemsetAsync(E.guard + 2, E.tc ? 1 : 0, sizeof(uint32_t), st));
   if (E.tc) {
     c->last_tc_probs = (int)probs16.size();
-    SA_TRY(tc_launch(probs16, E.a16.ldw, E.bins, E.guard, E.guard + SA_TC_COLS_AT, st, ev_begin(c, SA_PHASE_GEMM),
-                     ev_end(c, SA_PHASE_GEMM), keep, use));
+    cudaEvent_t g0 = ev_begin(c, gemm_phase);
+    cudaEvent_t g1 = ev_end(c, gemm_phase);
+    if (g0) c->last_gemm_phase = gemm_phase;
+    SA_TRY(tc_launch(probs16, E.a16.ldw, E.bins, E.guard, E.guard + SA_TC_COLS_AT, st, g0, g1, keep, use));
     for (const auto& cv : E.conv)
       SA_TRY(to_u8_launch(cv.p16, cv.n, stride_u16(E.bins), E.bins, cv.p8, stride_u8(E.bins), E.guard, st, true));
   }
@@ -265,12 +269,6 @@ sa_status sa_ctx_create(int cuda_device, sa_ctx** out) {
     delete c;
     return fail(SA_E_NOMEM, "context allocation failed");
   }
-  for (int i = 0; i < 2 * SA_PHASE_COUNT; ++i) {
-    if (cudaEventCreate(&c->ev[i]) != cudaSuccess) {
-      delete c;
-      return fail(SA_E_CUDA, "cudaEventCreate failed");
-    }
-  }
   *out = c;
   return SA_OK;
 }
@@ -294,8 +292,10 @@ sa_status sa_ctx_attach_comm(sa_ctx* ctx, const sa_comm_ops* ops, int nranks, in
 sa_status sa_ctx_destroy(sa_ctx* ctx) {
   if (!ctx) return SA_OK;
   cudaSetDevice(ctx->device);
-  for (int i = 0; i < 2 * SA_PHASE_COUNT; ++i)
-    if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+  for (int i = 0; i < SA_PHASE_COUNT; ++i)
+    for (int j = 0; j < SA_PHASE_RING; ++j)
+      for (int b = 0; b < 2; ++b)
+        if (ctx->ev[i][j][b]) cudaEventDestroy(ctx->ev[i][j][b]);
   if (ctx->dcount) cudaFree(ctx->dcount);
   if (ctx->hpinned) cudaFreeHost(ctx->hpinned);
   if (ctx->hstage) cudaFreeHost(ctx->hstage);
@@ -354,6 +354,14 @@ sa_status sa_selftest_f_division(int32_t cuda_device, int64_t* mismatches_h) {
 sa_status sa_ctx_set_timing(sa_ctx* ctx, int enable) {
   if (!ctx) return fail(SA_E_INVAL, "ctx is NULL");
   ctx->timing = enable != 0;
+  for (int i = 0; i < SA_PHASE_COUNT; ++i) ctx->ev_count[i] = 0;
+  ctx->last_gemm_phase = -1;
+  return SA_OK;
+}
+
+static sa_status phase_slot_ms(sa_ctx* ctx, int ph, int slot, float* ms) {
+  SA_CUDA(cudaEventSynchronize(ctx->ev[ph][slot][1]));
+  SA_CUDA(cudaEventElapsedTime(ms, ctx->ev[ph][slot][0], ctx->ev[ph][slot][1]));
   return SA_OK;
 }
 
@@ -363,22 +371,54 @@ sa_status sa_ctx_phase_ms(sa_ctx* ctx, float* ms_h) {
   SA_CUDA(cudaSetDevice(ctx->device));
   for (int i = 0; i < SA_PHASE_COUNT; ++i) {
     ms_h[i] = 0.f;
-    if (!ctx->ev_used[i]) continue;
-    SA_CUDA(cudaEventSynchronize(ctx->ev[2 * i + 1]));
-    SA_CUDA(cudaEventElapsedTime(&ms_h[i], ctx->ev[2 * i], ctx->ev[2 * i + 1]));
+    int ph = i;
+    if (i == SA_PHASE_GEMM && ctx->last_gemm_phase >= 0) ph = ctx->last_gemm_phase;   // the last K2T GEMM of any call
+    if (ctx->ev_count[ph] == 0) continue;
+    SA_TRY(phase_slot_ms(ctx, ph, ctx->ev_cur[ph], &ms_h[i]));
   }
   return SA_OK;
+}
+
+int32_t sa_ctx_phase_history(sa_ctx* ctx, int32_t phase, float* ms_h, int32_t max) {
+  g_err.clear();
+  if (!ctx || !ms_h || phase < 0 || phase >= SA_PHASE_COUNT || max < 0) {
+    fail(SA_E_INVAL, "bad argument");
+    return -1;
+  }
+  if (cudaSetDevice(ctx->device) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  const int64_t cnt = ctx->ev_count[phase];
+  const int n = (int)std::min<int64_t>(std::min<int64_t>(cnt, SA_PHASE_RING), max);
+  for (int t = 0; t < n; ++t) {
+    const int64_t occ = cnt - n + t;   // oldest kept first
+    if (phase_slot_ms(ctx, phase, (int)(occ % SA_PHASE_RING), &ms_h[t]) != SA_OK) return -1;
+  }
+  return n;
 }
 
 }  // extern "C"
 
 namespace sa {
+// A new occurrence of phase ph: its begin event (nullptr when timing is off or
+// the events cannot be created).  ev_end returns the end event of the same
+// occurrence, so call ev_begin first.
 static inline cudaEvent_t ev_begin(sa_ctx* c, int ph) {
   if (!c->timing) return nullptr;
-  c->ev_used[ph] = true;
-  return c->ev[2 * ph];
+  const int slot = (int)(c->ev_count[ph] % SA_PHASE_RING);
+  for (int b = 0; b < 2; ++b)
+    if (!c->ev[ph][slot][b] && cudaEventCreate(&c->ev[ph][slot][b]) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+  c->ev_cur[ph] = slot;
+  ++c->ev_count[ph];
+  return c->ev[ph][slot][0];
 }
-static inline cudaEvent_t ev_end(sa_ctx* c, int ph) { return c->timing ? c->ev[2 * ph + 1] : nullptr; }
+static inline cudaEvent_t ev_end(sa_ctx* c, int ph) {
+  return c->timing && c->ev_count[ph] > 0 ? c->ev[ph][c->ev_cur[ph]][1] : nullptr;
+}
 static inline sa_status rec(cudaEvent_t e, cudaStream_t st) {
   if (e) SA_CUDA(cudaEventRecord(e, st));
   return SA_OK;
@@ -596,7 +636,7 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
       apply_form(c, pr);
       probs.push_back(pr);
     }
-    SA_TRY(launch_ops(c, E, probs, st, nullptr, nullptr, &carry));
+    SA_TRY(launch_ops(c, E, probs, st, nullptr, nullptr, SA_PHASE_GEMM_S2A, &carry));
   }
   SA_TRY(rec(ev_end(c, SA_PHASE_S2A), st));
 
@@ -640,7 +680,7 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
     pr.sym = 0;
     pr.keyA = gkey;
     apply_form(c, pr);
-    SA_TRY(launch_ops(c, E2, {pr}, st, nullptr, nullptr, nullptr, &carry));
+    SA_TRY(launch_ops(c, E2, {pr}, st, nullptr, nullptr, SA_PHASE_GEMM_S2D, nullptr, &carry));
   }
   SA_TRY(rec(ev_end(c, SA_PHASE_S2D), st));
 
@@ -912,7 +952,8 @@ sa_status sa_kmer_rank(sa_ctx* ctx, const uint16_t* q_prof, const int32_t* q_nk,
   pr.num = numerators;
   pr.ld = npool;
   apply_form(ctx, pr);
-  SA_TRY(launch_ops(ctx, E, {pr}, st, ev_begin(ctx, SA_PHASE_RANK), ev_end(ctx, SA_PHASE_RANK)));
+  cudaEvent_t r0 = ev_begin(ctx, SA_PHASE_RANK);
+  SA_TRY(launch_ops(ctx, E, {pr}, st, r0, ev_end(ctx, SA_PHASE_RANK), SA_PHASE_GEMM));
   if (rank_f64) SA_TRY(keys_to_f64_launch(keys, nq, npool, rank_f64, st, ctx->rank_form, std::log1p(ctx->delta)));
   return SA_OK;
 }
@@ -1075,7 +1116,8 @@ sa_status sa_bucket_similarity(sa_ctx* ctx, const uint16_t* profiles, const int3
   pr.num = numerators;
   pr.sim = similarity;
   pr.ld = n;
-  SA_TRY(launch_ops(ctx, E, {pr}, st, ev_begin(ctx, SA_PHASE_S5), ev_end(ctx, SA_PHASE_S5)));
+  cudaEvent_t s0 = ev_begin(ctx, SA_PHASE_S5);
+  SA_TRY(launch_ops(ctx, E, {pr}, st, s0, ev_end(ctx, SA_PHASE_S5), SA_PHASE_GEMM_S5));
   return SA_OK;
 }
 
@@ -1090,17 +1132,30 @@ sa_status sa_guide_tree(sa_ctx* ctx, const double* similarity, int32_t n, int64_
   return upgma_launch(similarity, n, ld, merges, heights, (cudaStream_t)stream);
 }
 
-sa_status sa_pack_upper_u16(sa_ctx* ctx, const uint16_t* matrix, int32_t n, int64_t ld, uint16_t* packed,
-                            void* stream) {
+}  // extern "C"
+namespace sa {
+template <class T>
+static sa_status pack_upper(sa_ctx* ctx, const T* matrix, int32_t n, int64_t ld, T* packed, void* stream) {
   g_err.clear();
   if (!ctx) return fail(SA_E_INVAL, "ctx is NULL");
   if (n < 0 || ld < n) return fail(SA_E_INVAL, "bad n / ld");
   if (n == 0) return SA_OK;
   if (!matrix || !packed) return fail(SA_E_INVAL, "NULL required pointer");
   SA_CUDA(cudaSetDevice(ctx->device));
-  pack_upper_kernel<<<(unsigned)std::min<int64_t>(n, 148 * 16), 256, 0, (cudaStream_t)stream>>>(matrix, n, ld, packed);
+  pack_upper_kernel<T><<<(unsigned)std::min<int64_t>(n, 148 * 16), 256, 0, (cudaStream_t)stream>>>(matrix, n, ld, packed);
   SA_LAUNCHED();
   return SA_OK;
+}
+}  // namespace sa
+extern "C" {
+
+sa_status sa_pack_upper_u16(sa_ctx* ctx, const uint16_t* matrix, int32_t n, int64_t ld, uint16_t* packed,
+                            void* stream) {
+  return pack_upper(ctx, matrix, n, ld, packed, stream);
+}
+
+sa_status sa_pack_upper_f64(sa_ctx* ctx, const double* matrix, int32_t n, int64_t ld, double* packed, void* stream) {
+  return pack_upper(ctx, matrix, n, ld, packed, stream);
 }
 
 sa_status sa_bucket_similarity_batch(sa_ctx* ctx, int32_t nbuckets, const uint16_t* profiles, const int32_t* nkmers,
@@ -1139,7 +1194,8 @@ sa_status sa_bucket_similarity_batch(sa_ctx* ctx, int32_t nbuckets, const uint16
     pr.ld = ld_h ? ld_h[b] : nb;
     probs.push_back(pr);
   }
-  SA_TRY(launch_ops(ctx, E, probs, st, ev_begin(ctx, SA_PHASE_S5), ev_end(ctx, SA_PHASE_S5)));
+  cudaEvent_t s0 = ev_begin(ctx, SA_PHASE_S5);
+  SA_TRY(launch_ops(ctx, E, probs, st, s0, ev_end(ctx, SA_PHASE_S5), SA_PHASE_GEMM_S5));
   return SA_OK;
 }
 

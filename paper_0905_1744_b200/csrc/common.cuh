@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <algorithm>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -63,6 +64,37 @@ struct Scratch {
     return static_cast<T*>(p);
   }
 };
+
+// One-time setup per (call site, device): kernel attributes
+// (cudaFuncSetAttribute is per device) and device tables.  `f` runs under the
+// site's mutex the first time a thread reaches the site with a given current
+// device; concurrent contexts on several threads or devices are safe.
+struct DeviceOnce {
+  std::mutex m;
+  bool done[64] = {};
+  template <class F>
+  sa_status run(F&& f) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(SA_E_CUDA, "cudaGetDevice failed");
+    }
+    std::lock_guard<std::mutex> g(m);
+    if (dev < 64 && done[dev]) return SA_OK;
+    const sa_status s = f();
+    if (s == SA_OK && dev < 64) done[dev] = true;
+    return s;
+  }
+};
+// SM count of the current device (148 on B200).
+inline int device_sms() {
+  int dev = 0, s = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 148;
+  }
+  return s > 0 ? s : 148;
+}
 
 #define SA_ALLOC(var, T, n)                                                        \
   T* var = scratch.alloc<T>(n);                                                    \
@@ -202,8 +234,12 @@ struct sa_ctx {
   sa_comm_ops comm{};
   bool has_comm = false;
   bool timing = false;
-  cudaEvent_t ev[2 * SA_PHASE_COUNT] = {};
-  bool ev_used[SA_PHASE_COUNT] = {};
+  // phase events: a ring of SA_PHASE_RING (begin, end) pairs per phase,
+  // created on first use; ev_count = occurrences recorded, ev_cur = last slot
+  cudaEvent_t ev[SA_PHASE_COUNT][SA_PHASE_RING][2] = {};
+  int64_t ev_count[SA_PHASE_COUNT] = {};
+  int ev_cur[SA_PHASE_COUNT] = {};
+  int last_gemm_phase = -1;     // the specific phase of the last K2T GEMM record
   int last_enc = -1;            // ENC_* of the last min-sum call, or ENC_AUTO
   bool last_tc = false;         // the last auto call tried the tensor-core engine first
   int last_tc_probs = 0;        // problems of that K2T call

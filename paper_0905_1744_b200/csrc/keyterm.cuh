@@ -28,15 +28,23 @@ static __global__ void recip_kernel() {
   g_etab[d] = (uint32_t)e;
 }
 
-static sa_status ensure_recip_tables_tu(cudaStream_t st) {
-  static bool ready[64] = {};   // per translation unit (the tables are per TU)
-  int dev = 0;
-  SA_CUDA(cudaGetDevice(&dev));
-  if (dev < 64 && ready[dev]) return SA_OK;
-  recip_kernel<<<256, 256, 0, st>>>();
-  SA_LAUNCHED();
-  if (dev < 64) ready[dev] = true;
-  return SA_OK;
+// Filled once per device (and per translation unit, which owns its copy of the
+// tables), synchronously: the kernel runs on a private stream that is
+// synchronised before any caller's work can read the tables, whatever stream
+// that work is on (a stream-ordered fill raced with other streams).
+static sa_status ensure_recip_tables_tu(cudaStream_t) {
+  static DeviceOnce once;
+  return once.run([]() -> sa_status {
+    cudaStream_t s = nullptr;
+    SA_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    recip_kernel<<<256, 256, 0, s>>>();
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    if (e != cudaSuccess) return fail(SA_E_CUDA, "reciprocal tables: %s", cudaGetErrorString(e));
+    return SA_OK;
+  });
 }
 
 // floor(C * 2^64 / D) accumulated into a 96-bit (lo, hi) register pair.

@@ -510,8 +510,6 @@ minsum_tma_kernel(const __grid_constant__ MsBatch batch, const __grid_constant__
   }
 }
 
-static int g_num_sms = 0;
-
 // Pipeline of the engine (SA_K2_PIPE): "tma" (default) = TMA tensor loads +
 // mbarrier ring (engine B), "cpasync" = per-thread cp.async + CTA barrier per
 // stage (engine A).
@@ -544,15 +542,16 @@ static sa_status encode_rows_map(CUtensorMap* m, const uint32_t* base, int64_t r
 
 template <bool SYM, int ENC, int VAR>
 static sa_status launch_one(const MsBatch& b, int64_t tiles, int ldw, const uint32_t* guard, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
+  static DeviceOnce once;
+  SA_TRY(once.run([]() -> sa_status {
     SA_CUDA(cudaFuncSetAttribute(minsum_kernel<SYM, ENC, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, MS_SMEM));
     SA_CUDA(cudaFuncSetAttribute(minsum_tma_kernel<SYM, ENC, VAR, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  MS_TMA_SMEM));
     SA_CUDA(cudaFuncSetAttribute(minsum_tma_kernel<SYM, ENC, VAR, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  MS_TMA_SMEM));
-    configured = true;
-  }
+    return SA_OK;
+  }));
+  const int g_num_sms = device_sms();
   const int64_t grid = tiles < g_num_sms ? tiles : g_num_sms;
   if (use_tma_pipe()) {
     MsMaps maps;
@@ -602,11 +601,6 @@ sa_status minsum_launch(const std::vector<MsProblem>& probs_in, int ldw, int enc
                         cudaEvent_t ev0, cudaEvent_t ev1, const uint32_t* guard) {
   if (ldw % MS_BKW != 0) return fail(SA_E_INVAL, "profile row stride must be a multiple of 64 bins");
   SA_TRY(ensure_recip_tables(st));
-  if (g_num_sms == 0) {
-    int dev = 0;
-    SA_CUDA(cudaGetDevice(&dev));
-    SA_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-  }
   // split into batches of at most MS_MAXPROB problems of the same symmetry
   std::vector<MsProblem> probs;
   for (const auto& p : probs_in)

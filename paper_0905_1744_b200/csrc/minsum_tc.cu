@@ -832,13 +832,13 @@ struct KeyMatEpi {
                                            const uint32_t (&v)[16], int lane, const uint8_t* ent, uint8_t* xp,
                                            int stores) const {
     constexpr bool want_num = (MODE & EPI_NUM) != 0;
-    const int ld = (int)E.ld;
+    const int64_t ld = E.ld;   // 64-bit offsets: n_b * ld may exceed 2^31
     uint16_t* const num = E.num;
     double* const sim = E.sim;
     uint8_t* const fb = xp + 64 * 16;
     const bool vst = stores != 8;
     uint32_t w[8];
-    int om = c0 * ld + s.row_g;
+    int64_t om = (int64_t)c0 * ld + s.row_g;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       double Fp = 0.0;
@@ -865,7 +865,7 @@ struct KeyMatEpi {
       for (int k = 0; k < 4; ++k) {
         const int rho = (lane >> 2) + 8 * k, u = lane & 3;
         const double2 f2 = *reinterpret_cast<const double2*>(fb + rho * 64 + ((u ^ ((rho >> 1) & 3)) * 16));
-        if (vst) __stcs(reinterpret_cast<double2*>(sim + (wrow0 + rho) * ld + c0 + h * 8 + u * 2), f2);
+        if (vst) __stcs(reinterpret_cast<double2*>(sim + (int64_t)(wrow0 + rho) * ld + c0 + h * 8 + u * 2), f2);
       }
       __syncwarp();
     }
@@ -879,7 +879,7 @@ struct KeyMatEpi {
       for (int k = 0; k < 2; ++k) {
         const int rho = (lane >> 1) + 16 * k, u = lane & 1;
         const uint4 c8 = *reinterpret_cast<const uint4*>(xp + rho * 32 + ((u ^ ((rho >> 2) & 1)) * 16));
-        if (vst) __stcs(reinterpret_cast<uint4*>(num + (wrow0 + rho) * ld + c0 + u * 8), c8);
+        if (vst) __stcs(reinterpret_cast<uint4*>(num + (int64_t)(wrow0 + rho) * ld + c0 + u * 8), c8);
       }
       __syncwarp();
     }
@@ -906,7 +906,7 @@ struct KeyMatEpi {
       // row: conflict-free both ways).  Element offsets fit 32 bits (n_b ld < 2^31).
       constexpr int Q = CW / 8;                          // 16-byte units per buffer row
       constexpr int QSH = CW == 16 ? 2 : 1;              // swizzle: unit ^ ((row >> QSH) % Q)
-      const int ld = (int)E.ld;
+      const int64_t ld = E.ld;   // 64-bit offsets: n_b * ld may exceed 2^31
       uint16_t* const num = E.num;
       double* const sim = E.sim;
       if constexpr (VD) {
@@ -917,7 +917,7 @@ struct KeyMatEpi {
       }
       {
         uint32_t w[CW / 2];
-        int om = c0 * ld + s.row_g;
+        int64_t om = (int64_t)c0 * ld + s.row_g;
 #pragma unroll
         for (int j = 0; j < CW; ++j) {
           const uint32_t C = v[j];
@@ -950,7 +950,7 @@ struct KeyMatEpi {
         dc = yd.y;
       }
       constexpr int RPP = 32 / CW;
-      int od = (wrow0 + lane / CW) * ld + c0 + cl;
+      int64_t od = (int64_t)(wrow0 + lane / CW) * ld + c0 + cl;
 #pragma unroll
       for (int pss = 0; pss < CW; ++pss) {
         const int i = pss * RPP + lane / CW;              // buffer row = warp row
@@ -1045,6 +1045,13 @@ __global__ void f_division_check_kernel(unsigned long long* bad) {
     nb += (__double_as_longlong(a) != __double_as_longlong(b)) ? 1ull : 0ull;
   }
   if (nb) atomicAdd(bad, nb);
+}
+
+// Zero a key array when the launch was declined (see tc_launch).
+__global__ void tc_reset_keys_kernel(sa_key128* __restrict__ keys, int64_t n, const uint32_t* __restrict__ state) {
+  if (!tc_infeasible(state)) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    keys[i] = sa_key128{0, 0};
 }
 
 // ------------------------------------------------------------- host ----
@@ -1148,14 +1155,9 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
                     uint32_t* cols_out, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1, TcCarry* keep,
                     const TcCarry* use) {
   SA_TRY(ensure_recip_tables_tu(st));
-  static int g_num_sms = 0;
-  if (g_num_sms == 0) {
-    int dev = 0;
-    SA_CUDA(cudaGetDevice(&dev));
-    SA_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-  }
-  static bool configured = false;
-  if (!configured) {
+  const int g_num_sms = device_sms();
+  static DeviceOnce once;
+  SA_TRY(once.run([]() -> sa_status {
     SA_CUDA(cudaFuncSetAttribute(tc_hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  2 * (TC_LCAP - TC_HREG) * TC_WPL * 4));
     SA_CUDA(cudaFuncSetAttribute(tc_hist_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1164,9 +1166,8 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     if (cs == SA_OK) cs = tc_configure_all<true, 1>();
     if (cs == SA_OK) cs = tc_configure_all<false, 2>();
     if (cs == SA_OK) cs = tc_configure_all<true, 2>();
-    if (cs != SA_OK) return cs;
-    configured = true;
-  }
+    return cs;
+  }));
   const int stride16 = 2 * ldw16;
   const bool fp4 = tc_fp4_operands();
   const bool pairs = tc_pairs();
@@ -1432,6 +1433,23 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       if (fpass_here && P.sim) SA_TRY(ratio_launch(epi.e[q].num, P.nkA, P.nkB, P.na, P.nb, P.ld, P.sim, st, state));
     }
     i0 = i1;
+  }
+  // A launch of more than MAXPROB problems runs chunk by chunk: if a later
+  // chunk is declined (state[1]), the earlier chunks' GEMMs have already added
+  // their key terms, and the fallback engine recomputes every problem -- so
+  // the keys go back to zero first (device-guarded: nothing happens when K2T
+  // completed the launch).  Matrices are overwritten by the fallback anyway.
+  if (probs.size() > (size_t)tc::MAXPROB) {
+    for (const auto& P : probs) {
+      if (P.keyA) {
+        tc_reset_keys_kernel<<<64, 256, 0, st>>>(P.keyA, P.na, state);
+        SA_LAUNCHED();
+      }
+      if (P.sym && P.keyB && P.keyB != P.keyA) {
+        tc_reset_keys_kernel<<<64, 256, 0, st>>>(P.keyB, P.nb, state);
+        SA_LAUNCHED();
+      }
+    }
   }
   return SA_OK;
 }

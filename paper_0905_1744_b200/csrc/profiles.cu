@@ -126,11 +126,14 @@ sa_status profiles_launch(const uint8_t* residues, const int64_t* offsets, int32
                           cudaStream_t st) {
   if (n <= 0) return SA_OK;
   const int smem = stride * 2;
-  static int configured_smem = 48 * 1024;
-  if (smem > configured_smem) {
-    SA_CUDA(cudaFuncSetAttribute(profiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured_smem = smem;
-  }
+  // both kernels may take up to 227 KB of dynamic shared memory (the attribute
+  // is a per-device ceiling; each launch passes what it needs)
+  static DeviceOnce once;
+  SA_TRY(once.run([]() -> sa_status {
+    SA_CUDA(cudaFuncSetAttribute(profiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    SA_CUDA(cudaFuncSetAttribute(profiles_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    return SA_OK;
+  }));
   int dev = 0, sms = 0, per_sm = 0;
   SA_CUDA(cudaGetDevice(&dev));
   SA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -145,11 +148,6 @@ sa_status profiles_launch(const uint8_t* residues, const int64_t* offsets, int32
     return e ? atoi(e) : 1;
   }();
   if (bulk && 2 * smem <= 227 * 1024) {   // two row buffers fit (bins <= 58 112)
-    static int configured_bulk = 0;
-    if (2 * smem > 48 * 1024 && 2 * smem > configured_bulk) {
-      SA_CUDA(cudaFuncSetAttribute(profiles_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * smem));
-      configured_bulk = 2 * smem;
-    }
     int per_sm_b = 0;
     SA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_b, profiles_bulk_kernel, 256, 2 * smem));
     if (per_sm_b < 1) per_sm_b = 1;
