@@ -137,6 +137,18 @@ int sa_ctx_engine(const sa_ctx* ctx);
  * the device.  Problems are: one per block (sa_partition S2a), one (S2d,
  * sa_kmer_rank), one per sa_bucket_similarity call. */
 int32_t sa_ctx_tc_columns(const sa_ctx* ctx, int32_t* cols_h, int32_t max);
+/* K2T only: how each problem of the last min-sum call on this context handled
+ * threshold layers >= 2: mode_h[i] = 1 when problem i ran
+ * SPARSE (tensor cores on layer 1 only, plus exact correction terms
+ * min(c_i, c_j) - 1 for every bin both rows repeat, added in the GEMM
+ * epilogue), 0 when it ran DENSE (layers >= 2 as MMA columns); terms_h[i]
+ * (nullable) = its number of correction terms (pair, bin).  Problems in call
+ * order as for sa_ctx_tc_columns; at most `max`.  Returns how many were
+ * written (0 when the last call did not run K2T, -1 on a CUDA error).
+ * Synchronises the device.  Environment: SA_K2T_SPARSE=0 disables the sparse
+ * path; SA_K2T_SPARSE_BUDGET=b (default 8) makes a problem sparse when its
+ * terms number at most pairs / b. */
+int32_t sa_ctx_tc_sparse(const sa_ctx* ctx, int32_t* mode_h, int64_t* terms_h, int32_t max);
 /* Self-test of the division-free F = C / D the K2T matrix epilogue uses
  * (Markstein correction on RN(1/D)): compares it bit for bit
  * with IEEE round-to-nearest division for every 0 <= C <= D <= 65535 on
@@ -217,6 +229,8 @@ typedef struct {
   int64_t* candidates;       /* [p*(p-1)] S3b: sorted regular samples Y (global ids) */
   int32_t* exact_fallbacks_h;/* host int: ambiguous key comparisons resolved exactly */
   int32_t* uncertified_h;    /* host int: (d^F form) comparisons inside the error window */
+  uint16_t* global_num;      /* [n_local][p*samples_per_block] S2d numerators C (row-major, columns in S's
+                                (q, j) order), written by the S2d GEMM epilogue itself          */
 } sa_partition_debug;
 
 /* Algorithm 2 steps 1-11, the rank-based sample sort:

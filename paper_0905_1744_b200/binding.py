@@ -29,7 +29,7 @@ EXPORTED = ["sa_ctx_create", "sa_ctx_attach_comm", "sa_ctx_destroy", "sa_last_er
             "sa_partition", "sa_redistribute", "sa_bucket_similarity", "sa_exact_rank_compare", "sa_ctx_engine",
             "sa_ctx_set_rank_form", "sa_ctx_tc_columns", "sa_ctx_tc_operand", "sa_selftest_f_division",
             "sa_bucket_similarity_batch", "sa_pack_upper_u16", "sa_pack_upper_f64", "sa_guide_tree",
-            "sa_ctx_phase_history"]
+            "sa_ctx_phase_history", "sa_ctx_tc_sparse"]
 SA_RANK_F, SA_RANK_DF = 0, 1
 
 
@@ -63,7 +63,7 @@ class sa_partition_debug(ctypes.Structure):
                 ("sample_idx", ctypes.c_void_p), ("global_key", ctypes.c_void_p), ("global_f64", ctypes.c_void_p),
                 ("global_order", ctypes.c_void_p), ("candidates", ctypes.c_void_p),
                 ("exact_fallbacks_h", ctypes.POINTER(ctypes.c_int32)),
-                ("uncertified_h", ctypes.POINTER(ctypes.c_int32))]
+                ("uncertified_h", ctypes.POINTER(ctypes.c_int32)), ("global_num", ctypes.c_void_p)]
 
 
 _lib = None
@@ -108,6 +108,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "sa_ctx_engine": (ctypes.c_int, [P]),
         "sa_ctx_tc_columns": (ctypes.c_int32, [P, P, ctypes.c_int32]),
         "sa_ctx_tc_operand": (ctypes.c_int, [P]),
+        "sa_ctx_tc_sparse": (ctypes.c_int32, [P, P, P, ctypes.c_int32]),
         "sa_selftest_f_division": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(ctypes.c_int64)]),
         "sa_ctx_set_rank_form": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_double]),
     }
@@ -217,6 +218,16 @@ class Context:
         """SA_RANK_F (mean F, exact) or SA_RANK_DF (mean -ln(Delta + F), Eq. 2-3)."""
         _check(load_library().sa_ctx_set_rank_form(self.handle, int(form), float(delta)))
 
+    def tc_sparse(self) -> list[tuple[int, int]]:
+        """(mode, correction terms) of each problem of the last K2T call:
+        mode 1 = layers >= 2 as sparse epilogue corrections, 0 = as MMA columns."""
+        mode = np.zeros(64, dtype=np.int32)
+        terms = np.zeros(64, dtype=np.int64)
+        n = int(load_library().sa_ctx_tc_sparse(self.handle, mode.ctypes.data, terms.ctypes.data, 64))
+        if n < 0:
+            raise SaError(SA_E_CUDA, "sa_ctx_tc_sparse failed")
+        return [(int(mode[i]), int(terms[i])) for i in range(n)]
+
     def set_timing(self, enable: bool = True):
         _check(load_library().sa_ctx_set_timing(self.handle, int(enable)))
 
@@ -295,7 +306,8 @@ def pivot_global_idx(pivots: torch.Tensor) -> torch.Tensor:
 
 
 def sa_partition(ctx: Context, p: int, samples_per_block: int, profiles, nkmers, offsets, bins: int,
-                 n_total: int, first_global: int, debug: bool = False, stream=None) -> PartitionOut:
+                 n_total: int, first_global: int, debug: bool = False, stream=None,
+                 want_global_num: bool = False) -> PartitionOut:
     """S2a-S3c (Algorithm 2 steps 2-11) on this rank's shard; see sa.h."""
     _dev(profiles, torch.uint16, "profiles")
     _dev(nkmers, torch.int32, "nkmers")
@@ -322,10 +334,13 @@ def sa_partition(ctx: Context, p: int, samples_per_block: int, profiles, nkmers,
             "global_order": torch.empty(n_local, dtype=torch.int64, device=dev),
             "candidates": torch.empty(max(p * (p - 1), 1), dtype=torch.int64, device=dev),
         }
+        if want_global_num:   # the S2d numerator matrix [n_local][s] (parity artifact)
+            dbg["global_num"] = torch.empty((n_local, s), dtype=torch.uint16, device=dev)
         dbg_struct = sa_partition_debug(*[_ptr(dbg[k]) for k in ["local_key", "local_f64", "local_order",
                                                                   "sample_idx", "global_key", "global_f64",
                                                                   "global_order", "candidates"]],
-                                        ctypes.pointer(fallbacks), ctypes.pointer(uncertified))
+                                        ctypes.pointer(fallbacks), ctypes.pointer(uncertified),
+                                        _ptr(dbg.get("global_num")))
     _check(load_library().sa_partition(
         ctx.handle, p, samples_per_block, _ptr(profiles), _ptr(nkmers), _ptr(offsets), bins, n_total, first_global,
         n_local, _ptr(bucket_of), _ptr(pivots),

@@ -344,6 +344,26 @@ int32_t sa_ctx_tc_columns(const sa_ctx* ctx, int32_t* cols_h, int32_t max) {
   return n;
 }
 
+int32_t sa_ctx_tc_sparse(const sa_ctx* ctx, int32_t* mode_h, int64_t* terms_h, int32_t max) {
+  if (!ctx || !mode_h || !ctx->last_tc || ctx->last_tc_probs <= 0) return 0;
+  if (cudaSetDevice(ctx->device) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess ||
+      cudaMemcpy(ctx->hpinned, ctx->dcount, SA_DCOUNT_WORDS * 4, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  if (!(ctx->hpinned[2] && !ctx->hpinned[1])) return 0;   // K2T declined: a fallback engine ran
+  const int n = std::min(ctx->last_tc_probs, SA_TC_COLS_MAX);
+  for (int i = 0; i < n && i < max; ++i) {
+    mode_h[i] = (int32_t)ctx->hpinned[SA_TC_MODE_AT + i];
+    if (terms_h) {
+      uint64_t t = 0;
+      std::memcpy(&t, &ctx->hpinned[SA_TC_TERMS_AT + 2 * i], 8);
+      terms_h[i] = (int64_t)t;
+    }
+  }
+  return std::min(n, max);
+}
+
 sa_status sa_selftest_f_division(int32_t cuda_device, int64_t* mismatches_h) {
   g_err.clear();
   if (!mismatches_h) return fail(SA_E_INVAL, "NULL argument");
@@ -679,6 +699,10 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
     pr.nb = s_all;
     pr.sym = 0;
     pr.keyA = gkey;
+    if (a.dbg && a.dbg->global_num) {   // parity artifact: the N x s numerator matrix
+      pr.num = a.dbg->global_num;
+      pr.ld = s_all;
+    }
     apply_form(c, pr);
     SA_TRY(launch_ops(c, E2, {pr}, st, nullptr, nullptr, SA_PHASE_GEMM_S2D, nullptr, &carry));
   }

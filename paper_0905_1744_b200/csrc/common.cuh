@@ -171,9 +171,13 @@ bool tc_last_fp4();       // the format of the last K2T launch
 sa_status ratio_launch(const uint16_t* num, const int32_t* nkA, const int32_t* nkB, int64_t na, int64_t nb,
                        int64_t ld, double* sim, cudaStream_t st, const uint32_t* state = nullptr);
 constexpr int SA_STAGE_BYTES = 1 << 16;   // ctx->hstage: mapped pinned staging for d2h_small
-constexpr int SA_DCOUNT_WORDS = 256;   // ctx->dcount: [0..3] guard words, [16..80) K2T column counts
+// ctx->dcount: [0..3] guard words, [16..80) K2T column counts, [80..144) K2T
+// sparse-layer mode per problem, [144..272) its correction terms (u64)
+constexpr int SA_DCOUNT_WORDS = 512;
 constexpr int SA_TC_COLS_AT = 16;
 constexpr int SA_TC_COLS_MAX = 64;
+constexpr int SA_TC_MODE_AT = 80;
+constexpr int SA_TC_TERMS_AT = 144;
 // Operand rows carried from one K2T launch to the next on the same u16 rows
 // (sa_partition: S2a's blocks -> S2d's query side): the rows with their first
 // dense layers already written and the OR of their seen-once planes.  The
@@ -189,6 +193,10 @@ struct TcCarry {
   int32_t* ndense = nullptr;         // [np] dense layers each problem of the building launch kept
   int np = 0;
   uint32_t* masks = nullptr;         // [nrows][2][256] layer-2 / layer-3 masks (minsum_tc.cu TcMasks)
+  int spec = 2;                      // dense layers its histogram pass wrote
+  const uint2* recs = nullptr;       // its sparse-layer records (tc_sparse.cuh), nullptr when off
+  const uint32_t* nrec = nullptr;
+  uint32_t rec_cap = 0;
 };
 sa_status tc_launch(const std::vector<MsProblem>& probs, int ldw16, int32_t bins, uint32_t* state,
                     uint32_t* cols_out, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1,

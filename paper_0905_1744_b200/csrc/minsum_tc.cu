@@ -35,6 +35,7 @@
 #include "common.cuh"
 #include "keyterm.cuh"
 #include "tc_gemm.cuh"
+#include "tc_sparse.cuh"
 
 namespace sa {
 
@@ -128,18 +129,35 @@ __device__ __forceinline__ void store_mask_columns(uint8_t* dst, uint32_t m, int
   }
 }
 
-// The first TC_SPEC dense layers are written by the histogram pass itself
-// (every bin of the layer, in bin order: the layout the column selection
-// gives a dense layer), so the profile rows are read once for both: the
-// selection later keeps nd dense layers; tc_dense_kernel adds layers
-// TC_SPEC + 1 .. nd when nd > TC_SPEC, and tc_build_kernel overwrites the
-// columns from nd * dw on when nd < TC_SPEC.
-constexpr int TC_SPEC = 2;
+// The first `spec` dense layers (a launch parameter: 1 when the launch expects
+// its problems to take the sparse path for layers >= 2, tc_sparse.cu, else 2)
+// are written by the histogram pass itself (every bin of the layer, in bin
+// order: the layout the column selection gives a dense layer), so the profile
+// rows are read once for both: the selection later keeps nd dense layers;
+// tc_dense_kernel adds layers spec + 1 .. nd when nd > spec, and
+// tc_build_kernel overwrites the columns from nd * dw on when nd < spec.
+constexpr int TC_SPEC_MAX = 2;
+
+// Records for the sparse layers (tc_sparse.cu): every (row, bin) whose count
+// reaches 2, as {row, bin | count << 16}, into this CTA's segment of
+// `rec_seg` (seg_cap records; the count goes to seg_cnt[blockIdx.x], and a
+// segment that overflows makes the whole launch dense).
+struct TcRecOut {
+  uint2* seg;
+  uint32_t* cnt;
+  uint32_t* povf;   // [MAXPROB]: the problem of a row whose record did not fit runs dense
+  uint32_t* incomplete;
+  uint32_t seg_cap;
+  int on;
+};
 
 template <bool FP4>
-__global__ void __launch_bounds__(TC_HIST_THREADS)
+__global__ void __launch_bounds__(TC_HIST_THREADS, 2)   // two CTAs per SM (<= 128 registers)
 tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut O, int stride16, int bins,
-               uint32_t* __restrict__ planes, uint32_t* __restrict__ state, int64_t hist_from, TcMasks mk) {
+               uint32_t* __restrict__ planes, uint32_t* __restrict__ state, int64_t hist_from, TcMasks mk, int spec,
+               TcRecOut ro) {
+  __shared__ uint32_t s_nrec;
+  if (threadIdx.x == 0) s_nrec = 0;
   constexpr int64_t ROWB = FP4 ? TC_KCAP / 2 : TC_KCAP;
   const int dw = (bins + 15) & ~15;                      // columns per dense layer
   const int64_t layer_bytes = FP4 ? dw / 2 : dw;
@@ -217,9 +235,9 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
 #pragma unroll
         for (int l = 0; l < TC_HREG; ++l) {
           const uint32_t m = (uint32_t)l < vmax ? layer_mask(v, (uint32_t)(l + 1) * 0x00010001u) : 0u;
-          if (l < TC_SPEC && h < cnt && in_cols) store_mask_columns<FP4>(orow + l * layer_bytes, m, dw - w * 32);
+          if (l < spec && h < cnt && in_cols) store_mask_columns<FP4>(orow + l * layer_bytes, m, dw - w * 32);
           if (l == 1 || l == 2) m23[l - 1] = m;
-          if ((uint32_t)l >= vmax && l >= TC_SPEC + 1) break;
+          if ((uint32_t)l >= vmax && l >= 3) break;   // layers 1-3: the masks above
           s2[l] |= s1[l] & m;
           s1[l] |= m;
         }
@@ -227,6 +245,24 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
           uint32_t* mr = mk.own + (g + h - hist_from) * TC_MROW;
           mr[w] = m23[0];
           mr[TC_MW + w] = m23[1];
+          if (ro.on) {
+            // records of the bins reaching 2 (sparse per row: ~8 of 8000 on
+            // the protein workloads); the count is re-read from the row (L1)
+            uint32_t m = m23[0];
+            while (m) {
+              const int bit = __ffs(m) - 1;
+              m &= m - 1;
+              const uint32_t c = __ldg(base + h * (int64_t)stride16 + bit);
+              const uint32_t pos = atomicAdd(&s_nrec, 1u);
+              if (pos < ro.seg_cap) {
+                ro.seg[(int64_t)blockIdx.x * ro.seg_cap + pos] =
+                    make_uint2((uint32_t)(g + h), (uint32_t)(w * 32 + bit) | (c << 16));
+              } else {
+                atomicOr(&ro.povf[O.prob[t]], 1u);
+                atomicOr(ro.incomplete, 1u);
+              }
+            }
+          }
         }
         const int top = (int)min(vmax, (uint32_t)TC_LCAP);
         for (int l = TC_HREG; l < top; ++l) {
@@ -250,6 +286,47 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((w & 31) == 0 && mx) atomicMax(&state[0], mx);
+  if (ro.on) {
+    __syncthreads();
+    if (threadIdx.x == 0) ro.cnt[blockIdx.x] = s_nrec;
+  }
+}
+
+// The hist CTAs' record segments -> one dense array after the carried
+// launch's records (`carried`: [0] count, [2] incomplete flag), total[0] = the
+// count.  A segment over its cap (a CTA whose rows repeat more bins than the
+// budget) keeps its first seg_cap records; the hist pass marked the problems
+// of the rows whose records did not fit (povf: they run dense).
+struct TcRecOvf {
+  int carried_prob;   // problem of the carried side 0
+  uint32_t* povf;     // [MAXPROB], zeroed by the caller
+};
+__global__ void tc_rec_compact_kernel(const uint2* __restrict__ seg, const uint32_t* __restrict__ cnt, int nseg,
+                                      uint32_t seg_cap, uint2* __restrict__ out, uint32_t out_cap,
+                                      uint32_t* __restrict__ total, const uint32_t* __restrict__ carried,
+                                      const TcRecOvf ov) {
+  __shared__ uint32_t s_base;
+  const int b = blockIdx.x;
+  if (threadIdx.x < 32) {
+    uint32_t sum = 0;
+    for (int i = threadIdx.x; i < b; i += 32) sum += min(cnt[i], seg_cap);
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (threadIdx.x == 0) s_base = sum + (carried ? carried[0] : 0u);
+  }
+  __syncthreads();
+  const uint32_t c = cnt[b], n = min(c, seg_cap);
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint32_t pos = s_base + i;
+    if (pos < out_cap) out[pos] = seg[(int64_t)b * seg_cap + i];
+  }
+  if (threadIdx.x == 0) {
+    (void)c;
+    if (b == 0 && carried && carried[2]) {   // the carried side's records are incomplete
+      atomicOr(&ov.povf[ov.carried_prob], 1u);
+      atomicOr(&total[2], 1u);
+    }
+    if (b == nseg - 1) total[0] = min(s_base + n, out_cap);
+  }
 }
 
 // OR of the seen-once planes of sides [0, nsides) (the carried query side of a
@@ -302,7 +379,7 @@ struct TcSel {
 __global__ void __launch_bounds__(1024)
 tc_select_kernel(const __grid_constant__ TcSel sel, const uint32_t* __restrict__ planes, int bins, int kbc,
                  uint32_t* __restrict__ collist, int32_t* __restrict__ kblocks, int32_t* __restrict__ ndense,
-                 uint32_t* __restrict__ state, uint32_t* __restrict__ cols_out) {
+                 uint32_t* __restrict__ state, uint32_t* __restrict__ cols_out, const int32_t* __restrict__ spmode) {
   __shared__ uint32_t warp_cnt[32];
   __shared__ uint32_t warp_pos[32];
   __shared__ uint32_t s_total, s_nd;
@@ -329,13 +406,17 @@ tc_select_kernel(const __grid_constant__ TcSel sel, const uint32_t* __restrict__
   }
   if (lane == 31) warp_cnt[wid] = x;
   __syncthreads();
+  // sparse problems (tc_sparse.cu): layer 1 only, every bin (layers >= 2 are
+  // the epilogue's correction entries)
+  const bool sparse = spmode && spmode[q] != 0;
   if (tid == 0) {
     uint32_t nd = 0;
     while (nd < 32 && 2 * warp_cnt[nd] >= (uint32_t)bins && warp_cnt[nd] > 0) ++nd;
+    if (sparse) nd = 1;
     uint32_t pos = nd * (uint32_t)dw;
     for (int w = 0; w < 32; ++w) {
       warp_pos[w] = w < (int)nd ? (uint32_t)w * dw : pos;
-      if (w >= (int)nd) pos += warp_cnt[w];
+      if (w >= (int)nd && !sparse) pos += warp_cnt[w];
     }
     s_total = pos;
     s_nd = nd;
@@ -345,7 +426,7 @@ tc_select_kernel(const __grid_constant__ TcSel sel, const uint32_t* __restrict__
   if (tid == 0 && cols_out && sel.first + q < SA_TC_COLS_MAX) cols_out[sel.first + q] = total;
   const uint32_t kpad = max((uint32_t)kbc, (total + kbc - 1u) / kbc * kbc);   // kbc columns per K block
   const bool too_many = kpad > (uint32_t)TC_KCAP;
-  const bool deep = reinterpret_cast<const volatile uint32_t*>(state)[0] > (uint32_t)TC_LCAP;
+  const bool deep = !sparse && reinterpret_cast<const volatile uint32_t*>(state)[0] > (uint32_t)TC_LCAP;
   if (too_many || deep) {
     if (tid == 0) {
       atomicOr(&state[1], 1u);
@@ -358,7 +439,7 @@ tc_select_kernel(const __grid_constant__ TcSel sel, const uint32_t* __restrict__
   const uint32_t layer = (uint32_t)wid + 1u;
   if ((uint32_t)wid < nd) {
     for (int t = lane; t < dw; t += 32) out[wid * dw + t] = t < bins ? ((uint32_t)t | (layer << 16)) : 0u;
-  } else {
+  } else if (!sparse) {
     uint32_t pos = warp_pos[wid] + x - cnt;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
@@ -400,16 +481,16 @@ template <bool FP4>
 __global__ void __launch_bounds__(256)
 tc_dense_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut O, int stride16, int bins,
                 const int32_t* __restrict__ ndense, const uint32_t* __restrict__ state,
-                const int32_t* __restrict__ carry_nd, int carry_np) {
+                const int32_t* __restrict__ carry_nd, int carry_np, int spec, int carry_spec) {
   constexpr int64_t ROWB = FP4 ? TC_KCAP / 2 : TC_KCAP;
   if (tc_infeasible(state)) return;
   int ndmax = 0;   // no problem keeps more dense layers than the histogram pass wrote: nothing to do
   for (int q = 0; q < TcOutProbs(O, S.n); ++q) ndmax = max(ndmax, ndense[q]);
-  // a carried side 0 (TcCarry) holds the layers below min(TC_SPEC, nd of every
+  // a carried side 0 (TcCarry) holds the layers below min(its spec, nd of every
   // problem of the launch that built it): its build overwrote the rest
-  int cfrom = TC_SPEC;
+  int cfrom = carry_spec;
   for (int q = 0; q < carry_np; ++q) cfrom = min(cfrom, carry_nd[q]);
-  if (ndmax <= TC_SPEC && !(carry_np > 0 && cfrom < ndense[O.prob[0]])) return;
+  if (ndmax <= spec && !(carry_np > 0 && cfrom < ndense[O.prob[0]])) return;
   const int dwc = ((bins + 15) & ~15) / 16;
   const int64_t items = S.row_begin[S.n] * dwc;
   for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items;
@@ -423,14 +504,14 @@ tc_dense_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut
       else hi = mid - 1;
     }
     const int nd = ndense[O.prob[lo]];
-    const int lfrom = (carry_np > 0 && lo == 0) ? cfrom : TC_SPEC;
+    const int lfrom = (carry_np > 0 && lo == 0) ? cfrom : spec;
     if (nd <= lfrom) continue;
     const int64_t r = g - S.row_begin[lo];
     const uint4* src = reinterpret_cast<const uint4*>(S.rows[lo] + r * (int64_t)stride16 + c * 16);
     const uint4 v0 = src[0], v1 = src[1];
     const uint32_t vs[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
     uint8_t* rowp = O.out[lo] + r * ROWB;
-    for (int l = lfrom; l < nd; ++l) {   // layers 1 .. TC_SPEC: written by tc_hist_kernel
+    for (int l = lfrom; l < nd; ++l) {   // layers 1 .. spec: written by tc_hist_kernel
       const uint32_t bias = (0x8000u - (uint32_t)(l + 1)) * 0x00010001u;
       uint32_t o[4];
 #pragma unroll
@@ -542,6 +623,14 @@ struct TcEpiProb {
   double delta, ln1pd;
   int32_t form;
   int32_t sym;
+  // sparse layers >= 2 (tc_sparse.cuh): the correction entries of key
+  // (row, column block) are ents[koff[key] .. koff[key + 1]), sorted by
+  // column, kpart[key] = their count per epilogue slice; koff / kpart point at
+  // this problem's keys (nullptr: no entries)
+  const uint32_t* koff;
+  const uint32_t* kpart;
+  const uint32_t* ents;
+  int32_t tn, slice, bn;
 };
 
 // Output matrices are written once and never re-read by the kernel: streaming
@@ -638,6 +727,8 @@ struct KeyMatEpi {
   struct State {
     uint64_t lo;      // row key, 96 bits
     uint32_t hi;
+    uint32_t q0, q1, q2, q3;   // the next correction entries of this thread's (row, slice), column order
+    uint32_t ep, ee;           // further entries: ents[ep .. ee)
     int nk;           // nk' of the row (sentinel -1: no row or nk = 0)
     int nk0;          // nk of the row (0 if none): the diagonal numerator C_ii
     int row_g;
@@ -667,6 +758,25 @@ struct KeyMatEpi {
       s.y = yd.x;
       s.d = yd.y;
     }
+    // correction entries of (row, column block, slice): the first four in
+    // registers (independent loads, issued before the accumulator wait)
+    s.ep = s.ee = 0;
+    s.q0 = s.q1 = s.q2 = s.q3 = 0xFFFFFFFFu;
+    if (E.koff && s.rv) {
+      const int64_t key = (int64_t)s.row_g * E.tn + T.col0 / E.bn;
+      const uint32_t kb = __ldg(E.koff + key), ke = __ldg(E.koff + key + 1), pc = __ldg(E.kpart + key);
+      const uint32_t part = (uint32_t)(cbeg / E.slice);
+      const uint32_t before = part == 0 ? 0u : __vsadu4(pc & ((1u << (8 * part)) - 1u), 0u);   // slices < part
+      const uint32_t avail = ke - kb;
+      const uint32_t n = before < avail ? min((pc >> (8 * part)) & 0xffu, avail - before) : 0u;
+      const uint32_t b = kb + before, e = b + n;
+      if (n > 0) s.q0 = __ldg(E.ents + b);
+      if (n > 1) s.q1 = __ldg(E.ents + b + 1);
+      if (n > 2) s.q2 = __ldg(E.ents + b + 2);
+      if (n > 3) s.q3 = __ldg(E.ents + b + 3);
+      s.ep = b + min(n, 4u);
+      s.ee = e;
+    }
     if constexpr (KEYS || SIM) {
       for (int c = cbeg + lane; c < cend; c += 32) {
         const bool cv = c < T.rb;
@@ -679,6 +789,28 @@ struct KeyMatEpi {
       }
     }
     __syncwarp();
+  }
+
+  // Layers >= 2 of the chunk's pairs (tc_sparse.cu): add the entries whose
+  // column falls in [col, col + CW) to the accumulator values.  Warp-uniform
+  // loop: one pass per entry depth any lane still has in the chunk (usually
+  // none or one); a pass applies each lane's head entry with a predicated add
+  // per column (no dynamic register indexing) and pops it.
+  template <int CW>
+  __device__ __forceinline__ void correct(State& s, int col, uint32_t (&v)[CW]) const {
+    const uint32_t lim = (uint32_t)(col + CW) << 16;
+    while (__any_sync(0xffffffffu, s.q0 < lim)) {
+      if (s.q0 < lim) {
+        const uint32_t jj = (s.q0 >> 16) - (uint32_t)col, d = s.q0 & 0xffffu;
+#pragma unroll
+        for (int j = 0; j < CW; ++j) v[j] += jj == (uint32_t)j ? d : 0u;
+        s.q0 = s.q1;
+        s.q1 = s.q2;
+        s.q2 = s.q3;
+        s.q3 = s.ep < s.ee ? __ldg(e[0].ents + s.ep) : 0xFFFFFFFFu;
+        s.ep += s.ep < s.ee ? 1u : 0u;
+      }
+    }
   }
 
   // F = C / D (reading Z19, division-free) with D = min(nk'_row, nk'_col)
@@ -1151,6 +1283,41 @@ static sa_status tc_encode_map(CUtensorMap* m, const uint8_t* base, int64_t rows
 }
 
 
+// Epilogue geometry of a launch's MODE (mirrors tc_gemm_mode): epilogue warps
+// and chunk width -> the column slice each warp owns (the sparse entries are
+// keyed by it).
+struct EpiGeo {
+  int ew, cw;
+};
+static EpiGeo epi_geo(int mode, int keysw, int matsw, bool fp4, bool pairs) {
+  const int cw_all = fp4 ? 16 : 32;
+  if (mode == EPI_KEYS) return keysw == 16 ? EpiGeo{16, 16} : keysw == 12 ? EpiGeo{12, 16} : EpiGeo{8, cw_all};
+  if (mode == EPI_NUM || mode == EPI_SIM) return {16, 16};
+  if ((mode & EPI_KEYS) == 0) {
+    if ((matsw == 20 || matsw == 12) && pairs) return {matsw, 16};
+    return matsw != 8 ? EpiGeo{16, 16} : EpiGeo{8, 16};
+  }
+  return {8, cw_all};
+}
+
+// Sparse layers >= 2 (tc_sparse.cu): SA_K2T_SPARSE=0 disables them (every
+// problem keeps its layers >= 2 as MMA columns, round-1 behaviour);
+// SA_K2T_SPARSE_BUDGET = b: a problem goes sparse when its correction terms
+// number at most pairs / b (default 8).
+// SA_K2T_SPARSE=2 forces it (tests): every problem whose terms fit a large
+// buffer (64 per pair, at most 2^28 in all) goes sparse.
+static int sparse_setting() {
+  const char* e = getenv("SA_K2T_SPARSE");
+  return e ? atoi(e) : 1;
+}
+static bool sparse_enabled() { return sparse_setting() != 0; }
+static int sparse_budget() {
+  const char* e = getenv("SA_K2T_SPARSE_BUDGET");
+  const int b = e ? atoi(e) : 8;
+  return b >= 1 ? b : 8;
+}
+constexpr int SP_REC_PER_ROW = 48;   // record budget per row (overflow: the launch stays dense)
+
 sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t bins, uint32_t* state,
                     uint32_t* cols_out, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1, TcCarry* keep,
                     const TcCarry* use) {
@@ -1174,10 +1341,32 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
   g_last_fp4.store(fp4 ? 1 : 0);
   const int64_t rowb = fp4 ? TC_KCAP / 2 : TC_KCAP;
   const int kbc = fp4 ? 256 : 128;
+  const int BN = fp4 ? tc::Geo<true>::BN : tc::Geo<false>::BN;
   static const bool fpass = [] {
     const char* e = getenv("SA_K2T_FPASS");
     return e && atoi(e) != 0;
   }();
+  static const int debug = [] {   // SA_K2T_DEBUG: component switches for experiments (tc_gemm.cuh, KeyMatEpi)
+    const char* e = getenv("SA_K2T_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  // epilogue warps (16 for keys: with layer 1 alone the key epilogue, not the
+  // MMA, bounds S2a / S2d, and more warps hide its latency -- config 4:
+  // S2a GEMM 3.16 / 2.67 / 2.60 ms with 8 / 12 / 16; 12 for the matrices on
+  // CTA pairs), read per launch
+  const int keysw = [] {
+    const char* e = getenv("SA_K2T_KEYSW");
+    const int w = e ? atoi(e) : 16;
+    return w == 8 || w == 12 ? w : 16;
+  }();
+  const int matsw = [] {
+    const char* e = getenv("SA_K2T_MATSW");
+    const int w = e ? atoi(e) : 12;   // CTA pairs: 12 (one CTA: 12 is not built, 16 runs)
+    return w == 8 || w == 12 || w == 20 ? w : 16;
+  }();
+  const bool sp_on = sparse_enabled() && bins <= SP_BINS;
+  const int spec = sp_on ? 1 : TC_SPEC_MAX;   // dense layers the histogram pass writes
+  const int budget = sparse_budget();
   std::vector<MsProblem> probs;
   for (const auto& p : probs_in)
     if (p.na > 0 && p.nb > 0) probs.push_back(p);
@@ -1208,6 +1397,23 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       sel.side_b[q] = P.sym ? -1 : add_side(P.B, P.nb, q);
       if (!P.sym) sides_nk.nk[sel.side_b[q]] = P.nkB;
     }
+    // the epilogue MODE of this launch (keys and F in one launch would need
+    // both column tables: F then goes through the F pass -- numerators in the
+    // epilogue, ratio_kernel after) and its geometry
+    bool any_keys = false;
+    for (int q = 0; q < np; ++q) any_keys = any_keys || probs[i0 + q].keyA;
+    const bool fpass_here = fpass || any_keys;
+    int mode = 0;
+    bool all_sym = true;
+    for (int q = 0; q < np; ++q) {
+      const MsProblem& P = probs[i0 + q];
+      mode |= (P.keyA ? EPI_KEYS : 0) | ((P.num || (fpass_here && P.sim)) ? EPI_NUM : 0) |
+              ((!fpass_here && P.sim) ? EPI_SIM : 0);
+      all_sym = all_sym && P.sym;
+    }
+    const EpiGeo geo = epi_geo(mode, keysw, matsw, fp4, pairs);
+    const int slice = tc::slice_of(geo.ew, geo.cw, fp4);
+
     SA_ALLOC(planes, uint32_t, (size_t)sides.n * 2 * TC_PLANE);
     SA_ALLOC(collist, uint32_t, (size_t)np * TC_KCAP);
     SA_ALLOC(kblocks, int32_t, np);
@@ -1224,6 +1430,7 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     bool keeping = keep && keep->scratch && i0 == 0 && probs.size() <= (size_t)tc::MAXPROB;
     for (int sd = 1; keeping && sd < sides.n; ++sd)
       keeping = sides.rows[sd] == sides.rows[0] + (sides.row_begin[sd] - sides.row_begin[0]) * (int64_t)stride16;
+    Scratch* kscr = keeping ? keep->scratch : &scratch;   // where the carried state lives
     uint8_t* side_out[2 * tc::MAXPROB];
     uint8_t* kept = keeping ? keep->scratch->alloc<uint8_t>((size_t)R * rowb) : nullptr;
     if (keeping && !kept) return fail(SA_E_NOMEM, "scratch allocation of K2T operand rows failed");
@@ -1243,16 +1450,58 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     TcMasks mk{};
     mk.split = hfrom;
     mk.carried = carried ? use->masks : nullptr;
-    mk.own = (kept ? keep->scratch : &scratch)->alloc<uint32_t>((size_t)(R - hfrom) * TC_MROW);
+    mk.own = kscr->alloc<uint32_t>((size_t)(R - hfrom) * TC_MROW);
     if (!mk.own) return fail(SA_E_NOMEM, "scratch allocation of K2T layer masks failed");
     const int hx = (int)std::max<int64_t>(
         1, std::min<int64_t>((R - hfrom + TC_HIST_ROWS - 1) / TC_HIST_ROWS, 4 * g_num_sms));
     const int hsm = 2 * (TC_LCAP - TC_HREG) * TC_WPL * 4;
+    // sparse-layer records: per hist CTA a segment, then one dense array (after
+    // the carried launch's records, when there are any)
+    TcRecOut ro{};
+    SpBuffers spb;
+    uint32_t rec_cap = 0;
+    if (sp_on) {
+      const int64_t per_cta = (R - hfrom + hx - 1) / hx;
+      const int rec_per_row = sparse_setting() == 2 ? 8 * SP_REC_PER_ROW : SP_REC_PER_ROW;
+      ro.seg_cap = (uint32_t)(per_cta * rec_per_row + 64);
+      ro.seg = scratch.alloc<uint2>((size_t)hx * ro.seg_cap);
+      ro.cnt = scratch.alloc<uint32_t>(hx);
+      ro.on = 1;
+      const int64_t cap64 = (int64_t)hx * ro.seg_cap + (carried && use->recs ? use->rec_cap : 0);
+      rec_cap = (uint32_t)std::min<int64_t>(cap64, (int64_t)1 << 31);
+      spb.recs = kscr->alloc<uint2>(rec_cap);
+      spb.nrec = kscr->alloc<uint32_t>(4);   // [0] records, [2] incomplete (some segment overflowed)
+      spb.povf = scratch.alloc<uint32_t>(tc::MAXPROB);
+      ro.povf = spb.povf;
+      ro.incomplete = spb.nrec + 2;
+      if (!ro.seg || !ro.cnt || !spb.recs || !spb.nrec || !spb.povf)
+        return fail(SA_E_NOMEM, "scratch allocation of K2T sparse records failed");
+      SA_CUDA(cudaMemsetAsync(spb.nrec, 0, 4 * sizeof(uint32_t), st));
+      SA_CUDA(cudaMemsetAsync(spb.povf, 0, tc::MAXPROB * sizeof(uint32_t), st));
+      if (carried && use->recs) SA_TRY(sp_copy_records(use->recs, use->nrec, use->rec_cap, spb.recs, spb.nrec + 1,
+                                                       g_num_sms, st));
+    }
     if (fp4)
-      tc_hist_kernel<true><<<hx, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, hfrom, mk);
+      tc_hist_kernel<true><<<hx, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, hfrom, mk,
+                                                             spec, ro);
     else
-      tc_hist_kernel<false><<<hx, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, hfrom, mk);
+      tc_hist_kernel<false><<<hx, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, hfrom, mk,
+                                                              spec, ro);
     SA_LAUNCHED();
+    if (sp_on) {
+      // a carried side without records (its launch ran with sparse layers off) cannot go sparse
+      const bool carry_ok = !carried || use->recs;
+      TcRecOvf ov{};
+      ov.carried_prob = outs.prob[0];
+      ov.povf = spb.povf;
+      tc_rec_compact_kernel<<<hx, 256, 0, st>>>(ro.seg, ro.cnt, hx, ro.seg_cap, spb.recs, rec_cap, spb.nrec,
+                                                 carried ? spb.nrec + 1 : nullptr, ov);
+      SA_LAUNCHED();
+      if (!carry_ok) {   // carried rows without records (their launch ran with sparse layers off): dense
+        SA_CUDA(cudaMemsetAsync(spb.povf, 0xFF, tc::MAXPROB * sizeof(uint32_t), st));
+        SA_CUDA(cudaMemsetAsync(spb.nrec + 2, 0xFF, sizeof(uint32_t), st));
+      }
+    }
     if (kept) {
       uint32_t* s1 = keep->scratch->alloc<uint32_t>(TC_PLANE);
       if (!s1) return fail(SA_E_NOMEM, "scratch allocation of K2T planes failed");
@@ -1267,8 +1516,76 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       keep->ndense = ndense;
       keep->np = np;
       keep->masks = mk.own;
+      keep->spec = spec;
+      keep->recs = sp_on ? spb.recs : nullptr;
+      keep->nrec = sp_on ? spb.nrec : nullptr;
+      keep->rec_cap = rec_cap;
     }
-    tc_select_kernel<<<np, 1024, 0, st>>>(sel, planes, bins, kbc, collist, kblocks, ndense, state, cols_out);
+    // plan of the sparse layers: which problems take them (device-decided)
+    SpLaunch L{};
+    if (sp_on) {
+      for (int sd = 0; sd <= sides.n; ++sd) L.row_begin[sd] = sides.row_begin[sd];
+      L.nsides = sides.n;
+      L.nprob = np;
+      uint64_t kb = 0, ecap = 0;
+      int64_t na_all = 0;
+      for (int q = 0; q < np; ++q) {
+        const MsProblem& P = probs[i0 + q];
+        L.side_a[q] = sel.side_a[q];
+        L.side_b[q] = sel.side_b[q];
+        L.tn[q] = (int32_t)((P.nb + BN - 1) / BN);
+        L.key_base[q] = kb;
+        L.abase[q] = na_all;
+        na_all += P.na;
+        kb += (uint64_t)P.na * L.tn[q];
+        const uint64_t npair = P.sym ? (uint64_t)P.na * (P.na - 1) / 2 : (uint64_t)P.na * P.nb;
+        L.cap[q] = sparse_setting() == 2 ? std::min<uint64_t>(npair * 64, (uint64_t)1 << 28) : npair / budget;
+        ecap += L.cap[q];
+      }
+      L.key_base[np] = kb;
+      L.abase[np] = na_all;
+      L.nkeys = (int64_t)kb;
+      L.bn = BN;
+      L.slice = slice;
+      L.rec_cap = rec_cap;
+      // kpart packs one 8-bit count per epilogue slice: at most 4 slices (the
+      // 20-warp experiment geometry has 5 and stays dense)
+      L.enabled = ecap < ((uint64_t)1 << 32) && kb < ((uint64_t)1 << 32) && (BN + slice - 1) / slice <= 4 ? 1 : 0;
+      L.terms_out = (sel.first + np <= SA_TC_COLS_MAX && cols_out)
+                        ? reinterpret_cast<unsigned long long*>(state + SA_TC_TERMS_AT) + sel.first
+                        : nullptr;
+      spb.bincnt = scratch.alloc<uint32_t>((size_t)sides.n * SP_BINS);
+      spb.binoff = scratch.alloc<uint32_t>((size_t)sides.n * SP_BSTRIDE);
+      spb.sidebase = scratch.alloc<uint32_t>(sides.n);
+      spb.blist = scratch.alloc<uint2>(rec_cap);
+      spb.sorted = scratch.alloc<uint2>(rec_cap);
+      spb.rcnt = scratch.alloc<uint32_t>((size_t)R);
+      spb.rstart = scratch.alloc<uint32_t>((size_t)R + 1);
+      spb.rlist = scratch.alloc<uint32_t>(rec_cap);
+      spb.mode = scratch.alloc<int32_t>(np);
+      spb.flags = scratch.alloc<uint32_t>(4);
+      spb.rowcnt = scratch.alloc<uint32_t>((size_t)na_all);
+      spb.rowoff = scratch.alloc<uint32_t>((size_t)na_all + 1);
+      spb.koff = scratch.alloc<uint32_t>((size_t)kb + 1);
+      spb.kpart = scratch.alloc<uint32_t>((size_t)kb + 1);
+      spb.scan_tmp = scratch.alloc<uint32_t>((size_t)(std::max<int64_t>(R, na_all) / 4096) + 2);
+      spb.ents = scratch.alloc<uint32_t>((size_t)std::max<uint64_t>(ecap, 1));
+      if (!spb.bincnt || !spb.binoff || !spb.sidebase || !spb.blist || !spb.sorted || !spb.rcnt || !spb.rstart ||
+          !spb.rlist || !spb.mode || !spb.flags || !spb.rowcnt || !spb.rowoff || !spb.koff || !spb.kpart ||
+          !spb.scan_tmp || !spb.ents)
+        return fail(SA_E_NOMEM, "scratch allocation of K2T sparse-layer buffers failed");
+      SA_CUDA(cudaMemsetAsync(spb.bincnt, 0, (size_t)sides.n * SP_BINS * 4, st));
+      SA_CUDA(cudaMemsetAsync(spb.flags, 0, 16, st));
+      SA_CUDA(cudaMemsetAsync(spb.sidebase, 0, (size_t)sides.n * 4, st));
+      SA_CUDA(cudaMemsetAsync(spb.rcnt, 0, (size_t)R * 4, st));
+      SA_TRY(sp_build(L, spb, g_num_sms, st));
+      if (cols_out && sel.first + np <= SA_TC_COLS_MAX)
+        SA_CUDA(cudaMemcpyAsync(state + SA_TC_MODE_AT + sel.first, spb.mode, np * 4, cudaMemcpyDeviceToDevice, st));
+    } else if (cols_out && sel.first + np <= SA_TC_COLS_MAX) {
+      SA_CUDA(cudaMemsetAsync(state + SA_TC_MODE_AT + sel.first, 0, np * 4, st));
+    }
+    tc_select_kernel<<<np, 1024, 0, st>>>(sel, planes, bins, kbc, collist, kblocks, ndense, state, cols_out,
+                                          sp_on ? spb.mode : nullptr);
     SA_LAUNCHED();
     uint4* kinfo = scratch.alloc<uint4>((size_t)R);
     double2* yinfo = scratch.alloc<double2>((size_t)R);
@@ -1279,44 +1596,36 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     const int bx = (int)std::max<int64_t>(1, std::min<int64_t>(R, 4 * g_num_sms));
     const int32_t* cnd = carried ? use->ndense : nullptr;
     const int cnp = carried ? use->np : 0;
+    const int cspec = carried ? use->spec : spec;
     if (fp4) {
-      tc_dense_kernel<true><<<8 * g_num_sms, 256, 0, st>>>(sides, outs, stride16, bins, ndense, state, cnd, cnp);
+      tc_dense_kernel<true><<<8 * g_num_sms, 256, 0, st>>>(sides, outs, stride16, bins, ndense, state, cnd, cnp, spec,
+                                                           cspec);
       SA_LAUNCHED();
       tc_build_kernel<true><<<bx, TC_BUILD_THREADS, 0, st>>>(sides, outs, stride16, bins, collist, kblocks, ndense,
                                                              state, mk);
     } else {
-      tc_dense_kernel<false><<<8 * g_num_sms, 256, 0, st>>>(sides, outs, stride16, bins, ndense, state, cnd, cnp);
+      tc_dense_kernel<false><<<8 * g_num_sms, 256, 0, st>>>(sides, outs, stride16, bins, ndense, state, cnd, cnp, spec,
+                                                            cspec);
       SA_LAUNCHED();
       tc_build_kernel<false><<<bx, TC_BUILD_THREADS, 0, st>>>(sides, outs, stride16, bins, collist, kblocks, ndense,
                                                               state, mk);
     }
     SA_LAUNCHED();
+    if (sp_on) SA_TRY(sp_entries(L, spb, g_num_sms, st));
     // GEMM
     tc::Batch batch{};
     tc::Maps maps;
     std::memset(&maps, 0, sizeof maps);
-    static const int debug = [] {   // SA_K2T_DEBUG: component switches for experiments (tc_gemm.cuh, KeyMatEpi)
-      const char* e = getenv("SA_K2T_DEBUG");
-      return e ? atoi(e) : 0;
-    }();
     KeyMatEpi<EPI_ALL> epi{};
-    int mode = 0;
-    bool all_sym = true;
     epi.state = state;
     epi.dbg = debug;
     int64_t tiles = 0;
-    // keys and F in one launch would need both column tables: F then goes
-    // through the F pass (numerators in the epilogue, ratio_kernel after)
-    bool any_keys = false;
-    for (int q = 0; q < np; ++q) any_keys = any_keys || probs[i0 + q].keyA;
-    const bool fpass_here = fpass || any_keys;
     for (int q = 0; q < np; ++q) {
       const MsProblem& P = probs[i0 + q];
       tc::Problem& T = batch.p[q];
       T.na = P.na;
       T.nb = P.nb;
       T.sym = P.sym;
-      const int BN = fp4 ? tc::Geo<true>::BN : tc::Geo<false>::BN;
       T.tiles_n = (P.nb + BN - 1) / BN;
       T.tile_begin = tiles;
       T.kblocks = kblocks + q;
@@ -1357,8 +1666,14 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       E.delta = P.delta;
       E.ln1pd = P.ln1pd;
       E.sym = P.sym;
-      mode |= (P.keyA ? EPI_KEYS : 0) | (E.num ? EPI_NUM : 0) | (E.sim ? EPI_SIM : 0);
-      all_sym = all_sym && P.sym;
+      if (sp_on) {
+        E.koff = spb.koff + L.key_base[q];
+        E.kpart = spb.kpart + L.key_base[q];
+        E.ents = spb.ents;
+        E.tn = L.tn[q];
+        E.slice = slice;
+        E.bn = BN;
+      }
     }
     // every problem of the launch gets every output its MODE writes (the
     // epilogue's fast paths test no pointer): scratch for a problem that did
@@ -1402,23 +1717,7 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     batch.evict_last = evict_last;
     batch.debug = debug;
     const int64_t grid = pairs ? 2 * std::min<int64_t>(tiles, g_num_sms / 2) : std::min<int64_t>(tiles, g_num_sms);
-    // 16 epilogue warps x 16-column chunks (more warps to hide the store / F /
-    // key-term latency, fewer registers each); keys and matrices together
-    // (a rank call that also wants numerators) use 8 warps x 32 columns
-    // epilogue warps (16 or 8) of the key and matrix instantiations (read per launch)
-    // (8 key warps: fewer epilogue warps competing with the MMA / TMA warps for
-    // issue slots; the matrix epilogue needs its 16 to keep up with the stores)
-    const int keysw = [] {
-      const char* e = getenv("SA_K2T_KEYSW");
-      const int w = e ? atoi(e) : 8;
-      return w == 12 || w == 16 ? w : 8;
-    }();
-    const int matsw = [] {
-      const char* e = getenv("SA_K2T_MATSW");
-      const int w = e ? atoi(e) : 12;   // CTA pairs: 12 (one CTA: 12 is not built, 16 runs)
-      return w == 8 || w == 12 || w == 20 ? w : 16;
-    }();
-    if (ev0) SA_CUDA(cudaEventRecord(ev0, st));   // the GEMM kernel alone (SA_PHASE_GEMM)
+    if (ev0) SA_CUDA(cudaEventRecord(ev0, st));   // the GEMM kernel alone (SA_PHASE_GEMM*)
     if (pairs) {
       if (fp4) tc_gemm_mode<true, 2>(mode, keysw, matsw, grid, batch, maps, tiles, epi, st);
       else tc_gemm_mode<false, 2>(mode, keysw, matsw, grid, batch, maps, tiles, epi, st);

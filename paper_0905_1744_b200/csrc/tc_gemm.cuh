@@ -328,6 +328,8 @@ __device__ __forceinline__ Tile decode(const Batch& b, int64_t tile) {
 //                         uint8_t* tab) const;                       // before the accumulator wait
 //   template <int CW, bool FP4, int CG> __device__ void chunk(State&, const Tile&, int row, int col, const uint32_t (&v)[CW],
 //                         int lane, const uint8_t* tab, int tj, uint8_t* xp) const;   // all lanes, converged
+//   template <int CW> __device__ void correct(State&, int col, uint32_t (&v)[CW]) const;   // adjust the
+//                         accumulator chunk before chunk() (sparse layers, tc_sparse.cu), all lanes converged
 //   __device__ void end(State&, const Tile&, int row) const;
 // row = tile row of this thread (0..127), [cbeg, cend) = the warp's column
 // slice of the tile, col = first tile column of the chunk, tab = the warp's
@@ -467,6 +469,7 @@ gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps ma
 #pragma unroll
           for (int j = 0; j < CW; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + 8388608.0f) & 0x7FFFFFu;
         }
+        epi.template correct<CW>(es, col, v);
         epi.template chunk<CW, FP4, 1>(es, T, row, col, v, lane, tab, col - cbeg, xp);
       }
       fence_before();
@@ -779,6 +782,7 @@ gemm2_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps m
 #pragma unroll
           for (int j = 0; j < CW; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + 8388608.0f) & 0x7FFFFFu;
         }
+        epi.template correct<CW>(es, col, v);
         epi.template chunk<CW, FP4, 2>(es, T, row, col, v, lane, tab, col - cbeg, xp);
       }
       fence_before();

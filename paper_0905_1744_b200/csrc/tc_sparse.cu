@@ -12,17 +12,20 @@
 // rows that both repeat t contributes min(c_i, c_j) - 1.  This file builds, per
 // launch and on the device:
 //
-//   records   (row, bin, count) for every count >= 2 (appended by the histogram
-//             pass, minsum_tc.cu)
-//   bin lists per side: the rows repeating each bin (count + scan + scatter)
+//   records   (row, bin, count) for every count >= 2, appended by the histogram
+//             pass (minsum_tc.cu)
 //   plan      per problem: E = the number of (pair, bin) terms, exactly
 //             sum_t n_t (n_t - 1) / 2 (symmetric) or sum_t nA_t nB_t; the
 //             problem runs SPARSE (tensor cores on layer 1 only) iff E fits
 //             its entry budget, else DENSE (layers >= 2 as MMA columns)
-//   entries   one u32 per term, (column within the tile's column block << 16 |
-//             min - 1), grouped by key = (row, column block, epilogue slice)
-//             -- exactly the set of pairs one epilogue thread owns in one tile
-//             -- sorted by column, duplicates of a pair merged
+//   bin lists per side: the rows repeating each bin, sorted by row
+//   row lists the records of each row
+//   entries   per row a of a problem's A side, a k-way merge (by partner row)
+//             of the bin lists of a's repeated bins (partners b > a when
+//             symmetric): one u32 per partner, (column within the tile's
+//             column block << 16 | sum of min - 1 over the shared bins),
+//             ordered by partner; koff / kpart index them by key (a, column
+//             block) -- the pairs one epilogue thread owns in one tile
 //
 // The GEMM epilogue (KeyMatEpi::correct) adds the entries to its accumulator
 // chunk before computing keys or F, so every downstream value sees the exact C.
@@ -36,23 +39,34 @@ __device__ __forceinline__ int sp_side_of(const SpLaunch& L, int64_t g) {
   while (s + 1 < L.nsides && L.row_begin[s + 1] <= g) ++s;
   return s;
 }
+__device__ __forceinline__ uint32_t sp_nrec(const SpLaunch& L, const uint32_t* nrec) {
+  return min(*nrec, L.rec_cap);   // records of overflowed segments are partial: their problems run dense
+}
 
-// ---------------------------------------------------------- bin counts ----
+// --------------------------------------------- bin counts, row counts ----
 __global__ void sp_bincount_kernel(const SpLaunch L, const uint2* __restrict__ recs, const uint32_t* __restrict__ nrec,
-                                   uint32_t* __restrict__ bincnt) {
-  const uint32_t n = min(*nrec, L.rec_cap);
+                                   uint32_t* __restrict__ bincnt, uint32_t* __restrict__ sidetot,
+                                   uint32_t* __restrict__ rcnt) {
+  __shared__ uint32_t st[2 * tc::MAXPROB];
+  if (threadIdx.x < 2 * tc::MAXPROB) st[threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t n = sp_nrec(L, nrec);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint2 r = recs[i];
     const int s = sp_side_of(L, r.x);
     atomicAdd(&bincnt[s * SP_BINS + (r.y & 0xffffu)], 1u);
+    atomicAdd(&rcnt[r.x], 1u);
+    atomicAdd(&st[s], 1u);
   }
+  __syncthreads();
+  if (threadIdx.x < L.nsides && st[threadIdx.x]) atomicAdd(&sidetot[threadIdx.x], st[threadIdx.x]);
 }
 
 // ------------------------------------------------------------- planning --
 // One CTA per problem: E = number of correction terms; sparse iff E <= cap and
-// the record buffer did not overflow.  flags[0] |= 1 when any problem is sparse.
+// none of its rows' record segments overflowed (povf).  flags[0] |= 1 when any problem is sparse.
 __global__ void __launch_bounds__(1024) sp_plan_kernel(const SpLaunch L, const uint32_t* __restrict__ bincnt,
-                                                       const uint32_t* __restrict__ nrec, int32_t* __restrict__ mode,
+                                                       const uint32_t* __restrict__ povf, int32_t* __restrict__ mode,
                                                        uint32_t* __restrict__ flags) {
   __shared__ unsigned long long part[32];
   const int q = blockIdx.x;
@@ -69,7 +83,7 @@ __global__ void __launch_bounds__(1024) sp_plan_kernel(const SpLaunch L, const u
   if (threadIdx.x == 0) {
     unsigned long long E = 0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) E += part[w];
-    const bool ok = L.enabled && *nrec <= L.rec_cap && E <= (unsigned long long)L.cap[q];
+    const bool ok = L.enabled && !povf[q] && E <= (unsigned long long)L.cap[q];
     mode[q] = ok ? 1 : 0;
     if (ok) atomicOr(&flags[0], 1u);
     if (L.terms_out) L.terms_out[q] = E;
@@ -77,12 +91,13 @@ __global__ void __launch_bounds__(1024) sp_plan_kernel(const SpLaunch L, const u
 }
 
 // --------------------------------------------------- bin lists (per side) --
-// One CTA per side: exclusive scan of its SP_BINS counts into binoff[side][t]
-// (bincnt keeps the counts: the scatter below consumes them with atomicSub).
+// One CTA per side: exclusive scan of its SP_BINS counts into
+// binoff[side][0..SP_BINS] (bincnt keeps the counts: the scatter below
+// consumes them with atomicSub).  Sides follow one another in the list array.
 __global__ void __launch_bounds__(1024) sp_binscan_kernel(const uint32_t* __restrict__ bincnt,
                                                           uint32_t* __restrict__ binoff,
                                                           const uint32_t* __restrict__ flags,
-                                                          const uint32_t* __restrict__ base_dev) {
+                                                          const uint32_t* __restrict__ sidetot) {
   if (!(flags[0] & 1u)) return;
   __shared__ uint32_t wsum[32];
   const int s = blockIdx.x;
@@ -113,9 +128,9 @@ __global__ void __launch_bounds__(1024) sp_binscan_kernel(const uint32_t* __rest
     wsum[lane] = z - y;
   }
   __syncthreads();
-  // sides are laid out one after another in the list array: side s starts
-  // after every record of sides < s (base_dev[s], from the side totals)
-  uint32_t run = base_dev[s] + wsum[w] + x - tot;
+  uint32_t sbase = 0;
+  for (int i = 0; i < s; ++i) sbase += sidetot[i];
+  uint32_t run = sbase + wsum[w] + x - tot;
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
     binoff[s * SP_BSTRIDE + threadIdx.x * PER + i] = run;
@@ -124,99 +139,375 @@ __global__ void __launch_bounds__(1024) sp_binscan_kernel(const uint32_t* __rest
   if (threadIdx.x == 1023) binoff[s * SP_BSTRIDE + SP_BINS] = run;   // the side's end
 }
 
-// side totals -> side bases (one thread; at most 2 * MAXPROB sides)
-__global__ void sp_sidebase_kernel(const SpLaunch L, const uint32_t* __restrict__ bincnt, uint32_t* __restrict__ base,
-                                   const uint32_t* __restrict__ flags) {
-  if (!(flags[0] & 1u)) return;
-  __shared__ uint32_t tot[2 * tc::MAXPROB];
-  const int s = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (s < L.nsides) {
-    uint32_t t = 0;
-    for (int b = lane; b < SP_BINS; b += 32) t += bincnt[s * SP_BINS + b];
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (lane == 0) tot[s] = t;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t run = 0;
-    for (int i = 0; i < L.nsides; ++i) {
-      base[i] = run;
-      run += tot[i];
-    }
-  }
-}
-
-// records -> bin lists: list entry = (row within its side, count)
+// records -> bin lists (entry = (row within its side, count)) and row lists
+// (entry = bin | count << 16); both in arbitrary order inside a list
 __global__ void sp_scatter_kernel(const SpLaunch L, const uint2* __restrict__ recs, const uint32_t* __restrict__ nrec,
                                   uint32_t* __restrict__ bincnt, const uint32_t* __restrict__ binoff,
-                                  uint2* __restrict__ blist, const uint32_t* __restrict__ flags) {
+                                  uint2* __restrict__ blist, uint32_t* __restrict__ rcnt,
+                                  const uint32_t* __restrict__ rstart, uint32_t* __restrict__ rlist,
+                                  const uint32_t* __restrict__ flags) {
   if (!(flags[0] & 1u)) return;
-  const uint32_t n = min(*nrec, L.rec_cap);
+  const uint32_t n = sp_nrec(L, nrec);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint2 r = recs[i];
     const int s = sp_side_of(L, r.x);
     const uint32_t bin = r.y & 0xffffu;
     const uint32_t pos = binoff[s * SP_BSTRIDE + bin] + atomicSub(&bincnt[s * SP_BINS + bin], 1u) - 1u;
     blist[pos] = make_uint2((uint32_t)(r.x - L.row_begin[s]), r.y >> 16);
+    rlist[rstart[r.x] + atomicSub(&rcnt[r.x], 1u) - 1u] = r.y;
   }
 }
 
-// -------------------------------------------------------------- pairs ----
-// One warp per (problem, bin) of the sparse problems.  FILL = false: count the
-// terms per key; FILL = true: write them (kcnt is consumed by atomicSub, so
-// the positions inside a key are arbitrary -- sp_sort_kernel orders them).
-// Rows in a list are in scatter order; a symmetric pair is (min, max).
-template <bool FILL>
-__global__ void __launch_bounds__(256) sp_pairs_kernel(const SpLaunch L, const uint32_t* __restrict__ binoff,
-                                                       const uint2* __restrict__ blist, const int32_t* __restrict__ mode,
-                                                       uint32_t* __restrict__ kcnt, const uint32_t* __restrict__ koff,
-                                                       uint32_t* __restrict__ ents, const uint32_t* __restrict__ flags) {
+// One warp per (side, bin) list: rank sort by row (rows are distinct inside a
+// list), out of place.  O(n^2 / 32) per list: the lists are short (a bin's
+// rows with count >= 2; ~15 on the config-4 buckets).
+__global__ void __launch_bounds__(256) sp_listsort_kernel(const SpLaunch L, const uint32_t* __restrict__ binoff,
+                                                          const uint2* __restrict__ blist, uint2* __restrict__ sorted,
+                                                          const uint32_t* __restrict__ flags) {
   if (!(flags[0] & 1u)) return;
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); item < (int64_t)L.nprob * SP_BINS;
+  for (int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); item < (int64_t)L.nsides * SP_BINS;
        item += nw) {
-    const int q = (int)(item / SP_BINS), t = (int)(item % SP_BINS);
-    if (!mode[q]) continue;
-    const int sa_ = L.side_a[q], sb = L.side_b[q];
-    const uint32_t a0 = binoff[sa_ * SP_BSTRIDE + t];
-    const uint32_t na = binoff[sa_ * SP_BSTRIDE + t + 1] - a0;
-    if (na == 0) continue;
-    const uint64_t key0 = L.key_base[q];
-    const uint32_t tn = (uint32_t)L.tn[q], np = (uint32_t)L.nparts, bn = (uint32_t)L.bn, sl = (uint32_t)L.slice;
-    uint32_t b0 = a0, nb = na;
-    if (sb >= 0) {
-      b0 = binoff[sb * SP_BSTRIDE + t];
-      nb = binoff[sb * SP_BSTRIDE + t + 1] - b0;
+    const int s = (int)(item / SP_BINS), t = (int)(item % SP_BINS);
+    const uint32_t b = binoff[s * SP_BSTRIDE + t], n = binoff[s * SP_BSTRIDE + t + 1] - b;
+    if (n == 0) continue;
+    if (n == 1) {
+      if (lane == 0) sorted[b] = blist[b];
+      continue;
     }
-    // lanes take rows x of side A; symmetric problems pair x with the later
-    // list entries only (each unordered pair once, as (min row, max row))
-    for (uint32_t x = lane; x < na; x += 32) {
-      const uint2 ex = blist[a0 + x];
-      for (uint32_t y = sb < 0 ? x + 1 : 0; y < nb; ++y) {
-        const uint2 ey = blist[b0 + y];
-        const uint32_t ra = sb < 0 ? min(ex.x, ey.x) : ex.x, rb = sb < 0 ? max(ex.x, ey.x) : ey.x;
-        const uint32_t jl = rb % bn;
-        const uint64_t key = key0 + ((uint64_t)ra * tn + rb / bn) * np + jl / sl;
-        if (FILL) {
-          const uint32_t pos = koff[key] + atomicSub(&kcnt[key], 1u) - 1u;
-          ents[pos] = (jl << 16) | (min(ex.y, ey.y) - 1u);
-        } else {
-          atomicAdd(&kcnt[key], 1u);
-        }
-      }
+    for (uint32_t i = lane; i < n; i += 32) {
+      const uint2 x = blist[b + i];
+      uint32_t rank = 0;
+      for (uint32_t j = 0; j < n; ++j) rank += blist[b + j].x < x.x ? 1u : 0u;
+      sorted[b + rank] = x;
     }
   }
 }
 
-// ----------------------------------------------------------- key scan ----
+// ------------------------------------------------------------ row merge --
+struct SpRow {
+  int q;          // problem
+  uint32_t r;     // row within the problem's A side
+  uint32_t g;     // row in the launch (flattened sides)
+};
+__device__ __forceinline__ SpRow sp_row_of(const SpLaunch& L, uint32_t ai) {
+  int q = 0;
+  while (q + 1 < L.nprob && (uint32_t)L.abase[q + 1] <= ai) ++q;
+  SpRow R;
+  R.q = q;
+  R.r = ai - (uint32_t)L.abase[q];
+  R.g = (uint32_t)L.row_begin[L.side_a[q]] + R.r;
+  return R;
+}
+// first position in the sorted list [b, e) whose row exceeds r
+__device__ __forceinline__ uint32_t sp_upper(const uint2* __restrict__ list, uint32_t b, uint32_t e, uint32_t r) {
+  while (b < e) {
+    const uint32_t m = (b + e) >> 1;
+    if (list[m].x <= r) b = m + 1;
+    else e = m;
+  }
+  return b;
+}
+
+// Terms of each A-side row (before merging the bins of one partner): one warp
+// per row, lanes over the row's records.
+constexpr int SP_FILL_WARPS = 4;
+__global__ void __launch_bounds__(32 * SP_FILL_WARPS) sp_rowcount_kernel(
+    const SpLaunch L, const int32_t* __restrict__ mode, const uint32_t* __restrict__ binoff,
+    const uint2* __restrict__ sorted, const uint32_t* __restrict__ rstart, const uint32_t* __restrict__ rlist,
+    uint32_t* __restrict__ rowcnt, const uint32_t* __restrict__ flags) {
+  const int lane = threadIdx.x & 31;
+  const bool any = (flags[0] & 1u) != 0;
+  const uint32_t NA = (uint32_t)L.abase[L.nprob];
+  const uint32_t nwarps = gridDim.x * SP_FILL_WARPS;
+  for (uint32_t ai = blockIdx.x * SP_FILL_WARPS + (threadIdx.x >> 5); ai < NA; ai += nwarps) {
+    const SpRow R = sp_row_of(L, ai);
+    uint32_t cnt = 0;
+    if (any && mode[R.q]) {
+      const bool sym = L.side_b[R.q] < 0;
+      const int ps = sym ? L.side_a[R.q] : L.side_b[R.q];
+      for (uint32_t i = rstart[R.g] + lane; i < rstart[R.g + 1]; i += 32) {
+        const uint32_t t = rlist[i] & 0xffffu;
+        const uint32_t b = binoff[ps * SP_BSTRIDE + t], e = binoff[ps * SP_BSTRIDE + t + 1];
+        cnt += e - (sym ? sp_upper(sorted, b, e, R.r) : b);
+      }
+      for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    }
+    if (lane == 0) rowcnt[ai] = cnt;
+  }
+}
+
+// Entries of each A-side row, one warp per row.  Raw terms (partner b,
+// min(c_a, c_b) - 1) come from the tails of the sorted lists of the row's
+// repeated bins (partners b > a when symmetric).  The entries are one u32 per
+// distinct partner, (column within its column block << 16 | summed term), in
+// partner order from rowoff[ai]; koff / kpart are written for every column
+// block J of the row (empty blocks: position, 0); slots left by partners that
+// share several bins hold SP_DEAD.  Two ways, by the row's raw term count:
+//   <= SP_ROWBUF (nearly every row): raw terms into a shared buffer, a warp
+//      bitonic sort by (b << 32 | term), one entry per run of equal b, and the
+//      block counts through a shared per-block counter array;
+//   larger (long, repetitive sequences): a sweep over the column blocks the
+//      partners fall in, each repeated bin a cursor kept in shared memory,
+//      terms added into a per-column shared accumulator per block.
+constexpr int SP_ROWBUF = 512;   // raw terms per warp buffer (power of two)
+constexpr int SP_TN_MAX = 1024;  // column blocks of the per-block counters (more: lower-bound keys)
+constexpr int SP_CURSORS = 128;   // cursor state of the sweep: 2.5 KB, inside the raw buffer
+constexpr int SP_BN_MAX = 256;   // column-block width (240 e2m1, 256 u8)
+
+__device__ __forceinline__ uint32_t sp_lower_b(const unsigned long long* buf, uint32_t n, uint32_t b) {
+  uint32_t lo = 0, hi = n;   // first i with (buf[i] >> 32) >= b
+  while (lo < hi) {
+    const uint32_t m = (lo + hi) >> 1;
+    if ((uint32_t)(buf[m] >> 32) < b) lo = m + 1;
+    else hi = m;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(32 * SP_FILL_WARPS) sp_rowfill_kernel(
+    const SpLaunch L, const int32_t* __restrict__ mode, const uint32_t* __restrict__ binoff,
+    const uint2* __restrict__ sorted, const uint32_t* __restrict__ rstart, const uint32_t* __restrict__ rlist,
+    const uint32_t* __restrict__ rowoff, uint32_t* __restrict__ ents, uint32_t* __restrict__ koff,
+    uint32_t* __restrict__ kpart, const uint32_t* __restrict__ flags) {
+  __shared__ unsigned long long s_buf[SP_FILL_WARPS][SP_ROWBUF];   // raw terms; cursors of the sweep
+  __shared__ uint32_t s_acc[SP_FILL_WARPS][SP_TN_MAX];             // per-block counters; sweep accumulator
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  unsigned long long* buf = s_buf[wib];
+  uint32_t* acc = s_acc[wib];
+  // the sweep's cursor state overlays the raw buffer (4 KB): position, end, own count, current partner
+  uint32_t* cur = reinterpret_cast<uint32_t*>(buf);
+  uint32_t* end = cur + SP_CURSORS;
+  uint32_t* own = end + SP_CURSORS;
+  uint2* val = reinterpret_cast<uint2*>(own + SP_CURSORS);
+  const bool any = (flags[0] & 1u) != 0;
+  const uint32_t bn = (uint32_t)L.bn, sl = (uint32_t)L.slice;
+  const uint32_t NA = (uint32_t)L.abase[L.nprob];
+  const uint32_t nwarps = gridDim.x * SP_FILL_WARPS;
+  for (uint32_t c = lane; c < SP_TN_MAX; c += 32) acc[c] = 0u;
+  __syncwarp();
+  for (uint32_t ai = blockIdx.x * SP_FILL_WARPS + wib; ai < NA; ai += nwarps) {
+    const SpRow R = sp_row_of(L, ai);
+    const uint32_t tn = (uint32_t)L.tn[R.q];
+    const uint64_t kbase = L.key_base[R.q] + (uint64_t)R.r * tn;
+    const uint32_t p0 = rowoff[ai], p1 = rowoff[ai + 1], nraw = p1 - p0;
+    uint32_t pos = p0, curJ = 0;   // (sweep) blocks < curJ are written
+    const bool active = any && mode[R.q] && nraw > 0;
+    const bool sym = L.side_b[R.q] < 0;
+    const int ps = sym ? L.side_a[R.q] : L.side_b[R.q];
+    const uint32_t r0 = rstart[R.g], k = rstart[R.g + 1] - r0;
+    if (active && nraw <= (uint32_t)SP_ROWBUF) {
+      // ---- raw terms -> buffer (lanes take records; positions by a warp scan)
+      uint32_t base = 0;
+      for (uint32_t i0 = 0; i0 < k; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        uint32_t pb = 0, pe = 0, o = 0;
+        if (i < k) {
+          const uint32_t rr = rlist[r0 + i];
+          const uint32_t t = rr & 0xffffu;
+          o = rr >> 16;
+          pb = binoff[ps * SP_BSTRIDE + t];
+          pe = binoff[ps * SP_BSTRIDE + t + 1];
+          if (sym) pb = sp_upper(sorted, pb, pe, R.r);
+        }
+        const uint32_t len = pe - pb;
+        uint32_t x = len;
+        for (int sh = 1; sh < 32; sh <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, x, sh);
+          if (lane >= sh) x += y;
+        }
+        uint32_t w = base + x - len;
+        for (uint32_t p = pb; p < pe; ++p) {
+          const uint2 e = sorted[p];
+          buf[w++] = ((unsigned long long)e.x << 32) | (min(o, e.y) - 1u);
+        }
+        base += __shfl_sync(0xffffffffu, x, 31);
+      }
+      uint32_t n2 = 32;
+      while (n2 < nraw) n2 <<= 1;
+      for (uint32_t i = nraw + lane; i < n2; i += 32) buf[i] = ~0ull;
+      __syncwarp();
+      // ---- bitonic sort of the n2 keys
+      for (uint32_t size = 2; size <= n2; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+          for (uint32_t h = lane; h < n2 / 2; h += 32) {   // one compare-exchange per lane and pass
+            const uint32_t i = ((h & ~(stride - 1)) << 1) | (h & (stride - 1)), j = i + stride;
+            const unsigned long long a = buf[i], c = buf[j];
+            if ((a > c) == ((i & size) == 0)) {
+              buf[i] = c;
+              buf[j] = a;
+            }
+          }
+          __syncwarp();
+        }
+      // ---- one entry per distinct partner (run heads, ballot scan); the merged
+      // list goes back to the buffer's front (reads of a batch precede its writes,
+      // which land at or below the batch's positions)
+      uint32_t outn = 0;
+      for (uint32_t i0 = 0; i0 < nraw; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        bool head = false;
+        uint32_t b = 0, d = 0;
+        if (i < nraw) {
+          b = (uint32_t)(buf[i] >> 32);
+          head = i == 0 || (uint32_t)(buf[i - 1] >> 32) != b;
+          if (head) {
+            d = (uint32_t)buf[i];
+            for (uint32_t j = i + 1; j < nraw && (uint32_t)(buf[j] >> 32) == b; ++j) d += (uint32_t)buf[j];
+          }
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, head);
+        __syncwarp();
+        if (head) {
+          const uint32_t o = outn + __popc(m & ((1u << lane) - 1u));
+          const uint32_t J = b / bn, jl = b - J * bn;
+          ents[p0 + o] = (jl << 16) | d;
+          buf[o] = ((unsigned long long)b << 32) | d;
+          if (tn <= (uint32_t)SP_TN_MAX) atomicAdd(&acc[J], 1u << (8 * (jl / sl)));
+        }
+        __syncwarp();
+        outn += __popc(m);
+      }
+      // ---- keys of every block
+      if (tn <= (uint32_t)SP_TN_MAX) {
+        uint32_t run = p0;
+        for (uint32_t j0 = 0; j0 < tn; j0 += 32) {
+          const uint32_t j = j0 + lane;
+          const uint32_t pc = j < tn ? acc[j] : 0u;
+          const uint32_t tot = __vsadu4(pc, 0u);
+          uint32_t x = tot;
+          for (int sh = 1; sh < 32; sh <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, sh);
+            if (lane >= sh) x += y;
+          }
+          if (j < tn) {
+            koff[kbase + j] = run + x - tot;
+            kpart[kbase + j] = pc;
+            acc[j] = 0u;
+          }
+          run += __shfl_sync(0xffffffffu, x, 31);
+        }
+      } else {
+        for (uint32_t j = lane; j < tn; j += 32) {
+          const uint32_t bJ = j * bn, ib = sp_lower_b(buf, outn, bJ);
+          koff[kbase + j] = p0 + ib;
+          uint32_t pc = 0, prev = ib;
+          for (uint32_t sidx = 1; sidx <= 4; ++sidx) {
+            const uint32_t bnd = min(bJ + sidx * sl, bJ + bn);
+            const uint32_t ie = sp_lower_b(buf, outn, bnd);
+            pc |= (ie - prev) << (8 * (sidx - 1));
+            prev = ie;
+            if (bnd == bJ + bn) break;
+          }
+          kpart[kbase + j] = pc;
+        }
+      }
+      for (uint32_t i = p0 + outn + lane; i < p1; i += 32) ents[i] = SP_DEAD;
+      __syncwarp();
+      continue;
+    }
+    if (active) {
+      // ---- long row: sweep over the column blocks
+      const bool cached = k <= (uint32_t)SP_CURSORS;
+      if (cached) {
+        for (uint32_t i = lane; i < k; i += 32) {
+          const uint32_t rr = rlist[r0 + i];
+          const uint32_t t = rr & 0xffffu;
+          const uint32_t b = binoff[ps * SP_BSTRIDE + t], e = binoff[ps * SP_BSTRIDE + t + 1];
+          const uint32_t p = sym ? sp_upper(sorted, b, e, R.r) : b;
+          cur[i] = p;
+          end[i] = e;
+          own[i] = rr >> 16;
+          val[i] = p < e ? sorted[p] : make_uint2(0xFFFFFFFFu, 0u);
+        }
+        __syncwarp();
+      }
+      while (true) {
+        uint32_t mn = 0xFFFFFFFFu;   // the next block: the smallest current partner
+        if (cached) {
+          for (uint32_t i = lane; i < k; i += 32) mn = min(mn, val[i].x);
+        } else {
+          for (uint32_t i = lane; i < k; i += 32) {
+            const uint32_t rr = rlist[r0 + i];
+            const uint32_t t = rr & 0xffffu;
+            const uint32_t b = binoff[ps * SP_BSTRIDE + t], e = binoff[ps * SP_BSTRIDE + t + 1];
+            const uint32_t lo = sym ? max(curJ * bn, R.r + 1u) : curJ * bn;
+            const uint32_t p = lo == 0 ? b : sp_upper(sorted, b, e, lo - 1u);
+            if (p < e) mn = min(mn, sorted[p].x);
+          }
+        }
+        for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        if (mn == 0xFFFFFFFFu) break;
+        const uint32_t J = mn / bn, lo_b = J * bn, hi_b = lo_b + bn;
+        for (uint32_t j = curJ + lane; j < J; j += 32) {   // empty blocks before J
+          koff[kbase + j] = pos;
+          kpart[kbase + j] = 0u;
+        }
+        if (cached) {
+          for (uint32_t i = lane; i < k; i += 32) {
+            uint2 v = val[i];
+            if (v.x >= hi_b) continue;
+            uint32_t p = cur[i];
+            const uint32_t e = end[i], o = own[i];
+            while (v.x < hi_b) {
+              atomicAdd(&acc[v.x - lo_b], min(o, v.y) - 1u);
+              ++p;
+              v = p < e ? sorted[p] : make_uint2(0xFFFFFFFFu, 0u);
+            }
+            cur[i] = p;
+            val[i] = v;
+          }
+        } else {
+          for (uint32_t i = lane; i < k; i += 32) {
+            const uint32_t rr = rlist[r0 + i];
+            const uint32_t t = rr & 0xffffu, o = rr >> 16;
+            const uint32_t b = binoff[ps * SP_BSTRIDE + t], e = binoff[ps * SP_BSTRIDE + t + 1];
+            const uint32_t lo = sym ? max(lo_b, R.r + 1u) : lo_b;
+            for (uint32_t p = lo == 0 ? b : sp_upper(sorted, b, e, lo - 1u); p < e; ++p) {
+              const uint2 v = sorted[p];
+              if (v.x >= hi_b) break;
+              atomicAdd(&acc[v.x - lo_b], min(o, v.y) - 1u);
+            }
+          }
+        }
+        __syncwarp();
+        koff[kbase + J] = pos;
+        uint32_t pc = 0;
+        for (uint32_t c0 = 0; c0 < bn; c0 += 32) {
+          const uint32_t c = c0 + lane;
+          const uint32_t d = c < bn ? acc[c] : 0u;
+          const uint32_t m = __ballot_sync(0xffffffffu, d != 0u);
+          if (d) {
+            ents[pos + __popc(m & ((1u << lane) - 1u))] = (c << 16) | d;
+            acc[c] = 0u;
+          }
+          uint32_t inc = d ? 1u << (8 * (c / sl)) : 0u;
+          for (int o = 16; o > 0; o >>= 1) inc += __shfl_xor_sync(0xffffffffu, inc, o);
+          pc += inc;
+          pos += __popc(m);
+        }
+        if (lane == 0) kpart[kbase + J] = pc;
+        __syncwarp();
+        curJ = J + 1;
+      }
+    }
+    for (uint32_t j = curJ + lane; j < tn; j += 32) {
+      koff[kbase + j] = pos;
+      kpart[kbase + j] = 0u;
+    }
+    for (uint32_t i = pos + lane; i < p1; i += 32) ents[i] = SP_DEAD;
+    __syncwarp();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) koff[L.nkeys] = rowoff[NA];
+}
+
+// ----------------------------------------------------------- u32 scan ----
 // Exclusive scan of n u32 counts into out[0..n] (out[n] = total), 3 phases:
 // per-4096 block sums, one CTA scanning the block sums, block-local scans.
 constexpr int SP_SCAN_BLOCK = 4096;
 __global__ void __launch_bounds__(1024) sp_scan_sums_kernel(const uint32_t* __restrict__ in, int64_t n,
-                                                            uint32_t* __restrict__ sums,
-                                                            const uint32_t* __restrict__ flags) {
-  if (!(flags[0] & 1u)) return;
+                                                            uint32_t* __restrict__ sums) {
   const int64_t b0 = (int64_t)blockIdx.x * SP_SCAN_BLOCK;
   uint32_t s = 0;
   for (int64_t i = b0 + threadIdx.x; i < min(n, b0 + SP_SCAN_BLOCK); i += blockDim.x) s += in[i];
@@ -230,9 +521,7 @@ __global__ void __launch_bounds__(1024) sp_scan_sums_kernel(const uint32_t* __re
     sums[blockIdx.x] = t;
   }
 }
-__global__ void __launch_bounds__(1024) sp_scan_top_kernel(uint32_t* __restrict__ sums, int64_t nb,
-                                                           const uint32_t* __restrict__ flags) {
-  if (!(flags[0] & 1u)) return;
+__global__ void __launch_bounds__(1024) sp_scan_top_kernel(uint32_t* __restrict__ sums, int64_t nb) {
   __shared__ uint32_t w[32];
   __shared__ uint32_t carry;
   if (threadIdx.x == 0) carry = 0;
@@ -268,9 +557,7 @@ __global__ void __launch_bounds__(1024) sp_scan_top_kernel(uint32_t* __restrict_
 }
 __global__ void __launch_bounds__(1024) sp_scan_final_kernel(const uint32_t* __restrict__ in, int64_t n,
                                                              const uint32_t* __restrict__ sums,
-                                                             uint32_t* __restrict__ out,
-                                                             const uint32_t* __restrict__ flags) {
-  if (!(flags[0] & 1u)) return;
+                                                             uint32_t* __restrict__ out) {
   __shared__ uint32_t w[32];
   constexpr int PER = SP_SCAN_BLOCK / 1024;
   const int64_t b0 = (int64_t)blockIdx.x * SP_SCAN_BLOCK + threadIdx.x * PER;
@@ -307,74 +594,58 @@ __global__ void __launch_bounds__(1024) sp_scan_final_kernel(const uint32_t* __r
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = sums[gridDim.x];
 }
 
-// ------------------------------------------------------- sort + merge ----
-// One thread per key: insertion sort of its entries by value (column, then
-// term), terms of the same column summed into one entry (a pair sharing
-// several repeated bins), the freed tail filled with SP_DEAD (never matched).
-__global__ void sp_sort_kernel(const uint32_t* __restrict__ koff, int64_t nkeys, uint32_t* __restrict__ ents,
-                               const uint32_t* __restrict__ flags) {
-  if (!(flags[0] & 1u)) return;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nkeys; k += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t b = koff[k], e = koff[k + 1];
-    if (e - b < 2) continue;
-    for (uint32_t i = b + 1; i < e; ++i) {
-      const uint32_t x = ents[i];
-      uint32_t j = i;
-      while (j > b && ents[j - 1] > x) {
-        ents[j] = ents[j - 1];
-        --j;
-      }
-      ents[j] = x;
-    }
-    uint32_t w = b;
-    for (uint32_t i = b + 1; i < e; ++i) {
-      if ((ents[i] >> 16) == (ents[w] >> 16)) ents[w] += ents[i] & 0xffffu;
-      else ents[++w] = ents[i];
-    }
-    for (uint32_t i = w + 1; i < e; ++i) ents[i] = SP_DEAD;
-  }
+static sa_status scan_u32(const uint32_t* in, int64_t n, uint32_t* out, uint32_t* tmp, cudaStream_t st) {
+  const int64_t nblk = std::max<int64_t>(1, (n + SP_SCAN_BLOCK - 1) / SP_SCAN_BLOCK);
+  sp_scan_sums_kernel<<<(unsigned)nblk, 1024, 0, st>>>(in, n, tmp);
+  SA_LAUNCHED();
+  sp_scan_top_kernel<<<1, 1024, 0, st>>>(tmp, nblk);
+  SA_LAUNCHED();
+  sp_scan_final_kernel<<<(unsigned)nblk, 1024, 0, st>>>(in, n, tmp, out);
+  SA_LAUNCHED();
+  return SA_OK;
 }
 
 // carried records (a previous launch's, e.g. S2a's rows for S2d's query side)
+// (nsrc: the carried launch's nrec words, [0] count, [2] incomplete; ndst =
+// nrec + 1 of the new launch: its [1] carried count, [3] carried incomplete)
 __global__ void sp_copy_records_kernel(const uint2* __restrict__ src, const uint32_t* __restrict__ nsrc,
                                        uint32_t src_cap, uint2* __restrict__ dst, uint32_t* __restrict__ ndst) {
-  const uint32_t n = min(*nsrc, src_cap);
-  if (blockIdx.x == 0 && threadIdx.x == 0) *ndst = *nsrc;   // overflow carries over
+  const uint32_t n = min(nsrc[0], src_cap);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ndst[0] = n;
+    ndst[2] = nsrc[2];   // the carried launch's incomplete flag
+  }
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i];
 }
 
 // ------------------------------------------------------------- host ----
 sa_status sp_build(SpLaunch& L, SpBuffers& B, int sms, cudaStream_t st) {
-  const int nb_rec = sms * 4;
-  sp_bincount_kernel<<<nb_rec, 256, 0, st>>>(L, B.recs, B.nrec, B.bincnt);
+  sp_bincount_kernel<<<sms * 4, 256, 0, st>>>(L, B.recs, B.nrec, B.bincnt, B.sidebase, B.rcnt);
   SA_LAUNCHED();
-  sp_plan_kernel<<<L.nprob, 1024, 0, st>>>(L, B.bincnt, B.nrec, B.mode, B.flags);
+  sp_plan_kernel<<<L.nprob, 1024, 0, st>>>(L, B.bincnt, B.povf, B.mode, B.flags);
   SA_LAUNCHED();
   return SA_OK;
 }
 
 sa_status sp_entries(SpLaunch& L, SpBuffers& B, int sms, cudaStream_t st) {
-  sp_sidebase_kernel<<<1, 32 * 2 * tc::MAXPROB, 0, st>>>(L, B.bincnt, B.sidebase, B.flags);
-  SA_LAUNCHED();
   sp_binscan_kernel<<<L.nsides, 1024, 0, st>>>(B.bincnt, B.binoff, B.flags, B.sidebase);
   SA_LAUNCHED();
-  sp_scatter_kernel<<<sms * 4, 256, 0, st>>>(L, B.recs, B.nrec, B.bincnt, B.binoff, B.blist, B.flags);
+  const int64_t R = L.row_begin[L.nsides];
+  SA_TRY(scan_u32(B.rcnt, R, B.rstart, B.scan_tmp, st));
+  sp_scatter_kernel<<<sms * 4, 256, 0, st>>>(L, B.recs, B.nrec, B.bincnt, B.binoff, B.blist, B.rcnt, B.rstart,
+                                             B.rlist, B.flags);
   SA_LAUNCHED();
-  // bincnt is now all zero again; binoff keeps the list starts
-  const int pw = sms * 8;   // blocks of 8 warps
-  sp_pairs_kernel<false><<<pw, 256, 0, st>>>(L, B.binoff, B.blist, B.mode, B.kcnt, nullptr, nullptr, B.flags);
+  sp_listsort_kernel<<<sms * 8, 256, 0, st>>>(L, B.binoff, B.blist, B.sorted, B.flags);
   SA_LAUNCHED();
-  const int64_t n = L.nkeys;
-  const int64_t nblk = (n + SP_SCAN_BLOCK - 1) / SP_SCAN_BLOCK;
-  sp_scan_sums_kernel<<<(unsigned)nblk, 1024, 0, st>>>(B.kcnt, n, B.scan_tmp, B.flags);
+  const int64_t NA = L.abase[L.nprob];
+  const unsigned fb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((NA + SP_FILL_WARPS - 1) / SP_FILL_WARPS,
+                                                                       (int64_t)sms * 16));
+  sp_rowcount_kernel<<<fb, 32 * SP_FILL_WARPS, 0, st>>>(L, B.mode, B.binoff, B.sorted, B.rstart, B.rlist, B.rowcnt,
+                                                        B.flags);
   SA_LAUNCHED();
-  sp_scan_top_kernel<<<1, 1024, 0, st>>>(B.scan_tmp, nblk, B.flags);
-  SA_LAUNCHED();
-  sp_scan_final_kernel<<<(unsigned)nblk, 1024, 0, st>>>(B.kcnt, n, B.scan_tmp, B.koff, B.flags);
-  SA_LAUNCHED();
-  sp_pairs_kernel<true><<<pw, 256, 0, st>>>(L, B.binoff, B.blist, B.mode, B.kcnt, B.koff, B.ents, B.flags);
-  SA_LAUNCHED();
-  sp_sort_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, sms * 16), 256, 0, st>>>(B.koff, n, B.ents, B.flags);
+  SA_TRY(scan_u32(B.rowcnt, NA, B.rowoff, B.scan_tmp, st));
+  sp_rowfill_kernel<<<fb, 32 * SP_FILL_WARPS, 0, st>>>(L, B.mode, B.binoff, B.sorted, B.rstart, B.rlist, B.rowoff,
+                                                       B.ents, B.koff, B.kpart, B.flags);
   SA_LAUNCHED();
   return SA_OK;
 }

@@ -256,9 +256,12 @@ def test_guide_tree_on_a_config_bucket(ctx):
 
 
 def test_tc_falls_back_on_deep_counts(ctx, monkeypatch):
-    """K2T tracks 32 threshold layers: a bin count of 33..255 must hand the call
-    to the uint8 SAD engine on the device, exactly."""
+    """With the sparse layers off (SA_K2T_SPARSE=0), K2T tracks 32 threshold
+    layers as MMA columns: a bin count of 33..255 must hand the call to the
+    uint8 SAD engine on the device, exactly (with them on, the same set stays
+    on K2T: tests/test_gpu_sparse.py)."""
     monkeypatch.setenv("SA_ENGINE", "auto")
+    monkeypatch.setenv("SA_K2T_SPARSE", "0")
     rng = np.random.default_rng(81)
     seqs = [rng.integers(0, 20, size=int(rng.integers(3, 400))) for _ in range(150)]
     seqs[3] = np.concatenate([np.full(40, 4, np.uint8), seqs[3]])     # 38 x EEE
@@ -277,8 +280,10 @@ def test_tc_falls_back_on_deep_counts(ctx, monkeypatch):
 
 def test_tc_falls_back_on_column_overflow(ctx, monkeypatch):
     """Long sequences whose 3-mers repeat ~6 times keep more than 32768 layer
-    columns: K2T must decline and the SAD engine must run, exactly."""
+    columns: with the sparse layers off, K2T must decline and the SAD engine
+    must run, exactly."""
     monkeypatch.setenv("SA_ENGINE", "auto")
+    monkeypatch.setenv("SA_K2T_SPARSE", "0")
     rng = np.random.default_rng(82)
     seqs = [rng.integers(0, 20, size=48000) for _ in range(3)] + \
         [rng.integers(0, 20, size=int(rng.integers(3, 400))) for _ in range(20)]
@@ -331,8 +336,10 @@ def test_tc_layers_random(ctx, monkeypatch, n, hi, dup, fp4, pair):
 
 def test_large_counts_fall_back_to_u16(ctx, monkeypatch):
     """A bin count above 255 (here 298 copies of AAA) cannot use the uint8
-    SAD encoding; the auto engine must detect it and stay exact."""
+    SAD encoding; with the sparse layers off the auto engine must detect it
+    and stay exact."""
     monkeypatch.setenv("SA_ENGINE", "auto")
+    monkeypatch.setenv("SA_K2T_SPARSE", "0")
     rng = np.random.default_rng(8)
     seqs = [np.zeros(300, np.uint8), np.zeros(260, np.uint8)] + \
         [rng.integers(0, 20, size=int(rng.integers(3, 400))) for _ in range(140)]

@@ -36,6 +36,8 @@ struct WriteEpi {
     for (int j = 0; j < CW; ++j)
       if (col + j < T.rb) out[j] = (int32_t)v[j];
   }
+  template <int CW>
+  __device__ void correct(State&, int, uint32_t (&)[CW]) const {}
   __device__ void end(State&, const Tile&, int) const {}
 };
 
