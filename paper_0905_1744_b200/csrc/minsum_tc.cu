@@ -631,6 +631,8 @@ struct TcEpiProb {
   const uint32_t* kpart;
   const uint32_t* ents;
   int32_t tn, slice, bn;
+  int32_t tma;   // bit 0: matrices leave by TMA tensor stores (KeyMatEpi::tma_chunk; omap of this problem
+                 // valid); bit 1: n % 8 == 0 (the boxes never cross a row end inside a 16-byte unit)
 };
 
 // Output matrices are written once and never re-read by the kernel: streaming
@@ -693,8 +695,14 @@ enum { EPI_KEYS = 1, EPI_NUM = 2, EPI_SIM = 4, EPI_ALL = 7 };
 // empty (n < k, Z4) row or column 0 with no extra test: r = e = 0 gives key
 // term 0, C = D is impossible, y = 0 gives F = 0.  The lanes read the entries
 // of the chunk's columns as shared-memory broadcasts.
+// Output tensor maps of the TMA-store matrix epilogue, per problem (in the
+// kernel's parameter space, as TMA requires): F direct (16 x 32 box, 128-byte
+// swizzle), F mirrored (16 x 16), C direct (16 x 32), C mirrored (32 x 16).
+enum { OM_FD = 0, OM_FM = 1, OM_CD = 2, OM_CM = 3, OM_N = 4 };
+
 template <int MODE>
 struct KeyMatEpi {
+  CUtensorMap omap[OM_N * tc::MAXPROB];   // first member: 64-byte aligned
   TcEpiProb e[tc::MAXPROB];
   const uint32_t* state;
   int dbg;   // experiments only (SA_K2T_DEBUG bit 8: matrix stores skipped)
@@ -720,8 +728,18 @@ struct KeyMatEpi {
   __host__ __device__ static constexpr bool row_table(bool FP4, int CW, int CG) {
     return SIM && FP4 && !vec_direct(CW, CG);
   }
+  // TMA-store staging (CTA pairs, C and F): per warp, one chunk (tma_chunk),
+  // 10 KB; the vector-store buffers of the fallback path (3 KB) fit inside
+  __host__ __device__ static constexpr bool tma_out(int CW, int CG) {
+    return MODE == (EPI_NUM | EPI_SIM) && CG == 2 && CW == 16;
+  }
   __host__ __device__ static constexpr int xpose_bytes(int CW, bool FP4, int CG) {
-    return (MATS ? 64 * CW : 0) + (vec_direct(CW, CG) ? 32 * 8 * 8 : 0) + (row_table(FP4, CW, CG) ? 32 * 16 : 0);
+    return tma_out(CW, CG) ? 10240
+                           : (MATS ? 64 * CW : 0) + (vec_direct(CW, CG) ? 32 * 8 * 8 : 0) +
+                                 (row_table(FP4, CW, CG) ? 32 * 16 : 0);
+  }
+  __device__ void finish(int lane) const {
+    if (MATS && lane == 0) tc::bulk_wait0();   // TMA stores of the last chunks complete before exit
   }
 
   struct State {
@@ -1017,6 +1035,56 @@ struct KeyMatEpi {
     }
   }
 
+  // The chunk's 32 x 16 pairs (lanes = rows, every pair strictly above the
+  // diagonal) through shared memory and four TMA tensor stores: F and C of
+  // the direct block (rows wrow0.., columns c0..) and of its mirror (rows
+  // c0.., columns wrow0..).  Staging (10 KB per warp, 1024-aligned):
+  //   [0, 4K)     F direct [32 rows][128 B], 16-byte unit u of row r at u ^ (r & 7) (SWIZZLE_128B)
+  //   [4K, 8K)    F mirrored [16 rows][256 B] (a warp writes one whole row per store)
+  //   [8K, 9K)    C direct [32 rows][32 B]
+  //   [9K, 10K)   C mirrored [16 rows][64 B]
+  // Lane 0 owns the bulk group: before rewriting the buffer it waits until
+  // the previous chunk's stores have read it.  (Measured alternatives, config
+  // 4 S5 GEMM: this, 8 warps 3.74 ms; 8-column halves with 5 KB staging, 16
+  // warps 4.35 / 8 warps 3.99 ms; direct rows from registers + mirrored half
+  // by TMA, 16 warps 4.79 ms; per-thread stores only, 12 warps 3.73 ms.)
+  __device__ __forceinline__ void tma_chunk(const State& s, int pi, int c0, int wrow0, const uint32_t (&v)[16],
+                                            int lane, const uint8_t* ent, uint8_t* xp) const {
+    double F[16];
+    uint32_t w[8];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t C = v[j];
+      if (j & 1) w[j >> 1] |= C << 16;
+      else w[j >> 1] = C;
+      const double2 yd = *reinterpret_cast<const double2*>(ent + j * TAB_BYTES + YOFF);
+      F[j] = fsel_dbg(C, s.y, s.d, yd.x, yd.y);
+    }
+    if (lane == 0) tc::bulk_wait_read0();
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      *reinterpret_cast<double2*>(xp + lane * 128 + ((u ^ (lane & 7)) * 16)) = make_double2(F[2 * u], F[2 * u + 1]);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) *reinterpret_cast<double*>(xp + 4096 + j * 256 + lane * 8) = F[j];
+    *reinterpret_cast<uint4*>(xp + 8192 + lane * 32) = make_uint4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<uint4*>(xp + 8192 + lane * 32 + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+    uint16_t* cm = reinterpret_cast<uint16_t*>(xp + 9216);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) cm[j * 32 + lane] = (uint16_t)v[j];
+    tc::fence_async_smem();
+    __syncwarp();
+    if (lane == 0 && !(dbg & 8)) {
+      const uint32_t xs = tc::s_addr(xp);
+      const CUtensorMap* om = omap + OM_N * pi;
+      tc::tma_store_2d(om + OM_FD, xs, c0, wrow0);
+      tc::tma_store_2d(om + OM_FM, xs + 4096, wrow0, c0);
+      tc::tma_store_2d(om + OM_CD, xs + 8192, c0, wrow0);
+      tc::tma_store_2d(om + OM_CM, xs + 9216, wrow0, c0);
+      tc::bulk_commit();
+    }
+  }
+
   // the numerator / F matrices of a chunk (the host sets num (sim) on every
   // problem of a launch whose MODE has NUM (SIM))
   template <bool SYM, int CW, bool FP4, int CG>
@@ -1029,6 +1097,19 @@ struct KeyMatEpi {
     constexpr bool VD = vec_direct(CW, CG);
     const bool rows_all = wrow0 + 32 <= T.row0 + T.ra;   // warp-uniform
     const double2* rtab = reinterpret_cast<const double2*>(xp + 64 * CW);   // written by chunk() at tj = 0
+    if constexpr (SYM && tma_out(CW, CG)) {
+      // every pair strictly above the diagonal: TMA tensor stores.  Ragged
+      // rows and columns are clipped by the maps' bounds -- at 16-byte
+      // granularity in the inner (column) dimension, so when a row's end is
+      // not 16-byte aligned for uint16 (n % 8 != 0) the chunks that cross it
+      // take the per-thread path, which never touches the padding columns.
+      if (upper && E.tma && ((E.tma & 2) || (c0 + CW <= T.col0 + T.rb && wrow0 + 32 <= T.row0 + T.ra))) {
+        tma_chunk(s, T.pi, c0, wrow0, v, lane, ent, xp);
+        return;
+      }
+      if (lane == 0) tc::bulk_wait_read0();   // the staging buffer is about to be reused by the path below
+      __syncwarp();
+    }
     if (upper && ncols == CW && rows_all) {
       const int stores = dbg & 56;
       // ---- fast path (all 32 rows and CW columns exist, no diagonal).
@@ -1215,7 +1296,9 @@ static void tc_gemm(int64_t grid, const tc::Batch& batch, const tc::Maps& maps, 
                                           tc::smem2_of(EW, CW, FP4, Epi::TAB_BYTES, Epi::xpose_bytes(CW, FP4, 2)), st>>>(
         batch, maps, tiles, k);
 }
-// the (epilogue mode, geometry) instantiations a launch can pick
+// the (epilogue mode, geometry) instantiations a launch can pick.  Matrices
+// (NUM | SIM) on CTA pairs: 8 epilogue warps with TMA tensor stores (10 KB of
+// staging per warp, 4 pipeline stages beside it); one CTA: 16 or 8 warps.
 template <bool FP4, int CG>
 static sa_status tc_configure_all() {
   constexpr int CW_ALL = FP4 ? 16 : 32;
@@ -1224,12 +1307,9 @@ static sa_status tc_configure_all() {
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_KEYS>, 8, CW_ALL, FP4, CG>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM>, 16, 16, FP4, CG>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_SIM>, 16, 16, FP4, CG>();
-  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4, CG>();
+  if constexpr (CG == 1)
+    if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4, CG>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 8, 16, FP4, CG>();
-  if constexpr (CG == 2) {   // 12 / 20 epilogue warps: CTA pairs only
-    if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 20, 16, FP4, CG>();
-    if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 12, 16, FP4, CG>();
-  }
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_KEYS | EPI_NUM>, 8, CW_ALL, FP4, CG>();
   return cs;
 }
@@ -1237,23 +1317,15 @@ template <bool FP4, int CG>
 static void tc_gemm_mode(int mode, int keysw, int matsw, int64_t grid, const tc::Batch& batch, const tc::Maps& maps,
                          int64_t tiles, const KeyMatEpi<EPI_ALL>& epi, cudaStream_t st) {
   constexpr int CW_ALL = FP4 ? 16 : 32;
-  // 16 epilogue warps x 16-column chunks (more warps to hide the store / F /
-  // key-term latency, fewer registers each); keys and matrices together
-  // (a rank call that also wants numerators) use 8 warps
   if (mode == EPI_KEYS && keysw == 16) tc_gemm<KeyMatEpi<EPI_KEYS>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
   else if (mode == EPI_KEYS && keysw == 12)
     tc_gemm<KeyMatEpi<EPI_KEYS>, 12, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
   else if (mode == EPI_KEYS) tc_gemm<KeyMatEpi<EPI_KEYS>, 8, CW_ALL, FP4, CG>(grid, batch, maps, tiles, epi, st);
   else if (mode == EPI_NUM) tc_gemm<KeyMatEpi<EPI_NUM>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
   else if (mode == EPI_SIM) tc_gemm<KeyMatEpi<EPI_SIM>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
-  else if ((mode & EPI_KEYS) == 0 && (matsw == 20 || matsw == 12) && CG == 2) {
-    if constexpr (CG == 2) {
-      if (matsw == 20) tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 20, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
-      else tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 12, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
-    }
-  } else if ((mode & EPI_KEYS) == 0 && matsw != 8)
-    tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
-  else if ((mode & EPI_KEYS) == 0)
+  else if ((mode & EPI_KEYS) == 0 && matsw != 8 && CG == 1) {
+    if constexpr (CG == 1) tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
+  } else if ((mode & EPI_KEYS) == 0)
     tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 8, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
   else tc_gemm<KeyMatEpi<EPI_KEYS | EPI_NUM>, 8, CW_ALL, FP4, CG>(grid, batch, maps, tiles, epi, st);   // never with F
 }
@@ -1283,6 +1355,28 @@ static sa_status tc_encode_map(CUtensorMap* m, const uint8_t* base, int64_t rows
 }
 
 
+// Output maps of the TMA-store matrix epilogue (KeyMatEpi::tma_chunk) for an
+// na x nb matrix with row stride ld elements: columns are the inner dimension.
+static sa_status tc_encode_out(CUtensorMap* m, void* base, CUtensorMapDataType dt, int esize, int64_t na, int64_t nb,
+                               int64_t ld, int box_cols, int box_rows, CUtensorMapSwizzle swz) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return fail(SA_E_CUDA, "cuTensorMapEncodeTiled is unavailable");
+  const cuuint64_t dims[2] = {(cuuint64_t)nb, (cuuint64_t)na};
+  const cuuint64_t strides[1] = {(cuuint64_t)(ld * esize)};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(m, dt, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         swz,
+                         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SA_E_CUDA, "cuTensorMapEncodeTiled (K2T output) failed (%d)", (int)r);
+  return SA_OK;
+}
+// SA_K2T_TMA_STORE=0: the matrix epilogue's per-thread stores instead of TMA tensor stores
+static bool tma_store_enabled() {
+  const char* e = getenv("SA_K2T_TMA_STORE");
+  return !(e && atoi(e) == 0);
+}
+
 // Epilogue geometry of a launch's MODE (mirrors tc_gemm_mode): epilogue warps
 // and chunk width -> the column slice each warp owns (the sparse entries are
 // keyed by it).
@@ -1293,10 +1387,7 @@ static EpiGeo epi_geo(int mode, int keysw, int matsw, bool fp4, bool pairs) {
   const int cw_all = fp4 ? 16 : 32;
   if (mode == EPI_KEYS) return keysw == 16 ? EpiGeo{16, 16} : keysw == 12 ? EpiGeo{12, 16} : EpiGeo{8, cw_all};
   if (mode == EPI_NUM || mode == EPI_SIM) return {16, 16};
-  if ((mode & EPI_KEYS) == 0) {
-    if ((matsw == 20 || matsw == 12) && pairs) return {matsw, 16};
-    return matsw != 8 ? EpiGeo{16, 16} : EpiGeo{8, 16};
-  }
+  if ((mode & EPI_KEYS) == 0) return (matsw != 8 && !pairs) ? EpiGeo{16, 16} : EpiGeo{8, 16};
   return {8, cw_all};
 }
 
@@ -1359,10 +1450,10 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     const int w = e ? atoi(e) : 16;
     return w == 8 || w == 12 ? w : 16;
   }();
-  const int matsw = [] {
+  const int matsw = [] {   // matrix-epilogue warps, one CTA: 16 (default) or 8; CTA pairs: 8
     const char* e = getenv("SA_K2T_MATSW");
-    const int w = e ? atoi(e) : 12;   // CTA pairs: 12 (one CTA: 12 is not built, 16 runs)
-    return w == 8 || w == 12 || w == 20 ? w : 16;
+    const int w = e ? atoi(e) : 16;
+    return w == 8 ? 8 : 16;
   }();
   const bool sp_on = sparse_enabled() && bins <= SP_BINS;
   const int spec = sp_on ? 1 : TC_SPEC_MAX;   // dense layers the histogram pass writes
@@ -1673,6 +1764,22 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
         E.tn = L.tn[q];
         E.slice = slice;
         E.bn = BN;
+      }
+      // the matrices leave by TMA tensor stores (CTA pairs, NUM | SIM, symmetric,
+      // rows a multiple of 16 bytes apart, 16-byte aligned bases)
+      E.tma = 0;
+      if (pairs && mode == (EPI_NUM | EPI_SIM) && P.sym && E.num && E.sim && tma_store_enabled() && P.ld % 8 == 0 &&
+          (reinterpret_cast<uintptr_t>(E.num) & 15) == 0 && (reinterpret_cast<uintptr_t>(E.sim) & 15) == 0) {
+        CUtensorMap* om = epi.omap + OM_N * q;
+        SA_TRY(tc_encode_out(om + OM_FD, E.sim, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, P.na, P.nb, P.ld, 16, 32,
+                             CU_TENSOR_MAP_SWIZZLE_128B));
+        SA_TRY(tc_encode_out(om + OM_FM, E.sim, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, P.na, P.nb, P.ld, 32, 16,
+                             CU_TENSOR_MAP_SWIZZLE_NONE));
+        SA_TRY(tc_encode_out(om + OM_CD, E.num, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, P.na, P.nb, P.ld, 16, 32,
+                             CU_TENSOR_MAP_SWIZZLE_NONE));
+        SA_TRY(tc_encode_out(om + OM_CM, E.num, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, P.na, P.nb, P.ld, 32, 16,
+                             CU_TENSOR_MAP_SWIZZLE_NONE));
+        E.tma = 1 | (P.nb % 8 == 0 ? 2 : 0);   // bit 1: every row end 16-byte aligned (no edge fallback)
       }
     }
     // every problem of the launch gets every output its MODE writes (the

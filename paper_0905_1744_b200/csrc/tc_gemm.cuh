@@ -105,6 +105,19 @@ __device__ __forceinline__ void tma_2d_hint(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(s_addr(bar)), "l"(policy)
       : "memory");
 }
+// TMA tensor store shared -> global (bulk-group completion) and its fences
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the shared-memory sources of every committed group have been read (the buffer is free again)
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// generic-proxy shared-memory writes -> visible to the async proxy (TMA reads)
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -331,6 +344,7 @@ __device__ __forceinline__ Tile decode(const Batch& b, int64_t tile) {
 //   template <int CW> __device__ void correct(State&, int col, uint32_t (&v)[CW]) const;   // adjust the
 //                         accumulator chunk before chunk() (sparse layers, tc_sparse.cu), all lanes converged
 //   __device__ void end(State&, const Tile&, int row) const;
+//   __device__ void finish(int lane) const;                        // once per epilogue warp, at exit
 // row = tile row of this thread (0..127), [cbeg, cend) = the warp's column
 // slice of the tile, col = first tile column of the chunk, tab = the warp's
 // table (TAB_BYTES x SLICE bytes, 16-byte aligned), tj = col - cbeg, xp = the
@@ -477,6 +491,7 @@ gemm_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps ma
       if (lane == 0) bar_arrive(&tempty[buf]);
       epi.end(es, T, row);
     }
+    epi.finish(lane);
   }
   fence_before();
   __syncthreads();
@@ -621,25 +636,32 @@ __host__ __device__ constexpr uint32_t idesc2_mxf4() {
 
 template <class Epi, int EW, int CW, bool FP4>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(threads_of(EW), 1)
-gemm2_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps maps, int64_t total_tiles, Epi epi) {
+gemm2_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps maps, int64_t total_tiles,
+             const __grid_constant__ Epi epi) {
   using G = Geo2<FP4>;
   constexpr int BN = G::BN, BNH = G::BNH, STAGE_BYTES = G::STAGE_BYTES;
   constexpr int XB = Epi::xpose_bytes(CW, FP4, 2);
   constexpr int NST = stages2_of(EW, CW, FP4, Epi::TAB_BYTES, XB);
   static_assert(NST >= 3, "CTA-pair stages");
   static_assert(EW % 4 == 0 && BN % CW == 0, "epilogue geometry");
+  // per-warp scratch of a multiple of 1024 bytes (the TMA-store staging of
+  // the matrix epilogue: SWIZZLE_128B boxes need 1024-byte alignment) sits
+  // right after the (1024-aligned) stages; otherwise after the tables
+  constexpr bool XALIGN = XB > 0 && XB % 1024 == 0;
+  constexpr int XFRONT = XALIGN ? EW * XB : 0;
   constexpr int EPI_WARPS = EW;
   if (epi.skip()) return;   // uniform over the grid (device state word)
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const uint32_t raw_s = s_addr(smem_raw);
   const uint32_t base_s = (raw_s + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (base_s - raw_s);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * STAGE_BYTES);
+  uint8_t* xp_all = smem + NST * STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * STAGE_BYTES + XFRONT);
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint8_t* tab_all = smem + NST * STAGE_BYTES + 512;
+  uint8_t* tab_all = smem + NST * STAGE_BYTES + XFRONT + 512;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
@@ -759,8 +781,8 @@ gemm2_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps m
     const int quad = warp & 3, part = warp >> 2;
     const int row = quad * 32 + lane;
     constexpr int SLICE = slice_of(EW, CW, FP4);
-    uint8_t* tab = tab_all + warp * (SLICE * Epi::TAB_BYTES + XB);
-    uint8_t* xp = tab + SLICE * Epi::TAB_BYTES;
+    uint8_t* tab = tab_all + warp * (SLICE * Epi::TAB_BYTES + (XALIGN ? 0 : XB));
+    uint8_t* xp = XALIGN ? xp_all + warp * XB : tab + SLICE * Epi::TAB_BYTES;
     const int cbeg = part * SLICE, cend = min(cbeg + SLICE, BN);
     const uint32_t tempty_leader = map_to_rank(s_addr(&tempty[0]), 0);
     const bool no_epi = (batch.debug & 4) != 0;
@@ -790,6 +812,7 @@ gemm2_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps m
       if (lane == 0) bar_arrive_cluster(tempty_leader + buf * 8u);
       epi.end(es, T, row);
     }
+    epi.finish(lane);
   }
   fence_before();
   __syncthreads();

@@ -39,6 +39,7 @@ struct WriteEpi {
   template <int CW>
   __device__ void correct(State&, int, uint32_t (&)[CW]) const {}
   __device__ void end(State&, const Tile&, int) const {}
+  __device__ void finish(int) const {}
 };
 
 static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
