@@ -193,6 +193,7 @@ struct TcCarry {
   int32_t* ndense = nullptr;         // [np] dense layers each problem of the building launch kept
   int np = 0;
   uint32_t* masks = nullptr;         // [nrows][2][256] layer-2 / layer-3 masks (minsum_tc.cu TcMasks)
+  int masks_valid = 1;               // its histogram pass wrote the layer masks
   int spec = 2;                      // dense layers its histogram pass wrote
   const uint2* recs = nullptr;       // its sparse-layer records (tc_sparse.cuh), nullptr when off
   const uint32_t* nrec = nullptr;

@@ -98,6 +98,8 @@ struct TcMasks {
   uint32_t* own;                // rows [split, R): row g at own + (g - split) * TC_MROW
   const uint32_t* carried;      // rows [0, split)
   int64_t split;
+  int own_valid, carried_valid; // 0: not written (sparse launches skip them): the build reads the profile row
+  __device__ __forceinline__ bool valid(int64_t g) const { return g < split ? carried_valid != 0 : own_valid != 0; }
   __device__ __forceinline__ const uint32_t* row(int64_t g) const {
     return g < split ? carried + g * TC_MROW : own + (g - split) * TC_MROW;
   }
@@ -155,7 +157,7 @@ template <bool FP4>
 __global__ void __launch_bounds__(TC_HIST_THREADS, 2)   // two CTAs per SM (<= 128 registers)
 tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut O, int stride16, int bins,
                uint32_t* __restrict__ planes, uint32_t* __restrict__ state, int64_t hist_from, TcMasks mk, int spec,
-               TcRecOut ro) {
+               TcRecOut ro, int deep_planes, const int32_t* __restrict__ only_dense) {
   __shared__ uint32_t s_nrec;
   if (threadIdx.x == 0) s_nrec = 0;
   constexpr int64_t ROWB = FP4 ? TC_KCAP / 2 : TC_KCAP;
@@ -202,6 +204,10 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
       side = t;
     }
     const int cnt = (int)min((int64_t)TC_HIST_ROWS, min(r1, S.row_begin[t + 1]) - g);
+    if (only_dense && only_dense[O.prob[t]]) {   // planes pass: rows of sparse problems need no deep planes
+      g += cnt;
+      continue;
+    }
     bool deep4[TC_HIST_ROWS];
 #pragma unroll
     for (int h = 0; h < TC_HIST_ROWS; ++h) deep4[h] = false;
@@ -232,19 +238,35 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
         const bool in_cols = w * 32 < dw;
         uint8_t* orow = O.out[t] + (g - S.row_begin[t] + h) * ROWB + (FP4 ? w * 16 : w * 32);
         uint32_t m23[2] = {0u, 0u};   // [c >= 2], [c >= 3] of the thread's 32 bins
+        if (deep_planes) {
+          // every layer's seen-once / seen-twice planes (the dense path's column
+          // selection); a planes-only pass (only_dense) skips layer 1 and writes nothing
 #pragma unroll
-        for (int l = 0; l < TC_HREG; ++l) {
-          const uint32_t m = (uint32_t)l < vmax ? layer_mask(v, (uint32_t)(l + 1) * 0x00010001u) : 0u;
-          if (l < spec && h < cnt && in_cols) store_mask_columns<FP4>(orow + l * layer_bytes, m, dw - w * 32);
-          if (l == 1 || l == 2) m23[l - 1] = m;
-          if ((uint32_t)l >= vmax && l >= 3) break;   // layers 1-3: the masks above
-          s2[l] |= s1[l] & m;
-          s1[l] |= m;
+          for (int l = 0; l < TC_HREG; ++l) {
+            const uint32_t m = (uint32_t)l < vmax ? layer_mask(v, (uint32_t)(l + 1) * 0x00010001u) : 0u;
+            if (l < spec && h < cnt && in_cols && !only_dense)
+              store_mask_columns<FP4>(orow + l * layer_bytes, m, dw - w * 32);
+            if (l == 1 || l == 2) m23[l - 1] = m;
+            if ((uint32_t)l >= vmax && l >= 3) break;   // layers 1-3: the masks above
+            if (l == 0 && only_dense) continue;
+            s2[l] |= s1[l] & m;
+            s1[l] |= m;
+          }
+        } else {
+          // sparse-path launch: layer 1 only (operand columns and its planes);
+          // [c >= 2] just for the records, and only where a count reaches 2
+          const uint32_t m = layer_mask(v, 0x00010001u);
+          if (h < cnt && in_cols) store_mask_columns<FP4>(orow, m, dw - w * 32);
+          s2[0] |= s1[0] & m;
+          s1[0] |= m;
+          if (vmax >= 2u) m23[0] = layer_mask(v, 0x00020002u);
         }
         if (h < cnt) {
           uint32_t* mr = mk.own + (g + h - hist_from) * TC_MROW;
-          mr[w] = m23[0];
-          mr[TC_MW + w] = m23[1];
+          if (mk.own_valid) {
+            mr[w] = m23[0];
+            mr[TC_MW + w] = m23[1];
+          }
           if (ro.on) {
             // records of the bins reaching 2 (sparse per row: ~8 of 8000 on
             // the protein workloads); the count is re-read from the row (L1)
@@ -264,7 +286,7 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
             }
           }
         }
-        const int top = (int)min(vmax, (uint32_t)TC_LCAP);
+        const int top = deep_planes ? (int)min(vmax, (uint32_t)TC_LCAP) : 0;
         for (int l = TC_HREG; l < top; ++l) {
           const uint32_t m = layer_mask(v, (uint32_t)(l + 1) * 0x00010001u);
           uint32_t* d1 = &deep[(l - TC_HREG) * TC_WPL + w];
@@ -278,7 +300,7 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
 #pragma unroll
     for (int h = 0; h < TC_HIST_ROWS; ++h) {
       const uint32_t b4 = __ballot_sync(0xffffffffu, deep4[h]);
-      if ((w & 31) == 0 && h < cnt) mk.own[(g + h - hist_from) * TC_MROW + TC_MDEEP + (w >> 5)] = b4;
+      if ((w & 31) == 0 && h < cnt && mk.own_valid) mk.own[(g + h - hist_from) * TC_MROW + TC_MDEEP + (w >> 5)] = b4;
     }
     g += cnt;
   }
@@ -574,6 +596,7 @@ tc_build_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut
       const int h = item / ns, c = c0 + item % ns;
       const uint16_t* row = S.rows[t] + (rbase + h) * (int64_t)stride16;
       const uint32_t* mrow = mk.row(g + h);
+      const bool mv = mk.valid(g + h);
       uint32_t o[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -584,9 +607,9 @@ tc_build_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut
         for (int b = 0; b < 4; ++b) {
           const uint32_t layer = es[b] >> 16, bin = es[b] & 0xffffu;
           uint32_t bit;
-          if (layer == 2u || layer == 3u)   // from the row's layer mask
+          if (mv && (layer == 2u || layer == 3u))   // from the row's layer mask
             bit = (__ldg(mrow + (layer - 2u) * TC_MW + (bin >> 5)) >> (bin & 31u)) & 1u;
-          else if (layer >= 4u && !((__ldg(mrow + TC_MDEEP + (bin >> 10)) >> ((bin >> 5) & 31u)) & 1u))
+          else if (mv && layer >= 4u && !((__ldg(mrow + TC_MDEEP + (bin >> 10)) >> ((bin >> 5) & 31u)) & 1u))
             bit = 0u;                       // no count >= 4 in the bin's 32-bin word
           else
             bit = (layer != 0u && (uint32_t)__ldg(row + bin) >= layer) ? 1u : 0u;
@@ -1541,8 +1564,13 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     TcMasks mk{};
     mk.split = hfrom;
     mk.carried = carried ? use->masks : nullptr;
-    mk.own = kscr->alloc<uint32_t>((size_t)(R - hfrom) * TC_MROW);
-    if (!mk.own) return fail(SA_E_NOMEM, "scratch allocation of K2T layer masks failed");
+    // the layer-2/3 masks serve the build of listed (dense-path) columns; a
+    // launch expecting the sparse path skips them (a dense problem then reads
+    // its counts from the profile rows)
+    mk.own_valid = sp_on ? 0 : 1;
+    mk.carried_valid = carried ? use->masks_valid : 0;
+    mk.own = mk.own_valid ? kscr->alloc<uint32_t>((size_t)(R - hfrom) * TC_MROW) : nullptr;
+    if (mk.own_valid && !mk.own) return fail(SA_E_NOMEM, "scratch allocation of K2T layer masks failed");
     const int hx = (int)std::max<int64_t>(
         1, std::min<int64_t>((R - hfrom + TC_HIST_ROWS - 1) / TC_HIST_ROWS, 4 * g_num_sms));
     const int hsm = 2 * (TC_LCAP - TC_HREG) * TC_WPL * 4;
@@ -1572,12 +1600,15 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       if (carried && use->recs) SA_TRY(sp_copy_records(use->recs, use->nrec, use->rec_cap, spb.recs, spb.nrec + 1,
                                                        g_num_sms, st));
     }
+    // sparse-path launches build layer 1 and the records only; the deeper
+    // planes of the problems that end up dense come from a second, planes-only
+    // pass over just their rows (after the plan)
     if (fp4)
       tc_hist_kernel<true><<<hx, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, hfrom, mk,
-                                                             spec, ro);
+                                                             spec, ro, sp_on ? 0 : 1, nullptr);
     else
       tc_hist_kernel<false><<<hx, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, hfrom, mk,
-                                                              spec, ro);
+                                                              spec, ro, sp_on ? 0 : 1, nullptr);
     SA_LAUNCHED();
     if (sp_on) {
       // a carried side without records (its launch ran with sparse layers off) cannot go sparse
@@ -1607,6 +1638,7 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       keep->ndense = ndense;
       keep->np = np;
       keep->masks = mk.own;
+      keep->masks_valid = mk.own_valid;
       keep->spec = spec;
       keep->recs = sp_on ? spb.recs : nullptr;
       keep->nrec = sp_on ? spb.nrec : nullptr;
@@ -1631,6 +1663,7 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
         kb += (uint64_t)P.na * L.tn[q];
         const uint64_t npair = P.sym ? (uint64_t)P.na * (P.na - 1) / 2 : (uint64_t)P.na * P.nb;
         L.cap[q] = sparse_setting() == 2 ? std::min<uint64_t>(npair * 64, (uint64_t)1 << 28) : npair / budget;
+        if (L.tn[q] > SP_TN_MAX || P.nb >= (1 << 23)) L.cap[q] = 0;   // key / block-counter limits of the row build
         ecap += L.cap[q];
       }
       L.key_base[np] = kb;
@@ -1670,6 +1703,20 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       SA_CUDA(cudaMemsetAsync(spb.sidebase, 0, (size_t)sides.n * 4, st));
       SA_CUDA(cudaMemsetAsync(spb.rcnt, 0, (size_t)R * 4, st));
       SA_TRY(sp_build(L, spb, g_num_sms, st));
+      {
+        // the dense problems' planes for layers >= 2 (all rows, carried ones included)
+        TcMasks mk0{};
+        TcRecOut ro0{};
+        const int hx0 = (int)std::max<int64_t>(1, std::min<int64_t>((R + TC_HIST_ROWS - 1) / TC_HIST_ROWS,
+                                                                     4 * g_num_sms));
+        if (fp4)
+          tc_hist_kernel<true><<<hx0, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, 0, mk0,
+                                                                  spec, ro0, 1, spb.mode);
+        else
+          tc_hist_kernel<false><<<hx0, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, 0,
+                                                                   mk0, spec, ro0, 1, spb.mode);
+        SA_LAUNCHED();
+      }
       if (cols_out && sel.first + np <= SA_TC_COLS_MAX)
         SA_CUDA(cudaMemcpyAsync(state + SA_TC_MODE_AT + sel.first, spb.mode, np * 4, cudaMemcpyDeviceToDevice, st));
     } else if (cols_out && sel.first + np <= SA_TC_COLS_MAX) {

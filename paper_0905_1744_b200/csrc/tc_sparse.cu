@@ -245,25 +245,59 @@ __global__ void __launch_bounds__(32 * SP_FILL_WARPS) sp_rowcount_kernel(
 // partner order from rowoff[ai]; koff / kpart are written for every column
 // block J of the row (empty blocks: position, 0); slots left by partners that
 // share several bins hold SP_DEAD.  Two ways, by the row's raw term count:
-//   <= SP_ROWBUF (nearly every row): raw terms into a shared buffer, a warp
-//      bitonic sort by (b << 32 | term), one entry per run of equal b, and the
-//      block counts through a shared per-block counter array;
+//   <= SP_ROWBUF (nearly every row): raw terms into shared arrays, a warp
+//      bitonic sort of the keys (partner << 9 | slot) -- in registers up to
+//      128 terms --, one entry per run of equal partners, and the block counts
+//      through a shared per-block counter array;
 //   larger (long, repetitive sequences): a sweep over the column blocks the
 //      partners fall in, each repeated bin a cursor kept in shared memory,
 //      terms added into a per-column shared accumulator per block.
 constexpr int SP_ROWBUF = 512;   // raw terms per warp buffer (power of two)
-constexpr int SP_TN_MAX = 1024;  // column blocks of the per-block counters (more: lower-bound keys)
 constexpr int SP_CURSORS = 128;   // cursor state of the sweep: 2.5 KB, inside the raw buffer
 constexpr int SP_BN_MAX = 256;   // column-block width (240 e2m1, 256 u8)
 
-__device__ __forceinline__ uint32_t sp_lower_b(const unsigned long long* buf, uint32_t n, uint32_t b) {
-  uint32_t lo = 0, hi = n;   // first i with (buf[i] >> 32) >= b
-  while (lo < hi) {
-    const uint32_t m = (lo + hi) >> 1;
-    if ((uint32_t)(buf[m] >> 32) < b) lo = m + 1;
-    else hi = m;
+// Ascending sort of the n <= 32 E keys key[0..n) by one warp in registers:
+// bitonic network on 32 E slots (element t * 32 + lane in register t, pads
+// 0xFFFFFFFF); strides below 32 exchange through shuffles, larger ones
+// between a lane's registers.  The sorted keys go back to key[].
+template <int E>
+__device__ __forceinline__ void sp_warp_sort(uint32_t* key, uint32_t n, int lane) {
+  uint32_t v[E];
+#pragma unroll
+  for (int t = 0; t < E; ++t) v[t] = (uint32_t)(t * 32 + lane) < n ? key[t * 32 + lane] : 0xFFFFFFFFu;
+#pragma unroll
+  for (int size = 2; size <= 32 * E; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= 32) {
+#pragma unroll
+        for (int t = 0; t < E; ++t) {
+          const int t2 = t ^ (stride >> 5);
+          if (t2 > t) {
+            const bool up = (((t * 32 + lane) & size) == 0);
+            const uint32_t a = v[t], b = v[t2];
+            if ((a > b) == up) {
+              v[t] = b;
+              v[t2] = a;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < E; ++t) {
+          const int i = t * 32 + lane;
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, v[t], stride);
+          const bool up = (i & size) == 0, lower = (lane & stride) == 0;
+          v[t] = (lower == up) ? min(v[t], o) : max(v[t], o);
+        }
+      }
+    }
   }
-  return lo;
+  __syncwarp();
+#pragma unroll
+  for (int t = 0; t < E; ++t)
+    if ((uint32_t)(t * 32 + lane) < n) key[t * 32 + lane] = v[t];
+  __syncwarp();
 }
 
 __global__ void __launch_bounds__(32 * SP_FILL_WARPS) sp_rowfill_kernel(
@@ -298,7 +332,10 @@ __global__ void __launch_bounds__(32 * SP_FILL_WARPS) sp_rowfill_kernel(
     const int ps = sym ? L.side_a[R.q] : L.side_b[R.q];
     const uint32_t r0 = rstart[R.g], k = rstart[R.g + 1] - r0;
     if (active && nraw <= (uint32_t)SP_ROWBUF) {
-      // ---- raw terms -> buffer (lanes take records; positions by a warp scan)
+      // ---- raw terms -> shared arrays: key = partner << 9 | slot, term[slot]
+      // (lanes take records; slots by a warp scan)
+      uint32_t* key = reinterpret_cast<uint32_t*>(buf);
+      uint32_t* term = key + SP_ROWBUF;
       uint32_t base = 0;
       for (uint32_t i0 = 0; i0 < k; i0 += 32) {
         const uint32_t i = i0 + lane;
@@ -318,90 +355,78 @@ __global__ void __launch_bounds__(32 * SP_FILL_WARPS) sp_rowfill_kernel(
           if (lane >= sh) x += y;
         }
         uint32_t w = base + x - len;
-        for (uint32_t p = pb; p < pe; ++p) {
+        for (uint32_t p = pb; p < pe; ++p, ++w) {
           const uint2 e = sorted[p];
-          buf[w++] = ((unsigned long long)e.x << 32) | (min(o, e.y) - 1u);
+          key[w] = (e.x << 9) | w;
+          term[w] = min(o, e.y) - 1u;
         }
         base += __shfl_sync(0xffffffffu, x, 31);
       }
-      uint32_t n2 = 32;
-      while (n2 < nraw) n2 <<= 1;
-      for (uint32_t i = nraw + lane; i < n2; i += 32) buf[i] = ~0ull;
       __syncwarp();
-      // ---- bitonic sort of the n2 keys
-      for (uint32_t size = 2; size <= n2; size <<= 1)
-        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-          for (uint32_t h = lane; h < n2 / 2; h += 32) {   // one compare-exchange per lane and pass
-            const uint32_t i = ((h & ~(stride - 1)) << 1) | (h & (stride - 1)), j = i + stride;
-            const unsigned long long a = buf[i], c = buf[j];
-            if ((a > c) == ((i & size) == 0)) {
-              buf[i] = c;
-              buf[j] = a;
+      // ---- sort the keys: in registers up to 128 (shuffle bitonic), else in shared memory
+      if (nraw <= 32) sp_warp_sort<1>(key, nraw, lane);
+      else if (nraw <= 64) sp_warp_sort<2>(key, nraw, lane);
+      else if (nraw <= 128) sp_warp_sort<4>(key, nraw, lane);
+      else {
+        uint32_t n2 = 256;
+        while (n2 < nraw) n2 <<= 1;
+        for (uint32_t i = nraw + lane; i < n2; i += 32) key[i] = 0xFFFFFFFFu;
+        __syncwarp();
+        for (uint32_t size = 2; size <= n2; size <<= 1)
+          for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t h = lane; h < n2 / 2; h += 32) {   // one compare-exchange per lane and pass
+              const uint32_t i = ((h & ~(stride - 1)) << 1) | (h & (stride - 1)), j = i + stride;
+              const uint32_t a = key[i], c = key[j];
+              if ((a > c) == ((i & size) == 0)) {
+                key[i] = c;
+                key[j] = a;
+              }
             }
+            __syncwarp();
           }
-          __syncwarp();
-        }
-      // ---- one entry per distinct partner (run heads, ballot scan); the merged
-      // list goes back to the buffer's front (reads of a batch precede its writes,
-      // which land at or below the batch's positions)
+      }
+      // ---- one entry per distinct partner (run heads, ballot scan), each
+      // head summing its run's terms; per-block slice counters
       uint32_t outn = 0;
       for (uint32_t i0 = 0; i0 < nraw; i0 += 32) {
         const uint32_t i = i0 + lane;
         bool head = false;
         uint32_t b = 0, d = 0;
         if (i < nraw) {
-          b = (uint32_t)(buf[i] >> 32);
-          head = i == 0 || (uint32_t)(buf[i - 1] >> 32) != b;
+          const uint32_t kv = key[i];
+          b = kv >> 9;
+          head = i == 0 || (key[i - 1] >> 9) != b;
           if (head) {
-            d = (uint32_t)buf[i];
-            for (uint32_t j = i + 1; j < nraw && (uint32_t)(buf[j] >> 32) == b; ++j) d += (uint32_t)buf[j];
+            d = term[kv & 511u];
+            for (uint32_t j = i + 1; j < nraw && (key[j] >> 9) == b; ++j) d += term[key[j] & 511u];
           }
         }
         const uint32_t m = __ballot_sync(0xffffffffu, head);
-        __syncwarp();
         if (head) {
-          const uint32_t o = outn + __popc(m & ((1u << lane) - 1u));
           const uint32_t J = b / bn, jl = b - J * bn;
-          ents[p0 + o] = (jl << 16) | d;
-          buf[o] = ((unsigned long long)b << 32) | d;
-          if (tn <= (uint32_t)SP_TN_MAX) atomicAdd(&acc[J], 1u << (8 * (jl / sl)));
+          ents[p0 + outn + __popc(m & ((1u << lane) - 1u))] = (jl << 16) | d;
+          atomicAdd(&acc[J], 1u << (8 * (jl / sl)));
         }
-        __syncwarp();
         outn += __popc(m);
       }
-      // ---- keys of every block
-      if (tn <= (uint32_t)SP_TN_MAX) {
-        uint32_t run = p0;
-        for (uint32_t j0 = 0; j0 < tn; j0 += 32) {
-          const uint32_t j = j0 + lane;
-          const uint32_t pc = j < tn ? acc[j] : 0u;
-          const uint32_t tot = __vsadu4(pc, 0u);
-          uint32_t x = tot;
-          for (int sh = 1; sh < 32; sh <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, sh);
-            if (lane >= sh) x += y;
-          }
-          if (j < tn) {
-            koff[kbase + j] = run + x - tot;
-            kpart[kbase + j] = pc;
-            acc[j] = 0u;
-          }
-          run += __shfl_sync(0xffffffffu, x, 31);
+      __syncwarp();
+      // ---- keys of every block: slice counts and a scan of the block totals
+      uint32_t run = p0;
+      for (uint32_t j0 = 0; j0 < tn; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        const uint32_t pc = j < tn ? acc[j] : 0u;
+        const uint32_t tot = __vsadu4(pc, 0u);
+        uint32_t x = tot;
+        for (int sh = 1; sh < 32; sh <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, x, sh);
+          if (lane >= sh) x += y;
         }
-      } else {
-        for (uint32_t j = lane; j < tn; j += 32) {
-          const uint32_t bJ = j * bn, ib = sp_lower_b(buf, outn, bJ);
-          koff[kbase + j] = p0 + ib;
-          uint32_t pc = 0, prev = ib;
-          for (uint32_t sidx = 1; sidx <= 4; ++sidx) {
-            const uint32_t bnd = min(bJ + sidx * sl, bJ + bn);
-            const uint32_t ie = sp_lower_b(buf, outn, bnd);
-            pc |= (ie - prev) << (8 * (sidx - 1));
-            prev = ie;
-            if (bnd == bJ + bn) break;
-          }
+        if (j < tn) {
+          koff[kbase + j] = run + x - tot;
           kpart[kbase + j] = pc;
+          acc[j] = 0u;
         }
+        run += __shfl_sync(0xffffffffu, x, 31);
       }
       for (uint32_t i = p0 + outn + lane; i < p1; i += 32) ents[i] = SP_DEAD;
       __syncwarp();

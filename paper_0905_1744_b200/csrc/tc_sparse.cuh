@@ -10,6 +10,7 @@ namespace sa {
 constexpr int SP_BINS = 8192;                 // bins per side (TC_MAX_BINS)
 constexpr int SP_BSTRIDE = SP_BINS + 1;       // binoff row: SP_BINS starts + the side's end
 constexpr uint32_t SP_DEAD = 0xFFFF0000u;     // merged-away entry: column 0xFFFF is never in a tile
+constexpr int SP_TN_MAX = 1024;               // column blocks per sparse problem (the row build's counters)
 
 // A correction entry: (column within the tile's column block) << 16 | term,
 // term = sum over the pair's shared repeated bins of min(c_i, c_j) - 1.
