@@ -184,6 +184,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-n", type=int, default=2400)
     ap.add_argument("--no-similarity", action="store_true", help="S5 numerators only (not the default)")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "torch"],
+                    help="N > 1: libsa's NCCL communicator (default) or torch.distributed callbacks")
     args = ap.parse_args()
 
     from sa_synth.generator import CONFIGS, generate
@@ -220,7 +222,12 @@ def main():
 
     ctx = B.Context(local)
     if world > 1:
-        ctx.attach_comm(B.TorchComm(device=dev))
+        if args.comm == "nccl":   # libsa's own NCCL communicator: no Python in any collective
+            obj = [B.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            ctx.attach_nccl(obj[0], world, rank)
+        else:                     # torch.distributed callbacks (sa_comm_ops)
+            ctx.attach_comm(B.TorchComm(device=dev))
     ctx.set_timing(True)
     hp = HotPath(ctx, cfg.p, cfg.samples_per_block, want_similarity=not args.no_similarity)
     # every step runs on a dedicated (non-default) stream, so the e2e leg's

@@ -88,6 +88,24 @@ sa_status sa_ctx_create(int cuda_device, sa_ctx** out);
  * also for nranks == 1; a context that never attaches makes every exchange a
  * local copy.  `ops` is copied; its `user` pointer must stay valid. */
 sa_status sa_ctx_attach_comm(sa_ctx* ctx, const sa_comm_ops* ops, int nranks, int rank);
+/* libsa's own NCCL communicator: every exchange of
+ * Algorithm 2 then runs as NCCL collectives on the call's stream, with no
+ * host code in between -- C1 sample profiles, C2 regular-sample records and
+ * C3 count rows by ncclAllGather, C4 the personalised all-to-all (P:625-641,
+ * P:1265) by one group of ncclSend / ncclRecv.  sa_nccl_unique_id writes
+ * ncclGetUniqueId's 128 bytes (call it on one rank, share them);
+ * sa_ctx_attach_nccl is collective (ncclCommInitRank): every rank of the
+ * group calls it with the same id and its own rank.  It takes precedence over
+ * sa_ctx_attach_comm callbacks; the communicator is destroyed with the
+ * context.  NCCL is resolved at run time (the process's libnccl.so.2, e.g.
+ * PyTorch's): SA_E_COMM when it is missing or NCCL fails; SA_E_STATE when a
+ * communicator is already attached. */
+sa_status sa_nccl_unique_id(void* id_h);
+sa_status sa_ctx_attach_nccl(sa_ctx* ctx, const void* id_h, int nranks, int rank);
+/* Synchronises `stream`, then reports (and clears) the sticky device error
+ * flags of the asynchronous calls (sa_kmer_profiles: SA_E_RANGE) and any
+ * asynchronous NCCL error of the attached communicator (SA_E_COMM). */
+sa_status sa_ctx_check(sa_ctx* ctx, void* stream);
 sa_status sa_ctx_destroy(sa_ctx* ctx);
 const char* sa_last_error(void);
 /* Number of libsa kernels launched through this process since load. */
@@ -195,9 +213,12 @@ int32_t sa_profile_stride(int32_t bins);
  * the word (reading Z21); nkmers[i] = max(0, n_i - k + 1) (Eq. 1 denominator
  * term).  residues: uint8 codes 0..alphabet-1, CSR by offsets[0..n].
  * profiles: [n][sa_profile_stride(alphabet^k)] uint16 (padding zeroed).
- * SA_E_INVAL: NULL pointer with n > 0, k < 1, alphabet < 2, alphabet^k > 65536.
- * SA_E_RANGE: a residue >= alphabet, or nk > 65535 (counts / numerators are
- * uint16).  n == 0 is a no-op. */
+ * SA_E_INVAL (returned): NULL pointer with n > 0, k < 1, alphabet < 2,
+ * alphabet^k > 65536.  The call is asynchronous (no host synchronisation):
+ * a residue >= alphabet or nk > 65535 (counts / numerators are uint16) sets
+ * the context's sticky device flags, reported as SA_E_RANGE by sa_ctx_check
+ * or by the next sa_partition on any rank (at its count exchange, C3); the
+ * outputs are then unspecified.  n == 0 is a no-op. */
 sa_status sa_kmer_profiles(sa_ctx* ctx, const uint8_t* residues, const int64_t* offsets, int32_t n,
                            int32_t k, int32_t alphabet, uint16_t* profiles, int32_t* nkmers, void* stream);
 

@@ -29,7 +29,7 @@ EXPORTED = ["sa_ctx_create", "sa_ctx_attach_comm", "sa_ctx_destroy", "sa_last_er
             "sa_partition", "sa_redistribute", "sa_bucket_similarity", "sa_exact_rank_compare", "sa_ctx_engine",
             "sa_ctx_set_rank_form", "sa_ctx_tc_columns", "sa_ctx_tc_operand", "sa_selftest_f_division",
             "sa_bucket_similarity_batch", "sa_pack_upper_u16", "sa_pack_upper_f64", "sa_guide_tree",
-            "sa_ctx_phase_history", "sa_ctx_tc_sparse"]
+            "sa_ctx_phase_history", "sa_ctx_tc_sparse", "sa_nccl_unique_id", "sa_ctx_attach_nccl", "sa_ctx_check"]
 SA_RANK_F, SA_RANK_DF = 0, 1
 
 
@@ -109,6 +109,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "sa_ctx_tc_columns": (ctypes.c_int32, [P, P, ctypes.c_int32]),
         "sa_ctx_tc_operand": (ctypes.c_int, [P]),
         "sa_ctx_tc_sparse": (ctypes.c_int32, [P, P, P, ctypes.c_int32]),
+        "sa_nccl_unique_id": (ctypes.c_int, [P]),
+        "sa_ctx_attach_nccl": (ctypes.c_int, [P, P, ctypes.c_int, ctypes.c_int]),
+        "sa_ctx_check": (ctypes.c_int, [P, VP]),
         "sa_selftest_f_division": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(ctypes.c_int64)]),
         "sa_ctx_set_rank_form": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_double]),
     }
@@ -161,6 +164,13 @@ def sa_exact_rank_compare(Ca, nka: int, Cb, nkb: int, nk_pool) -> int:
                                                     nkp.shape[0]))
 
 
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through libsa (sa_nccl_unique_id): 128 bytes."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().sa_nccl_unique_id(buf))
+    return buf.raw
+
+
 def sa_launch_count() -> int:
     return int(load_library().sa_launch_count())
 
@@ -190,6 +200,19 @@ class Context:
             self.close()
         except Exception:
             pass
+
+    def attach_nccl(self, unique_id: bytes, nranks: int, rank: int):
+        """libsa's own NCCL communicator (sa_ctx_attach_nccl; collective): every
+        rank passes the same 128-byte id (nccl_unique_id() on one rank, shared
+        by the caller, e.g. with torch.distributed.broadcast_object_list)."""
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        _check(load_library().sa_ctx_attach_nccl(self.handle, buf, nranks, rank))
+        self.nranks, self.rank = nranks, rank
+
+    def check(self, stream=None):
+        """sa_ctx_check: synchronise the stream, raise the sticky device errors
+        of the asynchronous calls (SA_E_RANGE) or an NCCL asynchronous error."""
+        _check(load_library().sa_ctx_check(self.handle, _stream(stream)))
 
     def attach_comm(self, comm: "TorchComm"):
         ops = comm.ops()
@@ -248,8 +271,11 @@ class Context:
 
 # ------------------------------------------------------------- S1 .. S5 ----
 def sa_kmer_profiles(ctx: Context, residues: torch.Tensor, offsets: torch.Tensor, k: int = 3, alphabet: int = 20,
-                     profiles: torch.Tensor | None = None, nkmers: torch.Tensor | None = None, stream=None):
-    """S1: returns (profiles uint16 [n][stride], nkmers int32 [n]) (sa.h)."""
+                     profiles: torch.Tensor | None = None, nkmers: torch.Tensor | None = None, stream=None,
+                     check: bool = False):
+    """S1: returns (profiles uint16 [n][stride], nkmers int32 [n]) (sa.h).
+    Asynchronous: range errors surface at ctx.check() (check=True calls it
+    here) or at sa_partition's count exchange."""
     _dev(residues, torch.uint8, "residues")
     _dev(offsets, torch.int64, "offsets")
     n = offsets.numel() - 1
@@ -262,6 +288,8 @@ def sa_kmer_profiles(ctx: Context, residues: torch.Tensor, offsets: torch.Tensor
         nkmers = torch.empty(max(n, 0), dtype=torch.int32, device=dev)
     _check(load_library().sa_kmer_profiles(ctx.handle, _ptr(residues), _ptr(offsets), n, k, alphabet,
                                            _ptr(profiles), _ptr(nkmers), _stream(stream)))
+    if check:
+        ctx.check(stream)
     return profiles, nkmers
 
 
@@ -514,13 +542,17 @@ class TorchComm:
     host buffers in the CPU tests).  Plumbing only: allgather and a variable
     all-to-all of bytes, ordered on the caller's stream."""
 
-    def __init__(self, group=None, device="cuda"):
+    def __init__(self, group=None, device="cuda", stage_host: bool = False):
+        """stage_host: the buffers are device memory but the process group's
+        backend is host-only (gloo): each collective copies through host
+        memory (the multi-process test on one GPU, tests/test_gpu_two_process.py)."""
         import torch.distributed as dist
         self.dist = dist
         self.group = group
         self.nranks = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.device = torch.device(device)
+        self.stage_host = stage_host
         self.errors = []
 
     def _with_stream(self, stream_ptr):
@@ -531,6 +563,13 @@ class TorchComm:
 
     def allgather(self, user, send, recv, nbytes, stream):
         try:
+            if self.stage_host:
+                with self._with_stream(stream):
+                    src = raw_tensor(send, nbytes, self.device).cpu()
+                    parts = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(self.nranks)]
+                    self.dist.all_gather(parts, src, group=self.group)
+                    raw_tensor(recv, nbytes * self.nranks, self.device).copy_(torch.cat(parts))
+                return 0
             with self._with_stream(stream):
                 src = raw_tensor(send, nbytes, self.device)
                 dst = raw_tensor(recv, nbytes * self.nranks, self.device)
@@ -554,7 +593,14 @@ class TorchComm:
             with self._with_stream(stream):
                 src = raw_tensor(send, sum(sb), self.device)
                 dst = raw_tensor(recv, sum(rb), self.device)
-                self.dist.all_to_all_single(dst, src, output_split_sizes=rb, input_split_sizes=sb, group=self.group)
+                if self.stage_host:
+                    hd = torch.empty(sum(rb), dtype=torch.uint8)
+                    self.dist.all_to_all_single(hd, src.cpu(), output_split_sizes=rb, input_split_sizes=sb,
+                                                group=self.group)
+                    dst.copy_(hd)
+                else:
+                    self.dist.all_to_all_single(dst, src, output_split_sizes=rb, input_split_sizes=sb,
+                                                group=self.group)
             return 0
         except Exception as e:
             self.errors.append(repr(e))

@@ -26,7 +26,8 @@ def sources():
 
 
 def headers():
-    return glob.glob(os.path.join(PKG, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "sa.h")]
+    return (glob.glob(os.path.join(PKG, "csrc", "*.cuh")) + glob.glob(os.path.join(PKG, "csrc", "*.h")) +
+            [os.path.join(ROOT, "include", "sa.h")])
 
 
 def up_to_date() -> bool:
@@ -87,7 +88,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"libsa build failed: {os.path.basename(src)}")
         if verbose:
             sys.stderr.write(r.stderr)
-    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", *[_obj(s) for s in sources()], "-o", LIB + ".tmp"]
+    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", *[_obj(s) for s in sources()], "-ldl", "-o", LIB + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "comm.h"
 
 namespace sa {
 
@@ -261,7 +262,8 @@ sa_status sa_ctx_create(int cuda_device, sa_ctx** out) {
   }
   sa_ctx* c = new sa_ctx();
   c->device = cuda_device;
-  if (cudaMalloc(&c->dcount, SA_DCOUNT_WORDS * 4) != cudaSuccess ||
+  if (cudaMalloc(&c->dcount, SA_DCOUNT_WORDS * 4) != cudaSuccess || cudaMalloc(&c->derr, 16) != cudaSuccess ||
+      cudaMemset(c->derr, 0, 16) != cudaSuccess ||
       cudaHostAlloc(&c->hpinned, SA_DCOUNT_WORDS * 4, cudaHostAllocDefault) != cudaSuccess ||
       cudaHostAlloc(&c->hstage, SA_STAGE_BYTES, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
       cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->dstage), c->hstage, 0) != cudaSuccess) {
@@ -289,6 +291,41 @@ sa_status sa_ctx_attach_comm(sa_ctx* ctx, const sa_comm_ops* ops, int nranks, in
   return SA_OK;
 }
 
+sa_status sa_nccl_unique_id(void* id_h) {
+  g_err.clear();
+  if (!id_h) return fail(SA_E_INVAL, "id_h is NULL");
+  return nccl_unique_id(id_h);
+}
+
+sa_status sa_ctx_attach_nccl(sa_ctx* ctx, const void* id_h, int nranks, int rank) {
+  g_err.clear();
+  if (!ctx || !id_h) return fail(SA_E_INVAL, "NULL argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SA_E_INVAL, "bad nranks/rank %d/%d", nranks, rank);
+  if (ctx->nccl) return fail(SA_E_STATE, "an NCCL communicator is already attached");
+  SA_CUDA(cudaSetDevice(ctx->device));
+  void* comm = nullptr;
+  SA_TRY(nccl_init(&comm, id_h, nranks, rank));
+  ctx->nccl = comm;
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  ctx->has_comm = false;   // the NCCL communicator takes precedence over callbacks
+  return SA_OK;
+}
+
+sa_status sa_ctx_check(sa_ctx* ctx, void* stream) {
+  g_err.clear();
+  if (!ctx) return fail(SA_E_INVAL, "ctx is NULL");
+  SA_CUDA(cudaSetDevice(ctx->device));
+  SA_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  uint32_t h = 0;
+  SA_CUDA(cudaMemcpy(&h, ctx->derr, 4, cudaMemcpyDeviceToHost));
+  if (h) SA_CUDA(cudaMemset(ctx->derr, 0, 4));
+  if (ctx->nccl) SA_TRY(nccl_check(ctx->nccl));
+  if (h & ERR_RESIDUE) return fail(SA_E_RANGE, "residue outside the alphabet (detected by sa_kmer_profiles)");
+  if (h & ERR_NK) return fail(SA_E_RANGE, "a sequence has more than 65535 k-mers (detected by sa_kmer_profiles)");
+  return SA_OK;
+}
+
 sa_status sa_ctx_destroy(sa_ctx* ctx) {
   if (!ctx) return SA_OK;
   cudaSetDevice(ctx->device);
@@ -296,7 +333,9 @@ sa_status sa_ctx_destroy(sa_ctx* ctx) {
     for (int j = 0; j < SA_PHASE_RING; ++j)
       for (int b = 0; b < 2; ++b)
         if (ctx->ev[i][j][b]) cudaEventDestroy(ctx->ev[i][j][b]);
+  if (ctx->nccl) nccl_destroy(ctx->nccl);
   if (ctx->dcount) cudaFree(ctx->dcount);
+  if (ctx->derr) cudaFree(ctx->derr);
   if (ctx->hpinned) cudaFreeHost(ctx->hpinned);
   if (ctx->hstage) cudaFreeHost(ctx->hstage);
   delete ctx;
@@ -445,6 +484,7 @@ static inline sa_status rec(cudaEvent_t e, cudaStream_t st) {
 }
 
 static sa_status comm_allgather(sa_ctx* c, const void* send, void* recv, int64_t bytes, cudaStream_t st) {
+  if (c->nccl) return nccl_allgather(c->nccl, send, recv, bytes, st);
   if (!c->has_comm) {
     if (send != recv && bytes > 0) SA_CUDA(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, st));
     return SA_OK;
@@ -844,15 +884,29 @@ static sa_status partition_pass(sa_ctx* c, const PartArgs& a, bool exact, int64_
 
   // ---- C3: count exchange (the one mandatory host block).  Each rank's record
   // is [p counts][p residue bytes][four u32 uncertified-comparison counters].
-  const int recw = 2 * a.p + 2;
+  // ... plus the rank's sticky error flags (sa_kmer_profiles), so that every
+  // rank sees any rank's range error and all fail together
+  const int recw = 2 * a.p + 3;
   SA_ALLOC(xrec, int64_t, recw);
   SA_ALLOC(xall, int64_t, (size_t)recw * G);
   SA_CUDA(cudaMemcpyAsync(xrec, counts_d, 2 * a.p * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
   SA_CUDA(cudaMemcpyAsync(xrec + 2 * a.p, amb_cnt, 4 * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+  SA_CUDA(cudaMemcpyAsync(xrec + 2 * a.p + 2, c->derr, 8, cudaMemcpyDeviceToDevice, st));
   SA_TRY(comm_allgather(c, xrec, xall, (int64_t)recw * 8, st));
   std::vector<int64_t> xh((size_t)recw * G);
   SA_TRY(d2h_small(c, xh.data(), xall, xh.size() * 8, st));
   int64_t amb_total = 0;
+  uint32_t errs = 0;
+  for (int g = 0; g < G; ++g) {
+    uint32_t e2[2];
+    std::memcpy(e2, &xh[(size_t)g * recw + 2 * a.p + 2], sizeof e2);
+    errs |= e2[0];
+  }
+  if (errs) {
+    SA_CUDA(cudaMemsetAsync(c->derr, 0, 4, st));
+    if (errs & ERR_RESIDUE) return fail(SA_E_RANGE, "residue outside the alphabet (sa_kmer_profiles, some rank)");
+    return fail(SA_E_RANGE, "a sequence has more than 65535 k-mers (sa_kmer_profiles, some rank)");
+  }
   for (int g = 0; g < G; ++g) {
     uint32_t cnt4[4];
     std::memcpy(cnt4, &xh[(size_t)g * recw + 2 * a.p], sizeof cnt4);
@@ -934,14 +988,10 @@ sa_status sa_kmer_profiles(sa_ctx* ctx, const uint8_t* residues, const int64_t* 
   if (!offsets || !profiles || !nkmers) return fail(SA_E_INVAL, "NULL required pointer");
   cudaStream_t st = (cudaStream_t)stream;
   SA_CUDA(cudaSetDevice(ctx->device));
-  Scratch scratch(st);
-  SA_ALLOC(err, uint32_t, 1);
-  SA_CUDA(cudaMemsetAsync(err, 0, 4, st));
-  SA_TRY(profiles_launch(residues, offsets, n, k, alphabet, profile_stride((int32_t)bins), profiles, nkmers, err, st));
-  uint32_t h = 0;
-  SA_TRY(d2h_small(ctx, &h, err, 4, st));
-  if (h & ERR_RESIDUE) return fail(SA_E_RANGE, "residue outside the alphabet (code >= %d)", alphabet);
-  if (h & ERR_NK) return fail(SA_E_RANGE, "a sequence has more than 65535 k-mers (uint16 counts)");
+  // asynchronous: range errors go to the context's sticky device flags,
+  // surfaced by sa_ctx_check or at sa_partition's count exchange
+  SA_TRY(profiles_launch(residues, offsets, n, k, alphabet, profile_stride((int32_t)bins), profiles, nkmers, ctx->derr,
+                         st));
   return SA_OK;
 }
 
@@ -1047,7 +1097,7 @@ sa_status sa_redistribute(sa_ctx* ctx, int32_t p, const uint8_t* residues, const
   SA_ALLOC(lens, int64_t, std::max(n, 1));
   SA_ALLOC(part, int64_t, (n + 1023) / 1024 + 2);
   SA_TRY(bucket_perm_launch(bucket_of, n, p, hist, base, perm, st));
-  if (!ctx->has_comm) {   // single rank, no communicator: the send layout is the receive layout
+  if (!ctx->has_comm && !ctx->nccl) {   // single rank, no communicator: the send layout is the receive layout
     SA_TRY(perm_meta_launch(perm, n, offsets, bucket_of, first_global, lens, recv_global_idx, recv_bucket, st));
     SA_TRY(scan_launch(lens, n, recv_offsets, part, st));
     SA_TRY(copy_seqs_launch(perm, n, residues, offsets, recv_residues, recv_offsets, st));
@@ -1085,11 +1135,18 @@ sa_status sa_redistribute(sa_ctx* ctx, int32_t p, const uint8_t* residues, const
   SA_TRY(scan_launch(lens, n, soffs, part, st));
   SA_TRY(copy_seqs_launch(perm, n, residues, offsets, sres, soffs, st));
   SA_TRY(pack_meta_launch(perm, n, offsets, bucket_of, first_global, smeta, st));
-  if (ctx->comm.alltoallv(ctx->comm.user, smeta, sm_b.data(), sm_d.data(), rmeta, rm_b.data(), rm_d.data(), (void*)st))
-    return fail(SA_E_COMM, "alltoallv (meta) callback failed");
-  if (ctx->comm.alltoallv(ctx->comm.user, sres, sbytes.data(), sbytes_d.data(), rres, rbytes.data(), rbytes_d.data(),
-                          (void*)st))
-    return fail(SA_E_COMM, "alltoallv (residues) callback failed");
+  if (ctx->nccl) {
+    SA_TRY(nccl_alltoallv(ctx->nccl, G, r, smeta, sm_b.data(), sm_d.data(), rmeta, rm_b.data(), rm_d.data(), st));
+    SA_TRY(nccl_alltoallv(ctx->nccl, G, r, sres, sbytes.data(), sbytes_d.data(), rres, rbytes.data(), rbytes_d.data(),
+                          st));
+  } else {
+    if (ctx->comm.alltoallv(ctx->comm.user, smeta, sm_b.data(), sm_d.data(), rmeta, rm_b.data(), rm_d.data(),
+                            (void*)st))
+      return fail(SA_E_COMM, "alltoallv (meta) callback failed");
+    if (ctx->comm.alltoallv(ctx->comm.user, sres, sbytes.data(), sbytes_d.data(), rres, rbytes.data(), rbytes_d.data(),
+                            (void*)st))
+      return fail(SA_E_COMM, "alltoallv (residues) callback failed");
+  }
   // ---- receive side: [src][bucket] -> [bucket][src] (ascending global id, Z17)
   const int nseg = G * pb;
   std::vector<char> segs_h(segcopy_size() * nseg);

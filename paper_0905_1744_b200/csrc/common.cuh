@@ -241,7 +241,9 @@ struct sa_ctx {
   int nranks = 1;
   int rank = 0;
   sa_comm_ops comm{};
-  bool has_comm = false;
+  bool has_comm = false;        // callbacks attached (sa_ctx_attach_comm)
+  void* nccl = nullptr;         // libsa's own NCCL communicator (sa_ctx_attach_nccl)
+  uint32_t* derr = nullptr;     // device: sticky error flags of the asynchronous calls (ERR_*)
   bool timing = false;
   // phase events: a ring of SA_PHASE_RING (begin, end) pairs per phase,
   // created on first use; ev_count = occurrences recorded, ev_cur = last slot

@@ -803,7 +803,7 @@ struct KeyMatEpi {
     // registers (independent loads, issued before the accumulator wait)
     s.ep = s.ee = 0;
     s.q0 = s.q1 = s.q2 = s.q3 = 0xFFFFFFFFu;
-    if (E.koff && s.rv) {
+    if (E.koff && s.rv && !(dbg & 256)) {   // (SA_K2T_DEBUG 256: experiment, corrections skipped)
       const int64_t key = (int64_t)s.row_g * E.tn + T.col0 / E.bn;
       const uint32_t kb = __ldg(E.koff + key), ke = __ldg(E.koff + key + 1), pc = __ldg(E.kpart + key);
       const uint32_t part = (uint32_t)(cbeg / E.slice);
@@ -820,7 +820,7 @@ struct KeyMatEpi {
     }
     if constexpr (KEYS || SIM) {
       for (int c = cbeg + lane; c < cend; c += 32) {
-        const bool cv = c < T.rb;
+        const bool cv = c < T.rb && !(dbg & 128);   // (SA_K2T_DEBUG 128: experiment, column tables not loaded)
         uint8_t* ent = tab + (c - cbeg) * TAB_BYTES;
         if constexpr (KEYS)
           *reinterpret_cast<uint4*>(ent + KOFF) =

@@ -147,3 +147,34 @@ def test_nccl_communicator_one_rank_matches():
             assert np.array_equal(rr[ro[j]:ro[j + 1]], ds.seq(int(gid[j])))
     finally:
         dist.destroy_process_group()
+
+
+def test_libsa_nccl_communicator_one_rank():
+    """libsa's own NCCL communicator (sa_nccl_unique_id / sa_ctx_attach_nccl):
+    a 1-rank group, so every exchange of sa_partition (ncclAllGather) and
+    sa_redistribute (the packed all-to-all path, its own block by device copy)
+    runs through NCCL on the caller's stream with no Python in between; the
+    artifacts equal the golden partition.  (Two ranks need two GPUs.)"""
+    require_gpu()
+    cfg = CONFIGS[2]
+    ds = generate(cfg)
+    g, meta = load_golden(2)
+    ctx = B.Context(0)
+    ctx.attach_nccl(B.nccl_unique_id(), 1, 0)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        res = torch.from_numpy(ds.residues.copy()).cuda()
+        offs = torch.from_numpy(ds.offsets.copy()).cuda()
+        out = HotPath(ctx, cfg.p, cfg.samples_per_block).step(res, offs, ds.n, 0, debug=True)
+    torch.cuda.synchronize()
+    ctx.check()
+    assert np.array_equal(out.part.bucket_of.cpu().numpy(), g["bucket_of"])
+    assert np.array_equal(out.part.debug["sample_idx"].cpu().numpy(), g["sample_idx"])
+    gid = out.recv_global_idx.cpu().numpy()
+    assert np.array_equal(gid, np.concatenate([np.flatnonzero(g["bucket_of"] == b) for b in range(cfg.p)]))
+    rr, ro = out.recv_residues.cpu().numpy(), out.recv_offsets.cpu().numpy()
+    for j in range(0, len(gid), 97):
+        assert np.array_equal(rr[ro[j]:ro[j + 1]], ds.seq(int(gid[j])))
+    with pytest.raises(B.SaError) as e:
+        ctx.attach_nccl(B.nccl_unique_id(), 1, 0)
+    assert e.value.status == B.SA_E_STATE

@@ -73,11 +73,24 @@ def test_profiles_small_alphabets_ragged(ctx, alphabet, k):
 
 
 def test_profiles_errors(ctx):
+    """Argument errors are returned by the call; range errors are detected on
+    the device and surface asynchronously (sa.h): at sa_ctx_check, or at
+    sa_partition's count exchange -- with no host synchronisation in S1."""
     ds = from_sequences([np.array([0, 1, 2, 3], np.uint8), np.array([0, 20, 1, 2], np.uint8)])
     res, offs = to_dev(ds)
+    B.sa_kmer_profiles(ctx, res, offs)          # enqueued, returns at once
     with pytest.raises(B.SaError) as e:
-        B.sa_kmer_profiles(ctx, res, offs)
+        ctx.check()
     assert e.value.status == B.SA_E_RANGE
+    ctx.check()                                 # the flag was consumed
+    with pytest.raises(B.SaError) as e:
+        B.sa_kmer_profiles(ctx, res, offs, check=True)
+    assert e.value.status == B.SA_E_RANGE
+    P, nk = B.sa_kmer_profiles(ctx, res, offs)  # ... and sa_partition reports it at C3
+    with pytest.raises(B.SaError) as e:
+        B.sa_partition(ctx, 1, 1, P, nk, offs, 8000, 2, 0)
+    assert e.value.status == B.SA_E_RANGE
+    ctx.check()
     with pytest.raises(B.SaError) as e:
         B.sa_kmer_profiles(ctx, res, offs, k=0)
     assert e.value.status == B.SA_E_INVAL
@@ -88,7 +101,7 @@ def test_profiles_errors(ctx):
     big = from_sequences([np.zeros(65540, np.uint8)])
     r2, o2 = to_dev(big)
     with pytest.raises(B.SaError) as e:
-        B.sa_kmer_profiles(ctx, r2, o2)
+        B.sa_kmer_profiles(ctx, r2, o2, check=True)
     assert e.value.status == B.SA_E_RANGE
     # empty set is a no-op
     P, nk = B.sa_kmer_profiles(ctx, torch.zeros(1, dtype=torch.uint8, device="cuda"),
