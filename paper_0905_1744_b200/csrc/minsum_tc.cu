@@ -674,6 +674,26 @@ __device__ __forceinline__ void st_out_if(int fl, double* p, double v) {
   else if (fl == 16) *p = v;
   else if (fl == 32) asm volatile("st.global.L1::no_allocate.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
+// K2T's key accumulators: while its GEMM runs, a key's two 64-bit words hold
+// (X, Y) with key = Y 2^32 + X, so a 96-bit partial sum hi 2^64 + lo goes in
+// with two fire-and-forget adds, X += lo mod 2^32, Y += hi 2^32 + lo / 2^32
+// (no returned value, no carry chain; X stays below 2^64 for any realistic
+// number of partials: < 2^32 each).  tc_key_finalize_kernel turns (X, Y) into
+// the 128-bit key after the launch.
+__device__ __forceinline__ void red_add_key_xy(sa_key128* k, uint64_t lo, uint32_t hi) {
+  const unsigned long long x = lo & 0xffffffffull, y = ((unsigned long long)hi << 32) | (lo >> 32);
+  if (x) asm volatile("red.global.add.u64 [%0], %1;" ::"l"(&k->lo), "l"(x) : "memory");
+  if (y) asm volatile("red.global.add.u64 [%0], %1;" ::"l"(&k->hi), "l"(y) : "memory");
+}
+__global__ void tc_key_finalize_kernel(sa_key128* __restrict__ keys, int64_t n, const uint32_t* __restrict__ state) {
+  if (reinterpret_cast<const volatile uint32_t*>(state)[1] != 0u) return;   // declined: the fallback wrote true keys
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = keys[i].lo, y = keys[i].hi;
+    const uint64_t lo = x + (y << 32);
+    keys[i] = sa_key128{lo, (y >> 32) + (lo < x ? 1ull : 0ull)};
+  }
+}
+
 // 96-bit (lo, hi) add
 __device__ __forceinline__ void add96(uint64_t& lo, uint32_t& hi, uint64_t blo, uint32_t bhi) {
   lo += blo;
@@ -913,7 +933,7 @@ struct KeyMatEpi {
     }
     // lane bits 4,3,2 name the column: 4 * b4 + 2 * b3 + b2
     const int jc = jbase + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-    if ((lane & 3) == 0 && (lo | hi) && jc < ncols) atomic_add_key(keys + c0 + jc, lo, hi);
+    if ((lane & 3) == 0 && (lo | hi) && jc < ncols) red_add_key_xy(keys + c0 + jc, lo, hi);
   }
 
   // CW columns [col, col + CW) of this thread's row; lanes = 32 consecutive rows.
@@ -1235,7 +1255,7 @@ struct KeyMatEpi {
 
   __device__ void end(State& s, const tc::Tile& T, int row) const {
     const TcEpiProb& E = e[T.pi];
-    if (KEYS && E.keyA && s.rv && (s.lo | s.hi)) atomic_add_key(E.keyA + s.row_g, s.lo, s.hi);
+    if (KEYS && E.keyA && s.rv && (s.lo | s.hi)) red_add_key_xy(E.keyA + s.row_g, s.lo, s.hi);
     (void)row;
   }
 };
@@ -1683,6 +1703,8 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       spb.sidebase = scratch.alloc<uint32_t>(sides.n);
       spb.blist = scratch.alloc<uint2>(rec_cap);
       spb.sorted = scratch.alloc<uint2>(rec_cap);
+      spb.bslot = scratch.alloc<uint32_t>(rec_cap);
+      spb.spos = scratch.alloc<uint32_t>(rec_cap);
       spb.rcnt = scratch.alloc<uint32_t>((size_t)R);
       spb.rstart = scratch.alloc<uint32_t>((size_t)R + 1);
       spb.rlist = scratch.alloc<uint32_t>(rec_cap);
@@ -1694,7 +1716,8 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
       spb.kpart = scratch.alloc<uint32_t>((size_t)kb + 1);
       spb.scan_tmp = scratch.alloc<uint32_t>((size_t)(std::max<int64_t>(R, na_all) / 4096) + 2);
       spb.ents = scratch.alloc<uint32_t>((size_t)std::max<uint64_t>(ecap, 1));
-      if (!spb.bincnt || !spb.binoff || !spb.sidebase || !spb.blist || !spb.sorted || !spb.rcnt || !spb.rstart ||
+      if (!spb.bincnt || !spb.binoff || !spb.sidebase || !spb.blist || !spb.sorted || !spb.bslot || !spb.spos ||
+          !spb.rcnt || !spb.rstart ||
           !spb.rlist || !spb.mode || !spb.flags || !spb.rowcnt || !spb.rowoff || !spb.koff || !spb.kpart ||
           !spb.scan_tmp || !spb.ents)
         return fail(SA_E_NOMEM, "scratch allocation of K2T sparse-layer buffers failed");
@@ -1870,6 +1893,21 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     }();
     batch.evict_last = evict_last;
     batch.debug = debug;
+    // decoded tile table (every GEMM warp reads its tile's coordinates with one load)
+    uint2* ttab = scratch.alloc<uint2>((size_t)std::max<int64_t>(tiles, 1));
+    if (!ttab) return fail(SA_E_NOMEM, "scratch allocation of the K2T tile table failed");
+    {
+      const unsigned tb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((tiles + 255) / 256, 4 * g_num_sms));
+      if (pairs) {
+        if (fp4) tc::tile_table_kernel<tc::Geo<true>::BN, tc::TBM2><<<tb, 256, 0, st>>>(batch, tiles, ttab);
+        else tc::tile_table_kernel<tc::Geo<false>::BN, tc::TBM2><<<tb, 256, 0, st>>>(batch, tiles, ttab);
+      } else {
+        if (fp4) tc::tile_table_kernel<tc::Geo<true>::BN, tc::BM><<<tb, 256, 0, st>>>(batch, tiles, ttab);
+        else tc::tile_table_kernel<tc::Geo<false>::BN, tc::BM><<<tb, 256, 0, st>>>(batch, tiles, ttab);
+      }
+      SA_LAUNCHED();
+    }
+    batch.table = ttab;
     const int64_t grid = pairs ? 2 * std::min<int64_t>(tiles, g_num_sms / 2) : std::min<int64_t>(tiles, g_num_sms);
     if (ev0) SA_CUDA(cudaEventRecord(ev0, st));   // the GEMM kernel alone (SA_PHASE_GEMM*)
     if (pairs) {
@@ -1884,6 +1922,18 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     for (int q = 0; q < np; ++q) {
       const MsProblem& P = probs[i0 + q];
       if (fpass_here && P.sim) SA_TRY(ratio_launch(epi.e[q].num, P.nkA, P.nkB, P.na, P.nb, P.ld, P.sim, st, state));
+      // (X, Y) key accumulators -> 128-bit keys (a symmetric problem's column
+      // sums go to the same array as its row sums)
+      if (P.keyA) {
+        tc_key_finalize_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((P.na + 255) / 256, 4 * g_num_sms)),
+                                 256, 0, st>>>(P.keyA, P.na, state);
+        SA_LAUNCHED();
+      }
+      if (P.sym && P.keyB && P.keyB != P.keyA) {
+        tc_key_finalize_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((P.nb + 255) / 256, 4 * g_num_sms)),
+                                 256, 0, st>>>(P.keyB, P.nb, state);
+        SA_LAUNCHED();
+      }
     }
     i0 = i1;
   }

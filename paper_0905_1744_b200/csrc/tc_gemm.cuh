@@ -243,6 +243,7 @@ struct Problem {
 };
 struct Batch {
   Problem p[MAXPROB];
+  const uint2* table;   // nullable: decoded tiles (tile_table_kernel), {pi | ti << 8, tj} per tile
   int n;
   int group;        // GROUP: row blocks per group of the tile order (below)
   int evict_last;   // operand L2 policies (side_policy bits; 0: no hint)
@@ -291,7 +292,34 @@ __host__ __device__ inline int64_t problem_tiles(int64_t na, int64_t nb, bool sy
 }
 
 template <int BN, int TBM = BM>
+__device__ __forceinline__ Tile decode_slow(const Batch& b, int64_t tile);
+
+// Tile of a flat tile index: from the launch's decoded table (one 8-byte load)
+// when there is one, else computed (the group / triangle arithmetic below).
+template <int BN, int TBM = BM>
 __device__ __forceinline__ Tile decode(const Batch& b, int64_t tile) {
+  if (!b.table) return decode_slow<BN, TBM>(b, tile);
+  const uint2 e = b.table[tile];
+  const int pi = (int)(e.x & 0xffu), ti = (int)(e.x >> 8), tj = (int)e.y;
+  const Problem& P = b.p[pi];
+  Tile T;
+  T.pi = pi;
+  T.row0 = ti * TBM;
+  T.col0 = tj * BN;
+  T.ra = min(TBM, P.na - T.row0);
+  T.rb = min(BN, P.nb - T.col0);
+  return T;
+}
+template <int BN, int TBM>
+__global__ void tile_table_kernel(const __grid_constant__ Batch b, int64_t total, uint2* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const Tile T = decode_slow<BN, TBM>(b, t);
+    out[t] = make_uint2((uint32_t)T.pi | ((uint32_t)(T.row0 / TBM) << 8), (uint32_t)(T.col0 / BN));
+  }
+}
+
+template <int BN, int TBM>
+__device__ __forceinline__ Tile decode_slow(const Batch& b, int64_t tile) {
   int pi = 0;
   while (pi + 1 < b.n && b.p[pi + 1].tile_begin <= tile) ++pi;
   const Problem& P = b.p[pi];

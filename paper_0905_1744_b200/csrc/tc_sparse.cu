@@ -145,7 +145,7 @@ __global__ void sp_scatter_kernel(const SpLaunch L, const uint2* __restrict__ re
                                   uint32_t* __restrict__ bincnt, const uint32_t* __restrict__ binoff,
                                   uint2* __restrict__ blist, uint32_t* __restrict__ rcnt,
                                   const uint32_t* __restrict__ rstart, uint32_t* __restrict__ rlist,
-                                  const uint32_t* __restrict__ flags) {
+                                  uint32_t* __restrict__ bslot, const uint32_t* __restrict__ flags) {
   if (!(flags[0] & 1u)) return;
   const uint32_t n = sp_nrec(L, nrec);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -153,17 +153,21 @@ __global__ void sp_scatter_kernel(const SpLaunch L, const uint2* __restrict__ re
     const int s = sp_side_of(L, r.x);
     const uint32_t bin = r.y & 0xffffu;
     const uint32_t pos = binoff[s * SP_BSTRIDE + bin] + atomicSub(&bincnt[s * SP_BINS + bin], 1u) - 1u;
+    const uint32_t slot = rstart[r.x] + atomicSub(&rcnt[r.x], 1u) - 1u;
     blist[pos] = make_uint2((uint32_t)(r.x - L.row_begin[s]), r.y >> 16);
-    rlist[rstart[r.x] + atomicSub(&rcnt[r.x], 1u) - 1u] = r.y;
+    bslot[pos] = slot;   // the record's row-list slot, for its position after the list sort
+    rlist[slot] = r.y;
   }
 }
 
 // One warp per (side, bin) list: rank sort by row (rows are distinct inside a
-// list), out of place.  O(n^2 / 32) per list: the lists are short (a bin's
+// list), out of place; spos[row-list slot] = the sorted position of that
+// record's own entry (a symmetric row's partners are the list's tail after it).  O(n^2 / 32) per list: the lists are short (a bin's
 // rows with count >= 2; ~15 on the config-4 buckets).
 __global__ void __launch_bounds__(256) sp_listsort_kernel(const SpLaunch L, const uint32_t* __restrict__ binoff,
                                                           const uint2* __restrict__ blist, uint2* __restrict__ sorted,
-                                                          const uint32_t* __restrict__ flags) {
+                                                          const uint32_t* __restrict__ bslot,
+                                                          uint32_t* __restrict__ spos, const uint32_t* __restrict__ flags) {
   if (!(flags[0] & 1u)) return;
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -173,7 +177,10 @@ __global__ void __launch_bounds__(256) sp_listsort_kernel(const SpLaunch L, cons
     const uint32_t b = binoff[s * SP_BSTRIDE + t], n = binoff[s * SP_BSTRIDE + t + 1] - b;
     if (n == 0) continue;
     if (n == 1) {
-      if (lane == 0) sorted[b] = blist[b];
+      if (lane == 0) {
+        sorted[b] = blist[b];
+        spos[bslot[b]] = b;
+      }
       continue;
     }
     for (uint32_t i = lane; i < n; i += 32) {
@@ -181,6 +188,7 @@ __global__ void __launch_bounds__(256) sp_listsort_kernel(const SpLaunch L, cons
       uint32_t rank = 0;
       for (uint32_t j = 0; j < n; ++j) rank += blist[b + j].x < x.x ? 1u : 0u;
       sorted[b + rank] = x;
+      spos[bslot[b + i]] = b + rank;   // where the record's own row sits in its sorted list
     }
   }
 }
@@ -215,7 +223,7 @@ __device__ __forceinline__ uint32_t sp_upper(const uint2* __restrict__ list, uin
 constexpr int SP_FILL_WARPS = 4;
 __global__ void __launch_bounds__(32 * SP_FILL_WARPS) sp_rowcount_kernel(
     const SpLaunch L, const int32_t* __restrict__ mode, const uint32_t* __restrict__ binoff,
-    const uint2* __restrict__ sorted, const uint32_t* __restrict__ rstart, const uint32_t* __restrict__ rlist,
+    const uint32_t* __restrict__ spos, const uint32_t* __restrict__ rstart, const uint32_t* __restrict__ rlist,
     uint32_t* __restrict__ rowcnt, const uint32_t* __restrict__ flags) {
   const int lane = threadIdx.x & 31;
   const bool any = (flags[0] & 1u) != 0;
@@ -230,7 +238,7 @@ __global__ void __launch_bounds__(32 * SP_FILL_WARPS) sp_rowcount_kernel(
       for (uint32_t i = rstart[R.g] + lane; i < rstart[R.g + 1]; i += 32) {
         const uint32_t t = rlist[i] & 0xffffu;
         const uint32_t b = binoff[ps * SP_BSTRIDE + t], e = binoff[ps * SP_BSTRIDE + t + 1];
-        cnt += e - (sym ? sp_upper(sorted, b, e, R.r) : b);
+        cnt += e - (sym ? spos[i] + 1u : b);
       }
       for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     }
@@ -302,7 +310,8 @@ __device__ __forceinline__ void sp_warp_sort(uint32_t* key, uint32_t n, int lane
 
 __global__ void __launch_bounds__(32 * SP_FILL_WARPS) sp_rowfill_kernel(
     const SpLaunch L, const int32_t* __restrict__ mode, const uint32_t* __restrict__ binoff,
-    const uint2* __restrict__ sorted, const uint32_t* __restrict__ rstart, const uint32_t* __restrict__ rlist,
+    const uint2* __restrict__ sorted, const uint32_t* __restrict__ spos, const uint32_t* __restrict__ rstart,
+    const uint32_t* __restrict__ rlist,
     const uint32_t* __restrict__ rowoff, uint32_t* __restrict__ ents, uint32_t* __restrict__ koff,
     uint32_t* __restrict__ kpart, const uint32_t* __restrict__ flags) {
   __shared__ unsigned long long s_buf[SP_FILL_WARPS][SP_ROWBUF];   // raw terms; cursors of the sweep
@@ -344,9 +353,8 @@ __global__ void __launch_bounds__(32 * SP_FILL_WARPS) sp_rowfill_kernel(
           const uint32_t rr = rlist[r0 + i];
           const uint32_t t = rr & 0xffffu;
           o = rr >> 16;
-          pb = binoff[ps * SP_BSTRIDE + t];
+          pb = sym ? spos[r0 + i] + 1u : binoff[ps * SP_BSTRIDE + t];
           pe = binoff[ps * SP_BSTRIDE + t + 1];
-          if (sym) pb = sp_upper(sorted, pb, pe, R.r);
         }
         const uint32_t len = pe - pb;
         uint32_t x = len;
@@ -355,6 +363,7 @@ __global__ void __launch_bounds__(32 * SP_FILL_WARPS) sp_rowfill_kernel(
           if (lane >= sh) x += y;
         }
         uint32_t w = base + x - len;
+#pragma unroll 4
         for (uint32_t p = pb; p < pe; ++p, ++w) {
           const uint2 e = sorted[p];
           key[w] = (e.x << 9) | w;
@@ -440,7 +449,7 @@ __global__ void __launch_bounds__(32 * SP_FILL_WARPS) sp_rowfill_kernel(
           const uint32_t rr = rlist[r0 + i];
           const uint32_t t = rr & 0xffffu;
           const uint32_t b = binoff[ps * SP_BSTRIDE + t], e = binoff[ps * SP_BSTRIDE + t + 1];
-          const uint32_t p = sym ? sp_upper(sorted, b, e, R.r) : b;
+          const uint32_t p = sym ? spos[r0 + i] + 1u : b;
           cur[i] = p;
           end[i] = e;
           own[i] = rr >> 16;
@@ -658,19 +667,19 @@ sa_status sp_entries(SpLaunch& L, SpBuffers& B, int sms, cudaStream_t st) {
   const int64_t R = L.row_begin[L.nsides];
   SA_TRY(scan_u32(B.rcnt, R, B.rstart, B.scan_tmp, st));
   sp_scatter_kernel<<<sms * 4, 256, 0, st>>>(L, B.recs, B.nrec, B.bincnt, B.binoff, B.blist, B.rcnt, B.rstart,
-                                             B.rlist, B.flags);
+                                             B.rlist, B.bslot, B.flags);
   SA_LAUNCHED();
-  sp_listsort_kernel<<<sms * 8, 256, 0, st>>>(L, B.binoff, B.blist, B.sorted, B.flags);
+  sp_listsort_kernel<<<sms * 8, 256, 0, st>>>(L, B.binoff, B.blist, B.sorted, B.bslot, B.spos, B.flags);
   SA_LAUNCHED();
   const int64_t NA = L.abase[L.nprob];
   const unsigned fb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((NA + SP_FILL_WARPS - 1) / SP_FILL_WARPS,
                                                                        (int64_t)sms * 16));
-  sp_rowcount_kernel<<<fb, 32 * SP_FILL_WARPS, 0, st>>>(L, B.mode, B.binoff, B.sorted, B.rstart, B.rlist, B.rowcnt,
+  sp_rowcount_kernel<<<fb, 32 * SP_FILL_WARPS, 0, st>>>(L, B.mode, B.binoff, B.spos, B.rstart, B.rlist, B.rowcnt,
                                                         B.flags);
   SA_LAUNCHED();
   SA_TRY(scan_u32(B.rowcnt, NA, B.rowoff, B.scan_tmp, st));
-  sp_rowfill_kernel<<<fb, 32 * SP_FILL_WARPS, 0, st>>>(L, B.mode, B.binoff, B.sorted, B.rstart, B.rlist, B.rowoff,
-                                                       B.ents, B.koff, B.kpart, B.flags);
+  sp_rowfill_kernel<<<fb, 32 * SP_FILL_WARPS, 0, st>>>(L, B.mode, B.binoff, B.sorted, B.spos, B.rstart, B.rlist,
+                                                       B.rowoff, B.ents, B.koff, B.kpart, B.flags);
   SA_LAUNCHED();
   return SA_OK;
 }

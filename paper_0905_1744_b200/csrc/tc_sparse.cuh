@@ -45,6 +45,8 @@ struct SpBuffers {
   uint32_t* sidebase = nullptr; // [nsides] record totals per side (zeroed by the caller)
   uint2* blist = nullptr;       // [rec_cap] bin lists as scattered
   uint2* sorted = nullptr;      // [rec_cap] bin lists sorted by row
+  uint32_t* bslot = nullptr;    // [rec_cap] row-list slot of each bin-list entry
+  uint32_t* spos = nullptr;     // [rec_cap] per row-list slot: the record's position in its sorted bin list
   uint32_t* rcnt = nullptr;     // [R] records per launch row (zeroed by the caller)
   uint32_t* rstart = nullptr;   // [R + 1]
   uint32_t* rlist = nullptr;    // [rec_cap] row lists: bin | count << 16
