@@ -771,13 +771,14 @@ struct KeyMatEpi {
   __host__ __device__ static constexpr bool row_table(bool FP4, int CW, int CG) {
     return SIM && FP4 && !vec_direct(CW, CG);
   }
-  // TMA-store staging (CTA pairs, C and F): per warp, one chunk (tma_chunk),
-  // 10 KB; the vector-store buffers of the fallback path (3 KB) fit inside
+  // TMA-store staging (CTA pairs, C and F): per warp, the direct half of a
+  // chunk (tma_chunk), 5 KB; the vector-store buffers of the fallback path
+  // (3 KB) fit inside
   __host__ __device__ static constexpr bool tma_out(int CW, int CG) {
     return MODE == (EPI_NUM | EPI_SIM) && CG == 2 && CW == 16;
   }
   __host__ __device__ static constexpr int xpose_bytes(int CW, bool FP4, int CG) {
-    return tma_out(CW, CG) ? 10240
+    return tma_out(CW, CG) ? 5120
                            : (MATS ? 64 * CW : 0) + (vec_direct(CW, CG) ? 32 * 8 * 8 : 0) +
                                  (row_table(FP4, CW, CG) ? 32 * 16 : 0);
   }
@@ -1079,20 +1080,21 @@ struct KeyMatEpi {
   }
 
   // The chunk's 32 x 16 pairs (lanes = rows, every pair strictly above the
-  // diagonal) through shared memory and four TMA tensor stores: F and C of
-  // the direct block (rows wrow0.., columns c0..) and of its mirror (rows
-  // c0.., columns wrow0..).  Staging (10 KB per warp, 1024-aligned):
-  //   [0, 4K)     F direct [32 rows][128 B], 16-byte unit u of row r at u ^ (r & 7) (SWIZZLE_128B)
-  //   [4K, 8K)    F mirrored [16 rows][256 B] (a warp writes one whole row per store)
-  //   [8K, 9K)    C direct [32 rows][32 B]
-  //   [9K, 10K)   C mirrored [16 rows][64 B]
-  // Lane 0 owns the bulk group: before rewriting the buffer it waits until
-  // the previous chunk's stores have read it.  (Measured alternatives, config
-  // 4 S5 GEMM: this, 8 warps 3.74 ms; 8-column halves with 5 KB staging, 16
-  // warps 4.35 / 8 warps 3.99 ms; direct rows from registers + mirrored half
-  // by TMA, 16 warps 4.79 ms; per-thread stores only, 12 warps 3.73 ms.)
-  __device__ __forceinline__ void tma_chunk(const State& s, int pi, int c0, int wrow0, const uint32_t (&v)[16],
-                                            int lane, const uint8_t* ent, uint8_t* xp) const {
+  // diagonal).  The mirrored block (rows c0.., columns wrow0..) leaves straight
+  // from registers: for each column j the warp's 32 lanes hold 32 consecutive
+  // elements of mirrored row c0 + j, one coalesced store each (256 B of F,
+  // 64 B of C, whole sectors).  The direct block (rows wrow0.., columns c0..)
+  // has lanes = rows, so it goes through shared memory (F [32 rows][128 B],
+  // 16-byte unit u of row r at u ^ (r & 7), SWIZZLE_128B; C [32 rows][32 B];
+  // 5 KB per warp) and leaves by two TMA tensor stores.  Shared-memory bandwidth
+  // is what the CTA shares with the MMA's operand reads and the TMA operand
+  // loads, so only the half that needs a transpose is staged.  Lane 0 owns the
+  // bulk group: before rewriting the buffer it waits until the previous
+  // chunk's stores have read it.  (Measured, config 4 S5 GEMM: both halves
+  // through shared memory, 8 warps 3.74 ms; 8-column halves, 16 warps 4.35 ms;
+  // direct rows from registers + mirror by TMA, 16 warps 4.79 ms.)
+  __device__ __forceinline__ void tma_chunk(const State& s, int pi, int c0, int wrow0, int ncols, const uint32_t (&v)[16],
+                                            int lane, const uint8_t* ent, uint8_t* xp, const TcEpiProb& E) const {
     double F[16];
     uint32_t w[8];
 #pragma unroll
@@ -1103,27 +1105,31 @@ struct KeyMatEpi {
       const double2 yd = *reinterpret_cast<const double2*>(ent + j * TAB_BYTES + YOFF);
       F[j] = fsel_dbg(C, s.y, s.d, yd.x, yd.y);
     }
+    if (s.rv && !(dbg & 8)) {
+      double* fm = E.sim + (int64_t)c0 * E.ld + s.row_g;
+      uint16_t* cmr = E.num + (int64_t)c0 * E.ld + s.row_g;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j < ncols) {
+          __stcs(fm + (int64_t)j * E.ld, F[j]);
+          __stcs(reinterpret_cast<unsigned short*>(cmr + (int64_t)j * E.ld), (unsigned short)v[j]);
+        }
+      }
+    }
     if (lane == 0) tc::bulk_wait_read0();
     __syncwarp();
 #pragma unroll
     for (int u = 0; u < 8; ++u)
       *reinterpret_cast<double2*>(xp + lane * 128 + ((u ^ (lane & 7)) * 16)) = make_double2(F[2 * u], F[2 * u + 1]);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) *reinterpret_cast<double*>(xp + 4096 + j * 256 + lane * 8) = F[j];
-    *reinterpret_cast<uint4*>(xp + 8192 + lane * 32) = make_uint4(w[0], w[1], w[2], w[3]);
-    *reinterpret_cast<uint4*>(xp + 8192 + lane * 32 + 16) = make_uint4(w[4], w[5], w[6], w[7]);
-    uint16_t* cm = reinterpret_cast<uint16_t*>(xp + 9216);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) cm[j * 32 + lane] = (uint16_t)v[j];
+    *reinterpret_cast<uint4*>(xp + 4096 + lane * 32) = make_uint4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<uint4*>(xp + 4096 + lane * 32 + 16) = make_uint4(w[4], w[5], w[6], w[7]);
     tc::fence_async_smem();
     __syncwarp();
     if (lane == 0 && !(dbg & 8)) {
       const uint32_t xs = tc::s_addr(xp);
       const CUtensorMap* om = omap + OM_N * pi;
       tc::tma_store_2d(om + OM_FD, xs, c0, wrow0);
-      tc::tma_store_2d(om + OM_FM, xs + 4096, wrow0, c0);
-      tc::tma_store_2d(om + OM_CD, xs + 8192, c0, wrow0);
-      tc::tma_store_2d(om + OM_CM, xs + 9216, wrow0, c0);
+      tc::tma_store_2d(om + OM_CD, xs + 4096, c0, wrow0);
       tc::bulk_commit();
     }
   }
@@ -1146,8 +1152,8 @@ struct KeyMatEpi {
       // granularity in the inner (column) dimension, so when a row's end is
       // not 16-byte aligned for uint16 (n % 8 != 0) the chunks that cross it
       // take the per-thread path, which never touches the padding columns.
-      if (upper && E.tma && ((E.tma & 2) || (c0 + CW <= T.col0 + T.rb && wrow0 + 32 <= T.row0 + T.ra))) {
-        tma_chunk(s, T.pi, c0, wrow0, v, lane, ent, xp);
+      if (upper && E.tma && ((E.tma & 2) || c0 + CW <= T.col0 + T.rb)) {
+        tma_chunk(s, T.pi, c0, wrow0, ncols, v, lane, ent, xp, E);
         return;
       }
       if (lane == 0) tc::bulk_wait_read0();   // the staging buffer is about to be reused by the path below
@@ -1340,8 +1346,8 @@ static void tc_gemm(int64_t grid, const tc::Batch& batch, const tc::Maps& maps, 
         batch, maps, tiles, k);
 }
 // the (epilogue mode, geometry) instantiations a launch can pick.  Matrices
-// (NUM | SIM) on CTA pairs: 8 epilogue warps with TMA tensor stores (10 KB of
-// staging per warp, 4 pipeline stages beside it); one CTA: 16 or 8 warps.
+// (NUM | SIM): 8 (default) or 16 epilogue warps; on CTA pairs the direct halves
+// leave by TMA tensor stores (5 KB of staging per warp).
 template <bool FP4, int CG>
 static sa_status tc_configure_all() {
   constexpr int CW_ALL = FP4 ? 16 : 32;
@@ -1350,8 +1356,7 @@ static sa_status tc_configure_all() {
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_KEYS>, 8, CW_ALL, FP4, CG>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM>, 16, 16, FP4, CG>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_SIM>, 16, 16, FP4, CG>();
-  if constexpr (CG == 1)
-    if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4, CG>();
+  if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4, CG>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_NUM | EPI_SIM>, 8, 16, FP4, CG>();
   if (cs == SA_OK) cs = tc_configure<KeyMatEpi<EPI_KEYS | EPI_NUM>, 8, CW_ALL, FP4, CG>();
   return cs;
@@ -1366,9 +1371,9 @@ static void tc_gemm_mode(int mode, int keysw, int matsw, int64_t grid, const tc:
   else if (mode == EPI_KEYS) tc_gemm<KeyMatEpi<EPI_KEYS>, 8, CW_ALL, FP4, CG>(grid, batch, maps, tiles, epi, st);
   else if (mode == EPI_NUM) tc_gemm<KeyMatEpi<EPI_NUM>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
   else if (mode == EPI_SIM) tc_gemm<KeyMatEpi<EPI_SIM>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
-  else if ((mode & EPI_KEYS) == 0 && matsw != 8 && CG == 1) {
-    if constexpr (CG == 1) tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
-  } else if ((mode & EPI_KEYS) == 0)
+  else if ((mode & EPI_KEYS) == 0 && matsw != 8)
+    tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 16, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
+  else if ((mode & EPI_KEYS) == 0)
     tc_gemm<KeyMatEpi<EPI_NUM | EPI_SIM>, 8, 16, FP4, CG>(grid, batch, maps, tiles, epi, st);
   else tc_gemm<KeyMatEpi<EPI_KEYS | EPI_NUM>, 8, CW_ALL, FP4, CG>(grid, batch, maps, tiles, epi, st);   // never with F
 }
@@ -1430,7 +1435,7 @@ static EpiGeo epi_geo(int mode, int keysw, int matsw, bool fp4, bool pairs) {
   const int cw_all = fp4 ? 16 : 32;
   if (mode == EPI_KEYS) return keysw == 16 ? EpiGeo{16, 16} : keysw == 12 ? EpiGeo{12, 16} : EpiGeo{8, cw_all};
   if (mode == EPI_NUM || mode == EPI_SIM) return {16, 16};
-  if ((mode & EPI_KEYS) == 0) return (matsw != 8 && !pairs) ? EpiGeo{16, 16} : EpiGeo{8, 16};
+  if ((mode & EPI_KEYS) == 0) return matsw != 8 ? EpiGeo{16, 16} : EpiGeo{8, 16};
   return {8, cw_all};
 }
 
@@ -1493,10 +1498,10 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     const int w = e ? atoi(e) : 16;
     return w == 8 || w == 12 ? w : 16;
   }();
-  const int matsw = [] {   // matrix-epilogue warps, one CTA: 16 (default) or 8; CTA pairs: 8
+  const int matsw = [] {   // matrix-epilogue warps: 8 (default; config 4 S5 GEMM 3.59 ms vs 3.92 with 16) or 16
     const char* e = getenv("SA_K2T_MATSW");
-    const int w = e ? atoi(e) : 16;
-    return w == 8 ? 8 : 16;
+    const int w = e ? atoi(e) : 8;
+    return w == 16 ? 16 : 8;
   }();
   const bool sp_on = sparse_enabled() && bins <= SP_BINS;
   const int spec = sp_on ? 1 : TC_SPEC_MAX;   // dense layers the histogram pass writes
@@ -1843,11 +1848,7 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
         CUtensorMap* om = epi.omap + OM_N * q;
         SA_TRY(tc_encode_out(om + OM_FD, E.sim, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, P.na, P.nb, P.ld, 16, 32,
                              CU_TENSOR_MAP_SWIZZLE_128B));
-        SA_TRY(tc_encode_out(om + OM_FM, E.sim, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, P.na, P.nb, P.ld, 32, 16,
-                             CU_TENSOR_MAP_SWIZZLE_NONE));
         SA_TRY(tc_encode_out(om + OM_CD, E.num, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, P.na, P.nb, P.ld, 16, 32,
-                             CU_TENSOR_MAP_SWIZZLE_NONE));
-        SA_TRY(tc_encode_out(om + OM_CM, E.num, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, P.na, P.nb, P.ld, 32, 16,
                              CU_TENSOR_MAP_SWIZZLE_NONE));
         E.tma = 1 | (P.nb % 8 == 0 ? 2 : 0);   // bit 1: every row end 16-byte aligned (no edge fallback)
       }
