@@ -1105,14 +1105,14 @@ struct KeyMatEpi {
       const double2 yd = *reinterpret_cast<const double2*>(ent + j * TAB_BYTES + YOFF);
       F[j] = fsel_dbg(C, s.y, s.d, yd.x, yd.y);
     }
-    if (s.rv && !(dbg & 8)) {
+    if (s.rv && !(dbg & (8 | 512))) {   // (SA_K2T_DEBUG 512 / 1024: experiments, mirror / C stores skipped)
       double* fm = E.sim + (int64_t)c0 * E.ld + s.row_g;
       uint16_t* cmr = E.num + (int64_t)c0 * E.ld + s.row_g;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         if (j < ncols) {
           __stcs(fm + (int64_t)j * E.ld, F[j]);
-          __stcs(reinterpret_cast<unsigned short*>(cmr + (int64_t)j * E.ld), (unsigned short)v[j]);
+          if (!(dbg & 1024)) __stcs(reinterpret_cast<unsigned short*>(cmr + (int64_t)j * E.ld), (unsigned short)v[j]);
         }
       }
     }
@@ -1129,7 +1129,7 @@ struct KeyMatEpi {
       const uint32_t xs = tc::s_addr(xp);
       const CUtensorMap* om = omap + OM_N * pi;
       tc::tma_store_2d(om + OM_FD, xs, c0, wrow0);
-      tc::tma_store_2d(om + OM_CD, xs + 4096, c0, wrow0);
+      if (!(dbg & 1024)) tc::tma_store_2d(om + OM_CD, xs + 4096, c0, wrow0);
       tc::bulk_commit();
     }
   }
