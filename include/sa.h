@@ -335,10 +335,25 @@ sa_status sa_bucket_similarity_batch(sa_ctx* ctx, int32_t nbuckets, const uint16
  * IEEE round-to-nearest on every operation; merge height (1 - F_ab) / 2.
  * Inputs: similarity [n][ld] (device, row-major, symmetric; the diagonal is
  * ignored).  Outputs (device): merges [n-1][2] (a, b), heights [n-1], in
- * merge order (n = 1: nothing written).  One CTA runs the merges (they are
- * sequential); O(n^2) work.  SA_E_INVAL: n < 1, ld < n, NULL pointers. */
+ * merge order (n = 1: nothing written).  The merges are sequential; each
+ * is O(n): n < 1024 runs them on one CTA, larger n on every SM of the device
+ * (one cooperative launch, two device-wide barriers per merge; the same IEEE
+ * operations and tie orders, so the same tree; SA_UPGMA_GRID=0/1 forces
+ * either).  O(n^2) work, n^2 + O(n) doubles of scratch.  SA_E_INVAL: n < 1,
+ * ld < n, NULL pointers. */
 sa_status sa_guide_tree(sa_ctx* ctx, const double* similarity, int32_t n, int64_t ld, int32_t* merges,
                         double* heights, void* stream);
+
+/* The guide trees of `count` buckets at once (same definition and outputs as
+ * sa_guide_tree, tree i from similarity_h[i] [n_h[i]][ld_h[i]] into
+ * merges_h[i] / heights_h[i]): one cooperative launch whose resident blocks
+ * are shared out among the trees in proportion to n^2, each tree merging on
+ * its own blocks with its own barriers -- the trees' sequential merge chains
+ * run side by side.  Host arrays of device pointers; n = 1 trees are
+ * skipped.  Synchronises `stream` before returning (the launch's task table
+ * is host-built).  SA_E_INVAL: count < 0, bad n / ld, NULL pointers. */
+sa_status sa_guide_tree_batch(sa_ctx* ctx, int32_t count, const double* const* similarity_h, const int32_t* n_h,
+                              const int64_t* ld_h, int32_t* const* merges_h, double* const* heights_h, void* stream);
 
 /* Packed upper triangle (diagonal included) of a symmetric n x n uint16
  * matrix with row stride ld >= n: row i's columns i..n-1 at packed offset

@@ -29,6 +29,7 @@ EXPORTED = ["sa_ctx_create", "sa_ctx_attach_comm", "sa_ctx_destroy", "sa_last_er
             "sa_partition", "sa_redistribute", "sa_bucket_similarity", "sa_exact_rank_compare", "sa_ctx_engine",
             "sa_ctx_set_rank_form", "sa_ctx_tc_columns", "sa_ctx_tc_operand", "sa_selftest_f_division",
             "sa_bucket_similarity_batch", "sa_pack_upper_u16", "sa_pack_upper_f64", "sa_guide_tree",
+            "sa_guide_tree_batch",
             "sa_ctx_phase_history", "sa_ctx_tc_sparse", "sa_nccl_unique_id", "sa_ctx_attach_nccl", "sa_ctx_check"]
 SA_RANK_F, SA_RANK_DF = 0, 1
 
@@ -105,6 +106,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "sa_pack_upper_f64": (ctypes.c_int, [P, P, I32, ctypes.c_int64, P, VP]),
         "sa_ctx_phase_history": (ctypes.c_int32, [P, ctypes.c_int32, ctypes.POINTER(ctypes.c_float), ctypes.c_int32]),
         "sa_guide_tree": (ctypes.c_int, [P, P, I32, ctypes.c_int64, P, P, VP]),
+        "sa_guide_tree_batch": (ctypes.c_int, [P, I32, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_int32),
+                                               ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_void_p),
+                                               ctypes.POINTER(ctypes.c_void_p), VP]),
         "sa_ctx_engine": (ctypes.c_int, [P]),
         "sa_ctx_tc_columns": (ctypes.c_int32, [P, P, ctypes.c_int32]),
         "sa_ctx_tc_operand": (ctypes.c_int, [P]),
@@ -491,6 +495,29 @@ def sa_guide_tree(ctx: Context, similarity: torch.Tensor, stream=None):
     _check(load_library().sa_guide_tree(ctx.handle, ctypes.c_void_p(similarity.data_ptr()), n, similarity.stride(0),
                                         _ptr(merges), _ptr(heights), _stream(stream)))
     return merges, heights
+
+
+def sa_guide_tree_batch(ctx: Context, similarities, stream=None):
+    """N4 for several buckets in one launch (sa.h sa_guide_tree_batch): a list
+    of n x n fp64 CUDA views; returns [(merges, heights)] in the same order."""
+    sims = list(similarities)
+    for t in sims:
+        if t.dtype != torch.float64 or not t.is_cuda or t.dim() != 2 or t.shape[0] != t.shape[1] \
+                or t.stride(1) != 1:
+            raise ValueError("similarity must be an n x n float64 CUDA tensor with contiguous rows")
+    k = len(sims)
+    outs = []
+    for t in sims:
+        n = t.shape[0]
+        outs.append((torch.empty((max(n - 1, 0), 2), dtype=torch.int32, device=t.device),
+                     torch.empty(max(n - 1, 0), dtype=torch.float64, device=t.device)))
+    arr = lambda xs: (ctypes.c_void_p * max(k, 1))(*xs)  # noqa: E731
+    ns = (ctypes.c_int32 * max(k, 1))(*[t.shape[0] for t in sims])
+    lds = (ctypes.c_int64 * max(k, 1))(*[t.stride(0) for t in sims])
+    _check(load_library().sa_guide_tree_batch(ctx.handle, k, arr([t.data_ptr() for t in sims]), ns, lds,
+                                              arr([m.data_ptr() for m, _ in outs]),
+                                              arr([h.data_ptr() for _, h in outs]), _stream(stream)))
+    return outs
 
 
 def _pack_upper(fn: str, dtype, ctx: Context, matrix: torch.Tensor, packed: torch.Tensor | None, stream):

@@ -1213,6 +1213,22 @@ sa_status sa_guide_tree(sa_ctx* ctx, const double* similarity, int32_t n, int64_
   return upgma_launch(similarity, n, ld, merges, heights, (cudaStream_t)stream);
 }
 
+sa_status sa_guide_tree_batch(sa_ctx* ctx, int32_t count, const double* const* similarity_h, const int32_t* n_h,
+                              const int64_t* ld_h, int32_t* const* merges_h, double* const* heights_h, void* stream) {
+  g_err.clear();
+  if (!ctx) return fail(SA_E_INVAL, "ctx is NULL");
+  if (count < 0) return fail(SA_E_INVAL, "count < 0");
+  if (count == 0) return SA_OK;
+  if (!similarity_h || !n_h || !ld_h || !merges_h || !heights_h) return fail(SA_E_INVAL, "NULL required pointer");
+  for (int i = 0; i < count; ++i) {
+    if (n_h[i] < 1 || ld_h[i] < n_h[i]) return fail(SA_E_INVAL, "tree %d: bad n / ld", i);
+    if (n_h[i] > 1 && (!similarity_h[i] || !merges_h[i] || !heights_h[i]))
+      return fail(SA_E_INVAL, "tree %d: NULL required pointer", i);
+  }
+  SA_CUDA(cudaSetDevice(ctx->device));
+  return upgma_launch_batch(count, similarity_h, n_h, ld_h, merges_h, heights_h, (cudaStream_t)stream);
+}
+
 }  // extern "C"
 namespace sa {
 template <class T>

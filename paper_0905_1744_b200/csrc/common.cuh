@@ -165,6 +165,8 @@ constexpr int TC_MAX_BINS = 8192;
 sa_status f_division_selftest(int64_t* mismatches_h);
 // N4: UPGMA guide tree of an n x n similarity matrix (tree.cu)
 sa_status upgma_launch(const double* F, int32_t n, int64_t ld, int32_t* merges, double* heights, cudaStream_t st);
+sa_status upgma_launch_batch(int count, const double* const* F, const int32_t* n, const int64_t* ld,
+                             int32_t* const* merges, double* const* heights, cudaStream_t st);
 bool tc_fp4_operands();   // K2T operand format for the next launch: true = packed e2m1 (kind::mxf4), false = u8
 bool tc_last_fp4();       // the format of the last K2T launch
 // sim[i][j] = num[i][j] / min(nkA[i], nkB[j]) (fp64, IEEE RN; 0 when the min is 0), row stride ld.

@@ -226,13 +226,16 @@ def test_pack_upper_u16(ctx, n, ld_align):
     assert np.array_equal(packed, Co[np.triu_indices(n)])
 
 
+@pytest.mark.parametrize("grid", ["0", "1"])
 @pytest.mark.parametrize("n,seed,ties", [(1, 0, False), (2, 1, False), (3, 2, False), (57, 3, False),
                                          (300, 4, False), (64, 5, True)])
-def test_guide_tree_matches_oracle(ctx, n, seed, ties):
+def test_guide_tree_matches_oracle(ctx, monkeypatch, n, seed, ties, grid):
     """N4: sa_guide_tree on a bucket's S5 similarity matrix (random sets,
     duplicates -> exactly tied similarities) equals the oracle's UPGMA merge
-    for merge and height for height (bit-exact fp64)."""
+    for merge and height for height (bit-exact fp64); both the one-CTA merge
+    loop and the grid-wide cooperative one (SA_UPGMA_GRID)."""
     from oracle import tree
+    monkeypatch.setenv("SA_UPGMA_GRID", grid)
     ds = _rand_set(600 + seed, n, 0, 420, dup=(n // 3 if ties else 0))
     res, offs = to_dev(ds)
     P, nk = B.sa_kmer_profiles(ctx, res, offs)
@@ -243,6 +246,44 @@ def test_guide_tree_matches_oracle(ctx, n, seed, ties):
     mo, ho = tree.upgma(Fo)
     assert np.array_equal(merges.cpu().numpy().astype(np.int64), mo)
     assert np.array_equal(heights.cpu().numpy(), ho)
+
+
+@pytest.mark.parametrize("c", [3, 4])
+def test_guide_tree_grid_equals_one_cta_large(ctx, monkeypatch, c):
+    """A 2 500-member bucket of config 3 / 4 sequences: the grid-wide merge
+    loop and the one-CTA loop (identical IEEE operations and tie orders) build
+    the same tree bit for bit."""
+    ds = generate(CONFIGS[c]).subset(np.arange(2500))
+    res, offs = to_dev(ds)
+    P, nk = B.sa_kmer_profiles(ctx, res, offs)
+    _, sims = B.sa_bucket_similarity_batch(ctx, P, nk, [0, 2500], want_numerators=False, ld_align=16)
+    out = {}
+    for grid in ("0", "1"):
+        monkeypatch.setenv("SA_UPGMA_GRID", grid)
+        m, h = B.sa_guide_tree(ctx, sims[0])
+        out[grid] = (m.cpu().numpy(), h.cpu().numpy())
+    assert np.array_equal(out["0"][0], out["1"][0])
+    assert np.array_equal(out["0"][1], out["1"][1])
+    assert np.all(np.diff(out["1"][1]) >= 0)
+
+
+def test_guide_tree_batch_equals_single(ctx):
+    """sa_guide_tree_batch: trees of mixed sizes (a grid-sized one, one-CTA
+    sized ones, n = 2 and n = 1) built side by side in one launch equal the
+    one-at-a-time trees bit for bit."""
+    ds = generate(CONFIGS[3])
+    sizes = [1800, 700, 130, 2, 1]
+    res, offs = to_dev(ds.subset(np.arange(sum(sizes))))
+    P, nk = B.sa_kmer_profiles(ctx, res, offs)
+    bounds = np.concatenate([[0], np.cumsum(sizes)]).tolist()
+    _, sims = B.sa_bucket_similarity_batch(ctx, P, nk, bounds, want_numerators=False, ld_align=16)
+    outs = B.sa_guide_tree_batch(ctx, sims)
+    assert len(outs) == len(sizes)
+    for sim, (m, h), n in zip(sims, outs, sizes):
+        assert m.shape == (n - 1, 2) and h.shape == (n - 1,)
+        m1, h1 = B.sa_guide_tree(ctx, sim)
+        assert np.array_equal(m.cpu().numpy(), m1.cpu().numpy())
+        assert np.array_equal(h.cpu().numpy(), h1.cpu().numpy())
 
 
 def test_guide_tree_on_a_config_bucket(ctx):
