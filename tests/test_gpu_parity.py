@@ -109,6 +109,25 @@ def test_profiles_errors(ctx):
     assert P.shape[0] == 0 and nk.shape[0] == 0
 
 
+def test_profiles_no_host_sync(ctx):
+    """S1 never blocks the host (sa.h: range errors are sticky device flags,
+    surfaced at ctx.check / C3): with the stream busy behind a ~0.5 s sleep
+    kernel, sa_kmer_profiles returns while the stream is still busy, and its
+    results are the oracle's once the stream drains."""
+    ds = generate(CONFIGS[1])
+    res, offs = to_dev(ds)
+    B.sa_kmer_profiles(ctx, res, offs)      # one-time device setup happens here
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(1_000_000_000)    # ~0.5 s of device time ahead of S1
+        P, nk = B.sa_kmer_profiles(ctx, res, offs, stream=s)
+        busy = not s.query()
+    assert busy, "sa_kmer_profiles waited for its stream"
+    ctx.check(s)                            # the documented host block
+    assert np.array_equal(nk.cpu().numpy(), kmer.profiles(ds.residues, ds.offsets)[1])
+
+
 # --------------------------------------------------------------- S2 ------
 @pytest.mark.parametrize("nq,npool,dup", [(300, 200, 0), (129, 257, 5), (1, 1, 0), (5, 700, 0)])
 def test_kmer_rank_random(ctx, engine, nq, npool, dup):

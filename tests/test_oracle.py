@@ -426,3 +426,68 @@ def test_upgma_matches_scipy_average_linkage():
         assert np.allclose(h, Z[:, 2] / 2.0, rtol=0, atol=1e-12)
         assert np.all(np.diff(h) >= -1e-15)
         assert len(set(m[:, 1].tolist())) == n - 1 and np.all(m[:, 0] < m[:, 1])
+
+
+# ----------------------------------------------------- N4 tree, d^F form ---
+LN2_DIGITS = "0.693147180559945309417232121458176568075500134360255254120680"   # ln 2, 60 digits
+
+
+def test_cr_neg_log_powers_of_two():
+    """-ln(2^k) = -k ln 2: the correctly rounded double from the published
+    digits of ln 2 (decimal multiplication, no log call) equals cr_neg_log."""
+    from decimal import Decimal, localcontext
+    for k in list(range(-60, 61)) + [-1000, 1000]:
+        x = math.ldexp(1.0, k)
+        with localcontext() as c:
+            c.prec = 60
+            want = float(-k * Decimal(LN2_DIGITS))
+        assert tree.cr_neg_log(x) == want, k
+
+
+def test_cr_neg_log_against_libm():
+    """Within 1 ulp of libm's log everywhere (libm is not correctly rounded,
+    so 1 ulp is the bound, not 0), exactly +0 at x = 1, and monotone."""
+    rng = np.random.default_rng(11)
+    xs = np.concatenate([rng.uniform(0.02, 1.02, 3000), [0.02, 1.0, 1.02, 0.5 + 2 ** -40]])
+    prev = None
+    for x in sorted(xs.tolist()):
+        d = tree.cr_neg_log(x)
+        ref = -math.log(x)
+        assert abs(d - ref) <= math.ulp(ref) or d == ref, x
+        if prev is not None:
+            assert d <= prev
+        prev = d
+    assert math.copysign(1.0, tree.cr_neg_log(1.0)) == 1.0
+
+
+def test_upgma_dF_spec_examples():
+    """SPEC build_guide_tree in Eq. 2's distance: two sequences ->
+    one merge at height d^F/2; d(A,B) < d(A,C) = d(B,C) -> (A, B) first; F = 1
+    - Delta gives d = 0."""
+    F2 = np.array([[1.0, 0.3], [0.3, 1.0]])
+    m, h = tree.upgma_dF(F2, 0.02)
+    assert m.tolist() == [[0, 1]] and h[0] == tree.cr_neg_log(0.32) / 2.0
+    F3 = np.array([[1.0, 0.8, 0.2], [0.8, 1.0, 0.2], [0.2, 0.2, 1.0]])
+    m, h = tree.upgma_dF(F3, 0.02)
+    assert m.tolist() == [[0, 1], [0, 2]]
+    d = tree.dF_matrix(np.array([[1.0, 0.98], [0.98, 1.0]]), 0.02)
+    assert d[0, 1] == 0.0 and math.copysign(1.0, d[0, 1]) == 1.0
+
+
+def test_upgma_distance_matches_scipy_average_linkage():
+    """upgma_distance = average linkage: heights equal scipy's on the d^F matrix
+    of tie-free random similarities; merge order follows the smallest d."""
+    from scipy.cluster.hierarchy import linkage
+    from scipy.spatial.distance import squareform
+    rng = np.random.default_rng(6)
+    for n in (3, 9, 30):
+        A = rng.random((n, n))
+        F = (A + A.T) / 2
+        np.fill_diagonal(F, 1.0)
+        D = tree.dF_matrix(F, 0.02)
+        m, h = tree.upgma_distance(D)
+        Z = linkage(squareform(D, checks=False), method="average")
+        assert np.allclose(h, Z[:, 2] / 2.0, rtol=0, atol=1e-12)
+        assert np.all(np.diff(h) >= -1e-15)
+        # the d^F order reverses F's: on a 2-cluster matrix the same first merge as upgma(F)
+        assert m[0].tolist() == tree.upgma(F)[0][0].tolist()
