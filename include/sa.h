@@ -335,7 +335,9 @@ sa_status sa_bucket_similarity_batch(sa_ctx* ctx, int32_t nbuckets, const uint16
  * IEEE round-to-nearest on every operation; merge height (1 - F_ab) / 2.
  * Inputs: similarity [n][ld] (device, row-major, symmetric; the diagonal is
  * ignored).  Outputs (device): merges [n-1][2] (a, b), heights [n-1], in
- * merge order (n = 1: nothing written).  The merges are sequential; each
+ * merge order (n = 1: nothing written).  The distance is the context's tree
+ * form (sa_ctx_set_tree_form below; default d = 1 - F, heights (1 - F_ab) / 2
+ * as above).  The merges are sequential; each
  * is O(n): n < 1024 runs them on one CTA, larger n on every SM of the device
  * (one cooperative launch, two device-wide barriers per merge; the same IEEE
  * operations and tie orders, so the same tree; SA_UPGMA_GRID=0/1 forces
@@ -343,6 +345,26 @@ sa_status sa_bucket_similarity_batch(sa_ctx* ctx, int32_t nbuckets, const uint16
  * ld < n, NULL pointers. */
 sa_status sa_guide_tree(sa_ctx* ctx, const double* similarity, int32_t n, int64_t ld, int32_t* merges,
                         double* heights, void* stream);
+
+/* N4's distance (reading T4):
+ *   SA_TREE_F  (default, reading T1): d = 1 - F -- UPGMA is then average
+ *              linkage on F itself, every decision IEEE arithmetic on F;
+ *   SA_TREE_DF (Eq. 2; "Eq. 2 distances"): d_ij =
+ *              CR(-ln(RN(Delta + F_ij))), the double nearest the real -ln of
+ *              the once-rounded Delta + F; UPGMA on d as above with "largest
+ *              F" read as "smallest d", d(ab, c) = RN(RN(RN(n_a d_ac) +
+ *              RN(n_b d_bc)) / (n_a + n_b)), height d_ab / 2.
+ * The log is evaluated in double-double (~2^-100 relative error) and rounded
+ * once; an element whose double-double value lies too close to a rounding
+ * boundary to certify the rounding keeps the nearest double and is counted
+ * (sa_ctx_tree_uncertified) -- the window treatment of N1.  Applies to
+ * sa_guide_tree and sa_guide_tree_batch.  SA_E_INVAL: unknown form, Delta <=
+ * 0 or not finite for SA_TREE_DF. */
+enum { SA_TREE_F = 0, SA_TREE_DF = 1 };
+sa_status sa_ctx_set_tree_form(sa_ctx* ctx, int form, double delta);
+/* Uncertified correctly-rounded logs of the last tree call (0 for SA_TREE_F).
+ * Blocks on `stream` (the stream of that call). */
+sa_status sa_ctx_tree_uncertified(sa_ctx* ctx, int64_t* count_h, void* stream);
 
 /* The guide trees of `count` buckets at once (same definition and outputs as
  * sa_guide_tree, tree i from similarity_h[i] [n_h[i]][ld_h[i]] into

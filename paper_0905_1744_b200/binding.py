@@ -29,9 +29,10 @@ EXPORTED = ["sa_ctx_create", "sa_ctx_attach_comm", "sa_ctx_destroy", "sa_last_er
             "sa_partition", "sa_redistribute", "sa_bucket_similarity", "sa_exact_rank_compare", "sa_ctx_engine",
             "sa_ctx_set_rank_form", "sa_ctx_tc_columns", "sa_ctx_tc_operand", "sa_selftest_f_division",
             "sa_bucket_similarity_batch", "sa_pack_upper_u16", "sa_pack_upper_f64", "sa_guide_tree",
-            "sa_guide_tree_batch",
+            "sa_guide_tree_batch", "sa_ctx_set_tree_form", "sa_ctx_tree_uncertified",
             "sa_ctx_phase_history", "sa_ctx_tc_sparse", "sa_nccl_unique_id", "sa_ctx_attach_nccl", "sa_ctx_check"]
 SA_RANK_F, SA_RANK_DF = 0, 1
+SA_TREE_F, SA_TREE_DF = 0, 1
 
 
 class SaError(RuntimeError):
@@ -118,6 +119,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "sa_ctx_check": (ctypes.c_int, [P, VP]),
         "sa_selftest_f_division": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(ctypes.c_int64)]),
         "sa_ctx_set_rank_form": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_double]),
+        "sa_ctx_set_tree_form": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_double]),
+        "sa_ctx_tree_uncertified": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_int64), VP]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -244,6 +247,16 @@ class Context:
     def set_rank_form(self, form: int = SA_RANK_F, delta: float = 0.02):
         """SA_RANK_F (mean F, exact) or SA_RANK_DF (mean -ln(Delta + F), Eq. 2-3)."""
         _check(load_library().sa_ctx_set_rank_form(self.handle, int(form), float(delta)))
+
+    def set_tree_form(self, form: int = SA_TREE_F, delta: float = 0.02):
+        """N4's distance: SA_TREE_F (d = 1 - F) or SA_TREE_DF (d = CR(-ln(Delta + F)), Eq. 2)."""
+        _check(load_library().sa_ctx_set_tree_form(self.handle, int(form), float(delta)))
+
+    def tree_uncertified(self, stream=None) -> int:
+        """Uncertified correctly-rounded logs of the last tree call (blocks)."""
+        v = ctypes.c_int64(0)
+        _check(load_library().sa_ctx_tree_uncertified(self.handle, ctypes.byref(v), _stream(stream)))
+        return int(v.value)
 
     def tc_sparse(self) -> list[tuple[int, int]]:
         """(mode, correction terms) of each problem of the last K2T call:

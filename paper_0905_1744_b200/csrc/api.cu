@@ -77,6 +77,15 @@ static inline int64_t block_begin(int64_t q, int64_t N, int64_t p) { return q * 
 
 static int32_t profile_stride(int32_t bins) { return stride_u16(bins); }
 
+// tree form of the context (sa_ctx_set_tree_form)
+static inline TreeForm tree_form_of(const sa_ctx* c) {
+  TreeForm t;
+  t.form = c->tree_form;
+  t.delta = c->tree_delta;
+  t.unc = c->tree_unc;
+  return t;
+}
+
 // rank form of the context onto a key-producing problem (sa_ctx_set_rank_form)
 static inline void apply_form(const sa_ctx* c, MsProblem& pr) {
   pr.form = c->rank_form;
@@ -262,8 +271,8 @@ sa_status sa_ctx_create(int cuda_device, sa_ctx** out) {
   }
   sa_ctx* c = new sa_ctx();
   c->device = cuda_device;
-  if (cudaMalloc(&c->dcount, SA_DCOUNT_WORDS * 4) != cudaSuccess || cudaMalloc(&c->derr, 16) != cudaSuccess ||
-      cudaMemset(c->derr, 0, 16) != cudaSuccess ||
+  if (cudaMalloc(&c->dcount, SA_DCOUNT_WORDS * 4) != cudaSuccess || cudaMalloc(&c->derr, 32) != cudaSuccess ||
+      cudaMemset(c->derr, 0, 32) != cudaSuccess ||
       cudaHostAlloc(&c->hpinned, SA_DCOUNT_WORDS * 4, cudaHostAllocDefault) != cudaSuccess ||
       cudaHostAlloc(&c->hstage, SA_STAGE_BYTES, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
       cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->dstage), c->hstage, 0) != cudaSuccess) {
@@ -271,6 +280,7 @@ sa_status sa_ctx_create(int cuda_device, sa_ctx** out) {
     delete c;
     return fail(SA_E_NOMEM, "context allocation failed");
   }
+  c->tree_unc = reinterpret_cast<unsigned long long*>(c->derr + 4);
   *out = c;
   return SA_OK;
 }
@@ -339,6 +349,27 @@ sa_status sa_ctx_destroy(sa_ctx* ctx) {
   if (ctx->hpinned) cudaFreeHost(ctx->hpinned);
   if (ctx->hstage) cudaFreeHost(ctx->hstage);
   delete ctx;
+  return SA_OK;
+}
+
+sa_status sa_ctx_set_tree_form(sa_ctx* ctx, int form, double delta) {
+  g_err.clear();
+  if (!ctx) return fail(SA_E_INVAL, "ctx is NULL");
+  if (form != SA_TREE_F && form != SA_TREE_DF) return fail(SA_E_INVAL, "unknown tree form %d", form);
+  if (form == SA_TREE_DF && !(delta > 0.0 && std::isfinite(delta))) return fail(SA_E_INVAL, "Delta must be > 0");
+  ctx->tree_form = form;
+  if (form == SA_TREE_DF) ctx->tree_delta = delta;
+  return SA_OK;
+}
+
+sa_status sa_ctx_tree_uncertified(sa_ctx* ctx, int64_t* count_h, void* stream) {
+  g_err.clear();
+  if (!ctx || !count_h) return fail(SA_E_INVAL, "NULL argument");
+  SA_CUDA(cudaSetDevice(ctx->device));
+  unsigned long long v = 0;
+  SA_CUDA(cudaMemcpyAsync(&v, ctx->tree_unc, sizeof v, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  SA_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  *count_h = (int64_t)v;
   return SA_OK;
 }
 
@@ -1207,10 +1238,9 @@ sa_status sa_guide_tree(sa_ctx* ctx, const double* similarity, int32_t n, int64_
   g_err.clear();
   if (!ctx) return fail(SA_E_INVAL, "ctx is NULL");
   if (n < 1 || ld < n) return fail(SA_E_INVAL, "bad n / ld");
-  if (n == 1) return SA_OK;
-  if (!similarity || !merges || !heights) return fail(SA_E_INVAL, "NULL required pointer");
+  if (n > 1 && (!similarity || !merges || !heights)) return fail(SA_E_INVAL, "NULL required pointer");
   SA_CUDA(cudaSetDevice(ctx->device));
-  return upgma_launch(similarity, n, ld, merges, heights, (cudaStream_t)stream);
+  return upgma_launch(similarity, n, ld, merges, heights, tree_form_of(ctx), (cudaStream_t)stream);
 }
 
 sa_status sa_guide_tree_batch(sa_ctx* ctx, int32_t count, const double* const* similarity_h, const int32_t* n_h,
@@ -1226,7 +1256,8 @@ sa_status sa_guide_tree_batch(sa_ctx* ctx, int32_t count, const double* const* s
       return fail(SA_E_INVAL, "tree %d: NULL required pointer", i);
   }
   SA_CUDA(cudaSetDevice(ctx->device));
-  return upgma_launch_batch(count, similarity_h, n_h, ld_h, merges_h, heights_h, (cudaStream_t)stream);
+  return upgma_launch_batch(count, similarity_h, n_h, ld_h, merges_h, heights_h, tree_form_of(ctx),
+                            (cudaStream_t)stream);
 }
 
 }  // extern "C"

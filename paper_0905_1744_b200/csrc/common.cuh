@@ -164,9 +164,17 @@ sa_status to_u8_launch(const uint16_t* p16, int64_t n, int32_t stride16, int32_t
 constexpr int TC_MAX_BINS = 8192;
 sa_status f_division_selftest(int64_t* mismatches_h);
 // N4: UPGMA guide tree of an n x n similarity matrix (tree.cu)
-sa_status upgma_launch(const double* F, int32_t n, int64_t ld, int32_t* merges, double* heights, cudaStream_t st);
+// N4 distance form: SA_TREE_F (d = 1 - F) or SA_TREE_DF (d = CR(-ln(Delta + F)); uncertified
+// correctly-rounded logs are counted into *unc)
+struct TreeForm {
+  int form = SA_TREE_F;
+  double delta = 0.02;
+  unsigned long long* unc = nullptr;
+};
+sa_status upgma_launch(const double* F, int32_t n, int64_t ld, int32_t* merges, double* heights, const TreeForm& tf,
+                       cudaStream_t st);
 sa_status upgma_launch_batch(int count, const double* const* F, const int32_t* n, const int64_t* ld,
-                             int32_t* const* merges, double* const* heights, cudaStream_t st);
+                             int32_t* const* merges, double* const* heights, const TreeForm& tf, cudaStream_t st);
 bool tc_fp4_operands();   // K2T operand format for the next launch: true = packed e2m1 (kind::mxf4), false = u8
 bool tc_last_fp4();       // the format of the last K2T launch
 // sim[i][j] = num[i][j] / min(nkA[i], nkB[j]) (fp64, IEEE RN; 0 when the min is 0), row stride ld.
@@ -258,6 +266,9 @@ struct sa_ctx {
   int last_tc_probs = 0;        // problems of that K2T call
   int rank_form = SA_RANK_F;    // sa_ctx_set_rank_form
   double delta = 0.02;
+  int tree_form = SA_TREE_F;    // sa_ctx_set_tree_form
+  double tree_delta = 0.02;
+  unsigned long long* tree_unc = nullptr;   // device (inside derr's block): uncertified d^F logs of the last tree call
   uint32_t* dcount = nullptr;   // device: largest count of the last auto-dispatched call
   uint32_t* hpinned = nullptr;  // pinned host word for small readbacks
   // mapped pinned staging for the hot path's small readbacks (d2h_small): a

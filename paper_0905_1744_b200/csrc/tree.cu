@@ -17,6 +17,7 @@
 // bucket takes ~1.5 s (tools/tree_bench.py): ~120 us per merge, three
 // latency-bound passes over n entries on one SM.
 #include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include "common.cuh"
@@ -34,6 +35,113 @@ __device__ __forceinline__ bool pair_better(double v1, int a1, int b1, double v2
   if (v1 != v2) return v1 > v2;
   if (a1 != a2) return a1 < a2;
   return b1 < b2;
+}
+
+// ----------------------------------------------- d^F form (reading T4) ----
+// The working matrix of the d^F tree holds S = -d = CR(ln(RN(Delta + F))):
+// UPGMA's "smallest d" is then the same "largest S" the merge kernels look
+// for, and negation commutes with every RN operation of the update, so the
+// merges and heights (h0 = 0: height = -S / 2 = d / 2) are the d-space ones.
+// ln in double-double: x = m 2^e, m in [1/sqrt2, sqrt2), ln m = 2 atanh(s),
+// s = (m - 1) / (m + 1), |s| <= 0.1716, 21 terms of sum s^(2k+1) / (2k+1)
+// (truncation < 2^-104 relative), plus e ln 2; every step an error-free
+// transform or a double-double operation (relative error ~2^-104 each), so
+// the result is within 2^-96 |ln x| (a generous bound) of the real value.
+struct dd {
+  double hi, lo;
+};
+__device__ __forceinline__ dd dd_two_sum(double a, double b) {
+  const double s = __dadd_rn(a, b), bb = __dadd_rn(s, -a);
+  return {s, __dadd_rn(__dadd_rn(a, -__dadd_rn(s, -bb)), __dadd_rn(b, -bb))};
+}
+__device__ __forceinline__ dd dd_fast_two_sum(double a, double b) {   // |a| >= |b|
+  const double s = __dadd_rn(a, b);
+  return {s, __dadd_rn(b, -__dadd_rn(s, -a))};
+}
+__device__ __forceinline__ dd dd_add(dd a, dd b) {
+  dd s = dd_two_sum(a.hi, b.hi);
+  const dd t = dd_two_sum(a.lo, b.lo);
+  s.lo = __dadd_rn(s.lo, t.hi);
+  s = dd_fast_two_sum(s.hi, s.lo);
+  s.lo = __dadd_rn(s.lo, t.lo);
+  return dd_fast_two_sum(s.hi, s.lo);
+}
+__device__ __forceinline__ dd dd_mul(dd a, dd b) {
+  const double p = __dmul_rn(a.hi, b.hi);
+  double e = __fma_rn(a.hi, b.hi, -p);
+  e = __fma_rn(a.hi, b.lo, e);
+  e = __fma_rn(a.lo, b.hi, e);
+  return dd_fast_two_sum(p, e);
+}
+__device__ __forceinline__ dd dd_div(dd a, dd b) {
+  const double q1 = __ddiv_rn(a.hi, b.hi);
+  dd r = dd_add(a, dd_mul(dd{-q1, 0.0}, b));
+  const double q2 = __ddiv_rn(r.hi, b.hi);
+  r = dd_add(r, dd_mul(dd{-q2, 0.0}, b));
+  const double q3 = __ddiv_rn(r.hi, b.hi);
+  return dd_add(dd_fast_two_sum(q1, q2), dd{q3, 0.0});
+}
+
+constexpr int LN_TERMS = 21;
+__constant__ dd c_inv_odd[LN_TERMS];   // 1 / (2k + 1) in double-double
+static DeviceOnce g_ln_once;
+
+static sa_status ensure_ln_table() {
+  return g_ln_once.run([]() -> sa_status {
+    dd h[LN_TERMS];
+    for (int k = 0; k < LN_TERMS; ++k) {
+      const double d = 2.0 * k + 1.0;
+      h[k].hi = 1.0 / d;
+      h[k].lo = std::fma(-h[k].hi, d, 1.0) / d;   // the remainder 1 - hi d is exact
+    }
+    SA_CUDA(cudaMemcpyToSymbol(c_inv_odd, h, sizeof h));
+    return SA_OK;
+  });
+}
+
+// CR(ln x) for a finite x > 0; *certified = the rounding is proven correct
+__device__ double cr_log(double x, bool* certified) {
+  int e;
+  double m = frexp(x, &e);   // [0.5, 1)
+  if (m < 0.70710678118654752440) {
+    m = __dmul_rn(m, 2.0);
+    e -= 1;
+  }
+  const double num = __dadd_rn(m, -1.0);   // exact (Sterbenz)
+  const dd s = dd_div(dd{num, 0.0}, dd_two_sum(m, 1.0));
+  const dd s2 = dd_mul(s, s);
+  dd p = c_inv_odd[LN_TERMS - 1];
+  for (int k = LN_TERMS - 2; k >= 0; --k) p = dd_add(dd_mul(p, s2), c_inv_odd[k]);
+  dd r = dd_mul(s, p);
+  r.hi = __dmul_rn(r.hi, 2.0);
+  r.lo = __dmul_rn(r.lo, 2.0);
+  const dd ln2 = {6.93147180559945286227e-01, 2.31904681384629955842e-17};
+  r = dd_add(dd_mul(ln2, dd{(double)e, 0.0}), r);
+  // certified iff [r - E, r + E] stays between the midpoints around r.hi
+  const double E = ldexp(fabs(r.hi), -96);
+  const double up = __dadd_rn(nextafter(r.hi, 1.0 / 0.0), -r.hi);
+  const double dn = __dadd_rn(r.hi, -nextafter(r.hi, -1.0 / 0.0));
+  *certified = r.hi == 0.0 ? r.lo == 0.0
+                           : (__dadd_rn(r.lo, E) < __dmul_rn(up, 0.5) && __dadd_rn(r.lo, -E) > -__dmul_rn(dn, 0.5));
+  return r.hi;
+}
+
+__global__ void dF_matrix_kernel(const double* __restrict__ F, int64_t ldf, int n, double delta,
+                                 double* __restrict__ S, int64_t lds, unsigned long long* __restrict__ unc) {
+  unsigned long long bad = 0;
+  const int64_t total = (int64_t)n * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / n, j = t - i * n;
+    double v = 0.0;
+    if (i != j) {
+      bool ok;
+      v = cr_log(__dadd_rn(delta, F[i * ldf + j]), &ok);
+      bad += ok ? 0 : 1;
+    }
+    S[i * lds + j] = v;
+  }
+  for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(unc, bad);
 }
 
 // first row-bests: one warp per row
@@ -99,7 +207,7 @@ __global__ void __launch_bounds__(UT) upgma_merge_kernel(double* __restrict__ S,
                                                          double* __restrict__ bval, int32_t* __restrict__ bidx,
                                                          int32_t* __restrict__ size, uint8_t* __restrict__ active,
                                                          int32_t* __restrict__ resc, int32_t* __restrict__ merges,
-                                                         double* __restrict__ heights) {
+                                                         double* __restrict__ heights, double h0) {
   __shared__ double s_v[33];
   __shared__ int s_k[33], s_a[33], s_b[33];
   __shared__ int s_nres;
@@ -145,7 +253,7 @@ __global__ void __launch_bounds__(UT) upgma_merge_kernel(double* __restrict__ S,
     if (tid == 0) {
       merges[2 * m] = a;
       merges[2 * m + 1] = b;
-      heights[m] = __dmul_rn(__dadd_rn(1.0, -v), 0.5);
+      heights[m] = __dmul_rn(__dadd_rn(h0, -v), 0.5);
     }
     // 2. row / column a <- the size-weighted averages of rows a and b
     const double na = (double)size[a], nb = (double)size[b], nab = (double)(size[a] + size[b]);
@@ -253,6 +361,7 @@ struct UgTask {
   int32_t* merges;
   double* heights;
   unsigned* bar;     // [2] arrivals, generation
+  double h0;         // height = (h0 - best) / 2: 1 for F (d = 1 - F), 0 for -d (d^F)
 };
 
 // barrier over one task's blocks (all resident: cooperative launch)
@@ -379,7 +488,7 @@ __global__ void __launch_bounds__(UG_T) upgma_grid_kernel(const UgTask* __restri
     if (bid == 0 && tid == 0) {
       T.merges[2 * m] = a;
       T.merges[2 * m + 1] = b;
-      T.heights[m] = __dmul_rn(__dadd_rn(1.0, -v), 0.5);
+      T.heights[m] = __dmul_rn(__dadd_rn(T.h0, -v), 0.5);
     }
     // ---- 2. this block's columns c: row / column a, adoption or a rescan
     // flag for row c, and the partials
@@ -487,14 +596,22 @@ static int env_int(const char* name, int dflt) {
 }
 
 // Working copies and the first row-bests of one task.
-static sa_status upgma_prepare(Scratch& scratch, const double* F, int32_t n, int64_t ld, double*& S, int64_t& lds,
-                               double*& bval, int32_t*& bidx, cudaStream_t st) {
+static sa_status upgma_prepare(Scratch& scratch, const double* F, int32_t n, int64_t ld, const TreeForm& tf,
+                               double*& S, int64_t& lds, double*& bval, int32_t*& bidx, cudaStream_t st) {
   lds = (n + 1) & ~1;   // even: 16-byte row starts for the grid loop's scans
   SA_TRY(salloc(scratch, S, (size_t)n * lds));
   SA_TRY(salloc(scratch, bval, (size_t)n));
   SA_TRY(salloc(scratch, bidx, (size_t)n));
-  SA_CUDA(cudaMemcpy2DAsync(S, (size_t)lds * sizeof(double), F, (size_t)ld * sizeof(double), (size_t)n * sizeof(double),
-                            (size_t)n, cudaMemcpyDeviceToDevice, st));
+  if (tf.form == SA_TREE_DF) {
+    SA_TRY(ensure_ln_table());
+    const int64_t total = (int64_t)n * n;
+    dF_matrix_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)device_sms() * 8), 256, 0, st>>>(
+        F, ld, n, tf.delta, S, lds, tf.unc);
+    SA_LAUNCHED();
+  } else {
+    SA_CUDA(cudaMemcpy2DAsync(S, (size_t)lds * sizeof(double), F, (size_t)ld * sizeof(double),
+                              (size_t)n * sizeof(double), (size_t)n, cudaMemcpyDeviceToDevice, st));
+  }
   const int64_t warps = n;
   upgma_init_kernel<<<(unsigned)std::min<int64_t>((warps * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(S, n, lds, bval,
                                                                                                   bidx);
@@ -506,7 +623,8 @@ static sa_status upgma_prepare(Scratch& scratch, const double* F, int32_t n, int
 // blocks of one launch shared out in proportion to n^2 (the merges' work),
 // at least one per task.
 static sa_status upgma_grid_batch(int count, const double* const* F, const int32_t* n, const int64_t* ld,
-                                  int32_t* const* merges, double* const* heights, cudaStream_t st) {
+                                  int32_t* const* merges, double* const* heights, const TreeForm& tf,
+                                  cudaStream_t st) {
   int per_sm = 0;
   SA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, upgma_grid_kernel, UG_T, 0));
   const int bps = std::max(1, std::min(per_sm, env_int("SA_UPGMA_BPS", 1)));
@@ -544,7 +662,8 @@ static sa_status upgma_grid_batch(int count, const double* const* F, const int32
       T.G = std::min(g[k], std::max(1, (n[i] + 31) / 32));   // at least 32 rows per block
       T.g0 = g0;
       g0 += g[k];
-      SA_TRY(upgma_prepare(scratch, F[i], n[i], ld[i], T.S, T.ld, T.bval, T.bidx, st));
+      SA_TRY(upgma_prepare(scratch, F[i], n[i], ld[i], tf, T.S, T.ld, T.bval, T.bidx, st));
+      T.h0 = tf.form == SA_TREE_DF ? 0.0 : 1.0;
       SA_TRY(salloc(scratch, T.size, (size_t)n[i]));
       SA_TRY(salloc(scratch, T.active, (size_t)n[i]));
       SA_TRY(salloc(scratch, T.resc, (size_t)2 * n[i]));
@@ -586,25 +705,29 @@ static sa_status upgma_grid_batch(int count, const double* const* F, const int32
   return SA_OK;
 }
 
-sa_status upgma_launch(const double* F, int32_t n, int64_t ld, int32_t* merges, double* heights, cudaStream_t st) {
+sa_status upgma_launch(const double* F, int32_t n, int64_t ld, int32_t* merges, double* heights, const TreeForm& tf,
+                       cudaStream_t st) {
+  if (tf.unc) SA_CUDA(cudaMemsetAsync(tf.unc, 0, sizeof(unsigned long long), st));
   if (n <= 1) return SA_OK;
-  if (upgma_grid_enabled(n)) return upgma_grid_batch(1, &F, &n, &ld, &merges, &heights, st);
+  if (upgma_grid_enabled(n)) return upgma_grid_batch(1, &F, &n, &ld, &merges, &heights, tf, st);
   Scratch scratch(st);
   double *S, *bval;
   int32_t* bidx;
   int64_t lds;
-  SA_TRY(upgma_prepare(scratch, F, n, ld, S, lds, bval, bidx, st));
+  SA_TRY(upgma_prepare(scratch, F, n, ld, tf, S, lds, bval, bidx, st));
   SA_ALLOC(size, int32_t, n);
   SA_ALLOC(active, uint8_t, n);
   SA_ALLOC(resc, int32_t, n);
-  upgma_merge_kernel<<<1, UT, 0, st>>>(S, n, lds, bval, bidx, size, active, resc, merges, heights);
+  upgma_merge_kernel<<<1, UT, 0, st>>>(S, n, lds, bval, bidx, size, active, resc, merges, heights,
+                                       tf.form == SA_TREE_DF ? 0.0 : 1.0);
   SA_LAUNCHED();
   return SA_OK;
 }
 
 sa_status upgma_launch_batch(int count, const double* const* F, const int32_t* n, const int64_t* ld,
-                             int32_t* const* merges, double* const* heights, cudaStream_t st) {
-  return upgma_grid_batch(count, F, n, ld, merges, heights, st);
+                             int32_t* const* merges, double* const* heights, const TreeForm& tf, cudaStream_t st) {
+  if (tf.unc) SA_CUDA(cudaMemsetAsync(tf.unc, 0, sizeof(unsigned long long), st));
+  return upgma_grid_batch(count, F, n, ld, merges, heights, tf, st);
 }
 
 }  // namespace sa

@@ -305,6 +305,55 @@ def test_guide_tree_batch_equals_single(ctx):
         assert np.array_equal(h.cpu().numpy(), h1.cpu().numpy())
 
 
+@pytest.fixture
+def dF_tree(ctx):
+    ctx.set_tree_form(B.SA_TREE_DF, 0.02)
+    yield ctx
+    ctx.set_tree_form(B.SA_TREE_F)
+
+
+def test_guide_tree_dF_log_values(dF_tree):
+    """The d^F distance itself (reading T4): 2 x 2 trees, each one merge at
+    height d/2, give the device's CR(-ln(RN(Delta + F))) for 2 000 random F
+    and the edge values (F = 0, 1, 1 - Delta: d = +0) -- equal bit for bit to
+    the oracle's decimal-certified rounding, none uncertified."""
+    from oracle import tree
+    ctx = dF_tree
+    rng = np.random.default_rng(21)
+    fs = np.concatenate([rng.random(2000), [0.0, 1.0, 0.98, 0.5, 0.25, 1e-9, 0.999999]])
+    mats = []
+    for f in fs:
+        m = torch.full((2, 2), 1.0, dtype=torch.float64, device="cuda")
+        m[0, 1] = m[1, 0] = float(f)
+        mats.append(m)
+    outs = B.sa_guide_tree_batch(ctx, mats)
+    got = np.array([h.item() for _, h in outs])
+    want = np.array([tree.cr_neg_log(0.02 + float(f)) / 2.0 for f in fs])
+    bad = np.flatnonzero(got.view(np.uint64) != want.view(np.uint64))
+    assert bad.size == 0, [(float(fs[i]), float(got[i]), float(want[i])) for i in bad[:8]]
+    assert ctx.tree_uncertified() == 0
+
+
+@pytest.mark.parametrize("grid", ["0", "1"])
+def test_guide_tree_dF_matches_oracle(dF_tree, monkeypatch, grid):
+    """N4 in Eq. 2's distance on config-1 bucket-sized and duplicate-holding
+    sets: every merge and height equal to oracle.tree.upgma_dF (one-CTA and
+    grid loops)."""
+    from oracle import tree
+    monkeypatch.setenv("SA_UPGMA_GRID", grid)
+    ctx = dF_tree
+    for n, dup in ((3, 0), (57, 0), (180, 6)):
+        ds = _rand_set(1000 + n, n, 0, 300, dup=dup)
+        res, offs = to_dev(ds)
+        P, nk = B.sa_kmer_profiles(ctx, res, offs)
+        _, sims = B.sa_bucket_similarity_batch(ctx, P, nk, [0, n], want_numerators=False, ld_align=16)
+        m, h = B.sa_guide_tree(ctx, sims[0])
+        mo, ho = tree.upgma_dF(sims[0].cpu().numpy(), 0.02)
+        assert np.array_equal(m.cpu().numpy(), mo), n
+        assert np.array_equal(h.cpu().numpy().view(np.uint64), ho.view(np.uint64)), n
+        assert ctx.tree_uncertified() == 0
+
+
 def test_guide_tree_on_a_config_bucket(ctx):
     """N4 on config 1's largest bucket after the full partition; the oracle
     side takes that bucket's members from the oracle's golden partition and
