@@ -93,6 +93,14 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_first(self, timeout: float = 10.0):
+        """Block until nvidia-smi delivers its first sample: its start-up (NVML
+        initialisation, driver locks) must not overlap the timed region."""
+        t0 = time.time()
+        while self.proc is not None and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.02)
+        time.sleep(0.15)   # past the first sample's query as well
+
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -258,7 +266,7 @@ def main():
     barrier()
     torch.cuda.synchronize()
     clocks.start()
-    time.sleep(0.3)
+    clocks.wait_first()
     launches0 = B.sa_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)

@@ -1128,8 +1128,14 @@ struct KeyMatEpi {
     if (lane == 0 && !(dbg & 8)) {
       const uint32_t xs = tc::s_addr(xp);
       const CUtensorMap* om = omap + OM_N * pi;
-      tc::tma_store_2d(om + OM_FD, xs, c0, wrow0);
-      if (!(dbg & 1024)) tc::tma_store_2d(om + OM_CD, xs + 4096, c0, wrow0);
+      if (E.tma & 4) {   // evict-first: the output stream should not push the operand rows out of L2
+        const uint64_t pol = tc::policy_evict_first();
+        tc::tma_store_2d_hint(om + OM_FD, xs, c0, wrow0, pol);
+        if (!(dbg & 1024)) tc::tma_store_2d_hint(om + OM_CD, xs + 4096, c0, wrow0, pol);
+      } else {
+        tc::tma_store_2d(om + OM_FD, xs, c0, wrow0);
+        if (!(dbg & 1024)) tc::tma_store_2d(om + OM_CD, xs + 4096, c0, wrow0);
+      }
       tc::bulk_commit();
     }
   }
@@ -1419,6 +1425,13 @@ static sa_status tc_encode_out(CUtensorMap* m, void* base, CUtensorMapDataType d
   if (r != CUDA_SUCCESS) return fail(SA_E_CUDA, "cuTensorMapEncodeTiled (K2T output) failed (%d)", (int)r);
   return SA_OK;
 }
+// SA_K2T_STORE_HINT=1: the TMA tensor stores of the matrix epilogue carry an
+// L2 evict-first policy (0: no hint)
+static bool store_hint_setting() {
+  const char* e = getenv("SA_K2T_STORE_HINT");
+  return e ? atoi(e) != 0 : true;
+}
+
 // SA_K2T_TMA_STORE=0: the matrix epilogue's per-thread stores instead of TMA tensor stores
 static bool tma_store_enabled() {
   const char* e = getenv("SA_K2T_TMA_STORE");
@@ -1850,7 +1863,8 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
                              CU_TENSOR_MAP_SWIZZLE_128B));
         SA_TRY(tc_encode_out(om + OM_CD, E.num, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, P.na, P.nb, P.ld, 16, 32,
                              CU_TENSOR_MAP_SWIZZLE_NONE));
-        E.tma = 1 | (P.nb % 8 == 0 ? 2 : 0);   // bit 1: every row end 16-byte aligned (no edge fallback)
+        // bit 1: every row end 16-byte aligned (no edge fallback); bit 2: evict-first stores
+        E.tma = 1 | (P.nb % 8 == 0 ? 2 : 0) | (store_hint_setting() ? 4 : 0);
       }
     }
     // every problem of the launch gets every output its MODE writes (the

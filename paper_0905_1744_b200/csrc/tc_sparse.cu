@@ -362,14 +362,25 @@ __global__ void __launch_bounds__(32 * SP_FILL_WARPS) sp_rowfill_kernel(
           const uint32_t y = __shfl_up_sync(0xffffffffu, x, sh);
           if (lane >= sh) x += y;
         }
-        uint32_t w = base + x - len;
-#pragma unroll 4
-        for (uint32_t p = pb; p < pe; ++p, ++w) {
-          const uint2 e = sorted[p];
-          key[w] = (e.x << 9) | w;
-          term[w] = min(o, e.y) - 1u;
+        // the chunk's raw terms spread over the lanes (consecutive terms of a
+        // bin on consecutive lanes: independent, mostly coalesced loads); term
+        // w's bin = the largest lane j whose start (exclusive prefix) is <= w
+        const uint32_t start = x - len, total = __shfl_sync(0xffffffffu, x, 31);
+        for (uint32_t w0 = 0; w0 < total; w0 += 32) {
+          const uint32_t w = w0 + lane;
+          int j = 0;
+#pragma unroll
+          for (int s = 16; s > 0; s >>= 1)
+            if (__shfl_sync(0xffffffffu, start, j + s) <= w) j += s;
+          const uint32_t pj = __shfl_sync(0xffffffffu, pb, j) + (w - __shfl_sync(0xffffffffu, start, j));
+          const uint32_t oj = __shfl_sync(0xffffffffu, o, j);
+          if (w < total) {
+            const uint2 e = sorted[pj];
+            key[base + w] = (e.x << 9) | (base + w);
+            term[base + w] = min(oj, e.y) - 1u;
+          }
         }
-        base += __shfl_sync(0xffffffffu, x, 31);
+        base += total;
       }
       __syncwarp();
       // ---- sort the keys: in registers up to 128 (shuffle bitonic), else in shared memory
@@ -516,11 +527,10 @@ __global__ void __launch_bounds__(32 * SP_FILL_WARPS) sp_rowfill_kernel(
             ents[pos + __popc(m & ((1u << lane) - 1u))] = (c << 16) | d;
             acc[c] = 0u;
           }
-          uint32_t inc = d ? 1u << (8 * (c / sl)) : 0u;
-          for (int o = 16; o > 0; o >>= 1) inc += __shfl_xor_sync(0xffffffffu, inc, o);
-          pc += inc;
+          pc += d ? 1u << (8 * (c / sl)) : 0u;   // this lane's slice counts (<= 8 per slice: no carry)
           pos += __popc(m);
         }
+        for (int o = 16; o > 0; o >>= 1) pc += __shfl_xor_sync(0xffffffffu, pc, o);
         if (lane == 0) kpart[kbase + J] = pc;
         __syncwarp();
         curJ = J + 1;

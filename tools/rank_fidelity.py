@@ -10,11 +10,12 @@ Fig. "fig-global" and Table 1), on the synthetic workloads.
 Reports Table 1's statistics (max / min / mean of both, variance and standard
 deviation of their difference), Spearman and Kendall-style agreement, and how
 often a sequence lands in the same bucket when the partition pivots are
-applied to each rank, plus family purity of the buckets.  Both ranks are the
-F form (BASELINE.json O1); Table 1 itself used d^F ranks on unavailable data,
+applied to each rank, plus family purity of the buckets.  --form F (BASELINE.json
+O1, mean F) or dF (the paper's own Eq. 2-3 rank, mean -ln(Delta + F), the
+quantity Table 1 reports); Table 1 itself is on unavailable data,
 so its numbers are context, not a target (Z14).
 
-    python tools/rank_fidelity.py [--config 4]
+    python tools/rank_fidelity.py [--config 4] [--form dF]
 """
 import argparse
 import json
@@ -41,10 +42,14 @@ def spearman(a, b):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--form", choices=["F", "dF"], default="F")
+    ap.add_argument("--delta", type=float, default=0.02)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     ds = generate(cfg)
     ctx = B.Context(0)
+    if args.form == "dF":
+        ctx.set_rank_form(B.SA_RANK_DF, args.delta)
     res = torch.from_numpy(ds.residues.copy()).cuda()
     offs = torch.from_numpy(ds.offsets.copy()).cuda()
     P, nk = B.sa_kmer_profiles(ctx, res, offs)
@@ -98,7 +103,8 @@ def main():
     base = float((cnt * (cnt - 1) // 2).sum() / (n * (n - 1) // 2))
     d = glob - cent
     out = {
-        "config": cfg.name, "N": n, "sample_size": p * cfg.samples_per_block,
+        "config": cfg.name, "form": args.form, "delta": args.delta if args.form == "dF" else None,
+        "N": n, "sample_size": p * cfg.samples_per_block,
         "centralized_rank_ms": ms, "centralized_pairs": n * (n + 1) // 2,
         "centralized_pairs_per_s": n * (n + 1) / 2 / (ms / 1e3),
         "max_min_centralized": [float(cent.max()), float(cent.min())], "avg_centralized": float(cent.mean()),
@@ -110,7 +116,8 @@ def main():
         "bucket_sizes_centralized": np.bincount(bc, minlength=p).tolist(),
         "same_family_pair_fraction": {"globalized_buckets": purity(bg), "centralized_buckets": purity(bc),
                                       "no_partition": base},
-        "engine": ctx.engine(),
+        "engine": ctx.engine(), "operand": ctx.tc_operand() if ctx.engine() == "tc" else None,
+        "uncertified_partition_comparisons": int(part.uncertified),
     }
     print(json.dumps(out))
 
