@@ -74,15 +74,16 @@ class ClockSampler:
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_ms: int = 100):
         self.index = index
+        self.period_ms = period_ms
         self.proc = None
         self.lines = []
 
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -192,6 +193,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-n", type=int, default=2400)
     ap.add_argument("--no-similarity", action="store_true", help="S5 numerators only (not the default)")
+    ap.add_argument("--clock-period-ms", type=int, default=100,
+                    help="nvidia-smi sampling period during the timed region")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "torch"],
                     help="N > 1: libsa's NCCL communicator (default) or torch.distributed callbacks")
     args = ap.parse_args()
@@ -262,7 +265,7 @@ def main():
 
     # ------------------------------------------------ device-timed steps
     per_step = []
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local, period_ms=args.clock_period_ms)
     barrier()
     torch.cuda.synchronize()
     clocks.start()
@@ -542,7 +545,12 @@ def main():
                 "ms": phases["S1"],
                 "frac_of_hbm": (res_h.numel() + offs_h.numel() * 8 + (last - first) * 16004) /
                                (phases["S1"] / 1e3) / (float(peaks.get("hbm_gbs", 6551.0)) * 1e9)},
-            "phases_ms_rank0": phases, "bucket_sizes": [int(x) for x in sizes],
+            "phases_ms_rank0": phases,
+            # device time between one step's last event and the next step's
+            # first (per step, rank 0): the GPU waiting for the host to enqueue
+            "inter_step_gap_ms_rank0": max(0.0, total_ms / args.steps - (phases["S1"] + part_ms + phases["S1_received"]
+                                                                       + s5_ms)),
+            "bucket_sizes": [int(x) for x in sizes],
             "exact_fallbacks": out.part.exact_fallbacks,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk,
