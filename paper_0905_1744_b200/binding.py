@@ -16,7 +16,8 @@ import numpy as np
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libsa.so")
+# SA_LIBSA: another in-tree build of the same library (A/B experiments, scripts/build_variant.sh)
+LIB_PATH = os.environ.get("SA_LIBSA") or os.path.join(_PKG, "lib", "libsa.so")
 
 SA_OK, SA_E_INVAL, SA_E_RANGE, SA_E_CUDA, SA_E_COMM, SA_E_NOMEM, SA_E_STATE = range(7)
 STATUS_NAMES = {0: "SA_OK", 1: "SA_E_INVAL", 2: "SA_E_RANGE", 3: "SA_E_CUDA", 4: "SA_E_COMM",

@@ -731,7 +731,7 @@ enum { EPI_KEYS = 1, EPI_NUM = 2, EPI_SIM = 4, EPI_ALL = 7 };
 // Per-tile tables.  Every epilogue warp stages, for each column of its slice,
 // before the accumulator is ready (tc_gemm.cuh):
 //   key entry  {rl, rh, e, nk'}  reciprocal tables of D = nk' (EPI_KEYS)
-//   F entry    {y_lo, y_hi, nk', 0}  y = RN(1 / nk')        (EPI_SIM)
+//   F entry    {y, d}  y = RN(1 / nk'), d = nk'         (EPI_SIM)
 // with nk' = nk if the column exists and nk > 0, else -1 (tables of 0: r = e
 // = y = 0).  A pair then takes D = min(nk'_row, nk'_col) and the tables of
 // whichever side is smaller; the -1 sentinel makes every term of a missing or
@@ -1103,16 +1103,16 @@ struct KeyMatEpi {
       if (j & 1) w[j >> 1] |= C << 16;
       else w[j >> 1] = C;
       const double2 yd = *reinterpret_cast<const double2*>(ent + j * TAB_BYTES + YOFF);
-      F[j] = fsel_dbg(C, s.y, s.d, yd.x, yd.y);
+      F[j] = fsel(C, s.y, s.d, yd.x, yd.y);   // (no per-pair run-time switch: it costs a branch per pair)
     }
-    if (s.rv && !(dbg & (8 | 512))) {   // (SA_K2T_DEBUG 512 / 1024: experiments, mirror / C stores skipped)
+    if (s.rv && !(dbg & (8 | 512))) {   // (SA_K2T_DEBUG 512: experiment, mirrored stores skipped)
       double* fm = E.sim + (int64_t)c0 * E.ld + s.row_g;
       uint16_t* cmr = E.num + (int64_t)c0 * E.ld + s.row_g;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         if (j < ncols) {
           __stcs(fm + (int64_t)j * E.ld, F[j]);
-          if (!(dbg & 1024)) __stcs(reinterpret_cast<unsigned short*>(cmr + (int64_t)j * E.ld), (unsigned short)v[j]);
+          __stcs(reinterpret_cast<unsigned short*>(cmr + (int64_t)j * E.ld), (unsigned short)v[j]);
         }
       }
     }
