@@ -153,11 +153,28 @@ struct TcRecOut {
   int on;
 };
 
-template <bool FP4>
-__global__ void __launch_bounds__(TC_HIST_THREADS, 2)   // two CTAs per SM (<= 128 registers)
+// DEEP = false: the sparse-path launch's lean instantiation (layer 1 and the
+// records only; deep_planes must be 0): none of the deeper layers' code or
+// shared memory, so the instruction stream fits the cache (the general kernel
+// stalled 35% on instruction fetch on config 4, ncu) and more CTAs fit an SM.
+#ifndef SA_HIST_LEAN_ROWS
+#define SA_HIST_LEAN_ROWS 4
+#endif
+#ifndef SA_HIST_LEAN_MINB
+#define SA_HIST_LEAN_MINB 2
+#endif
+#ifndef SA_HIST_LEAN_GRID
+#define SA_HIST_LEAN_GRID 4   // CTAs per SM in the grid
+#endif
+template <bool DEEP>
+__host__ __device__ constexpr int hist_rows() { return DEEP ? TC_HIST_ROWS : SA_HIST_LEAN_ROWS; }
+template <bool FP4, bool DEEP>
+__global__ void __launch_bounds__(TC_HIST_THREADS, DEEP ? 2 : SA_HIST_LEAN_MINB)   // two CTAs per SM (<= 128 registers)
 tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut O, int stride16, int bins,
                uint32_t* __restrict__ planes, uint32_t* __restrict__ state, int64_t hist_from, TcMasks mk, int spec,
                TcRecOut ro, int deep_planes, const int32_t* __restrict__ only_dense) {
+  constexpr int TC_HIST_ROWS = hist_rows<DEEP>();
+  if constexpr (!DEEP) deep_planes = 0;
   __shared__ uint32_t s_nrec;
   if (threadIdx.x == 0) s_nrec = 0;
   constexpr int64_t ROWB = FP4 ? TC_KCAP / 2 : TC_KCAP;
@@ -167,7 +184,8 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
   constexpr int ND = TC_LCAP - TC_HREG;
   const int w = threadIdx.x;
   const bool active = w * 32 < stride16;
-  for (int l = 0; l < 2 * ND; ++l) deep[l * TC_WPL + w] = 0u;
+  if constexpr (DEEP)
+    for (int l = 0; l < 2 * ND; ++l) deep[l * TC_WPL + w] = 0u;
   // rows [hist_from, R): a carried side (TcCarry) comes first and is skipped
   const int64_t R = S.row_begin[S.n] - hist_from;
   const int64_t r0 = hist_from + blockIdx.x * R / gridDim.x, r1 = hist_from + (blockIdx.x + 1) * R / gridDim.x;
@@ -186,7 +204,7 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
       if (t2) atomicOr(&g2[l * TC_WPL + w], t2);
       s1[l] = s2[l] = 0u;
     }
-    for (int l = 0; l < deepest; ++l) {
+    for (int l = 0; l < (DEEP ? deepest : 0); ++l) {
       const uint32_t d1 = deep[l * TC_WPL + w];
       uint32_t d2 = deep[(ND + l) * TC_WPL + w];
       if (d1) d2 |= atomicOr(&g1[(TC_HREG + l) * TC_WPL + w], d1) & d1;
@@ -286,7 +304,7 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
             }
           }
         }
-        const int top = deep_planes ? (int)min(vmax, (uint32_t)TC_LCAP) : 0;
+        const int top = DEEP && deep_planes ? (int)min(vmax, (uint32_t)TC_LCAP) : 0;
         for (int l = TC_HREG; l < top; ++l) {
           const uint32_t m = layer_mask(v, (uint32_t)(l + 1) * 0x00010001u);
           uint32_t* d1 = &deep[(l - TC_HREG) * TC_WPL + w];
@@ -1477,9 +1495,9 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
   const int g_num_sms = device_sms();
   static DeviceOnce once;
   SA_TRY(once.run([]() -> sa_status {
-    SA_CUDA(cudaFuncSetAttribute(tc_hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SA_CUDA(cudaFuncSetAttribute(tc_hist_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  2 * (TC_LCAP - TC_HREG) * TC_WPL * 4));
-    SA_CUDA(cudaFuncSetAttribute(tc_hist_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SA_CUDA(cudaFuncSetAttribute(tc_hist_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  2 * (TC_LCAP - TC_HREG) * TC_WPL * 4));
     sa_status cs = tc_configure_all<false, 1>();
     if (cs == SA_OK) cs = tc_configure_all<true, 1>();
@@ -1609,8 +1627,9 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     mk.carried_valid = carried ? use->masks_valid : 0;
     mk.own = mk.own_valid ? kscr->alloc<uint32_t>((size_t)(R - hfrom) * TC_MROW) : nullptr;
     if (mk.own_valid && !mk.own) return fail(SA_E_NOMEM, "scratch allocation of K2T layer masks failed");
+    const int hrows = sp_on ? hist_rows<false>() : TC_HIST_ROWS;   // rows per CTA iteration
     const int hx = (int)std::max<int64_t>(
-        1, std::min<int64_t>((R - hfrom + TC_HIST_ROWS - 1) / TC_HIST_ROWS, 4 * g_num_sms));
+        1, std::min<int64_t>((R - hfrom + hrows - 1) / hrows, (sp_on ? SA_HIST_LEAN_GRID : 4) * g_num_sms));
     const int hsm = 2 * (TC_LCAP - TC_HREG) * TC_WPL * 4;
     // sparse-layer records: per hist CTA a segment, then one dense array (after
     // the carried launch's records, when there are any)
@@ -1641,12 +1660,20 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     // sparse-path launches build layer 1 and the records only; the deeper
     // planes of the problems that end up dense come from a second, planes-only
     // pass over just their rows (after the plan)
-    if (fp4)
-      tc_hist_kernel<true><<<hx, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, hfrom, mk,
-                                                             spec, ro, sp_on ? 0 : 1, nullptr);
-    else
-      tc_hist_kernel<false><<<hx, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, hfrom, mk,
-                                                              spec, ro, sp_on ? 0 : 1, nullptr);
+    if (sp_on) {
+      if (fp4)
+        tc_hist_kernel<true, false><<<hx, TC_HIST_THREADS, 0, st>>>(sides, outs, stride16, bins, planes, state, hfrom,
+                                                                     mk, spec, ro, 0, nullptr);
+      else
+        tc_hist_kernel<false, false><<<hx, TC_HIST_THREADS, 0, st>>>(sides, outs, stride16, bins, planes, state,
+                                                                      hfrom, mk, spec, ro, 0, nullptr);
+    } else if (fp4) {
+      tc_hist_kernel<true, true><<<hx, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, hfrom,
+                                                                   mk, spec, ro, 1, nullptr);
+    } else {
+      tc_hist_kernel<false, true><<<hx, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, hfrom,
+                                                                    mk, spec, ro, 1, nullptr);
+    }
     SA_LAUNCHED();
     if (sp_on) {
       // a carried side without records (its launch ran with sparse layers off) cannot go sparse
@@ -1751,10 +1778,10 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
         const int hx0 = (int)std::max<int64_t>(1, std::min<int64_t>((R + TC_HIST_ROWS - 1) / TC_HIST_ROWS,
                                                                      4 * g_num_sms));
         if (fp4)
-          tc_hist_kernel<true><<<hx0, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, 0, mk0,
+          tc_hist_kernel<true, true><<<hx0, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, 0, mk0,
                                                                   spec, ro0, 1, spb.mode);
         else
-          tc_hist_kernel<false><<<hx0, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, 0,
+          tc_hist_kernel<false, true><<<hx0, TC_HIST_THREADS, hsm, st>>>(sides, outs, stride16, bins, planes, state, 0,
                                                                    mk0, spec, ro0, 1, spb.mode);
         SA_LAUNCHED();
       }
