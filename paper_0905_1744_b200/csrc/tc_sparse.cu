@@ -308,17 +308,24 @@ __device__ __forceinline__ void sp_warp_sort(uint32_t* key, uint32_t n, int lane
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(32 * SP_FILL_WARPS) sp_rowfill_kernel(
+// Occupancy: the row fill is latency-bound (dependent gathers per row), so
+// the per-warp counter array is sized by the launch (accw = max(tn, bn)
+// words, dynamic shared memory) instead of SP_TN_MAX, and registers are
+// capped for SA_FILL_MINB CTAs per SM.
+#ifndef SA_FILL_MINB
+#define SA_FILL_MINB 10
+#endif
+__global__ void __launch_bounds__(32 * SP_FILL_WARPS, SA_FILL_MINB) sp_rowfill_kernel(
     const SpLaunch L, const int32_t* __restrict__ mode, const uint32_t* __restrict__ binoff,
     const uint2* __restrict__ sorted, const uint32_t* __restrict__ spos, const uint32_t* __restrict__ rstart,
     const uint32_t* __restrict__ rlist,
     const uint32_t* __restrict__ rowoff, uint32_t* __restrict__ ents, uint32_t* __restrict__ koff,
-    uint32_t* __restrict__ kpart, const uint32_t* __restrict__ flags) {
+    uint32_t* __restrict__ kpart, const uint32_t* __restrict__ flags, int accw) {
   __shared__ unsigned long long s_buf[SP_FILL_WARPS][SP_ROWBUF];   // raw terms; cursors of the sweep
-  __shared__ uint32_t s_acc[SP_FILL_WARPS][SP_TN_MAX];             // per-block counters; sweep accumulator
+  extern __shared__ uint32_t s_acc[];                              // [SP_FILL_WARPS][accw]: per-block counters; sweep accumulator
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   unsigned long long* buf = s_buf[wib];
-  uint32_t* acc = s_acc[wib];
+  uint32_t* acc = s_acc + wib * accw;
   // the sweep's cursor state overlays the raw buffer (4 KB): position, end, own count, current partner
   uint32_t* cur = reinterpret_cast<uint32_t*>(buf);
   uint32_t* end = cur + SP_CURSORS;
@@ -328,7 +335,7 @@ __global__ void __launch_bounds__(32 * SP_FILL_WARPS) sp_rowfill_kernel(
   const uint32_t bn = (uint32_t)L.bn, sl = (uint32_t)L.slice;
   const uint32_t NA = (uint32_t)L.abase[L.nprob];
   const uint32_t nwarps = gridDim.x * SP_FILL_WARPS;
-  for (uint32_t c = lane; c < SP_TN_MAX; c += 32) acc[c] = 0u;
+  for (uint32_t c = lane; c < (uint32_t)accw; c += 32) acc[c] = 0u;
   __syncwarp();
   for (uint32_t ai = blockIdx.x * SP_FILL_WARPS + wib; ai < NA; ai += nwarps) {
     const SpRow R = sp_row_of(L, ai);
@@ -688,8 +695,12 @@ sa_status sp_entries(SpLaunch& L, SpBuffers& B, int sms, cudaStream_t st) {
                                                         B.flags);
   SA_LAUNCHED();
   SA_TRY(scan_u32(B.rowcnt, NA, B.rowoff, B.scan_tmp, st));
-  sp_rowfill_kernel<<<fb, 32 * SP_FILL_WARPS, 0, st>>>(L, B.mode, B.binoff, B.sorted, B.spos, B.rstart, B.rlist,
-                                                       B.rowoff, B.ents, B.koff, B.kpart, B.flags);
+  int accw = L.bn;
+  for (int q = 0; q < L.nprob; ++q)
+    if (L.cap[q] > 0) accw = std::max(accw, (int)L.tn[q]);   // problems that can run sparse: tn <= SP_TN_MAX
+  accw = std::min((accw + 31) & ~31, SP_TN_MAX);
+  sp_rowfill_kernel<<<fb, 32 * SP_FILL_WARPS, SP_FILL_WARPS * accw * 4, st>>>(
+      L, B.mode, B.binoff, B.sorted, B.spos, B.rstart, B.rlist, B.rowoff, B.ents, B.koff, B.kpart, B.flags, accw);
   SA_LAUNCHED();
   return SA_OK;
 }

@@ -9,7 +9,7 @@ NAME=$1; SRC=$2; shift 2
 L=paper_0905_1744_b200/lib
 mkdir -p $L/obj_$NAME
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 \
-  -I include "$@" -c $SRC/minsum_tc.cu -o $L/obj_$NAME/minsum_tc.cu.o
-objs=$(ls $L/obj/*.o | grep -v minsum_tc.cu.o)
-/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static $objs $L/obj_$NAME/minsum_tc.cu.o -ldl -o $L/libsa_$NAME.so
+  -I include "$@" -c $SRC/${TU:-minsum_tc.cu} -o $L/obj_$NAME/${TU:-minsum_tc.cu}.o
+objs=$(ls $L/obj/*.o | grep -v ${TU:-minsum_tc.cu}.o)
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static $objs $L/obj_$NAME/${TU:-minsum_tc.cu}.o -ldl -o $L/libsa_$NAME.so
 echo "$L/libsa_$NAME.so"
