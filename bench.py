@@ -28,6 +28,7 @@ cpu_baseline = the CPU oracle (oracle/, as it stands) on a bounded sample of
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -266,6 +267,11 @@ def main():
     # ------------------------------------------------ device-timed steps
     per_step = []
     clocks = ClockSampler(local, period_ms=args.clock_period_ms)
+    # no garbage-collector pause inside a timed region (the step has one host
+    # block, C3, and its post-C3 launches keep the GPU fed only while the host
+    # thread runs: a collection there is a GPU-idle gap)
+    gc.collect()
+    gc.disable()
     barrier()
     torch.cuda.synchronize()
     clocks.start()
@@ -282,6 +288,7 @@ def main():
     e1.record(st)
     torch.cuda.synchronize()
     launches = B.sa_launch_count() - launches0
+    gc.enable()
     barrier()
     clk = clocks.stop()
     total_ms = max_over_ranks(e0.elapsed_time(e1))
@@ -485,6 +492,8 @@ def main():
         barrier()
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        gc.collect()
+        gc.disable()
         f0.record(st)
         d2h_bytes = 0
         for i in range(args.steps):
@@ -494,6 +503,7 @@ def main():
             d2h_bytes = d2h_tail(o, last=i == args.steps - 1)
         f1.record(st)
         torch.cuda.synchronize()
+        gc.enable()
         e2e_ms = max_over_ranks(f0.elapsed_time(f1))
         del d_packed, h_out
         what = ("bucket_of, received member ids, and every owned bucket's symmetric uint16 numerator matrix "
@@ -550,6 +560,9 @@ def main():
             # first (per step, rank 0): the GPU waiting for the host to enqueue
             "inter_step_gap_ms_rank0": max(0.0, total_ms / args.steps - (phases["S1"] + part_ms + phases["S1_received"]
                                                                        + s5_ms)),
+            # each timed step's device time, first event to last (rank 0): an
+            # outlier step shows here (a host stall between C3 and S4)
+            "step_ms_rank0": [round(ev["start"].elapsed_time(ev["S5"]), 3) for ev, _ in per_step],
             "bucket_sizes": [int(x) for x in sizes],
             "exact_fallbacks": out.part.exact_fallbacks,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
