@@ -388,6 +388,14 @@ def main():
                                   f"({opnd_bytes / 1e9:.3f} GB); over the GEMM kernel's CUDA-event time "
                                   f"(median of the timed steps)"),
                   "phase_frac_tensor_method": t_tensor * 1e3 / s5_ms, "ncu": ncu_note}
+        # the S5 floor is nearly all writes: against the write-only fill rate
+        # measured on this GPU type (tools/hbm_write_probe.py) as well
+        wpath = os.path.join(ROOT, "profiles", "r02s3_hbm_probe.jsonl")
+        if os.path.exists(wpath):
+            with open(wpath) as f:
+                wfill = max(json.loads(l)["write_only_gbs"] for l in f if l.strip()) * 1e9
+            common["frac_hbm_vs_write_fill"] = bytes_alg / wfill * 1e3 / gemm_ms
+            common["write_fill_gbs"] = wfill / 1e9
         if t_hbm >= t_tensor:
             roof = {"bound": "hbm", "achieved": bytes_alg / (gemm_ms / 1e3) / 1e9, "peak": hbm / 1e9,
                     "unit": "GB/s", "frac": t_hbm * 1e3 / gemm_ms, **common}
@@ -411,6 +419,60 @@ def main():
                                 f"bins per {'VABSDIFF4.U8.ACC' if engine == 'u8' else 'VIMNMX.U16x2'} x {nsm} SMs "
                                 f"x {sm_mhz_peak:.0f} MHz"),
                 "algorithmic": f"{EPS_BINS} bin-ops per pair x {my_s5_pairs} pairs / S5 CUDA-event time"}
+
+    # ------------------------------------- partition: GEMM rooflines, collectives
+    # The partition's dominant kernels are the two key GEMMs (S2a: every pair
+    # of each local block, S2d: every local sequence against the s samples);
+    # their method count is Eq. 1's 8000 bins per pair, as for S5.  Their
+    # outputs are 128-bit keys (no HBM floor to speak of): the tensor floor binds.
+    partition_roofline = None
+    if engine == "tc":
+        my_blocks = range(rank * cfg.p // world, (rank + 1) * cfg.p // world)
+        my_s2a = sum((bounds[q + 1] - bounds[q]) * (bounds[q + 1] - bounds[q] - 1) // 2 for q in my_blocks)
+        my_s2d = (bounds[my_blocks.stop] - bounds[my_blocks.start]) * cfg.p * cfg.samples_per_block
+        partition_roofline = {"bound": "tensor", "unit": "TOP/s", "peak": peak_t / 1e12,
+                              "peak_source": "as roofline.tensor_peak_source"}
+        for name, pr, ms in (("S2a_gemm", my_s2a, phases["S2a_gemm"]), ("S2d_gemm", my_s2d, phases["S2d_gemm"])):
+            ops = 2.0 * EPS_BINS * pr
+            partition_roofline[name] = {"pairs": int(pr), "kernel_ms": ms, "achieved": ops / (ms / 1e3) / 1e12,
+                                        "frac": ops / peak_t * 1e3 / ms}
+        ops_all = 2.0 * EPS_BINS * (my_s2a + my_s2d)
+        partition_roofline["partition_ms"] = part_ms
+        partition_roofline["frac_of_partition_time"] = ops_all / peak_t * 1e3 / part_ms
+    # Bytes each rank sends per step in the paper's exchanges (Alg. 2, P:1248-1267;
+    # DESIGN.md §6), from this step's sizes: C1 sample broadcast (profiles + nk +
+    # ids of the rank's s/G samples, allgather), C2 regular samples (32-byte
+    # records), C3 count exchange (2p + 3 int64 per rank), C4 all-to-all: the
+    # residues and 16-byte records of the rank's sequences whose bucket another
+    # rank owns.  At N = 1 nothing leaves the GPU.
+    stride = B.sa_profile_stride(hp.bins)
+    s_loc = cfg.p // world * cfg.samples_per_block
+    nb = np.asarray(out.part.bytes)
+    nc = np.asarray(out.part.counts)
+    own_of = [b * world // cfg.p for b in range(cfg.p)]
+    c4_seq = int(sum(nc[rank, b] for b in range(cfg.p) if own_of[b] != rank))
+    c4_bytes = int(sum(nb[rank, b] for b in range(cfg.p) if own_of[b] != rank)) + 16 * c4_seq
+    sent = {"C1_sample_allgather": s_loc * (stride * 2 + 4 + 8),
+            "C2_regular_samples_allgather": (cfg.p // world) * (cfg.p - 1) * 32,
+            "C3_count_allgather": (2 * cfg.p + 3) * 8,
+            "C4_alltoallv": c4_bytes}
+    collectives = {"n_ranks": world, "bytes_sent_per_rank_per_step": sent if world > 1 else {k: 0 for k in sent},
+                   "bytes_if_sharded_over_8": None}
+    if world == 1:
+        # what rank 0 would send at G = 8 (same data): C1 and C2 scale with the
+        # rank's blocks; C4 is 7/8 of its sequences' residues + records
+        g = 8
+        blk = [q * ds.n // cfg.p for q in range(cfg.p + 1)]
+        res_b = np.diff(ds.offsets)
+        r0 = range(0, cfg.p // g)
+        mine = np.arange(blk[r0.start], blk[r0.stop])
+        bo = out.part.bucket_of.cpu().numpy()[mine]
+        off = np.array([b * g // cfg.p != 0 for b in bo])
+        collectives["bytes_if_sharded_over_8"] = {
+            "C1_sample_allgather": (cfg.p // g) * cfg.samples_per_block * (stride * 2 + 4 + 8),
+            "C2_regular_samples_allgather": (cfg.p // g) * (cfg.p - 1) * 32,
+            "C3_count_allgather": (2 * cfg.p + 3) * 8,
+            "C4_alltoallv": int(res_b[mine][off].sum() + 16 * off.sum())}
 
     # --------------------------------------------- end-to-end (host buffers)
     def run_e2e(with_sim: bool):
@@ -565,7 +627,8 @@ def main():
             "step_ms_rank0": [round(ev["start"].elapsed_time(ev["S5"]), 3) for ev, _ in per_step],
             "bucket_sizes": [int(x) for x in sizes],
             "exact_fallbacks": out.part.exact_fallbacks,
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "roofline": roof, "partition_roofline": partition_roofline, "collectives": collectives,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

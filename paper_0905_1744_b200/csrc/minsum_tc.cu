@@ -819,32 +819,67 @@ struct KeyMatEpi {
 
   __device__ bool skip() const { return tc_infeasible(state); }
 
-  __device__ void begin(State& s, const tc::Tile& T, int row, int lane, int cbeg, int cend, uint8_t* tab) const {
+  // The per-tile loads (row info, the correction queue's index, the column
+  // tables) all issued together into registers (`prefetch`: the column
+  // tables as 4 x 32 unrolled, independent loads per lane -- slices up to 128
+  // columns, wider ones load the rest directly), then consumed (`begin_pf`).
+  // (Issuing tile t + 1's loads at the start of tile t measured neutral on
+  // S5; the unrolled form took the S2a GEMM 1.979 -> 1.956 ms.)
+  static constexpr int PFK = 4;
+  struct Pf {
+    uint4 kcol[PFK];
+    double2 ycol[PFK];
+    uint4 krow;
+    double2 yrow;
+    int nk0;
+    uint32_t kb, ke, pc;
+  };
+  __device__ __forceinline__ void prefetch(Pf& p, const tc::Tile& T, int row, int lane, int cbeg, int cend) const {
+    const TcEpiProb& E = e[T.pi];
+    const int row_g = T.row0 + row;
+    const bool rv = row < T.ra;
+    p.nk0 = rv ? __ldg(E.nkA + row_g) : 0;
+    if constexpr (KEYS) p.krow = rv ? __ldg(E.kinfoA + row_g) : make_uint4(0u, 0u, 0u, 0xffffffffu);
+    if constexpr (SIM) p.yrow = rv ? __ldg(E.yinfoA + row_g) : make_double2(0.0, 0.0);
+    p.kb = p.ke = p.pc = 0u;
+    if (E.koff && rv && !(dbg & 256)) {   // (SA_K2T_DEBUG 256: experiment, corrections skipped)
+      const int64_t key = (int64_t)row_g * E.tn + T.col0 / E.bn;
+      p.kb = __ldg(E.koff + key);
+      p.ke = __ldg(E.koff + key + 1);
+      p.pc = __ldg(E.kpart + key);
+    }
+#pragma unroll
+    for (int k = 0; k < PFK; ++k) {
+      const int c = cbeg + lane + 32 * k;
+      const bool cv = c < cend && c < T.rb && !(dbg & 128);   // (SA_K2T_DEBUG 128: experiment, no column tables)
+      if constexpr (KEYS) p.kcol[k] = cv ? __ldg(E.kinfoB + T.col0 + c) : make_uint4(0u, 0u, 0u, 0xffffffffu);
+      if constexpr (SIM) p.ycol[k] = cv ? __ldg(E.yinfoB + T.col0 + c) : make_double2(0.0, 0.0);
+    }
+  }
+  __device__ __forceinline__ void begin_pf(State& s, const tc::Tile& T, const Pf& p, int row, int lane, int cbeg,
+                                           int cend, uint8_t* tab) const {
     const TcEpiProb& E = e[T.pi];
     s.lo = 0;
     s.hi = 0;
     s.row_g = T.row0 + row;
     s.rv = row < T.ra;
-    s.nk0 = s.rv ? E.nkA[s.row_g] : 0;
+    s.nk0 = p.nk0;
     s.nk = s.nk0 > 0 ? s.nk0 : -1;
     if constexpr (KEYS) {
-      const uint4 k = s.rv ? __ldg(E.kinfoA + s.row_g) : make_uint4(0u, 0u, 0u, 0xffffffffu);
-      s.rl = k.x;
-      s.rh = k.y;
-      s.ek = k.z;
+      s.rl = p.krow.x;
+      s.rh = p.krow.y;
+      s.ek = p.krow.z;
     }
     if constexpr (SIM) {
-      const double2 yd = s.rv ? __ldg(E.yinfoA + s.row_g) : make_double2(0.0, 0.0);
-      s.y = yd.x;
-      s.d = yd.y;
+      s.y = p.yrow.x;
+      s.d = p.yrow.y;
     }
     // correction entries of (row, column block, slice): the first four in
     // registers (independent loads, issued before the accumulator wait)
     s.ep = s.ee = 0;
     s.q0 = s.q1 = s.q2 = s.q3 = 0xFFFFFFFFu;
-    if (E.koff && s.rv && !(dbg & 256)) {   // (SA_K2T_DEBUG 256: experiment, corrections skipped)
-      const int64_t key = (int64_t)s.row_g * E.tn + T.col0 / E.bn;
-      const uint32_t kb = __ldg(E.koff + key), ke = __ldg(E.koff + key + 1), pc = __ldg(E.kpart + key);
+    if (E.koff && s.rv && !(dbg & 256)) {
+      const uint32_t kb = p.kb, ke = p.ke, pc = p.pc;
       const uint32_t part = (uint32_t)(cbeg / E.slice);
       const uint32_t before = part == 0 ? 0u : __vsadu4(pc & ((1u << (8 * part)) - 1u), 0u);   // slices < part
       const uint32_t avail = ke - kb;
@@ -858,8 +893,17 @@ struct KeyMatEpi {
       s.ee = e;
     }
     if constexpr (KEYS || SIM) {
-      for (int c = cbeg + lane; c < cend; c += 32) {
-        const bool cv = c < T.rb && !(dbg & 128);   // (SA_K2T_DEBUG 128: experiment, column tables not loaded)
+#pragma unroll
+      for (int k = 0; k < PFK; ++k) {
+        const int c = cbeg + lane + 32 * k;
+        if (c < cend) {
+          uint8_t* ent = tab + (c - cbeg) * TAB_BYTES;
+          if constexpr (KEYS) *reinterpret_cast<uint4*>(ent + KOFF) = p.kcol[k];
+          if constexpr (SIM) *reinterpret_cast<double2*>(ent + YOFF) = p.ycol[k];
+        }
+      }
+      for (int c = cbeg + 32 * PFK + lane; c < cend; c += 32) {   // slices wider than 128 columns
+        const bool cv = c < T.rb && !(dbg & 128);
         uint8_t* ent = tab + (c - cbeg) * TAB_BYTES;
         if constexpr (KEYS)
           *reinterpret_cast<uint4*>(ent + KOFF) =
@@ -869,6 +913,11 @@ struct KeyMatEpi {
       }
     }
     __syncwarp();
+  }
+  __device__ void begin(State& s, const tc::Tile& T, int row, int lane, int cbeg, int cend, uint8_t* tab) const {
+    Pf p;
+    prefetch(p, T, row, lane, cbeg, cend);
+    begin_pf(s, T, p, row, lane, cbeg, cend, tab);
   }
 
   // Layers >= 2 of the chunk's pairs (tc_sparse.cu): add the entries whose

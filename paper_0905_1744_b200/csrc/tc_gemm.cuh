@@ -824,10 +824,14 @@ gemm2_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps m
     const bool no_epi = (batch.debug & 4) != 0;
     typename Epi::State es;
     uint32_t lt = 0;
-    for (int64_t tile = pair; tile < total_tiles; tile += npairs, ++lt) {
+    auto half_tile = [&](int64_t tile) {   // this CTA's half of the pair tile
       Tile T = decode<BN, TBM2>(batch, tile);
-      T.row0 += (int)rank * BM;                        // this CTA's half of the pair tile
+      T.row0 += (int)rank * BM;
       T.ra = max(0, min(BM, T.ra - (int)rank * BM));
+      return T;
+    };
+    for (int64_t tile = pair; tile < total_tiles; tile += npairs, ++lt) {
+      const Tile T = half_tile(tile);
       const uint32_t buf = lt & 1u;
       epi.begin(es, T, row, lane, cbeg, cend, tab);
       bar_wait(&tfull[buf], (lt >> 1) & 1u);
