@@ -90,9 +90,12 @@ profiles_bulk_kernel(const uint8_t* __restrict__ res, const int64_t* __restrict_
     const int64_t len = e - b;
     const int64_t nk = len >= k ? len - k + 1 : 0;
     const uint8_t* x = res + b;
+    // every residue of a sequence with nk > 0 lies in some k-mer: the range
+    // check rides on the k-mer reads (its own pass only when len < k)
     uint32_t bad = 0;
-    for (int64_t u = threadIdx.x; u < len; u += blockDim.x)
-      if (x[u] >= alphabet) bad = 1;
+    if (nk == 0)
+      for (int64_t u = threadIdx.x; u < len; u += blockDim.x)
+        if (x[u] >= alphabet) bad = 1;
     for (int64_t u = threadIdx.x; u < nk; u += blockDim.x) {
       uint32_t id = 0;
       bool ok = true;
@@ -102,6 +105,7 @@ profiles_bulk_kernel(const uint8_t* __restrict__ res, const int64_t* __restrict_
         id = id * (uint32_t)alphabet + r;
       }
       if (ok) atomicAdd(&hist[id >> 1], 1u << ((id & 1u) << 4));
+      else bad = 1;
     }
     if (bad) atomicOr(err, ERR_RESIDUE);
     if (threadIdx.x == 0) {
