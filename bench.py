@@ -191,6 +191,8 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--prewarm-s", type=float, default=0.3,
+                    help="seconds of untimed dense matmuls before the warm-up steps (GPU power state)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-n", type=int, default=2400)
     ap.add_argument("--no-similarity", action="store_true", help="S5 numerators only (not the default)")
@@ -259,6 +261,16 @@ def main():
         return float(t.item())
 
     names = ["start", "S1", "S4", "S1b", "S5"]
+    # bring the GPU out of its idle power state before the warm-up steps (a
+    # fresh box's first steps ran at half speed otherwise): ~0.3 s of dense
+    # matmuls on the step stream, untimed, no part of the workload
+    a = torch.randn(4096, 4096, device=dev, dtype=torch.bfloat16)
+    t_end = time.perf_counter() + args.prewarm_s
+    while time.perf_counter() < t_end:
+        for _ in range(20):
+            a = torch.tanh(a @ a)
+        torch.cuda.synchronize()
+    del a
     for _ in range(args.warmup):
         out = hp.step(res_d, offs_d, ds.n, first)
     torch.cuda.synchronize()
@@ -283,6 +295,7 @@ def main():
         # no host synchronisation inside the timed region: libsa only records
         # its phase events; they are read after the region (phase_history)
         ev = {k: torch.cuda.Event(enable_timing=True) for k in names}
+        ev["_host"] = []
         out = hp.step(res_d, offs_d, ds.n, first, events=ev)
         per_step.append(ev)
     e1.record(st)
@@ -606,7 +619,8 @@ def main():
                        "dataset_sha256": ds.sha256(), "parallelism": f"{world} rank(s), {cfg.p // world} "
                        "blocks/buckets each",
                        "l2": "inputs larger than L2 (profiles N x 16 KB = "
-                             f"{ds.n * 16000 / 1e9:.2f} GB per step)"},
+                             f"{ds.n * 16000 / 1e9:.2f} GB per step)",
+                       "prewarm_s": args.prewarm_s},
             "partition_ms": part_ms_max, "s5_ms": s5_ms_max,
             "pairs_per_step": {"S2a": s2a_pairs, "S2d": s2d_pairs, "S5": s5_pairs},
             "s5_pairs_per_s": s5_pairs / (s5_ms_max / 1e3),
@@ -625,6 +639,10 @@ def main():
             # each timed step's device time, first event to last (rank 0): an
             # outlier step shows here (a host stall between C3 and S4)
             "step_ms_rank0": [round(ev["start"].elapsed_time(ev["S5"]), 3) for ev, _ in per_step],
+            # host time of each step's enqueue segments (start -> S1 -> S4 -> S1b -> S5 marks), ms:
+            # a device-side outlier with a long host segment is a host stall
+            "host_segments_ms_rank0": [[round((b[1] - a[1]) * 1e3, 3) for a, b in zip(ev["_host"], ev["_host"][1:])]
+                                       for ev, _ in per_step],
             "bucket_sizes": [int(x) for x in sizes],
             "exact_fallbacks": out.part.exact_fallbacks,
             "roofline": roof, "partition_roofline": partition_roofline, "collectives": collectives,

@@ -13,6 +13,7 @@ with the same numbers.
 """
 from __future__ import annotations
 
+import time
 from dataclasses import dataclass, field
 
 import torch
@@ -90,6 +91,8 @@ class HotPath:
         def mark(name):
             if events is not None and name in events:
                 events[name].record(st)
+            if events is not None and "_host" in events:   # host timestamps (bench diagnostics)
+                events["_host"].append((name, time.perf_counter()))
 
         mark("start")
         prof, nk = B.sa_kmer_profiles(ctx, residues, offsets, self.k, self.alphabet, stream=stream)
