@@ -564,10 +564,13 @@ struct Geo2 {
 static_assert(Geo2<true>::STAGE_BYTES % 1024 == 0 && Geo2<false>::STAGE_BYTES % 1024 == 0, "stage alignment");
 constexpr int TBM2 = 2 * BM;   // pair-tile rows
 
+#ifndef SA_MAX_STAGES
+#define SA_MAX_STAGES 8
+#endif
 __host__ __device__ constexpr int stages2_of(int EW, int CW, bool FP4, int TB, int XB) {
   return (232448 - 1024 - 512 - EW * (slice_of(EW, CW, FP4) * TB + XB)) /
-                     (FP4 ? Geo2<true>::STAGE_BYTES : Geo2<false>::STAGE_BYTES) > 8
-             ? 8
+                     (FP4 ? Geo2<true>::STAGE_BYTES : Geo2<false>::STAGE_BYTES) > SA_MAX_STAGES
+             ? SA_MAX_STAGES
              : (232448 - 1024 - 512 - EW * (slice_of(EW, CW, FP4) * TB + XB)) /
                    (FP4 ? Geo2<true>::STAGE_BYTES : Geo2<false>::STAGE_BYTES);
 }
