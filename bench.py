@@ -471,7 +471,7 @@ def main():
             "C4_alltoallv": c4_bytes}
     collectives = {"n_ranks": world, "bytes_sent_per_rank_per_step": sent if world > 1 else {k: 0 for k in sent},
                    "bytes_if_sharded_over_8": None}
-    if world == 1:
+    if world == 1 and cfg.p % 8 == 0:
         # what rank 0 would send at G = 8 (same data): C1 and C2 scale with the
         # rank's blocks; C4 is 7/8 of its sequences' residues + records
         g = 8
@@ -480,7 +480,7 @@ def main():
         r0 = range(0, cfg.p // g)
         mine = np.arange(blk[r0.start], blk[r0.stop])
         bo = out.part.bucket_of.cpu().numpy()[mine]
-        off = np.array([b * g // cfg.p != 0 for b in bo])
+        off = np.array([b * g // cfg.p != 0 for b in bo], dtype=bool)
         collectives["bytes_if_sharded_over_8"] = {
             "C1_sample_allgather": (cfg.p // g) * cfg.samples_per_block * (stride * 2 + 4 + 8),
             "C2_regular_samples_allgather": (cfg.p // g) * (cfg.p - 1) * 32,

@@ -50,3 +50,11 @@ def test_mine_arm_json_line_is_consistent():
     ro = d["roofline"]
     assert abs(ro["frac"] - ro["achieved"] / ro["peak"]) <= 1e-9 and 0 < ro["frac"] < 1
     assert d["gpu_launches"] > 0
+    # per-step device times (sum = the timed total within event skew), partition GEMM
+    # rooflines, per-collective bytes (nothing leaves the GPU at N = 1)
+    assert len(d["step_ms_rank0"]) == 3 and len(d["host_segments_ms_rank0"]) == 3
+    assert sum(d["step_ms_rank0"]) <= 3 * d["ms_per_step"] * 1.01
+    pr = d["partition_roofline"]
+    for g in ("S2a_gemm", "S2d_gemm"):
+        assert pr[g]["pairs"] > 0 and abs(pr[g]["frac"] - pr[g]["achieved"] / pr["peak"]) <= 1e-9
+    assert all(v == 0 for v in d["collectives"]["bytes_sent_per_rank_per_step"].values())
