@@ -175,6 +175,11 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
                TcRecOut ro, int deep_planes, const int32_t* __restrict__ only_dense) {
   constexpr int TC_HIST_ROWS = hist_rows<DEEP>();
   if constexpr (!DEEP) deep_planes = 0;
+  if (only_dense) {   // the planes pass after the plan: nothing to do when every problem runs sparse
+    bool any_dense = false;
+    for (int t = 0; t < S.n; ++t) any_dense = any_dense || only_dense[O.prob[t]] == 0;
+    if (!any_dense) return;
+  }
   __shared__ uint32_t s_nrec;
   if (threadIdx.x == 0) s_nrec = 0;
   constexpr int64_t ROWB = FP4 ? TC_KCAP / 2 : TC_KCAP;
