@@ -37,8 +37,12 @@ def main():
     rb = [0]
     for n in SIZES:
         rb.append(rb[-1] + n)
-    nums = [B.padded_matrix(n, torch.uint16, P.device, 16) for n in SIZES]
-    sims = [B.padded_matrix(n, torch.float64, P.device, 16) for n in SIZES]
+    # SA_S5_LD="align,extra": row stride ld = n rounded up to align, plus extra
+    # (layout experiments; default 16,0 as HotPath)
+    la, lx = (int(x) for x in os.environ.get("SA_S5_LD", "16,0").split(","))
+    mat = lambda n, dt: torch.empty((n, -(-n // la) * la + lx), dtype=dt, device=P.device)[:, :n]
+    nums = [mat(n, torch.uint16) for n in SIZES]
+    sims = [mat(n, torch.float64) for n in SIZES]
     call = lambda: B.sa_bucket_similarity_batch(ctx, P, nk, rb, 8000, numerators=nums, similarity=sims)
     call()
     torch.cuda.synchronize()
@@ -51,7 +55,7 @@ def main():
         g.append(ctx.phase_ms()["gemm"])
     pairs = sum(n * (n - 1) // 2 for n in SIZES)
     byts = sum(n * n * 10 for n in SIZES)
-    print(json.dumps({"debug": os.environ.get("SA_K2T_DEBUG", "0"), "gemm_ms_min": min(g), "gemm_ms_med": float(np.median(g)),
+    print(json.dumps({"debug": os.environ.get("SA_K2T_DEBUG", "0"), "ld": [la, lx], "gemm_ms_min": min(g), "gemm_ms_med": float(np.median(g)),
                       "pairs": pairs, "hbm_floor_frac": byts / (min(g) * 1e-3) / 6448.4e9}))
 
 
