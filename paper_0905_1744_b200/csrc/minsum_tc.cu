@@ -1188,6 +1188,7 @@ struct KeyMatEpi {
         }
       }
     }
+    if (dbg & 4096) return;   // (SA_K2T_DEBUG 4096: experiment, no staging / TMA stores of the direct half)
     if (lane == 0) tc::bulk_wait_read0();
     __syncwarp();
 #pragma unroll
@@ -1989,6 +1990,11 @@ sa_status tc_launch(const std::vector<MsProblem>& probs_in, int ldw16, int32_t b
     }();
     batch.evict_last = evict_last;
     batch.debug = debug;
+    static const int serp = [] {   // SA_K2T_SERP=0: plain group order (tc::serp_index)
+      const char* e = getenv("SA_K2T_SERP");
+      return e ? atoi(e) : 1;
+    }();
+    batch.serp = serp;
     // decoded tile table (every GEMM warp reads its tile's coordinates with one load)
     uint2* ttab = scratch.alloc<uint2>((size_t)std::max<int64_t>(tiles, 1));
     if (!ttab) return fail(SA_E_NOMEM, "scratch allocation of the K2T tile table failed");

@@ -255,7 +255,8 @@ struct Batch {
   int n;
   int group;        // GROUP: row blocks per group of the tile order (below)
   int evict_last;   // operand L2 policies (side_policy bits; 0: no hint)
-  int debug;        // experiments only (SA_K2T_DEBUG): 1 no MMA, 2 no TMA loads, 4 no epilogue work
+  int debug;        // experiments only (SA_K2T_DEBUG): 1 no MMA, 2 no TMA loads, 4 no epilogue work, 8192 TMEM loads only
+  int serp;         // serpentine group order (serp_index): odd groups run backwards
 };
 struct alignas(64) Maps {
   CUtensorMap m[2 * MAXPROB];
@@ -318,10 +319,39 @@ __device__ __forceinline__ Tile decode(const Batch& b, int64_t tile) {
   T.rb = min(BN, P.nb - T.col0);
   return T;
 }
+// Serpentine group order: the tiles of every odd group of a problem run in
+// reverse, so a group's column sweep starts on the B column blocks the
+// previous group touched last (still in L2) instead of on the ones it touched
+// first (evicted first by the output stream).  Same tile set, same tiles per
+// launch; only the position of a tile in the flat order changes.
+template <int BN, int TBM>
+__device__ __forceinline__ int64_t serp_index(const Batch& b, int64_t tile) {
+  int pi = 0;
+  while (pi + 1 < b.n && b.p[pi + 1].tile_begin <= tile) ++pi;
+  const Problem& P = b.p[pi];
+  const int64_t t = tile - P.tile_begin;
+  const int tm = (P.na + TBM - 1) / TBM, tn = P.tiles_n;
+  const int GROUP = b.group;
+  int64_t gb, ge;
+  int gi;
+  if (!P.sym) {
+    const int64_t full = (int64_t)GROUP * tn;
+    gi = (int)(t / full);
+    gb = (int64_t)gi * full;
+    ge = min(gb + full, (int64_t)tm * tn);
+  } else {
+    int g0 = 0;
+    while (g0 + GROUP < tm && sym_tiles_before<BN, TBM>(g0 + GROUP, tn) <= t) g0 += GROUP;
+    gi = g0 / GROUP;
+    gb = sym_tiles_before<BN, TBM>(g0, tn);
+    ge = sym_tiles_before<BN, TBM>(min(g0 + GROUP, tm), tn);
+  }
+  return (gi & 1) ? P.tile_begin + gb + ge - 1 - t : tile;
+}
 template <int BN, int TBM>
 __global__ void tile_table_kernel(const __grid_constant__ Batch b, int64_t total, uint2* __restrict__ out) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const Tile T = decode_slow<BN, TBM>(b, t);
+    const Tile T = decode_slow<BN, TBM>(b, b.serp ? serp_index<BN, TBM>(b, t) : t);
     out[t] = make_uint2((uint32_t)T.pi | ((uint32_t)(T.row0 / TBM) << 8), (uint32_t)(T.col0 / BN));
   }
 }
@@ -847,6 +877,7 @@ gemm2_kernel(const __grid_constant__ Batch batch, const __grid_constant__ Maps m
 #pragma unroll
           for (int j = 0; j < CW; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + 8388608.0f) & 0x7FFFFFu;
         }
+        if (batch.debug & 8192) continue;   // (experiment: the TMEM loads alone)
         epi.template correct<CW>(es, col, v);
         epi.template chunk<CW, FP4, 2>(es, T, row, col, v, lane, tab, col - cbeg, xp);
       }
