@@ -1177,17 +1177,46 @@ struct KeyMatEpi {
       const double2 yd = *reinterpret_cast<const double2*>(ent + j * TAB_BYTES + YOFF);
       F[j] = fsel(C, s.y, s.d, yd.x, yd.y);   // (no per-pair run-time switch: it costs a branch per pair)
     }
-    if (s.rv && !(dbg & (8 | 512))) {   // (SA_K2T_DEBUG 512: experiment, mirrored stores skipped)
-      double* fm = E.sim + (int64_t)c0 * E.ld + s.row_g;
-      uint16_t* cmr = E.num + (int64_t)c0 * E.ld + s.row_g;
+    // the mirrored half (experiment builds: SA_MIRROR_V2 pairs lanes so that F leaves as 16-byte
+    // stores, two rows of one mirrored row per lane; SA_MIRROR_LAST issues it after the TMA stores)
+    auto mirror = [&]() {
+#ifdef SA_MIRROR_V2
+      if (ncols == 16 && __all_sync(0xffffffffu, s.rv) && !(dbg & (8 | 512))) {
+        const int odd = lane & 1;
+        double* fm2 = E.sim + (int64_t)(c0 + odd) * E.ld + (s.row_g - odd);
+        uint16_t* cmr = E.num + (int64_t)c0 * E.ld + s.row_g;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        if (j < ncols) {
-          __stcs(fm + (int64_t)j * E.ld, F[j]);
+        for (int j = 0; j < 16; j += 2) {
+          const double send = odd ? F[j] : F[j + 1];
+          const double recv = __shfl_xor_sync(0xffffffffu, send, 1);
+          const double2 o = odd ? make_double2(recv, F[j + 1]) : make_double2(F[j], recv);
+          __stcs(reinterpret_cast<double2*>(fm2 + (int64_t)j * E.ld), o);
           __stcs(reinterpret_cast<unsigned short*>(cmr + (int64_t)j * E.ld), (unsigned short)v[j]);
+          __stcs(reinterpret_cast<unsigned short*>(cmr + (int64_t)(j + 1) * E.ld), (unsigned short)v[j + 1]);
+        }
+        return;
+      }
+#endif
+      if (s.rv && !(dbg & (8 | 512))) {   // (SA_K2T_DEBUG 512: experiment, mirrored stores skipped)
+        double* fm = E.sim + (int64_t)c0 * E.ld + s.row_g;
+        uint16_t* cmr = E.num + (int64_t)c0 * E.ld + s.row_g;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (j < ncols) {
+            __stcs(fm + (int64_t)j * E.ld, F[j]);
+            __stcs(reinterpret_cast<unsigned short*>(cmr + (int64_t)j * E.ld), (unsigned short)v[j]);
+          }
         }
       }
+    };
+#ifdef SA_MIRROR_LAST
+    if (dbg & 4096) {
+      mirror();
+      return;
     }
+#else
+    mirror();
+#endif
     if (dbg & 4096) return;   // (SA_K2T_DEBUG 4096: experiment, no staging / TMA stores of the direct half)
     if (lane == 0) tc::bulk_wait_read0();
     __syncwarp();
@@ -1211,6 +1240,9 @@ struct KeyMatEpi {
       }
       tc::bulk_commit();
     }
+#ifdef SA_MIRROR_LAST
+    mirror();
+#endif
   }
 
   // the numerator / F matrices of a chunk (the host sets num (sim) on every
