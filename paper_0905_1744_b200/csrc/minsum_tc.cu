@@ -182,6 +182,8 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
   }
   __shared__ uint32_t s_nrec;
   if (threadIdx.x == 0) s_nrec = 0;
+  __syncthreads();
+  static_assert(tc::MAXPROB <= 32, "ovf_probs is a 32-bit problem mask");
   constexpr int64_t ROWB = FP4 ? TC_KCAP / 2 : TC_KCAP;
   const int dw = (bins + 15) & ~15;                      // columns per dense layer
   const int64_t layer_bytes = FP4 ? dw / 2 : dw;
@@ -198,6 +200,8 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
 #pragma unroll
   for (int l = 0; l < TC_HREG; ++l) s1[l] = s2[l] = 0u;
   uint32_t mx = 0;
+  uint32_t ovf_probs = 0;   // bit q: a record of problem q did not fit this CTA's segment
+  bool seg_full = false;
   int side = -1, deepest = 0;
   auto flush = [&](int sd) {
     uint32_t* g1 = planes + (int64_t)sd * 2 * TC_PLANE;
@@ -293,19 +297,29 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
           if (ro.on) {
             // records of the bins reaching 2 (sparse per row: ~8 of 8000 on
             // the protein workloads); the count is re-read from the row (L1)
+            // A full segment stays full: from then on a row with records only
+            // marks its problem, in a per-thread mask that reaches povf once,
+            // at the end of the kernel (long sequences, config 5: ~500 records
+            // per row against a budget of 48 -- one global atomic per lost
+            // record on the same two words took 1.1 ms of a 1.15 ms pass).
             uint32_t m = m23[0];
-            while (m) {
-              const int bit = __ffs(m) - 1;
-              m &= m - 1;
-              const uint32_t c = __ldg(base + h * (int64_t)stride16 + bit);
-              const uint32_t pos = atomicAdd(&s_nrec, 1u);
-              if (pos < ro.seg_cap) {
-                ro.seg[(int64_t)blockIdx.x * ro.seg_cap + pos] =
-                    make_uint2((uint32_t)(g + h), (uint32_t)(w * 32 + bit) | (c << 16));
-              } else {
-                atomicOr(&ro.povf[O.prob[t]], 1u);
-                atomicOr(ro.incomplete, 1u);
-              }
+            if (m) {
+              if (!seg_full && *reinterpret_cast<volatile uint32_t*>(&s_nrec) >= ro.seg_cap) seg_full = true;
+              if (seg_full) ovf_probs |= 1u << O.prob[t];
+              else
+                while (m) {
+                  const int bit = __ffs(m) - 1;
+                  m &= m - 1;
+                  const uint32_t pos = atomicAdd(&s_nrec, 1u);
+                  if (pos >= ro.seg_cap) {
+                    ovf_probs |= 1u << O.prob[t];
+                    seg_full = true;
+                    break;
+                  }
+                  const uint32_t c = __ldg(base + h * (int64_t)stride16 + bit);
+                  ro.seg[(int64_t)blockIdx.x * ro.seg_cap + pos] =
+                      make_uint2((uint32_t)(g + h), (uint32_t)(w * 32 + bit) | (c << 16));
+                }
             }
           }
         }
@@ -332,6 +346,11 @@ tc_hist_kernel(const __grid_constant__ TcSides S, const __grid_constant__ TcOut 
   for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((w & 31) == 0 && mx) atomicMax(&state[0], mx);
   if (ro.on) {
+    ovf_probs = __reduce_or_sync(0xffffffffu, ovf_probs);
+    if ((w & 31) == 0 && ovf_probs) {
+      for (uint32_t q = ovf_probs; q; q &= q - 1) atomicOr(&ro.povf[__ffs(q) - 1], 1u);
+      atomicOr(ro.incomplete, 1u);
+    }
     __syncthreads();
     if (threadIdx.x == 0) ro.cnt[blockIdx.x] = s_nrec;
   }
