@@ -288,13 +288,24 @@ def main():
     torch.cuda.synchronize()
     clocks.start()
     clocks.wait_first()
+    for _ in range(int(os.environ.get("SA_BENCH_SETTLE_STEPS", "0"))):   # diagnostics: untimed steps after the sampler's start-up
+        hp.step(res_d, offs_d, ds.n, first)
+    torch.cuda.synchronize()
     launches0 = B.sa_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # every step's events exist before the timed region (torch creates the CUDA
+    # event at its first record): no event creation inside the timed loop
+    pre = [{k: torch.cuda.Event(enable_timing=True) for k in names} for _ in range(args.steps)]
+    if os.environ.get("SA_BENCH_LAZY_EVENTS", "0") != "1":
+        for d in pre:
+            for e in d.values():
+                e.record(st)
+        torch.cuda.synchronize()
     e0.record(st)
-    for _ in range(args.steps):
+    for i in range(args.steps):
         # no host synchronisation inside the timed region: libsa only records
         # its phase events; they are read after the region (phase_history)
-        ev = {k: torch.cuda.Event(enable_timing=True) for k in names}
+        ev = pre[i]
         ev["_host"] = []
         out = hp.step(res_d, offs_d, ds.n, first, events=ev)
         per_step.append(ev)
