@@ -654,6 +654,10 @@ def main():
             # a device-side outlier with a long host segment is a host stall
             "host_segments_ms_rank0": [[round((b[1] - a[1]) * 1e3, 3) for a, b in zip(ev["_host"], ev["_host"][1:])]
                                        for ev, _ in per_step],
+            # device time of the step's segments between the same marks, and of libsa's phases, per step
+            "device_segments_ms_rank0": [[round(ev[a].elapsed_time(ev[b]), 3) for a, b in zip(names, names[1:])]
+                                         for ev, _ in per_step],
+            "phase_steps_ms_rank0": {k: [round(ph[k], 3) for _, ph in per_step] for k in ("S2a", "S2b", "S2c", "S2d", "S3")},
             "bucket_sizes": [int(x) for x in sizes],
             "exact_fallbacks": out.part.exact_fallbacks,
             "roofline": roof, "partition_roofline": partition_roofline, "collectives": collectives,
