@@ -4,9 +4,11 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <mutex>
 #include <string>
+#include <chrono>
 #include <vector>
 
 #include "../../include/sa.h"
@@ -41,26 +43,152 @@ void count_launch(int n = 1);
                         cudaGetErrorString(e_));                                     \
   } while (0)
 
+// Large scratch blocks kept by the library between calls (SA_SCRATCH_CACHE=1;
+// off by default).  The stream-ordered pool keeps freed memory too (release
+// threshold, api.cu), but was seen to re-map a 328 MB block in the middle of a
+// run (config 3, tenth timed step: cudaMallocAsync held the host 48-176 ms,
+// DESIGN.md section 7).  A block returned here carries an event recorded on the
+// stream that last used it; whoever takes it makes its stream wait on that
+// event, so reuse is ordered after the earlier work on any stream.  Blocks are
+// matched by exact size and device; the cache is bounded (count and bytes),
+// the oldest block going back to the pool.
+struct ScratchCache {
+  struct Blk {
+    void* p;
+    size_t bytes;
+    int dev;
+    cudaEvent_t ev;
+    cudaStream_t st;
+  };
+  static constexpr size_t MIN_BYTES = (size_t)1 << 20;
+  static constexpr size_t MAX_BLOCKS = 96;
+  static constexpr size_t MAX_BYTES = (size_t)24 << 30;
+  std::mutex m;
+  std::vector<Blk> blocks;
+  size_t held = 0;
+  static ScratchCache& get() {
+    static ScratchCache c;
+    return c;
+  }
+  static bool enabled() {
+    static const bool on = [] {
+      const char* e = getenv("SA_SCRATCH_CACHE");
+      return e && atoi(e) != 0;
+    }();
+    return on;
+  }
+  void* take(size_t bytes, int dev, cudaStream_t st) {
+    Blk b{};
+    {
+      std::lock_guard<std::mutex> g(m);
+      size_t i = 0;
+      for (; i < blocks.size(); ++i)
+        if (blocks[i].bytes == bytes && blocks[i].dev == dev) break;
+      if (i == blocks.size()) return nullptr;
+      b = blocks[i];
+      blocks.erase(blocks.begin() + (long)i);
+      held -= b.bytes;
+    }
+    if (b.st != st) cudaStreamWaitEvent(st, b.ev, 0);
+    cudaEventDestroy(b.ev);
+    return b.p;
+  }
+  // every kept block back to the pool (an allocation failed: the memory may be needed elsewhere)
+  bool flush(cudaStream_t st) {
+    std::vector<Blk> drop;
+    {
+      std::lock_guard<std::mutex> g(m);
+      drop.swap(blocks);
+      held = 0;
+    }
+    for (const Blk& d : drop) {
+      cudaStreamWaitEvent(st, d.ev, 0);
+      cudaFreeAsync(d.p, st);
+      cudaEventDestroy(d.ev);
+    }
+    return !drop.empty();
+  }
+  // false: not kept (the caller frees it)
+  bool give(void* p, size_t bytes, int dev, cudaStream_t st) {
+    cudaEvent_t ev = nullptr;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(ev, st) != cudaSuccess) {
+      cudaGetLastError();
+      if (ev) cudaEventDestroy(ev);
+      return false;
+    }
+    std::vector<Blk> drop;
+    {
+      std::lock_guard<std::mutex> g(m);
+      blocks.push_back(Blk{p, bytes, dev, ev, st});
+      held += bytes;
+      while (blocks.size() > MAX_BLOCKS || held > MAX_BYTES) {
+        drop.push_back(blocks.front());
+        held -= blocks.front().bytes;
+        blocks.erase(blocks.begin());
+      }
+    }
+    for (const Blk& d : drop) {   // back to the pool, after the work that last used it
+      cudaStreamWaitEvent(st, d.ev, 0);
+      cudaFreeAsync(d.p, st);
+      cudaEventDestroy(d.ev);
+    }
+    return true;
+  }
+};
+
 // Stream-ordered scratch: allocations are freed on the same stream when the
 // Scratch goes out of scope, so kernels enqueued before still see them.
 struct Scratch {
   cudaStream_t st;
   std::vector<void*> ptrs;
+  std::vector<size_t> sizes;
+  int dev = -1;
   bool oom = false;
-  explicit Scratch(cudaStream_t s) : st(s) {}
+  explicit Scratch(cudaStream_t s) : st(s) {
+    if (ScratchCache::enabled() && cudaGetDevice(&dev) != cudaSuccess) {
+      cudaGetLastError();
+      dev = -1;
+    }
+  }
   ~Scratch() {
-    for (void* p : ptrs) cudaFreeAsync(p, st);
+    for (size_t i = 0; i < ptrs.size(); ++i) {
+      if (dev >= 0 && sizes[i] >= ScratchCache::MIN_BYTES && ScratchCache::get().give(ptrs[i], sizes[i], dev, st))
+        continue;
+      cudaFreeAsync(ptrs[i], st);
+    }
   }
   template <class T>
   T* alloc(size_t n) {
     void* p = nullptr;
     const size_t bytes = std::max<size_t>(n * sizeof(T), 16);
-    if (cudaMallocAsync(&p, bytes, st) != cudaSuccess) {
+    if (dev >= 0 && bytes >= ScratchCache::MIN_BYTES && (p = ScratchCache::get().take(bytes, dev, st)) != nullptr) {
+      ptrs.push_back(p);
+      sizes.push_back(bytes);
+      return static_cast<T*>(p);
+    }
+    // SA_TRACE_ALLOC=1 (diagnostics): report pool allocations that hold the host for more than 0.3 ms
+    static const bool trace = [] {
+      const char* e = getenv("SA_TRACE_ALLOC");
+      return e && atoi(e) != 0;
+    }();
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaError_t rc = cudaMallocAsync(&p, bytes, st);
+    if (rc != cudaSuccess && dev >= 0 && ScratchCache::get().flush(st)) {
+      cudaGetLastError();
+      rc = cudaMallocAsync(&p, bytes, st);
+    }
+    if (trace) {
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      if (ms > 0.3) fprintf(stderr, "[sa] cudaMallocAsync(%zu bytes) held the host %.2f ms\n", bytes, ms);
+    }
+    if (rc != cudaSuccess) {
       cudaGetLastError();
       oom = true;
       return nullptr;
     }
     ptrs.push_back(p);
+    sizes.push_back(bytes);
     return static_cast<T*>(p);
   }
 };
