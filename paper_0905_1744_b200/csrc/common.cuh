@@ -43,8 +43,8 @@ void count_launch(int n = 1);
                         cudaGetErrorString(e_));                                     \
   } while (0)
 
-// Large scratch blocks kept by the library between calls (SA_SCRATCH_CACHE=1;
-// off by default).  The stream-ordered pool keeps freed memory too (release
+// Large scratch blocks kept by the library between calls (on by default;
+// SA_SCRATCH_CACHE=0 turns it off).  The stream-ordered pool keeps freed memory too (release
 // threshold, api.cu), but was seen to re-map a 328 MB block in the middle of a
 // run (config 3, tenth timed step: cudaMallocAsync held the host 48-176 ms,
 // DESIGN.md section 7).  A block returned here carries an event recorded on the
@@ -73,7 +73,7 @@ struct ScratchCache {
   static bool enabled() {
     static const bool on = [] {
       const char* e = getenv("SA_SCRATCH_CACHE");
-      return e && atoi(e) != 0;
+      return !e || atoi(e) != 0;  // on unless SA_SCRATCH_CACHE=0
     }();
     return on;
   }
